@@ -1,0 +1,380 @@
+#!/usr/bin/env python
+"""Benchmark of the hot path: one step = one tt_round_sum call (Alg. 7 + the
+truncation to rank r) on BASELINE.json's large config (config 5, reading "C":
+S=32 summands, d=50, I=256, summand rank 64, sketch rank 144 -> rank 128).
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference]
+                  [--workload large|sum10|gmres|single|tiny]
+
+N>1 runs under torchrun, one process per GPU; the summands are sharded across
+ranks and each sweep step allreduces the partial sketched core Y_n over NCCL
+(strong scaling of one rounding).  Rank 0 prints ONE JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "TT sum-roundings/sec and FP64 TFLOP/s (fraction of peak) at 1/2/4/8 B200"
+WORKLOADS = {
+    "large": dict(cfg="config5_large", args={}, desc="config 5 (reading C): S=32, d=50, I=256, "
+                  "summand rank 64 (signal 96 + 16/summand noise at 1e-6), sketch 144, rank 128"),
+    "sum10": dict(cfg="config3_sum10", args={}, desc="config 3: S=10, d=20, I=100, rank 60, sketch 70"),
+    "gmres": dict(cfg="config4_gmres", args={}, desc="config 4: S=20, d=12, I=128, rank 40, tol 1e-8, adaptive from 80"),
+    "single": dict(cfg="config2_single", args={}, desc="config 2: S=1, d=16, I=64, rank 50 -> 25, sketch 35"),
+    "tiny": dict(cfg="config1_tiny", args={}, desc="config 1: S=2, d=4, I=4, rank 3 each -> 4, sketch 6"),
+}
+
+
+def fp64_peak():
+    """FP64 tensor (DMMA) peak: MEASURED_PEAKS.json if it has one, else this repo's
+    own all-SM DMMA microbenchmark (profiles/fp64_peak.json, tools/fp64_peak.cu)."""
+    mp = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        v = json.load(open(mp)).get("fp64_tflops")
+        if v:
+            return float(v), "MEASURED_PEAKS.json fp64_tflops"
+    except Exception:
+        pass
+    p = os.path.join(ROOT, "profiles", "fp64_peak.json")
+    try:
+        v = json.load(open(p))
+        return float(v["fp64_dmma_tflops"]), "measured DMMA.8x8x4 all-SM microbenchmark (profiles/fp64_peak.json)"
+    except Exception:
+        return 40.0, "datasheet-class FP64 tensor figure (no measurement available)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def __enter__(self):
+        def run():
+            q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+            while not self._stop.is_set():
+                try:
+                    out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits"], capture_output=True,
+                                         text=True, timeout=5).stdout.strip()
+                    if out:
+                        self.samples.append([x.strip() for x in out.split(",")])
+                except Exception:
+                    pass
+                self._stop.wait(0.2)
+        self._t = threading.Thread(target=run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 3 + i and s[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def make_workload(name, device, seed_offset=0):
+    import ttsynth
+    w = WORKLOADS[name]
+    fn = getattr(ttsynth, w["cfg"])
+    return fn(device=device, **w["args"])
+
+
+def flops_of(wl, ranks_out):
+    from paper_2110_04393_b200 import cost
+    dims = wl.dims
+    tr = [[int(t[0].shape[0])] + [int(c.shape[2]) for c in t] for t in wl.terms]
+    sumR = [sum(r[n] for r in tr) for n in range(len(dims) + 1)]
+    l = cost.caps(dims, sumR, wl.ell)
+    kept = ranks_out if (wl.tol > 0 or (wl.rank and any(x > wl.rank for x in l[1:-1]))) else None
+    return cost.rounding_flops(dims, tr, l, kept), l
+
+
+def cpu_oracle_sample(name, budget_s=20.0):
+    """Time the oracle (as it stands) on a bounded sample of the workload: the same
+    S, I, ranks, sketch rank at reduced order d, scaled to the full config by the
+    exact flop ratio.  Returns (roundings/s for the full config, description, cores)."""
+    import numpy as np
+    import oracle
+    import ttsynth
+    from paper_2110_04393_b200 import cost
+    full = make_workload(name, "cpu") if name in ("tiny", "single") else None
+    w = WORKLOADS[name]
+    fn = getattr(ttsynth, w["cfg"])
+    d_full = {"large": 50, "sum10": 20, "gmres": 12, "single": 16, "tiny": 4}[name]
+    d_s = min(d_full, 4 if name == "large" else d_full)
+    sample = fn(device="cpu", d=d_s) if d_s != d_full else (full or fn(device="cpu"))
+    terms = [ttsynth.to_numpy(t) for t in sample.terms]
+    t0 = time.perf_counter()
+    reps = 0
+    while True:
+        r = oracle.round_sum(terms, ell=sample.ell, seed=1, rank=sample.rank, tol=sample.tol,
+                             adaptive=sample.adaptive)
+        reps += 1
+        if time.perf_counter() - t0 > budget_s or reps >= 50:
+            break
+    dt = (time.perf_counter() - t0) / reps
+    fs, _ = flops_of(sample, [1] + list(r.ranks) + [1])
+    # flops of the full config (ranks after truncation taken as the target rank)
+    fw = sample if d_s == d_full else None
+    if fw is None:
+        dims = [sample.dims[0]] * d_full
+        tr = [[1] + [int(sample.terms[0][1].shape[0])] * (d_full - 1) + [1]] * len(sample.terms)
+        sumR = [sum(x[n] for x in tr) for n in range(d_full + 1)]
+        l = cost.caps(dims, sumR, sample.ell)
+        kept = [1] + [min(sample.rank, x) for x in l[1:-1]] + [1]
+        ff = cost.rounding_flops(dims, tr, l, kept)["total"]
+    else:
+        ff = fs["total"]
+    rate = 1.0 / (dt * ff / fs["total"])
+    try:
+        from threadpoolctl import threadpool_info
+        cores = max([x.get("num_threads", 1) for x in threadpool_info()] + [1])
+    except Exception:
+        cores = os.cpu_count()
+    desc = (f"oracle (NumPy fp64, BLAS/LAPACK steps) on {w['desc']} at d={d_s} "
+            f"({reps} run(s), {dt:.2f} s each, {fs['total'] / dt / 1e9:.2f} GFLOP/s), "
+            f"scaled to d={d_full} by the exact flop ratio")
+    return rate, desc, cores, fs["total"] / dt
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="large", choices=list(WORKLOADS))
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        return reference_arm(args, world, rank)
+
+    import torch
+    import torch.distributed as dist
+    import paper_2110_04393_b200 as P
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+
+    wl = make_workload(args.workload, dev)
+    S = len(wl.terms)
+    lo, hi = (rank * S) // world, ((rank + 1) * S) // world
+    local_terms = wl.terms[lo:hi]
+    for t in wl.terms[:lo] + wl.terms[hi:]:
+        t.clear()
+    torch.cuda.synchronize()
+
+    nccl_id = None
+    if world > 1:
+        obj = [P.tt_get_nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    ctx = P.Context(local, stream=torch.cuda.current_stream(dev), nccl_id=nccl_id, rank=rank,
+                    world=world)
+    ctx.set_timing(True)
+    if wl.tol > 0:
+        kw = dict(mode="tol", tol=wl.tol, oversample=wl.ell, adaptive=wl.adaptive, rank=wl.rank)
+    else:
+        kw = dict(mode="rank", rank=wl.rank, oversample=wl.ell - wl.rank)
+
+    def step():
+        return ctx.tt_round_sum(local_terms, seed=1, **kw)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    res = None
+    for _ in range(max(3, args.warmup)):
+        res = step()
+    ranks_out = res.ranks
+    del res
+    barrier()
+    stream = torch.cuda.current_stream(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    phase = [0.0] * 8
+    n_l0 = P.tt_launch_count()
+    with ClockSampler(local) as clk:
+        barrier()
+        e0.record(stream)
+        for _ in range(args.steps):
+            r = step()
+            t = ctx.last_timing()
+            for i in range(len(t)):
+                phase[i] += t[i]
+            del r
+        e1.record(stream)
+        barrier()
+    launches = P.tt_launch_count() - n_l0
+    ms = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        tt = torch.tensor([ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+        ph = torch.tensor(phase, device=dev, dtype=torch.float64)
+        dist.all_reduce(ph, op=dist.ReduceOp.MAX)
+        phase = ph.tolist()
+    phase = [p / args.steps for p in phase]
+
+    fl, l = flops_of(wl, ranks_out)
+    peak, peak_src = fp64_peak()
+    value = 1000.0 / ms                       # roundings/s (one rounding per step, all ranks)
+    tflops = fl["total"] / (ms * 1e-3) / 1e12
+    # dominant kernel family: the phase-1 DMMA contractions (Alg. 3), timed live
+    p1_ms = phase[1]
+    p1_flops_local = fl["phase1"] * (hi - lo) / S
+    p1_achieved = p1_flops_local / (p1_ms * 1e-3) / 1e12 if p1_ms > 0 else None
+
+    e2e = None
+    if not args.no_e2e:
+        e2e = e2e_run(args, ctx, local_terms, kw, dev, world, dist if world > 1 else None)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        rate, desc, cores, gfs = cpu_oracle_sample(args.workload)
+        cpu = {"value": rate, "unit": "roundings/s", "cores": cores, "kind": "oracle",
+               "sample": desc}
+
+    if rank == 0:
+        traffic = None
+        prof = os.path.join(ROOT, "profiles", "traffic.json")
+        try:
+            traffic = json.load(open(prof)).get(args.workload)
+        except Exception:
+            pass
+        line = {
+            "metric": METRIC, "value": value, "unit": "roundings/s", "n_gpus": world,
+            "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (ttsynth, seeded; DESIGN.md input recipe)",
+            "config": {"workload": args.workload, "desc": WORKLOADS[args.workload]["desc"],
+                       "summands": S, "d": wl.d, "I": wl.dims[0], "sketch_rank": wl.ell,
+                       "rank": wl.rank, "tol": wl.tol, "parallelism": f"summands/{world}",
+                       "l2": "inputs (12.9 GB) larger than L2 (126 MB); no flush"},
+            "tflops": tflops, "fp64_peak_tflops": peak, "fp64_peak_source": peak_src,
+            "frac_of_fp64_peak": tflops / peak,
+            "flops_per_rounding": fl,
+            "phase_ms": {"sketch": phase[0], "phase1_contractions": phase[1],
+                         "sweep_gemms": phase[2], "qr": phase[3], "collectives": phase[4],
+                         "truncation": phase[5], "total": phase[6]},
+            "roofline": {"bound": "tensor", "kernel": "dgemm_kernel (phase-1 Alg. 3 contractions, DMMA.8x8x4)",
+                         "achieved": p1_achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": (p1_achieved / peak) if p1_achieved else None,
+                         "traffic": traffic,
+                         "algorithmic": "phase-1 flops = sum_j [2 R I l + sum_n (2 R^2 I l + 2 R I l^2)] (SURVEY 8d)"},
+            "gpu_launches": launches,
+            "ranks_out": ranks_out,
+            "clocks": clk.summary(),
+        }
+        if e2e is not None:
+            line["e2e"] = e2e
+        if cpu is not None:
+            line["cpu_baseline"] = cpu
+        print(json.dumps(line))
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def e2e_run(args, ctx, local_terms, kw, dev, world, dist):
+    """Same metric through the C-ABI with HOST (pinned) buffers: the H2D copies of
+    the inputs happen inside the call (overlapped with phase 1) and the result is
+    read back D2H into pinned memory, both inside the timed region."""
+    import torch
+    host = [[c.permute(2, 1, 0).contiguous().cpu().pin_memory().permute(2, 1, 0) for c in t]
+            for t in local_terms]
+    h2d = sum(c.numel() * 8 for t in host for c in t)
+    r = ctx.tt_round_sum(host, seed=1, **kw)
+    outs = [torch.empty((r.ranks[n + 1], r.dims[n], r.ranks[n]), dtype=torch.float64).pin_memory()
+            for n in range(r.d)]
+    d2h = sum(o.numel() * 8 for o in outs)
+    del r
+    import ctypes
+    from paper_2110_04393_b200 import _lib
+    L = _lib.load_library()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        r = ctx.tt_round_sum(host, seed=1, **kw)
+        for n in range(r.d):
+            _lib._check(L.tt_tensor_copy_core(r._h.ptr, n + 1, ctypes.c_void_p(outs[n].data_ptr())))
+        del r
+    torch.cuda.synchronize()
+    dt = (time.perf_counter() - t0) / args.e2e_steps
+    if dist:
+        tt = torch.tensor([dt], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        dt = float(tt.item())
+    del host
+    return {"value": 1.0 / dt, "unit": "roundings/s", "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "steps": args.e2e_steps,
+            "note": "host-clock over the whole call incl. H2D staging and D2H of the result"}
+
+
+def reference_arm(args, world, rank):
+    """--impl reference: the oracle (as it stands) on the host cores, rank 0 only."""
+    if rank != 0:
+        return
+    steps = []
+    desc = cores = None
+    for _ in range(args.warmup):
+        cpu_oracle_sample(args.workload, budget_s=2.0)
+    for _ in range(args.steps):
+        rate, desc, cores, _ = cpu_oracle_sample(args.workload, budget_s=10.0)
+        steps.append(1.0 / rate)
+    ms = 1000.0 * statistics.mean(steps)
+    value = 1000.0 / ms
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "roundings/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": args.workload,
+                                        "desc": WORKLOADS[args.workload]["desc"]},
+        "cpu_baseline": {"value": value, "unit": "roundings/s", "cores": cores,
+                         "kind": "oracle", "sample": desc},
+        "e2e": {"value": value, "unit": "roundings/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }))
+
+
+if __name__ == "__main__":
+    main()

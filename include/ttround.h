@@ -1,0 +1,192 @@
+/*
+ * ttround.h — C-ABI of the B200-native randomized TT-rounding library
+ * (libttround.so, built from paper_2110_04393_b200/csrc).
+ *
+ * Method: arXiv 2110.04393 ("Randomized algorithms for rounding in the
+ * Tensor-Train format").  Citations "P:n" are lines of the paper text
+ * (PAPER.md); DESIGN.md lists every reading of the paper the library makes
+ * (R1..R17) and is the companion of this header.
+ *
+ * ------------------------------------------------------------------------
+ * Conventions shared by every entry point
+ * ------------------------------------------------------------------------
+ * TT-tensor: d >= 2 cores X_n, n = 1..d, X_n in R^{R_{n-1} x I_n x R_n},
+ * R_0 = R_d = 1.  All values are IEEE fp64.
+ *
+ * Core layout ("a-fastest", column-major in (a, i, b)): element (a, i, b) of
+ * core n is stored at  a + R_{n-1} * (i + I_n * b).  Hence
+ *   V(X_n) is the column-major R_{n-1}I_n x R_n matrix at the same
+ *          address with leading dimension R_{n-1}I_n (row index a + R_{n-1} i;
+ *          the paper stacks slices, i.e. the same rows in another order), and
+ *   H(X_n) is the column-major R_{n-1} x I_n R_n matrix with leading
+ *          dimension R_{n-1} (column index i + I_n b; the paper's is b-fastest).
+ * Both unfoldings are reshape-only; the row/column permutations w.r.t. the
+ * paper are applied consistently to every operand, so every product of
+ * unfoldings the algorithms form is the paper's (R1).
+ * In PyTorch terms: a tensor of logical shape (R_{n-1}, I_n, R_n) with strides
+ * (1, R_{n-1}, R_{n-1} I_n), i.e. torch.empty(R_n, I_n, R_{n-1}).permute(2,1,0).
+ *
+ * Memory: input cores are BORROWED (read-only) and may live in device memory
+ * of the context's device or in host memory (pageable or pinned); host inputs
+ * are copied to the device inside the call, overlapped with the computation.
+ * Results (tt_tensor_t) and sketches (tt_sketch_t) are OWNED by the library and
+ * released with the matching *_destroy.  Every call is ordered on the
+ * context's CUDA stream and returns after the work completed (results are
+ * readable on return).  Calls on one context must not overlap (one thread at a
+ * time); different contexts are independent.
+ *
+ * Errors: every entry point returns an int, TT_OK (0) on success or a negative
+ * TT_ERR_* code; no exception crosses the ABI; out-parameters are untouched on
+ * error; tt_last_error() returns a thread-local message for the last failure.
+ * A rank capped below the request is not an error (TT_FLAG_RANK_CAPPED).
+ */
+#ifndef TTROUND_H
+#define TTROUND_H
+
+#include <stdint.h>
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- return codes ------------------------------------------------------- */
+#define TT_OK             0
+#define TT_ERR_ARG       -1   /* null pointer, d < 2, S < 1, bad mode/option       */
+#define TT_ERR_SHAPE     -2   /* dims differ across summands; bond ranks mismatch   */
+#define TT_ERR_RANK      -3   /* a rank < 1, or R_0 != 1 or R_d != 1                */
+#define TT_ERR_NONFINITE -4   /* (reserved) non-finite input detected               */
+#define TT_ERR_OOM       -5   /* device allocation failed                           */
+#define TT_ERR_CUDA      -6   /* CUDA runtime error (message in tt_last_error)      */
+#define TT_ERR_NCCL      -7   /* NCCL missing or failed                             */
+#define TT_ERR_NUMERIC   -8   /* QR/SVD breakdown even after the Householder fallback */
+
+/* ---- rounding modes (tt_round_opts.mode) -------------------------------- */
+#define TT_SKETCH_ONLY 0  /* Alg. 7 output with the (capped) sketch ranks l_n, left-orthogonal */
+#define TT_RANK        1  /* sketch with l = rank + oversample, then truncate to rank (R6)           */
+#define TT_TOL         2  /* sketch with l = oversample (initial), truncate to eps0 (R3-R5) */
+
+/* ---- result flags (tt_tensor_info) -------------------------------------- */
+#define TT_FLAG_RANK_CAPPED   1u  /* some l_n was capped below the request (R7)             */
+#define TT_FLAG_LEFT_ORTH     2u  /* cores 1..d-1 left-orthogonal (TT_SKETCH_ONLY)  */
+#define TT_FLAG_RIGHT_ORTH    4u  /* cores 2..d right-orthogonal (after truncation, R3)    */
+#define TT_FLAG_ZERO          8u  /* the sum was exactly zero: all ranks 1, zero cores (R16) */
+#define TT_FLAG_QR_FALLBACK  16u  /* a Householder fallback QR ran at least once           */
+
+typedef struct tt_ctx*    tt_ctx_t;
+typedef struct tt_sketch* tt_sketch_t;
+typedef struct tt_tensor* tt_tensor_t;
+
+/* A borrowed TT-tensor.  dims[d], ranks[d+1] (ranks[0] = ranks[d] = 1) and
+ * cores[d] are host arrays; cores[n] points to R_{n-1} I_n R_n doubles in the
+ * layout above (device memory of the context's device, or host memory). */
+typedef struct {
+  int32_t d;
+  const int64_t* dims;
+  const int64_t* ranks;
+  const double* const* cores;
+} tt_view;
+
+typedef struct {
+  int32_t  mode;        /* TT_SKETCH_ONLY | TT_RANK | TT_TOL                                  */
+  int32_t  adaptive;    /* TT_TOL only: grow l (x2) while a bond is saturated (R8)            */
+  int64_t  rank;        /* TT_RANK: target rank r (uniform); TT_TOL: optional extra cap (0=none) */
+  int64_t  oversample;  /* TT_RANK: p, sketch rank l = r + p; TT_SKETCH_ONLY/TT_TOL: l itself  */
+  double   tol;         /* TT_TOL: relative tolerance eps0 > 0 (Alg. 2)                */
+  uint64_t seed;        /* Philox key of the Gaussian sketch (Def. 3.1 / R9)                  */
+  int64_t  max_rank;    /* adaptive upper bound on l (0 = structural caps only)               */
+} tt_round_opts;
+
+/* ---- context ------------------------------------------------------------- */
+/* NCCL unique id (128 bytes) for tt_ctx_create; call on one rank, broadcast the
+ * bytes (e.g. torch.distributed), pass them to tt_ctx_create on every rank. */
+int tt_get_nccl_unique_id(uint8_t id[128]);
+
+/* Create a context on CUDA device `device` using stream `cuda_stream`
+ * (a cudaStream_t, or NULL for a library-created non-blocking stream).
+ * nccl_id == NULL or world == 1: single-GPU.  Otherwise the summands of a
+ * rounding are sharded across `world` processes (one per GPU); each passes its
+ * local summands and all receive the same result. */
+int tt_ctx_create(int device, void* cuda_stream, const uint8_t* nccl_id,
+                  int rank, int world, tt_ctx_t* out);
+int tt_ctx_destroy(tt_ctx_t ctx);
+
+/* ---- sketch (Def. 3.1) --------------------------------------- */
+/* Random Gaussian TT with ranks (1, l_1..l_{d-1}, 1): cores n = 2..d filled
+ * in place with N(0, 1/(l_{n-1} I_n l_n)) entries from Philox4x32-10 keyed by
+ * `seed`, counter (k_lo, k_hi, n, tag) for element pair k (R9).  Core 1 is
+ * never used by Alg. 3/5/7 (R10) and is not materialised.  ranks has d+1
+ * entries with ranks[0] = ranks[d] = 1 and must already be capped (R7). */
+int tt_sketch_create(tt_ctx_t ctx, int32_t d, const int64_t* dims,
+                     const int64_t* ranks, uint64_t seed, uint32_t tag,
+                     tt_sketch_t* out);
+/* Device pointer of core n (1-based, n >= 2) of a sketch (read-only). */
+int tt_sketch_core(tt_sketch_t sk, int32_t n, const double** core);
+int tt_sketch_destroy(tt_sketch_t sk);
+
+/* ---- the hot path: Alg. 7 + truncation ----------- */
+/* Round Y = sum_j Y^(j) of S_local summands (this process's shard).
+ *  1. caps l_n = min(l, l_{n-1} I_n, prod_{k>n} I_k, sum_j R^(j)_n)    (R7)
+ *  2. sketch R (Def. 3.1) — from opts->seed, or `sketch` if non-NULL (it must
+ *     have exactly the capped ranks, else TT_ERR_SHAPE)
+ *  3. W^(j)_n = PartialContractionsRL(Y^(j), R) for every summand     (Alg. 3)
+ *  4. left-to-right sweep: Y_n = V(X_n)[W^(1)_n; ...], Q_n = qr(Y_n),
+ *     M_n = Q_n^T V(X_n), fold M^(j)_n into core n+1 of every summand   (Alg. 7)
+ *  5. TT_RANK / TT_TOL: right-to-left QR+SVD truncation of the left-orthogonal
+ *     result (R3-R5), with adaptive growth of l in TT_TOL (R8).
+ * The result has ranks (1, k_1..k_{d-1}, 1) and is returned in *out. */
+int tt_round_sum(tt_ctx_t ctx, int32_t S_local, const tt_view* terms,
+                 const tt_round_opts* opts, tt_sketch_t sketch, tt_tensor_t* out);
+
+/* Deterministic TT-rounding of the assembled sum: Alg. 1 + Alg. 2
+ * with eps0 = opts->tol (and opts->rank as an optional rank cap).
+ * Not yet implemented in this build: returns TT_ERR_ARG with a message. */
+int tt_round_deterministic(tt_ctx_t ctx, int32_t S, const tt_view* terms,
+                           const tt_round_opts* opts, tt_tensor_t* out);
+
+/* <x, y> by the full right-to-left contraction (App. A); *out is a
+ * host double.  x and y must have equal dims. */
+int tt_inner(tt_ctx_t ctx, const tt_view* x, const tt_view* y, double* out);
+
+/* ---- results ------------------------------------------------------------- */
+/* Borrowed views of a result: *dims (d), *ranks (d+1), *cores (d device
+ * pointers, layout above), valid until tt_tensor_destroy. */
+int tt_tensor_info(tt_tensor_t t, int32_t* d, const int64_t** dims,
+                   const int64_t** ranks, double* const** cores, uint32_t* flags);
+/* Copy core n (1-based) to caller memory (host or device), R_{n-1} I_n R_n doubles. */
+int tt_tensor_copy_core(tt_tensor_t t, int32_t n, double* dst);
+/* Number of rounding passes the adaptive loop made (1 if not adaptive). */
+int tt_tensor_passes(tt_tensor_t t, int32_t* passes);
+int tt_tensor_destroy(tt_tensor_t t);
+
+/* ---- diagnostics --------------------------------------------------------- */
+const char* tt_last_error(void);
+/* Number of CUDA kernels this library launched since load (all contexts). */
+uint64_t tt_launch_count(void);
+/* Per-phase device times (ms) of the last tt_round_sum on ctx, measured with
+ * CUDA events on the context stream when timing is enabled:
+ * [0] sketch, [1] phase 1 (Alg. 3), [2] sweep GEMMs, [3] QR, [4] collectives,
+ * [5] truncation, [6] total.  Returns the number of entries written (<= n). */
+int tt_ctx_set_timing(tt_ctx_t ctx, int enable);
+int tt_ctx_last_timing(tt_ctx_t ctx, double* ms, int n);
+
+/* ---- kernel-level entry points (for the parity tests and bench) ---------- */
+/* C = alpha*op(A)*op(B) + beta*C, column-major fp64, device pointers; the
+ * FP64 tensor-core (DMMA) GEMM every contraction of the hot path runs on. */
+int tt_dgemm(tt_ctx_t ctx, int trans_a, int trans_b, int64_t m, int64_t n, int64_t k,
+             double alpha, const double* A, int64_t lda, const double* B, int64_t ldb,
+             double beta, double* C, int64_t ldc);
+/* Thin QR of the column-major m x n (m >= n) device matrix A: Q (m x n, ld m)
+ * and, if R != NULL, R (n x n upper triangular, ld n).  Returns TT_OK and sets
+ * *fallback = 1 if the Householder fallback ran. */
+int tt_qr(tt_ctx_t ctx, int64_t m, int64_t n, const double* A, int64_t lda,
+          double* Q, double* R, int* fallback);
+/* Singular values (descending) and right singular vectors of the column-major
+ * m x n (m >= n) device matrix A: AV (m x n, = U Sigma) and V (n x n). */
+int tt_svd_jacobi(tt_ctx_t ctx, int64_t m, int64_t n, const double* A, int64_t lda,
+                  double* AV, double* V, double* sigma);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TTROUND_H */

@@ -1,0 +1,957 @@
+// C-ABI of libttround (include/ttround.h) and the host-side sweep driver of the
+// hot path: caps -> sketch -> Alg. 3 per summand -> Alg. 7 sweep -> truncation.
+// Every arithmetic step runs in this library's CUDA kernels (gemm.cu, linalg.cu).
+#include <math.h>
+#include <stdarg.h>
+#include <string.h>
+
+#include <algorithm>
+#include <memory>
+#include <numeric>
+
+#include "common.cuh"
+
+namespace ttr {
+
+std::atomic<uint64_t> g_launches{0};
+
+static thread_local std::string t_err;
+
+void set_error(const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  t_err = buf;
+}
+const char* last_error() { return t_err.c_str(); }
+
+int dalloc(DBuf& b, size_t n, cudaStream_t s) {
+  b.release();
+  if (n == 0) n = 1;
+  void* p = nullptr;
+  cudaError_t e = cudaMallocAsync(&p, n * sizeof(double), s);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    set_error("device allocation of %zu bytes failed: %s", n * sizeof(double),
+              cudaGetErrorString(e));
+    return TT_ERR_OOM;
+  }
+  b.p = static_cast<double*>(p);
+  b.n = n;
+  b.s = s;
+  return TT_OK;
+}
+
+int ialloc(IBuf& b, size_t n, cudaStream_t s) {
+  void* p = nullptr;
+  cudaError_t e = cudaMallocAsync(&p, n * sizeof(int), s);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    set_error("device allocation failed: %s", cudaGetErrorString(e));
+    return TT_ERR_OOM;
+  }
+  b.p = static_cast<int*>(p);
+  b.s = s;
+  return TT_OK;
+}
+
+int nccl_unique_id(uint8_t id[128]);
+int nccl_comm_create(Ctx& c, const uint8_t* id, int rank, int world);
+int nccl_comm_destroy(Ctx& c);
+
+}  // namespace ttr
+
+using namespace ttr;
+
+struct tt_ctx : Ctx {};
+
+struct tt_sketch {
+  int d = 0;
+  std::vector<int64_t> dims, ranks;
+  uint64_t seed = 0;
+  uint32_t tag = 0;
+  std::vector<DBuf> cores;   // cores[n-1], n = 2..d (cores[0] unused)
+};
+
+struct tt_tensor {
+  int d = 0;
+  std::vector<int64_t> dims, ranks;
+  std::vector<DBuf> bufs;
+  std::vector<double*> ptrs;
+  uint32_t flags = 0;
+  int passes = 1;
+  cudaStream_t stream = nullptr;
+};
+
+namespace {
+
+
+// ------------------------------------------------------------------ helpers
+// Per-phase device time with CUDA events on the context stream (tt_ctx_set_timing):
+// 0 sketch, 1 phase 1 (Alg. 3), 2 sweep GEMMs, 3 QR, 4 collectives, 5 truncation, 6 total.
+struct PhaseTimer {
+  Ctx& c;
+  cudaEvent_t open[8] = {};
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> spans;
+  explicit PhaseTimer(Ctx& cc) : c(cc) {}
+  ~PhaseTimer() {
+    for (auto& sp : spans) {
+      cudaEventDestroy(sp.second.first);
+      cudaEventDestroy(sp.second.second);
+    }
+    for (auto e : open)
+      if (e) cudaEventDestroy(e);
+  }
+  void begin(int ph) {
+    if (!c.timing) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, c.stream);
+    if (open[ph]) cudaEventDestroy(open[ph]);
+    open[ph] = e;
+  }
+  void end(int ph) {
+    if (!c.timing || !open[ph]) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, c.stream);
+    spans.push_back({ph, {open[ph], e}});
+    open[ph] = nullptr;
+  }
+  void finish() {
+    if (!c.timing) return;
+    cudaStreamSynchronize(c.stream);
+    for (double& x : c.last_ms) x = 0.0;
+    for (auto& sp : spans) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, sp.second.first, sp.second.second);
+      c.last_ms[sp.first] += ms;
+    }
+  }
+};
+
+bool is_device_ptr(const void* p, int device) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) &&
+         a.device == device;
+}
+
+int validate(const tt_view* v, int S, std::vector<int64_t>& dims) {
+  if (!v || S < 1) {
+    set_error("need S >= 1 summands");
+    return TT_ERR_ARG;
+  }
+  const int d = v[0].d;
+  if (d < 2) {
+    set_error("a TT-tensor to round needs d >= 2 modes (got %d)", d);
+    return TT_ERR_ARG;
+  }
+  dims.assign(v[0].dims, v[0].dims + d);
+  for (int j = 0; j < S; ++j) {
+    const tt_view& t = v[j];
+    if (!t.dims || !t.ranks || !t.cores) {
+      set_error("summand %d: null dims/ranks/cores", j);
+      return TT_ERR_ARG;
+    }
+    if (t.d != d) {
+      set_error("summand %d has %d modes, expected %d", j, t.d, d);
+      return TT_ERR_SHAPE;
+    }
+    for (int n = 0; n < d; ++n)
+      if (t.dims[n] != dims[n] || t.dims[n] < 1) {
+        set_error("summand %d: dim %d is %lld, expected %lld", j, n + 1, (long long)t.dims[n],
+                  (long long)dims[n]);
+        return TT_ERR_SHAPE;
+      }
+    if (t.ranks[0] != 1 || t.ranks[d] != 1) {
+      set_error("summand %d: boundary ranks must be 1", j);
+      return TT_ERR_RANK;
+    }
+    for (int n = 0; n <= d; ++n)
+      if (t.ranks[n] < 1) {
+        set_error("summand %d: rank R_%d = %lld < 1", j, n, (long long)t.ranks[n]);
+        return TT_ERR_RANK;
+      }
+    for (int n = 0; n < d; ++n)
+      if (!t.cores[n]) {
+        set_error("summand %d: core %d is null", j, n + 1);
+        return TT_ERR_ARG;
+      }
+  }
+  return TT_OK;
+}
+
+// R7: l_n = min(l, l_{n-1} I_n, prod_{k>n} I_k, sum_j R_n), n = 1..d-1; l_0 = l_d = 1
+std::vector<int64_t> rank_caps(const std::vector<int64_t>& dims, const std::vector<int64_t>& sumR,
+                               int64_t ell) {
+  const int d = int(dims.size());
+  std::vector<int64_t> l(d + 1, 1);
+  for (int n = 1; n < d; ++n) {
+    int64_t tail = 1;
+    for (int k = n; k < d; ++k) {
+      tail *= dims[k];
+      if (tail > (int64_t(1) << 40)) break;
+    }
+    int64_t c = std::min({ell, l[n - 1] * dims[n - 1], tail, sumR[n]});
+    l[n] = std::max<int64_t>(1, c);
+  }
+  return l;
+}
+
+// Device copies of the summand cores (borrowed device pointers or staged host data).
+struct Terms {
+  int S = 0, d = 0;
+  std::vector<std::vector<const double*>> core;   // [j][n]
+  std::vector<std::vector<int64_t>> R;             // [j][n], n = 0..d
+  std::vector<DBuf> staged;
+  std::vector<cudaEvent_t> ready;                  // per core n (host staging), or empty
+  ~Terms() {
+    for (auto e : ready) cudaEventDestroy(e);
+  }
+};
+
+int stage_terms(Ctx& c, const tt_view* v, int S, Terms& T) {
+  T.S = S;
+  T.d = v[0].d;
+  const int d = T.d;
+  T.core.assign(S, std::vector<const double*>(d, nullptr));
+  T.R.assign(S, std::vector<int64_t>(d + 1));
+  bool any_host = false;
+  for (int j = 0; j < S; ++j) {
+    for (int n = 0; n <= d; ++n) T.R[j][n] = v[j].ranks[n];
+    for (int n = 0; n < d; ++n) {
+      T.core[j][n] = v[j].cores[n];
+      if (!is_device_ptr(v[j].cores[n], c.device)) any_host = true;
+    }
+  }
+  if (!any_host) return TT_OK;
+  // H2D staging on the copy stream, cores d..1 (phase 1 consumes them right to
+  // left), one event per core so the sweep overlaps the transfer
+  T.ready.resize(d);
+  for (auto& e : T.ready) TTR_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  cudaEvent_t start;
+  TTR_CUDA(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
+  TTR_CUDA(cudaEventRecord(start, c.stream));
+  TTR_CUDA(cudaStreamWaitEvent(c.copy_stream, start, 0));
+  cudaEventDestroy(start);
+  T.staged.resize(size_t(S) * d);
+  for (int n = d - 1; n >= 0; --n) {
+    for (int j = 0; j < S; ++j) {
+      if (is_device_ptr(v[j].cores[n], c.device)) continue;
+      const size_t cnt = size_t(T.R[j][n]) * v[j].dims[n] * T.R[j][n + 1];
+      DBuf& b = T.staged[size_t(j) * d + n];
+      TTR_TRY(dalloc(b, cnt, c.copy_stream));
+      TTR_CUDA(cudaMemcpyAsync(b.p, v[j].cores[n], cnt * sizeof(double), cudaMemcpyHostToDevice,
+                               c.copy_stream));
+      b.s = c.stream;   // freed on the compute stream after use
+      T.core[j][n] = b.p;
+    }
+    TTR_CUDA(cudaEventRecord(T.ready[n], c.copy_stream));
+  }
+  return TT_OK;
+}
+
+inline int wait_core(Ctx& c, const Terms& T, int n /*0-based*/) {
+  if (!T.ready.empty()) TTR_CUDA(cudaStreamWaitEvent(c.stream, T.ready[n], 0));
+  return TT_OK;
+}
+
+int make_sketch(Ctx& c, const std::vector<int64_t>& dims, const std::vector<int64_t>& l,
+                uint64_t seed, uint32_t tag, tt_sketch& sk) {
+  const int d = int(dims.size());
+  sk.d = d;
+  sk.dims = dims;
+  sk.ranks = l;
+  sk.seed = seed;
+  sk.tag = tag;
+  sk.cores.clear();
+  sk.cores.resize(d);
+  for (int n = 2; n <= d; ++n) {
+    const int64_t cnt = l[n - 1] * dims[n - 1] * l[n];
+    TTR_TRY(dalloc(sk.cores[n - 1], size_t(cnt), c.stream));
+    TTR_TRY(philox_fill(c, sk.cores[n - 1].p, cnt, seed, uint32_t(n), tag,
+                        1.0 / sqrt(double(cnt)), c.stream));
+  }
+  return TT_OK;
+}
+
+// ------------------------------------------------------------------ Alg. 7
+// X (output cores, ranks l) from the staged summands and the sketch.
+int alg7(Ctx& c, const Terms& T, const std::vector<int64_t>& dims, const std::vector<int64_t>& l,
+         const tt_sketch& sk, tt_tensor& out, PhaseTimer& tm) {
+  const int S = T.S, d = T.d;
+  cudaStream_t s = c.stream;
+  // local summed ranks and per-summand offsets
+  std::vector<int64_t> sumR(d + 1, 0);
+  std::vector<std::vector<int64_t>> off(d + 1, std::vector<int64_t>(S + 1, 0));
+  for (int n = 0; n <= d; ++n)
+    for (int j = 0; j < S; ++j) {
+      off[n][j + 1] = off[n][j] + T.R[j][n];
+      sumR[n] = off[n][j + 1];
+    }
+  // W stack per bond n = 1..d-1: sumR[n] x l[n] (ld sumR[n])
+  std::vector<size_t> woff(d + 1, 0);
+  size_t wtot = 0;
+  for (int n = 1; n < d; ++n) {
+    woff[n] = wtot;
+    wtot += size_t(sumR[n]) * l[n];
+  }
+  size_t zmax = 1, xmax = 1, ymax = 1, mmax = 1;
+  for (int n = 2; n < d; ++n) {
+    size_t z = 0;
+    for (int j = 0; j < S; ++j) z += size_t(T.R[j][n - 1]) * dims[n - 1] * l[n];
+    zmax = std::max(zmax, z);
+  }
+  for (int n = 1; n < d; ++n) {
+    xmax = std::max(xmax, size_t(l[n - 1]) * dims[n - 1] * sumR[n]);
+    ymax = std::max(ymax, size_t(l[n - 1]) * dims[n - 1] * l[n]);
+    mmax = std::max(mmax, size_t(l[n]) * sumR[n]);
+  }
+  DBuf Wst, Z, Xa, Xb, Yb, Mb, Stk;
+  TTR_TRY(dalloc(Wst, wtot, s));
+  if (d > 2) TTR_TRY(dalloc(Z, zmax, s));
+  TTR_TRY(dalloc(Xa, xmax, s));
+  TTR_TRY(dalloc(Xb, xmax, s));
+  TTR_TRY(dalloc(Yb, ymax, s));
+  TTR_TRY(dalloc(Mb, mmax, s));
+  TTR_TRY(dalloc(Stk, size_t(sumR[d - 1]) * dims[d - 1], s));
+
+  out.d = d;
+  out.dims = dims;
+  out.ranks = l;
+  out.bufs.clear();
+  out.bufs.resize(d);
+  for (int n = 1; n <= d; ++n)
+    TTR_TRY(dalloc(out.bufs[n - 1], size_t(l[n - 1]) * dims[n - 1] * l[n], s));
+
+  std::vector<GemmDesc> gd(S);
+  // ---------------- phase 1: Alg. 3 for every summand (batched), n = d .. 2
+  tm.begin(1);
+  {
+    TTR_TRY(wait_core(c, T, d - 1));
+    const double* G = sk.cores[d - 1].p;   // H(G_d): l_{d-1} x I_d (ld l_{d-1})
+    for (int j = 0; j < S; ++j)            // line 2: W_{d-1} = H(Y_d) H(G_d)^T
+      gd[j] = GemmDesc{T.core[j][d - 1], G, Wst.p + woff[d - 1] + off[d - 1][j],
+                       int(T.R[j][d - 1]), int(l[d - 1]), int(dims[d - 1]),
+                       int(T.R[j][d - 1]), int(l[d - 1]), int(sumR[d - 1])};
+    TTR_TRY(gemm(c, false, true, gd.data(), S, 1.0, 0.0, s));
+    for (int n = d - 1; n >= 2; --n) {     // lines 3-6
+      TTR_TRY(wait_core(c, T, n - 1));
+      const int64_t In = dims[n - 1];
+      std::vector<size_t> zoff(S + 1, 0);
+      for (int j = 0; j < S; ++j) zoff[j + 1] = zoff[j] + size_t(T.R[j][n - 1]) * In * l[n];
+      for (int j = 0; j < S; ++j)          // line 4: V(Z_n) = V(Y_n) W_n
+        gd[j] = GemmDesc{T.core[j][n - 1], Wst.p + woff[n] + off[n][j], Z.p + zoff[j],
+                         int(T.R[j][n - 1] * In), int(l[n]), int(T.R[j][n]),
+                         int(T.R[j][n - 1] * In), int(sumR[n]), int(T.R[j][n - 1] * In)};
+      TTR_TRY(gemm(c, false, false, gd.data(), S, 1.0, 0.0, s));
+      const double* Gn = sk.cores[n - 1].p;   // H(G_n): l_{n-1} x I_n l_n (ld l_{n-1})
+      for (int j = 0; j < S; ++j)          // line 5: W_{n-1} = H(Z_n) H(G_n)^T
+        gd[j] = GemmDesc{Z.p + zoff[j], Gn, Wst.p + woff[n - 1] + off[n - 1][j],
+                         int(T.R[j][n - 1]), int(l[n - 1]), int(In * l[n]), int(T.R[j][n - 1]),
+                         int(l[n - 1]), int(sumR[n - 1])};
+      TTR_TRY(gemm(c, false, true, gd.data(), S, 1.0, 0.0, s));
+    }
+  }
+  tm.end(1);
+  // ---------------- phase 2: Alg. 7 lines 6-16
+  TTR_TRY(wait_core(c, T, 0));
+  double* Xcur = Xa.p;
+  double* Xnext = Xb.p;
+  for (int j = 0; j < S; ++j)   // line 6: X_1 = [Y^(1)_1 ... Y^(s)_1]  (I_1 x sumR_1)
+    TTR_CUDA(cudaMemcpyAsync(Xcur + dims[0] * off[1][j], T.core[j][0],
+                             sizeof(double) * dims[0] * T.R[j][1], cudaMemcpyDeviceToDevice, s));
+  for (int n = 1; n <= d - 1; ++n) {
+    const int64_t In = dims[n - 1];
+    const int64_t m = l[n - 1] * In;
+    // line 9: Y_n = V(X_n) [W^(1)_n; ...; W^(s)_n]
+    tm.begin(2);
+    TTR_TRY(gemm1(c, false, false, int(m), int(l[n]), int(sumR[n]), 1.0, Xcur, int(m),
+                  Wst.p + woff[n], int(sumR[n]), 0.0, Yb.p, int(m), s));
+    tm.end(2);
+    tm.begin(4);
+    TTR_TRY(allreduce_sum(c, Yb.p, size_t(m) * l[n]));   // sum over GPUs
+    tm.end(4);
+    // line 10: [V(X_n), ~] = QR(Y_n)
+    tm.begin(3);
+    TTR_TRY(qr(c, m, l[n], Yb.p, m, false, out.bufs[n - 1].p, nullptr, s));
+    tm.end(3);
+    tm.begin(2);
+    // line 11: [M^(1) ... M^(s)] = V(X_n)^T Z_n
+    TTR_TRY(gemm1(c, true, false, int(l[n]), int(sumR[n]), int(m), 1.0, out.bufs[n - 1].p,
+                  int(m), Xcur, int(m), 0.0, Mb.p, int(l[n]), s));
+    if (n < d - 1) {
+      // line 13: H(X_{n+1}) = [M^(1) H(Y^(1)_{n+1}) ... M^(s) H(Y^(s)_{n+1})]
+      const int64_t In1 = dims[n];
+      for (int j = 0; j < S; ++j)
+        gd[j] = GemmDesc{Mb.p + l[n] * off[n][j], T.core[j][n],
+                         Xnext + l[n] * In1 * off[n + 1][j], int(l[n]),
+                         int(In1 * T.R[j][n + 1]), int(T.R[j][n]), int(l[n]), int(T.R[j][n]),
+                         int(l[n])};
+      TTR_TRY(gemm(c, false, false, gd.data(), S, 1.0, 0.0, s));
+      tm.end(2);
+      std::swap(Xcur, Xnext);
+    } else {
+      // line 15 (R1: M_{N-1}): X_N = sum_j M^(j) H(Y^(j)_N) = [M^(1) ...] [H(Y^(1)_N); ...]
+      const int64_t Id = dims[d - 1];
+      for (int j = 0; j < S; ++j)
+        TTR_CUDA(cudaMemcpy2DAsync(Stk.p + off[d - 1][j], sizeof(double) * sumR[d - 1],
+                                   T.core[j][d - 1], sizeof(double) * T.R[j][d - 1],
+                                   sizeof(double) * T.R[j][d - 1], Id, cudaMemcpyDeviceToDevice,
+                                   s));
+      TTR_TRY(gemm1(c, false, false, int(l[d - 1]), int(Id), int(sumR[d - 1]), 1.0, Mb.p,
+                    int(l[d - 1]), Stk.p, int(sumR[d - 1]), 0.0, out.bufs[d - 1].p,
+                    int(l[d - 1]), s));
+      tm.end(2);
+      tm.begin(4);
+      TTR_TRY(allreduce_sum(c, out.bufs[d - 1].p, size_t(l[d - 1]) * Id));
+      tm.end(4);
+    }
+  }
+  out.ptrs.resize(d);
+  for (int n = 0; n < d; ++n) out.ptrs[n] = out.bufs[n].p;
+  return TT_OK;
+}
+
+// ------------------------------------------------------------------ truncation
+// Mirrored Alg. 2 lines 3-10 on the left-orthogonal X (R3): n = d .. 2.
+int truncate(Ctx& c, tt_tensor& X, double tol, int64_t rmax, std::vector<int64_t>& ks) {
+  cudaStream_t s = c.stream;
+  const int d = X.d;
+  std::vector<int64_t>& r = X.ranks;
+  double eps = 0.0;
+  if (tol > 0.0) {
+    DBuf nrm;
+    TTR_TRY(dalloc(nrm, 1, s));
+    TTR_TRY(fro_norm(c, X.bufs[d - 1].p, r[d - 1] * X.dims[d - 1], nrm.p, s));
+    double h = 0.0;
+    TTR_CUDA(cudaMemcpyAsync(&h, nrm.p, sizeof(double), cudaMemcpyDeviceToHost, s));
+    TTR_CUDA(cudaStreamSynchronize(s));
+    eps = h * tol / sqrt(double(d - 1));
+  }
+  ks.assign(d + 1, 1);
+  IBuf kdev;
+  TTR_TRY(ialloc(kdev, 1, s));
+  for (int n = d; n >= 2; --n) {
+    const int64_t In = X.dims[n - 1];
+    const int64_t r0 = r[n - 1];
+    const int64_t mrow = In * r[n];
+    DBuf AV, V, sig, Q, R, Rt, newn, newp;
+    int64_t k = 0;
+    const int64_t rows_av = r0;
+    const int64_t cols = std::min(r0, mrow);
+    TTR_TRY(dalloc(AV, size_t(rows_av) * cols, s));
+    TTR_TRY(dalloc(V, size_t(cols) * cols, s));
+    TTR_TRY(dalloc(sig, size_t(cols), s));
+    if (mrow >= r0) {
+      TTR_TRY(dalloc(Q, size_t(mrow) * r0, s));
+      TTR_TRY(dalloc(R, size_t(r0) * r0, s));
+      TTR_TRY(dalloc(Rt, size_t(r0) * r0, s));
+      // [Q, R] = qr(H(X_n)^T)
+      TTR_TRY(qr(c, mrow, r0, X.bufs[n - 1].p, r0, true, Q.p, R.p, s));
+      // [U, S, V] = svd(R^T)
+      TTR_TRY(transpose(c, R.p, r0, r0, r0, Rt.p, r0, s));
+      TTR_TRY(svd_jacobi(c, r0, r0, Rt.p, r0, AV.p, V.p, sig.p, s));
+    } else {
+      // wide unfolding (I_n r_n < r_{n-1}): SVD of H(X_n) directly
+      TTR_TRY(svd_jacobi(c, r0, mrow, X.bufs[n - 1].p, r0, AV.p, V.p, sig.p, s));
+    }
+    if (tol > 0.0) {
+      TTR_TRY(eps_rank_dev(c, sig.p, int(cols), nullptr, eps, int(rmax), kdev.p, s));
+      int kh = 0;
+      TTR_CUDA(cudaMemcpyAsync(&kh, kdev.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+      TTR_CUDA(cudaStreamSynchronize(s));
+      k = kh;
+    } else {
+      k = std::min<int64_t>(cols, rmax > 0 ? rmax : cols);
+    }
+    ks[n - 1] = k;
+    // H(X_n) <- V_k^T Q^T  (or V_k^T)
+    TTR_TRY(dalloc(newn, size_t(k) * mrow, s));
+    if (mrow >= r0) {
+      TTR_TRY(gemm1(c, true, true, int(k), int(mrow), int(r0), 1.0, V.p, int(cols), Q.p,
+                    int(mrow), 0.0, newn.p, int(k), s));
+    } else {
+      TTR_TRY(transpose(c, V.p, mrow, k, mrow, newn.p, k, s));
+    }
+    // V(X_{n-1}) <- V(X_{n-1}) U_k S_k
+    const int64_t mp = r[n - 2] * X.dims[n - 2];
+    TTR_TRY(dalloc(newp, size_t(mp) * k, s));
+    TTR_TRY(gemm1(c, false, false, int(mp), int(k), int(r0), 1.0, X.bufs[n - 2].p, int(mp), AV.p,
+                  int(rows_av), 0.0, newp.p, int(mp), s));
+    X.bufs[n - 1] = std::move(newn);
+    X.bufs[n - 2] = std::move(newp);
+    r[n - 1] = k;
+  }
+  for (int n = 0; n < d; ++n) X.ptrs[n] = X.bufs[n].p;
+  return TT_OK;
+}
+
+int read_flags(Ctx& c, int* h, int n) {
+  TTR_CUDA(cudaMemcpyAsync(h, c.flags.p, sizeof(int) * n, cudaMemcpyDeviceToHost, c.stream));
+  TTR_CUDA(cudaStreamSynchronize(c.stream));
+  return TT_OK;
+}
+
+int make_zero(Ctx& c, const std::vector<int64_t>& dims, tt_tensor& out) {
+  const int d = int(dims.size());
+  out.d = d;
+  out.dims = dims;
+  out.ranks.assign(d + 1, 1);
+  out.bufs.clear();
+  out.bufs.resize(d);
+  out.ptrs.resize(d);
+  for (int n = 0; n < d; ++n) {
+    TTR_TRY(dalloc(out.bufs[n], size_t(dims[n]), c.stream));
+    TTR_CUDA(cudaMemsetAsync(out.bufs[n].p, 0, sizeof(double) * dims[n], c.stream));
+    out.ptrs[n] = out.bufs[n].p;
+  }
+  return TT_OK;
+}
+
+constexpr int kPMin = 5;   // adaptive saturation margin (R8)
+
+int round_sum_impl(tt_ctx* c, int S, const tt_view* terms, const tt_round_opts* o,
+                   tt_sketch* user_sk, tt_tensor** outp) {
+  std::vector<int64_t> dims;
+  TTR_TRY(validate(terms, S, dims));
+  if (!o) {
+    set_error("opts is null");
+    return TT_ERR_ARG;
+  }
+  const int d = int(dims.size());
+  int64_t ell;
+  double tol = 0.0;
+  int64_t rank = 0;
+  bool adaptive = false;
+  switch (o->mode) {
+    case TT_SKETCH_ONLY: ell = o->oversample; break;
+    case TT_RANK:
+      if (o->rank < 1 || o->oversample < 0) {
+        set_error("TT_RANK needs rank >= 1 and oversample >= 0");
+        return TT_ERR_ARG;
+      }
+      ell = o->rank + o->oversample;
+      rank = o->rank;
+      break;
+    case TT_TOL:
+      if (!(o->tol > 0.0)) {
+        set_error("TT_TOL needs tol > 0");
+        return TT_ERR_ARG;
+      }
+      ell = o->oversample;
+      tol = o->tol;
+      rank = std::max<int64_t>(0, o->rank);
+      adaptive = o->adaptive != 0 && user_sk == nullptr;
+      break;
+    default: set_error("unknown mode %d", o->mode); return TT_ERR_ARG;
+  }
+  if (ell < 1) {
+    set_error("sketch rank must be >= 1");
+    return TT_ERR_ARG;
+  }
+  TTR_CUDA(cudaSetDevice(c->device));
+  PhaseTimer tm(*c);
+  tm.begin(6);
+  Terms T;
+  TTR_TRY(stage_terms(*c, terms, S, T));
+  // global summed ranks (all shards)
+  std::vector<int64_t> sumR(d + 1, 0);
+  for (int n = 0; n <= d; ++n)
+    for (int j = 0; j < S; ++j) sumR[n] += T.R[j][n];
+  TTR_TRY(allreduce_sum_i64(*c, sumR.data(), sumR.size()));
+  const std::vector<int64_t> scap = rank_caps(dims, sumR, int64_t(1) << 40);
+  TTR_CUDA(cudaMemsetAsync(c->flags.p, 0, sizeof(int) * c->nflags, c->stream));
+
+  std::unique_ptr<tt_tensor> out(new tt_tensor);
+  out->stream = c->stream;
+  int64_t cur = ell;
+  int passes = 0;
+  for (;;) {
+    const std::vector<int64_t> l = rank_caps(dims, sumR, cur);
+    tt_sketch own;
+    const tt_sketch* sk = user_sk;
+    if (user_sk) {
+      if (user_sk->d != d || user_sk->ranks != l || user_sk->dims != dims) {
+        set_error("sketch ranks/dims do not match the capped ranks of this call");
+        return TT_ERR_SHAPE;
+      }
+    } else {
+      tm.begin(0);
+      TTR_TRY(make_sketch(*c, dims, l, o->seed, uint32_t(passes), own));
+      tm.end(0);
+      sk = &own;
+    }
+    tt_tensor X;
+    X.stream = c->stream;
+    TTR_TRY(alg7(*c, T, dims, l, *sk, X, tm));
+    ++passes;
+    bool capped = false;
+    for (int n = 1; n < d; ++n) capped |= l[n] < cur;
+    int fl[4];
+    TTR_TRY(read_flags(*c, fl, 4));
+    if (fl[2]) {   // zero sum (R16)
+      TTR_TRY(make_zero(*c, dims, *out));
+      out->flags = TT_FLAG_ZERO | (capped ? TT_FLAG_RANK_CAPPED : 0);
+      out->passes = passes;
+      break;
+    }
+    uint32_t flags = (capped ? TT_FLAG_RANK_CAPPED : 0) | (fl[1] ? TT_FLAG_QR_FALLBACK : 0);
+    bool need = false;
+    if (o->mode == TT_TOL) need = true;
+    if (o->mode == TT_RANK)
+      for (int n = 1; n < d; ++n) need |= l[n] > rank;
+    if (!need) {
+      *out = std::move(X);
+      out->flags = flags | TT_FLAG_LEFT_ORTH;
+      out->passes = passes;
+      break;
+    }
+    std::vector<int64_t> ks;
+    tm.begin(5);
+    TTR_TRY(truncate(*c, X, tol, rank, ks));
+    tm.end(5);
+    TTR_TRY(read_flags(*c, fl, 4));
+    flags |= (fl[1] ? TT_FLAG_QR_FALLBACK : 0);
+    bool done = true;
+    if (adaptive) {
+      bool sat = false;
+      for (int n = 1; n < d; ++n) sat |= (ks[n] > l[n] - kPMin) && (l[n] < scap[n]);
+      if (sat && !(o->max_rank > 0 && cur >= o->max_rank)) {
+        int64_t nxt = 2 * cur;
+        if (o->max_rank > 0) nxt = std::min(nxt, o->max_rank);
+        const int64_t smax = *std::max_element(scap.begin() + 1, scap.begin() + d);
+        if (nxt >= smax) nxt = smax;
+        if (nxt > cur) {
+          cur = nxt;
+          done = false;
+        }
+      }
+    }
+    if (done) {
+      *out = std::move(X);
+      out->flags = flags | TT_FLAG_RIGHT_ORTH;
+      out->passes = passes;
+      break;
+    }
+  }
+  tm.end(6);
+  TTR_CUDA(cudaStreamSynchronize(c->stream));
+  tm.finish();
+  int fl[4];
+  TTR_TRY(read_flags(*c, fl, 4));
+  if (fl[3] & 1) {
+    set_error("QR breakdown even after the Householder fallback");
+    return TT_ERR_NUMERIC;
+  }
+  *outp = out.release();
+  return TT_OK;
+}
+
+// run `f` catching C++ exceptions (none may cross the ABI)
+template <class F>
+int guarded(F&& f) {
+  try {
+    return f();
+  } catch (const std::bad_alloc&) {
+    set_error("host allocation failed");
+    return TT_ERR_OOM;
+  } catch (const std::exception& e) {
+    set_error("internal error: %s", e.what());
+    return TT_ERR_ARG;
+  } catch (...) {
+    set_error("internal error");
+    return TT_ERR_ARG;
+  }
+}
+
+int inner_impl(tt_ctx* c, const tt_view* x, const tt_view* y, double* out) {
+  std::vector<int64_t> dx, dy;
+  TTR_TRY(validate(x, 1, dx));
+  TTR_TRY(validate(y, 1, dy));
+  if (dx != dy) {
+    set_error("inner: dims differ");
+    return TT_ERR_SHAPE;
+  }
+  TTR_CUDA(cudaSetDevice(c->device));
+  Terms TX, TY;
+  TTR_TRY(stage_terms(*c, x, 1, TX));
+  TTR_TRY(stage_terms(*c, y, 1, TY));
+  cudaStream_t s = c->stream;
+  const int d = int(dx.size());
+  const auto& Rx = TX.R[0];
+  const auto& Ry = TY.R[0];
+  for (int n = 0; n < d; ++n) {
+    TTR_TRY(wait_core(*c, TX, n));
+    TTR_TRY(wait_core(*c, TY, n));
+  }
+  size_t zmax = 1, wmax = 1;
+  for (int n = 1; n <= d; ++n) {
+    zmax = std::max(zmax, size_t(Rx[n - 1]) * dx[n - 1] * Ry[n]);
+    wmax = std::max(wmax, size_t(Rx[n]) * Ry[n]);
+  }
+  DBuf W, Wn, Z;
+  TTR_TRY(dalloc(W, wmax, s));
+  TTR_TRY(dalloc(Wn, wmax, s));
+  TTR_TRY(dalloc(Z, zmax, s));
+  // W_{d-1} = H(X_d) H(Y_d)^T, then Z = V(X_n) W_n, W_{n-1} = H(Z) H(Y_n)^T, down to n = 1
+  TTR_TRY(gemm1(*c, false, true, int(Rx[d - 1]), int(Ry[d - 1]), int(dx[d - 1]), 1.0,
+                TX.core[0][d - 1], int(Rx[d - 1]), TY.core[0][d - 1], int(Ry[d - 1]), 0.0, W.p,
+                int(Rx[d - 1]), s));
+  for (int n = d - 1; n >= 1; --n) {
+    const int64_t mm = Rx[n - 1] * dx[n - 1];
+    TTR_TRY(gemm1(*c, false, false, int(mm), int(Ry[n]), int(Rx[n]), 1.0, TX.core[0][n - 1],
+                  int(mm), W.p, int(Rx[n]), 0.0, Z.p, int(mm), s));
+    TTR_TRY(gemm1(*c, false, true, int(Rx[n - 1]), int(Ry[n - 1]), int(dx[n - 1] * Ry[n]), 1.0,
+                  Z.p, int(Rx[n - 1]), TY.core[0][n - 1], int(Ry[n - 1]), 0.0, Wn.p,
+                  int(Rx[n - 1]), s));
+    std::swap(W, Wn);
+  }
+  double h = 0.0;
+  TTR_CUDA(cudaMemcpyAsync(&h, W.p, sizeof(double), cudaMemcpyDeviceToHost, s));
+  TTR_CUDA(cudaStreamSynchronize(s));
+  *out = h;
+  return TT_OK;
+}
+
+}  // namespace
+
+// ====================================================================== C-ABI
+extern "C" {
+
+const char* tt_last_error(void) { return ttr::last_error(); }
+
+uint64_t tt_launch_count(void) { return ttr::g_launches.load(); }
+
+int tt_get_nccl_unique_id(uint8_t id[128]) {
+  if (!id) return TT_ERR_ARG;
+  return guarded([&] { return nccl_unique_id(id); });
+}
+
+int tt_ctx_create(int device, void* cuda_stream, const uint8_t* nccl_id, int rank, int world,
+                  tt_ctx_t* out) {
+  if (!out) {
+    set_error("out is null");
+    return TT_ERR_ARG;
+  }
+  if (world < 1 || rank < 0 || rank >= world) {
+    set_error("bad rank/world (%d/%d)", rank, world);
+    return TT_ERR_ARG;
+  }
+  return guarded([&]() -> int {
+    std::unique_ptr<tt_ctx> c(new tt_ctx);
+    c->device = device;
+    TTR_CUDA(cudaSetDevice(device));
+    if (cuda_stream) {
+      c->stream = static_cast<cudaStream_t>(cuda_stream);
+    } else {
+      TTR_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+      c->own_stream = true;
+    }
+    TTR_CUDA(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+    TTR_CUDA(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device));
+    // keep freed pool memory cached between calls
+    cudaMemPool_t pool;
+    TTR_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t thr = UINT64_MAX;
+    TTR_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    c->nflags = 64;
+    TTR_TRY(ialloc(c->flags, size_t(c->nflags), c->stream));
+    TTR_CUDA(cudaMemsetAsync(c->flags.p, 0, sizeof(int) * c->nflags, c->stream));
+    c->rank = rank;
+    c->world = world;
+    if (world > 1) {
+      if (!nccl_id) {
+        set_error("world > 1 needs an NCCL unique id");
+        return TT_ERR_ARG;
+      }
+      TTR_TRY(nccl_comm_create(*c, nccl_id, rank, world));
+    }
+    TTR_CUDA(cudaStreamSynchronize(c->stream));
+    *out = c.release();
+    return TT_OK;
+  });
+}
+
+int tt_ctx_destroy(tt_ctx_t c) {
+  if (!c) return TT_OK;
+  return guarded([&]() -> int {
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->stream);
+    nccl_comm_destroy(*c);
+    c->gemm_ws.release();
+    c->scratch.release();
+    if (c->flags.p) cudaFreeAsync(c->flags.p, c->stream);
+    c->flags.p = nullptr;
+    cudaStreamSynchronize(c->stream);
+    cudaStreamDestroy(c->copy_stream);
+    if (c->own_stream) cudaStreamDestroy(c->stream);
+    delete c;
+    return TT_OK;
+  });
+}
+
+int tt_ctx_set_timing(tt_ctx_t c, int enable) {
+  if (!c) return TT_ERR_ARG;
+  c->timing = enable != 0;
+  return TT_OK;
+}
+
+int tt_ctx_last_timing(tt_ctx_t c, double* ms, int n) {
+  if (!c || !ms) return TT_ERR_ARG;
+  const int k = std::min(n, 8);
+  for (int i = 0; i < k; ++i) ms[i] = c->last_ms[i];
+  return k;
+}
+
+int tt_sketch_create(tt_ctx_t c, int32_t d, const int64_t* dims, const int64_t* ranks,
+                     uint64_t seed, uint32_t tag, tt_sketch_t* out) {
+  if (!c || !dims || !ranks || !out || d < 2) {
+    set_error("tt_sketch_create: bad arguments");
+    return TT_ERR_ARG;
+  }
+  return guarded([&]() -> int {
+    if (ranks[0] != 1 || ranks[d] != 1) {
+      set_error("sketch boundary ranks must be 1");
+      return TT_ERR_RANK;
+    }
+    for (int n = 0; n <= d; ++n)
+      if (ranks[n] < 1) {
+        set_error("sketch rank < 1");
+        return TT_ERR_RANK;
+      }
+    TTR_CUDA(cudaSetDevice(c->device));
+    std::unique_ptr<tt_sketch> sk(new tt_sketch);
+    std::vector<int64_t> dv(dims, dims + d), rv(ranks, ranks + d + 1);
+    TTR_TRY(make_sketch(*c, dv, rv, seed, tag, *sk));
+    TTR_CUDA(cudaStreamSynchronize(c->stream));
+    *out = sk.release();
+    return TT_OK;
+  });
+}
+
+int tt_sketch_core(tt_sketch_t sk, int32_t n, const double** core) {
+  if (!sk || !core || n < 2 || n > sk->d) {
+    set_error("tt_sketch_core: n must be in 2..d");
+    return TT_ERR_ARG;
+  }
+  *core = sk->cores[n - 1].p;
+  return TT_OK;
+}
+
+int tt_sketch_destroy(tt_sketch_t sk) {
+  if (!sk) return TT_OK;
+  cudaDeviceSynchronize();
+  for (auto& b : sk->cores) b.s = nullptr;   // the creating stream may be gone
+  delete sk;
+  return TT_OK;
+}
+
+int tt_round_sum(tt_ctx_t c, int32_t S_local, const tt_view* terms, const tt_round_opts* opts,
+                 tt_sketch_t sketch, tt_tensor_t* out) {
+  if (!c || !out) {
+    set_error("tt_round_sum: null ctx/out");
+    return TT_ERR_ARG;
+  }
+  return guarded([&] { return round_sum_impl(c, S_local, terms, opts, sketch, out); });
+}
+
+int tt_round_deterministic(tt_ctx_t, int32_t, const tt_view*, const tt_round_opts*,
+                           tt_tensor_t*) {
+  set_error("tt_round_deterministic is not implemented in this build (SURVEY §8f NEXT-1)");
+  return TT_ERR_ARG;
+}
+
+int tt_inner(tt_ctx_t c, const tt_view* x, const tt_view* y, double* out) {
+  if (!c || !x || !y || !out) {
+    set_error("tt_inner: null argument");
+    return TT_ERR_ARG;
+  }
+  return guarded([&] { return inner_impl(c, x, y, out); });
+}
+
+int tt_tensor_info(tt_tensor_t t, int32_t* d, const int64_t** dims, const int64_t** ranks,
+                   double* const** cores, uint32_t* flags) {
+  if (!t) return TT_ERR_ARG;
+  if (d) *d = t->d;
+  if (dims) *dims = t->dims.data();
+  if (ranks) *ranks = t->ranks.data();
+  if (cores) *cores = t->ptrs.data();
+  if (flags) *flags = t->flags;
+  return TT_OK;
+}
+
+int tt_tensor_copy_core(tt_tensor_t t, int32_t n, double* dst) {
+  if (!t || !dst || n < 1 || n > t->d) {
+    set_error("tt_tensor_copy_core: n must be in 1..d");
+    return TT_ERR_ARG;
+  }
+  const size_t cnt = size_t(t->ranks[n - 1]) * t->dims[n - 1] * t->ranks[n];
+  TTR_CUDA(cudaMemcpyAsync(dst, t->ptrs[n - 1], cnt * sizeof(double), cudaMemcpyDefault,
+                           t->stream));
+  TTR_CUDA(cudaStreamSynchronize(t->stream));
+  return TT_OK;
+}
+
+int tt_tensor_passes(tt_tensor_t t, int32_t* passes) {
+  if (!t || !passes) return TT_ERR_ARG;
+  *passes = t->passes;
+  return TT_OK;
+}
+
+int tt_tensor_destroy(tt_tensor_t t) {
+  if (!t) return TT_OK;
+  cudaDeviceSynchronize();
+  for (auto& b : t->bufs) b.s = nullptr;     // the creating stream may be gone
+  delete t;
+  return TT_OK;
+}
+
+int tt_dgemm(tt_ctx_t c, int ta, int tb, int64_t m, int64_t n, int64_t k, double alpha,
+             const double* A, int64_t lda, const double* B, int64_t ldb, double beta, double* C,
+             int64_t ldc) {
+  if (!c || !A || !B || !C || m < 0 || n < 0 || k < 1) {
+    set_error("tt_dgemm: bad arguments");
+    return TT_ERR_ARG;
+  }
+  return guarded([&]() -> int {
+    TTR_CUDA(cudaSetDevice(c->device));
+    TTR_TRY(gemm1(*c, ta != 0, tb != 0, int(m), int(n), int(k), alpha, A, int(lda), B, int(ldb),
+                  beta, C, int(ldc), c->stream));
+    TTR_CUDA(cudaStreamSynchronize(c->stream));
+    return TT_OK;
+  });
+}
+
+int tt_qr(tt_ctx_t c, int64_t m, int64_t n, const double* A, int64_t lda, double* Q, double* R,
+          int* fallback) {
+  if (!c || !A || !Q) return TT_ERR_ARG;
+  return guarded([&]() -> int {
+    TTR_CUDA(cudaSetDevice(c->device));
+    TTR_CUDA(cudaMemsetAsync(c->flags.p, 0, sizeof(int) * c->nflags, c->stream));
+    TTR_TRY(qr(*c, m, n, A, lda, false, Q, R, c->stream));
+    int fl[4];
+    TTR_TRY(read_flags(*c, fl, 4));
+    if (fallback) *fallback = fl[1] ? 1 : 0;
+    return TT_OK;
+  });
+}
+
+int tt_svd_jacobi(tt_ctx_t c, int64_t m, int64_t n, const double* A, int64_t lda, double* AV,
+                  double* V, double* sigma) {
+  if (!c || !A || !AV || !V || !sigma) return TT_ERR_ARG;
+  return guarded([&]() -> int {
+    TTR_CUDA(cudaSetDevice(c->device));
+    TTR_TRY(svd_jacobi(*c, m, n, A, lda, AV, V, sigma, c->stream));
+    TTR_CUDA(cudaStreamSynchronize(c->stream));
+    return TT_OK;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,166 @@
+// Internal shared definitions of libttround (not part of the C-ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "../../include/ttround.h"
+
+namespace ttr {
+
+// ---------------------------------------------------------------- errors
+void set_error(const char* fmt, ...);
+const char* last_error();
+
+struct Status {
+  int code = TT_OK;
+  bool ok() const { return code == TT_OK; }
+};
+
+#define TTR_CUDA(expr)                                                          \
+  do {                                                                          \
+    cudaError_t e__ = (expr);                                                   \
+    if (e__ != cudaSuccess) {                                                   \
+      ::ttr::set_error("%s:%d %s: %s", __FILE__, __LINE__, #expr,               \
+                       cudaGetErrorString(e__));                                \
+      return e__ == cudaErrorMemoryAllocation ? TT_ERR_OOM : TT_ERR_CUDA;       \
+    }                                                                           \
+  } while (0)
+
+#define TTR_TRY(expr)                                                           \
+  do {                                                                          \
+    int r__ = (expr);                                                           \
+    if (r__ != TT_OK) return r__;                                               \
+  } while (0)
+
+// every kernel launch of the library goes through this counter (tt_launch_count)
+extern std::atomic<uint64_t> g_launches;
+inline int launched() {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  cudaError_t e = cudaPeekAtLastError();
+  if (e != cudaSuccess) {
+    set_error("kernel launch failed: %s", cudaGetErrorString(e));
+    return TT_ERR_CUDA;
+  }
+  return TT_OK;
+}
+
+// ---------------------------------------------------------------- device buffers
+// Stream-ordered allocations from the device's default memory pool (kept
+// cached across calls: release threshold = max).
+struct DBuf {
+  double* p = nullptr;
+  size_t n = 0;
+  cudaStream_t s = nullptr;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  DBuf(DBuf&& o) noexcept { *this = std::move(o); }
+  DBuf& operator=(DBuf&& o) noexcept {
+    if (this != &o) {
+      release();
+      p = o.p; n = o.n; s = o.s;
+      o.p = nullptr; o.n = 0;
+    }
+    return *this;
+  }
+  ~DBuf() { release(); }
+  void release() {
+    if (p) cudaFreeAsync(p, s);
+    p = nullptr;
+    n = 0;
+  }
+};
+int dalloc(DBuf& b, size_t ndoubles, cudaStream_t s);
+
+struct IBuf {  // small int32 device buffer (flags, ranks)
+  int* p = nullptr;
+  cudaStream_t s = nullptr;
+  IBuf() = default;
+  IBuf(const IBuf&) = delete;
+  IBuf& operator=(const IBuf&) = delete;
+  ~IBuf() { if (p) cudaFreeAsync(p, s); }
+};
+int ialloc(IBuf& b, size_t n, cudaStream_t s);
+
+// ---------------------------------------------------------------- context
+struct NcclApi;
+
+struct Ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  cudaStream_t copy_stream = nullptr;   // H2D staging of host inputs
+  bool own_stream = false;
+  int rank = 0, world = 1;
+  void* comm = nullptr;                 // ncclComm_t
+  bool timing = false;
+  double last_ms[8] = {0};
+  int sm_count = 148;
+  // reusable scratch for small per-call host->device uploads
+  DBuf scratch;
+  // split-K partials of the GEMMs
+  DBuf gemm_ws;
+  // flags: [0] QR fallback used, [1] numeric breakdown, [2] zero sketch seen, [3..] ranks
+  IBuf flags;
+  int nflags = 0;
+};
+
+int allreduce_sum(Ctx& c, double* buf, size_t n);   // in place, fp64 sum on c.stream
+int allreduce_sum_i64(Ctx& c, int64_t* hostbuf, size_t n);
+
+// ---------------------------------------------------------------- GEMM
+// C = alpha * op(A) * op(B) + beta * C, column-major, per batch entry.
+struct GemmDesc {
+  const double* A;
+  const double* B;
+  double* C;
+  int M, N, K;
+  int lda, ldb, ldc;
+};
+constexpr int kMaxGemmBatch = 64;
+
+// Batched FP64 DMMA GEMM (all entries share ta/tb/alpha/beta).
+int gemm(Ctx& c, bool ta, bool tb, const GemmDesc* d, int nbatch, double alpha,
+         double beta, cudaStream_t s);
+inline int gemm1(Ctx& c, bool ta, bool tb, int M, int N, int K, double alpha,
+                 const double* A, int lda, const double* B, int ldb, double beta,
+                 double* C, int ldc, cudaStream_t s) {
+  GemmDesc d{A, B, C, M, N, K, lda, ldb, ldc};
+  return gemm(c, ta, tb, &d, 1, alpha, beta, s);
+}
+
+// ---------------------------------------------------------------- sketch
+int philox_fill(Ctx& c, double* out, int64_t count, uint64_t seed, uint32_t n,
+                uint32_t tag, double scale, cudaStream_t s);
+
+// ---------------------------------------------------------------- dense linalg
+// Thin QR of the m x n matrix op(A) (m >= n): trans=false: A is m x n (ld lda);
+// trans=true: A is n x m (ld lda) and the QR is of its transpose.
+// Q: m x n (ld m).  R (optional): n x n upper (ld n).  Flags written to
+// c.flags (fallback/breakdown).  Uses shifted CholeskyQR3 with a Householder
+// fallback.
+int qr(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, bool trans, double* Q,
+       double* R, cudaStream_t s);
+// One-sided Jacobi SVD of the m x n (m >= n) matrix A (ld lda): AV = U Sigma
+// (m x n, ld m), V (n x n, ld n), sigma (n) sorted descending.
+int svd_jacobi(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, double* AV,
+               double* V, double* sigma, cudaStream_t s);
+// k = eps-rank of sigma (n values, descending) given absolute eps and cap rmax
+// (0 = none), written to dst (device int).
+int eps_rank_dev(Ctx& c, const double* sigma, int n, const double* eps_dev, double eps_host,
+                 int rmax, int* dst, cudaStream_t s);
+// out = ||x||_F (device scalar)
+int fro_norm(Ctx& c, const double* x, int64_t n, double* out, cudaStream_t s);
+// dst (cols x rows, ld ldd) = src^T (src rows x cols, ld lds)
+int transpose(Ctx& c, const double* src, int64_t rows, int64_t cols, int64_t lds,
+              double* dst, int64_t ldd, cudaStream_t s);
+int fill_zero(Ctx& c, double* p, int64_t n, cudaStream_t s);
+// dst[i] = (flag && *flag) ? 0 : src? (helper for degenerate cases)
+int max_abs_is_zero(Ctx& c, const double* x, int64_t n, int* flag_dst, cudaStream_t s);
+
+}  // namespace ttr

@@ -1,0 +1,340 @@
+// FP64 tensor-core GEMM for sm_100a: mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4),
+// operands staged global -> shared memory by a multi-stage cp.async pipeline.
+//
+// Every contraction of the hot path (Alg. 3 lines 2/4/5, Alg. 7 lines 9/11/13/14,
+// the Gram/R^{-1} products of the QR and the truncation products) is a
+// column-major C = alpha*op(A)*op(B) + beta*C launched through gemm() below,
+// batched over summands with per-entry pointers/shapes, and split along K with
+// a fixed-order (deterministic) reduction when M*N alone cannot fill 148 SMs.
+//
+// On B200 tcgen05.mma has no f64 kind (ptxas rejects .kind::f64), so the
+// warp-level DMMA is the FP64 tensor path; see DESIGN.md §Kernels.
+#include "common.cuh"
+
+namespace ttr {
+
+namespace {
+
+constexpr int pad_for(int x) { return (20 - (x % 16)) % 16; }  // leading dim ≡ 4 (mod 16) doubles
+
+__device__ __forceinline__ void cp_async8(double* smem, const double* gmem, bool pred) {
+  unsigned saddr = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  int bytes = pred ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(saddr), "l"(gmem),
+               "r"(bytes));
+}
+__device__ __forceinline__ void cp_async16(double* smem, const double* gmem, int bytes) {
+  unsigned saddr = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(saddr), "l"(gmem),
+               "r"(bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm volatile(
+      "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(c0), "+d"(c1)
+      : "d"(a), "d"(b));
+}
+
+struct GemmParams {
+  GemmDesc d[kMaxGemmBatch];
+  int nbatch;
+  int tiles_m, tiles_n;
+  int kslices;
+  int kchunk;        // K per slice (multiple of BK)
+  double alpha, beta;
+  double* ws;        // split-K partials (kslices > 1)
+};
+
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool TA, bool TB>
+struct Cfg {
+  static constexpr int NT = WM * WN * 32;
+  static constexpr int TM = BM / WM, TN = BN / WN;
+  static constexpr int FM = TM / 8, FN = TN / 8;
+  static constexpr int LDA = TA ? (BK + pad_for(BK)) : (BM + pad_for(BM));
+  static constexpr int AEL = TA ? BM * LDA : BK * LDA;
+  static constexpr int LDB = TB ? (BN + pad_for(BN)) : (BK + pad_for(BK));
+  static constexpr int BEL = TB ? BK * LDB : BN * LDB;
+  static constexpr int SEL = AEL + BEL;
+  static constexpr size_t SMEM = size_t(STAGES) * SEL * sizeof(double);
+  static_assert(TM % 8 == 0 && TN % 8 == 0, "warp tile must be a multiple of 8");
+  static_assert(BK % 4 == 0, "BK multiple of 4");
+};
+
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool TA, bool TB>
+__global__ void __launch_bounds__(WM* WN * 32)
+    dgemm_kernel(const __grid_constant__ GemmParams P) {
+  using C = Cfg<BM, BN, BK, WM, WN, STAGES, TA, TB>;
+  extern __shared__ __align__(16) double smem[];
+
+  const int tn = blockIdx.x, tm = blockIdx.y;
+  const int b = blockIdx.z % P.nbatch;
+  const int ks = blockIdx.z / P.nbatch;
+  const GemmDesc& D = P.d[b];
+  const int m0 = tm * BM, n0 = tn * BN;
+  const bool tile_live = (m0 < D.M) && (n0 < D.N);
+  if (!tile_live && P.kslices == 1) return;
+
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int wm0 = (warp % WM) * C::TM;
+  const int wn0 = (warp / WM) * C::TN;
+
+  const int kbeg = ks * P.kchunk;
+  const int kend = min(D.K, kbeg + P.kchunk);
+  const int KT = (tile_live && kend > kbeg) ? (kend - kbeg + BK - 1) / BK : 0;
+
+  const double* __restrict__ A = D.A;
+  const double* __restrict__ B = D.B;
+  const int64_t lda = D.lda, ldb = D.ldb;
+
+  auto load_tile = [&](int slot, int k0) {
+    double* sA = smem + slot * C::SEL;
+    double* sB = sA + C::AEL;
+#pragma unroll 4
+    for (int idx = tid; idx < BM * BK; idx += C::NT) {
+      int m, k;
+      if (TA) { k = idx % BK; m = idx / BK; } else { m = idx % BM; k = idx / BM; }
+      const int gm = m0 + m, gk = k0 + k;
+      const bool p = (gm < D.M) && (gk < kend);
+      const double* src = p ? (TA ? A + gk + int64_t(gm) * lda : A + gm + int64_t(gk) * lda) : A;
+      double* dst = TA ? sA + m * C::LDA + k : sA + k * C::LDA + m;
+      cp_async8(dst, src, p);
+    }
+#pragma unroll 4
+    for (int idx = tid; idx < BN * BK; idx += C::NT) {
+      int n, k;
+      if (TB) { n = idx % BN; k = idx / BN; } else { k = idx % BK; n = idx / BK; }
+      const int gn = n0 + n, gk = k0 + k;
+      const bool p = (gn < D.N) && (gk < kend);
+      const double* src = p ? (TB ? B + gn + int64_t(gk) * ldb : B + gk + int64_t(gn) * ldb) : B;
+      double* dst = TB ? sB + k * C::LDB + n : sB + n * C::LDB + k;
+      cp_async8(dst, src, p);
+    }
+  };
+
+  double acc[C::FM][C::FN][2];
+#pragma unroll
+  for (int i = 0; i < C::FM; ++i)
+#pragma unroll
+    for (int j = 0; j < C::FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < KT) load_tile(s, kbeg + s * BK);
+    cp_async_commit();
+  }
+
+  for (int kt = 0; kt < KT; ++kt) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    const int nk = kt + STAGES - 1;
+    if (nk < KT) load_tile(nk % STAGES, kbeg + nk * BK);
+    cp_async_commit();
+
+    const double* sA = smem + (kt % STAGES) * C::SEL;
+    const double* sB = sA + C::AEL;
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      double af[C::FM], bf[C::FN];
+#pragma unroll
+      for (int i = 0; i < C::FM; ++i) {
+        const int m = wm0 + i * 8 + g;
+        af[i] = TA ? sA[m * C::LDA + kk + t] : sA[(kk + t) * C::LDA + m];
+      }
+#pragma unroll
+      for (int j = 0; j < C::FN; ++j) {
+        const int n = wn0 + j * 8 + g;
+        bf[j] = TB ? sB[(kk + t) * C::LDB + n] : sB[n * C::LDB + kk + t];
+      }
+#pragma unroll
+      for (int i = 0; i < C::FM; ++i)
+#pragma unroll
+        for (int j = 0; j < C::FN; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+  }
+  cp_async_wait<0>();
+
+  if (P.kslices == 1) {
+    const double alpha = P.alpha, beta = P.beta;
+    double* Cp = D.C;
+    const int64_t ldc = D.ldc;
+#pragma unroll
+    for (int i = 0; i < C::FM; ++i) {
+      const int m = m0 + wm0 + i * 8 + g;
+      if (m >= D.M) continue;
+#pragma unroll
+      for (int j = 0; j < C::FN; ++j) {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int n = n0 + wn0 + j * 8 + 2 * t + e;
+          if (n < D.N) {
+            double* cp = Cp + m + int64_t(n) * ldc;
+            double v = alpha * acc[i][j][e];
+            if (beta != 0.0) v += beta * *cp;
+            *cp = v;
+          }
+        }
+      }
+    }
+  } else {
+    // partial tile -> workspace [ks][b][tm][tn][BM x BN] (column-major in the tile)
+    const size_t tile = ((size_t(ks) * P.nbatch + b) * P.tiles_m + tm) * P.tiles_n + tn;
+    double* W = P.ws + tile * (BM * BN);
+#pragma unroll
+    for (int i = 0; i < C::FM; ++i) {
+      const int ml = wm0 + i * 8 + g;
+#pragma unroll
+      for (int j = 0; j < C::FN; ++j) {
+        const int nl = wn0 + j * 8 + 2 * t;
+        W[ml + nl * BM] = acc[i][j][0];
+        W[ml + (nl + 1) * BM] = acc[i][j][1];
+      }
+    }
+  }
+}
+
+// deterministic split-K reduction: slices summed in index order
+template <int BM, int BN>
+__global__ void splitk_reduce(const __grid_constant__ GemmParams P) {
+  const int tn = blockIdx.x, tm = blockIdx.y, b = blockIdx.z;
+  const GemmDesc& D = P.d[b];
+  const int m0 = tm * BM, n0 = tn * BN;
+  if (m0 >= D.M || n0 >= D.N) return;
+  const size_t stride = size_t(P.nbatch) * P.tiles_m * P.tiles_n * (BM * BN);
+  const size_t tile = ((size_t(b) * P.tiles_m + tm) * P.tiles_n + tn) * (BM * BN);
+  for (int e = threadIdx.x; e < BM * BN; e += blockDim.x) {
+    const int ml = e % BM, nl = e / BM;
+    const int m = m0 + ml, n = n0 + nl;
+    if (m >= D.M || n >= D.N) continue;
+    double s = 0.0;
+    for (int k = 0; k < P.kslices; ++k) s += P.ws[tile + k * stride + e];
+    double* cp = D.C + m + int64_t(n) * D.ldc;
+    double v = P.alpha * s;
+    if (P.beta != 0.0) v += P.beta * *cp;
+    *cp = v;
+  }
+}
+
+template <int BM, int BN, int BK, int WM, int WN, int STAGES>
+struct Shape {
+  static constexpr int bm = BM, bn = BN, bk = BK, wm = WM, wn = WN, st = STAGES;
+};
+
+template <class S, bool TA, bool TB>
+int launch_cfg(Ctx& c, GemmParams& P, int maxM, int maxN, int maxK, cudaStream_t s) {
+  using C = Cfg<S::bm, S::bn, S::bk, S::wm, S::wn, S::st, TA, TB>;
+  auto kern = dgemm_kernel<S::bm, S::bn, S::bk, S::wm, S::wn, S::st, TA, TB>;
+  static bool attr_set[64] = {false};
+  int dev = c.device;
+  if (!attr_set[dev & 63]) {
+    TTR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  int(C::SMEM)));
+    attr_set[dev & 63] = true;
+  }
+  P.tiles_m = (maxM + S::bm - 1) / S::bm;
+  P.tiles_n = (maxN + S::bn - 1) / S::bn;
+  // split-K: fill ~2 waves of SMs when the tile grid alone cannot
+  const int ctas_per_sm = std::max(1, int((200 * 1024) / C::SMEM));
+  const long tiles = long(P.tiles_m) * P.tiles_n * P.nbatch;
+  const long target = 2L * c.sm_count * ctas_per_sm;
+  const int ktiles = (maxK + S::bk - 1) / S::bk;
+  int ksl = 1;
+  if (tiles < target) {
+    ksl = int(std::min<long>((target + tiles - 1) / tiles, std::max(1, ktiles / 4)));
+    ksl = std::max(1, std::min(ksl, 64));
+  }
+  const int kchunk_tiles = (ktiles + ksl - 1) / ksl;
+  ksl = std::max(1, (ktiles + kchunk_tiles - 1) / std::max(1, kchunk_tiles));
+  P.kslices = ksl;
+  P.kchunk = kchunk_tiles * S::bk;
+  if (ksl > 1) {
+    const size_t need = size_t(ksl) * tiles * S::bm * S::bn;
+    if (c.gemm_ws.n < need) {
+      TTR_TRY(dalloc(c.gemm_ws, need + need / 4, s));
+    }
+    P.ws = c.gemm_ws.p;
+  } else {
+    P.ws = nullptr;
+  }
+  dim3 grid(P.tiles_n, P.tiles_m, P.nbatch * ksl);
+  if (grid.y > 65535 || grid.z > 65535) {
+    set_error("gemm grid too large (%d x %d x %d)", grid.x, grid.y, grid.z);
+    return TT_ERR_ARG;
+  }
+  kern<<<grid, C::NT, C::SMEM, s>>>(P);
+  TTR_TRY(launched());
+  if (ksl > 1) {
+    splitk_reduce<S::bm, S::bn><<<dim3(P.tiles_n, P.tiles_m, P.nbatch), 256, 0, s>>>(P);
+    TTR_TRY(launched());
+  }
+  return TT_OK;
+}
+
+// tile shapes (DESIGN.md §Kernels / K2): BM, BN, BK, warps_m, warps_n, stages
+using TallS = Shape<128, 48, 16, 4, 2, 4>;   // M >> N ~ l (phase-1 Z, Y_n, Q = Y R^-1)
+using WideS = Shape<48, 128, 16, 2, 4, 4>;   // N >> M ~ l (carry M^(j) H(T))
+using SqS = Shape<64, 64, 16, 2, 2, 4>;      // general / split-K
+using SmallS = Shape<32, 32, 16, 2, 2, 3>;   // tiny problems
+
+template <bool TA, bool TB>
+int dispatch(Ctx& c, GemmParams& P, int maxM, int maxN, int maxK, cudaStream_t s) {
+  // pick the shape that wastes least on ragged edges, preferring big tiles
+  auto waste = [&](int bm, int bn) {
+    const double tm = double((maxM + bm - 1) / bm) * bm, tn = double((maxN + bn - 1) / bn) * bn;
+    return (tm * tn) / (double(maxM) * maxN);
+  };
+  if (maxM <= 32 && maxN <= 32) return launch_cfg<SmallS, TA, TB>(c, P, maxM, maxN, maxK, s);
+  if (maxM >= 4 * maxN && maxN <= 160 && waste(128, 48) <= 1.35)
+    return launch_cfg<TallS, TA, TB>(c, P, maxM, maxN, maxK, s);
+  if (maxN >= 4 * maxM && maxM <= 160 && waste(48, 128) <= 1.35)
+    return launch_cfg<WideS, TA, TB>(c, P, maxM, maxN, maxK, s);
+  if (waste(64, 64) > 1.6 && waste(32, 32) < waste(64, 64))
+    return launch_cfg<SmallS, TA, TB>(c, P, maxM, maxN, maxK, s);
+  return launch_cfg<SqS, TA, TB>(c, P, maxM, maxN, maxK, s);
+}
+
+}  // namespace
+
+int gemm(Ctx& c, bool ta, bool tb, const GemmDesc* d, int nbatch, double alpha, double beta,
+         cudaStream_t s) {
+  int done = 0;
+  while (done < nbatch) {
+    const int nb = std::min(kMaxGemmBatch, nbatch - done);
+    GemmParams P;
+    int maxM = 0, maxN = 0, maxK = 0, live = 0;
+    for (int i = 0; i < nb; ++i) {
+      const GemmDesc& x = d[done + i];
+      if (x.M <= 0 || x.N <= 0) continue;
+      if (x.K <= 0) {
+        // C = beta*C: not needed by the library (K >= 1 always); refuse loudly
+        set_error("gemm with K = 0");
+        return TT_ERR_ARG;
+      }
+      P.d[live++] = x;
+      maxM = std::max(maxM, x.M);
+      maxN = std::max(maxN, x.N);
+      maxK = std::max(maxK, x.K);
+    }
+    done += nb;
+    if (live == 0) continue;
+    P.nbatch = live;
+    P.alpha = alpha;
+    P.beta = beta;
+    int r;
+    if (!ta && !tb) r = dispatch<false, false>(c, P, maxM, maxN, maxK, s);
+    else if (!ta && tb) r = dispatch<false, true>(c, P, maxM, maxN, maxK, s);
+    else if (ta && !tb) r = dispatch<true, false>(c, P, maxM, maxN, maxK, s);
+    else r = dispatch<true, true>(c, P, maxM, maxN, maxK, s);
+    TTR_TRY(r);
+  }
+  return TT_OK;
+}
+
+}  // namespace ttr

@@ -1,0 +1,125 @@
+"""GPU unit parity of the individual kernels behind the C-ABI (run with -m gpu).
+
+Expected values: plain fp64 CPU (torch / numpy) references and the oracle."""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    import paper_2110_04393_b200 as P
+    return P.Context(0)
+
+
+def colmajor(rows, cols, gen, device="cuda"):
+    return torch.randn((cols, rows), dtype=torch.float64, generator=gen).t().to(device)
+
+
+@pytest.mark.parametrize("ta", [False, True])
+@pytest.mark.parametrize("tb", [False, True])
+@pytest.mark.parametrize("mnk", [(1, 1, 1), (7, 5, 3), (129, 47, 33), (64, 144, 64),
+                                 (300, 35, 1000), (144, 144, 20000), (16384, 144, 64),
+                                 (144, 2048, 4096), (35, 1, 2240)])
+def test_dgemm_matches_fp64_reference(ctx, ta, tb, mnk):
+    m, n, k = mnk
+    g = torch.Generator().manual_seed(m * 7 + n * 3 + k)
+    A = colmajor(k, m, g) if ta else colmajor(m, k, g)
+    B = colmajor(n, k, g) if tb else colmajor(k, n, g)
+    C0 = colmajor(m, n, g)
+    Cg = C0.clone()
+    ctx.tt_dgemm(A, B, ta, tb, alpha=0.75, beta=-0.5, C_out=Cg)
+    Ah = A.cpu().t() if ta else A.cpu()
+    Bh = B.cpu().t() if tb else B.cpu()
+    ref = 0.75 * (Ah @ Bh) - 0.5 * C0.cpu()
+    err = (Cg.cpu() - ref).abs().max().item()
+    scale = (Ah.abs() @ Bh.abs()).max().item() + C0.abs().max().item()
+    assert err <= 1e-14 * max(1.0, math.sqrt(k)) * scale
+
+
+def test_dgemm_batched_ldc_offsets_via_library(ctx):
+    # C written into a sub-block of a larger matrix (ldc > m), beta = 0 must ignore NaNs
+    g = torch.Generator().manual_seed(5)
+    A, B = colmajor(50, 20, g), colmajor(20, 30, g)
+    big = torch.full((40, 80), float("nan"), dtype=torch.float64, device="cuda").t()  # 80 x 40
+    sub = big[10:60, 5:35]
+    ctx.tt_dgemm(A, B, C_out=sub)
+    assert torch.allclose(sub.cpu(), A.cpu() @ B.cpu(), rtol=1e-13, atol=1e-13)
+    assert torch.isnan(big[:10]).all() and torch.isnan(big[60:]).all()
+
+
+def test_sketch_matches_oracle_philox(ctx):
+    import oracle
+    dims = [5, 7, 3, 9]
+    ranks = [1, 4, 6, 5, 1]
+    sk = ctx.tt_sketch_create(dims, ranks, seed=0x123456789, tag=0)
+    for n in range(2, 5):
+        got = sk.core(n).cpu().numpy()
+        want = oracle.sketch_core(0x123456789, n, ranks[n - 1], dims[n - 1], ranks[n])
+        assert got.shape == want.shape
+        # integer words identical; libm vs CUDA log/sincos may differ by a few ulp
+        np.testing.assert_allclose(got, want, rtol=4 * 2.0 ** -52, atol=1e-300)
+        assert np.mean(got == want) > 0.5
+
+
+def test_sketch_large_count_and_odd_tail(ctx):
+    import oracle
+    dims = [3, 257, 3]
+    ranks = [1, 3, 3, 1]
+    sk = ctx.tt_sketch_create(dims, ranks, seed=77, tag=5)
+    got = sk.core(2).cpu().numpy()     # 3*257*3 = 2313 entries (odd)
+    want = oracle.sketch_core(77, 2, 3, 257, 3, tag=5)
+    np.testing.assert_allclose(got, want, rtol=4 * 2.0 ** -52)
+
+
+@pytest.mark.parametrize("m,n,cond", [(40, 7, 1e2), (2240, 35, 1e8), (7000, 70, 1e6),
+                                      (36864, 144, 1e4), (500, 1, 1.0), (100, 100, 10.0)])
+def test_qr_orthogonality_and_factorization(ctx, m, n, cond):
+    rng = np.random.default_rng(m + n)
+    U, _ = np.linalg.qr(rng.standard_normal((m, n)))
+    V, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    s = np.logspace(0, -math.log10(cond), n)
+    A = (U * s) @ V.T
+    Ad = torch.from_numpy(np.asfortranarray(A)).cuda()
+    Ad = Ad.t().contiguous().t()
+    Q, R, fb = ctx.tt_qr(Ad, want_r=True)
+    Qh, Rh = Q.cpu().numpy(), R.cpu().numpy()
+    assert np.linalg.norm(Qh.T @ Qh - np.eye(n)) < 1e-13 * math.sqrt(n)
+    assert np.linalg.norm(Qh @ Rh - A) <= 1e-13 * np.linalg.norm(A) * max(1, math.log10(cond))
+    assert np.allclose(np.tril(Rh, -1), 0)
+    # same projector as LAPACK Householder (the oracle's thin_qr)
+    Qo, _ = np.linalg.qr(A)
+    assert np.linalg.norm(Qh @ (Qh.T @ A) - Qo @ (Qo.T @ A)) < 1e-13 * np.linalg.norm(A)
+
+
+def test_qr_rank_deficient_uses_valid_basis(ctx):
+    rng = np.random.default_rng(3)
+    m, n, r = 2240, 35, 25
+    A = rng.standard_normal((m, r)) @ rng.standard_normal((r, n))
+    Ad = torch.from_numpy(A).cuda().t().contiguous().t()
+    Q, _, fb = ctx.tt_qr(Ad)
+    Qh = Q.cpu().numpy()
+    assert np.linalg.norm(Qh.T @ Qh - np.eye(n)) < 1e-12
+    assert np.linalg.norm(Qh @ (Qh.T @ A) - A) < 1e-12 * np.linalg.norm(A)
+
+
+@pytest.mark.parametrize("m,n", [(5, 5), (144, 144), (70, 33), (300, 80), (33, 33)])
+def test_jacobi_svd_matches_lapack(ctx, m, n):
+    rng = np.random.default_rng(m * n)
+    A = rng.standard_normal((m, n)) * np.logspace(0, -8, n)[None, :]
+    Ad = torch.from_numpy(A).cuda().t().contiguous().t()
+    AV, V, s = ctx.tt_svd_jacobi(Ad)
+    sh = s.cpu().numpy()
+    sref = np.linalg.svd(A, compute_uv=False)
+    np.testing.assert_allclose(sh, sref, rtol=1e-12, atol=1e-15 * sref[0])
+    Vh, AVh = V.cpu().numpy(), AV.cpu().numpy()
+    assert np.linalg.norm(Vh.T @ Vh - np.eye(n)) < 1e-13 * n
+    assert np.linalg.norm(A @ Vh - AVh) < 1e-13 * np.linalg.norm(A)
+    # AV has orthogonal columns with norms sigma
+    G = AVh.T @ AVh
+    assert np.linalg.norm(G - np.diag(np.diag(G))) < 1e-13 * sref[0] ** 2
+    assert np.all(np.diff(sh) <= 0)

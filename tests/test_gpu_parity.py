@@ -1,0 +1,193 @@
+"""End-to-end parity of tt_round_sum (CUDA, through the C-ABI) against the oracle.
+
+Both sides get identical input bits (ttsynth) and the same Philox sketch seed.
+The metric is the relative difference ‖X_gpu − X_oracle‖ / ‖X_oracle‖ computed
+in TT arithmetic by orthogonalising [X_gpu, −X_oracle] (R12), with the
+north-star bar 1e-10 (BASELINE.json).  Run with -m gpu."""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import ttsynth
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-10
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    import paper_2110_04393_b200 as P
+    return P.Context(0)
+
+
+def gpu_terms(terms):
+    return [[ttsynth._move(c, "cuda") for c in t] for t in terms]
+
+
+def run_both(ctx, terms, ell, rank=0, tol=0.0, adaptive=False, seed=1, sketch_only=False,
+             max_rank=0, host=False):
+    np_terms = [ttsynth.to_numpy(t) for t in terms]
+    ref = oracle.round_sum(np_terms, ell=ell, seed=seed, rank=rank, tol=tol, adaptive=adaptive,
+                           max_rank=max_rank, sketch_only=sketch_only)
+    if sketch_only:
+        mode, r, p = "sketch_only", 0, ell
+    elif tol > 0:
+        mode, r, p = "tol", rank, ell
+    else:
+        mode, r, p = "rank", rank, ell - rank
+    src = terms if host else gpu_terms(terms)
+    res = ctx.tt_round_sum(src, mode=mode, rank=r, oversample=p, tol=tol, seed=seed,
+                           adaptive=adaptive, max_rank=max_rank)
+    return res, ref
+
+
+def rel(res, ref):
+    X = res.numpy()
+    return oracle.rel_diff(X, ref.X), X
+
+
+def check(res, ref, tol=TOL):
+    assert res.ranks[1:-1] == list(ref.ranks), (res.ranks, ref.ranks)
+    r, X = rel(res, ref)
+    assert r <= tol, r
+    return r, X
+
+
+# ------------------------------------------------------------------ configs 1-4, full size
+def test_config1_tiny_full(ctx):
+    w = ttsynth.config1_tiny()
+    res, ref = run_both(ctx, w.terms, w.ell, rank=w.rank)
+    r, X = check(res, ref)
+    # closed form: best rank-4 approximation of the 16x16 unfolding
+    F = sum(oracle.full(ttsynth.to_numpy(t)) for t in w.terms)
+    U, s, Vt = np.linalg.svd(F.reshape(16, 16))
+    best = ((U[:, :4] * s[:4]) @ Vt[:4]).reshape(F.shape)
+    assert np.linalg.norm(oracle.full(X) - best) <= 1e-13 * np.linalg.norm(best)
+
+
+def test_config2_single_full(ctx):
+    w = ttsynth.config2_single()
+    res, ref = run_both(ctx, w.terms, w.ell, rank=w.rank)
+    check(res, ref)
+
+
+def test_config3_sum10_full(ctx):
+    w = ttsynth.config3_sum10()
+    res, ref = run_both(ctx, w.terms, w.ell, rank=w.rank)
+    check(res, ref)
+
+
+def test_config4_gmres_full(ctx):
+    w = ttsynth.config4_gmres()
+    res, ref = run_both(ctx, w.terms, w.ell, tol=w.tol, adaptive=True)
+    check(res, ref)
+    assert res.passes == ref.passes
+
+
+def test_config5_reduced_depth(ctx):
+    # config 5 shapes (S=32, I=256, summand rank 64, l=144 -> r=128) at d = 5
+    w = ttsynth.config5_large(d=5)
+    res, ref = run_both(ctx, w.terms, w.ell, rank=w.rank)
+    check(res, ref)
+
+
+# ------------------------------------------------------------------ modes and edge cases
+def test_sketch_only_is_left_orthogonal(ctx):
+    w = ttsynth.config3_sum10(d=6, I=20, S=4)
+    res, ref = run_both(ctx, w.terms, 30, sketch_only=True)
+    r, X = check(res, ref)
+    assert oracle.left_orth_residual(X) < 1e-12
+    import paper_2110_04393_b200 as P
+    assert res.flags & P.FLAG_LEFT_ORTH
+
+
+def test_two_modes_and_single_summand(ctx):
+    terms = ttsynth.random_terms(3, [17, 9], [[1, 5, 1]])
+    res, ref = run_both(ctx, terms, 4, rank=3)
+    check(res, ref)
+
+
+@pytest.mark.parametrize("seed", [11, 12])
+def test_ragged_summand_ranks_and_dims(ctx, seed):
+    dims = [3, 11, 5, 7, 2, 13]
+    rng = np.random.default_rng(seed)
+    tr = [[1] + [int(x) for x in rng.integers(1, 9, size=len(dims) - 1)] + [1] for _ in range(5)]
+    terms = ttsynth.random_terms(seed, dims, tr)
+    res, ref = run_both(ctx, terms, 9, rank=6)
+    check(res, ref)
+    res, ref = run_both(ctx, terms, 13, sketch_only=True)
+    check(res, ref)
+
+
+def test_exact_recovery_when_sketch_exceeds_rank(ctx):
+    terms = ttsynth.random_terms(21, [6, 6, 6, 6], [[1, 2, 3, 2, 1], [1, 3, 2, 2, 1]])
+    res, ref = run_both(ctx, terms, 8, sketch_only=True)
+    r, X = check(res, ref)
+    S = oracle.tt_add([ttsynth.to_numpy(t) for t in terms])
+    assert oracle.rel_diff(X, S) < 1e-12
+
+
+def test_zero_sum(ctx):
+    import paper_2110_04393_b200 as P
+    Z = [torch.zeros((1, 4, 2), dtype=torch.float64), torch.zeros((2, 4, 2), dtype=torch.float64),
+         torch.zeros((2, 4, 1), dtype=torch.float64)]
+    res = ctx.tt_round_sum(gpu_terms([Z, Z]), mode="rank", rank=2, oversample=2)
+    assert res.ranks == [1, 1, 1, 1] and res.flags & P.FLAG_ZERO
+    assert all(not np.any(c) for c in res.numpy())
+
+
+def test_tolerance_mode_without_adaptivity(ctx):
+    w = ttsynth.config4_gmres(d=6, I=32, R=12, S=5)
+    res, ref = run_both(ctx, w.terms, 20, tol=1e-6)
+    check(res, ref)
+
+
+def test_host_inputs_are_staged(ctx):
+    # e2e path of bench.py: host (pinned) buffers in, copies inside the call
+    w = ttsynth.config3_sum10(d=6, I=40, S=3)
+    pinned = [[c.permute(2, 1, 0).contiguous().pin_memory().permute(2, 1, 0) for c in t]
+              for t in w.terms]
+    res, ref = run_both(ctx, pinned, w.ell, rank=w.rank, host=True)
+    check(res, ref)
+
+
+def test_inner_product(ctx):
+    terms = ttsynth.random_terms(31, [5, 6, 7, 4], [[1, 3, 4, 2, 1], [1, 2, 5, 3, 1]])
+    x, y = terms
+    got = ctx.tt_inner(gpu_terms([x])[0], gpu_terms([y])[0])
+    want = oracle.inner(ttsynth.to_numpy(x), ttsynth.to_numpy(y))
+    assert abs(got - want) <= 1e-13 * max(1.0, abs(want)) * 10
+
+
+def test_user_sketch_matches_internal(ctx):
+    w = ttsynth.config3_sum10(d=5, I=16, S=3)
+    sumR = [1] + [sum(t[n].shape[2] for t in w.terms) for n in range(4)] + [1]
+    caps = [1] + oracle.rank_caps(w.dims, sumR, 12) + [1]
+    sk = ctx.tt_sketch_create(w.dims, caps, seed=9)
+    a = ctx.tt_round_sum(gpu_terms(w.terms), mode="sketch_only", oversample=12, seed=9)
+    b = ctx.tt_round_sum(gpu_terms(w.terms), mode="sketch_only", oversample=12, sketch=sk)
+    for x, y in zip(a.numpy(), b.numpy()):
+        assert np.array_equal(x, y)
+
+
+def test_determinism_bitwise(ctx):
+    w = ttsynth.config3_sum10(d=5, I=30, S=4)
+    t = gpu_terms(w.terms)
+    a = ctx.tt_round_sum(t, mode="rank", rank=20, oversample=5, seed=4).numpy()
+    b = ctx.tt_round_sum(t, mode="rank", rank=20, oversample=5, seed=4).numpy()
+    for x, y in zip(a, b):
+        assert np.array_equal(x, y)
+
+
+def test_errors_are_reported(ctx):
+    import paper_2110_04393_b200 as P
+    terms = ttsynth.random_terms(1, [4, 4, 4], [[1, 2, 2, 1], [1, 2, 2, 1]])
+    bad = [terms[0], [terms[1][0], terms[1][1], torch.zeros((2, 5, 1), dtype=torch.float64)]]
+    with pytest.raises(P.TTError) as e:
+        ctx.tt_round_sum(gpu_terms(bad), mode="rank", rank=2, oversample=1)
+    assert e.value.code == -2
+    with pytest.raises(P.TTError):
+        ctx.tt_round_sum(gpu_terms(terms), mode="tol", tol=0.0, oversample=3)
