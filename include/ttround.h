@@ -103,7 +103,8 @@ typedef struct {
 int tt_get_nccl_unique_id(uint8_t id[128]);
 
 /* Create a context on CUDA device `device` using stream `cuda_stream`
- * (a cudaStream_t, or NULL for a library-created non-blocking stream).
+ * (a cudaStream_t, or NULL for a library-created non-blocking stream; to run
+ * on the legacy default stream pass cudaStreamLegacy, i.e. (void*)0x1).
  * nccl_id == NULL or world == 1: single-GPU.  Otherwise the summands of a
  * rounding are sharded across `world` processes (one per GPU); each passes its
  * local summands and all receive the same result. */
@@ -168,6 +169,11 @@ uint64_t tt_launch_count(void);
  * [0] sketch, [1] phase 1 (Alg. 3), [2] sweep GEMMs, [3] QR, [4] collectives,
  * [5] truncation, [6] total.  Returns the number of entries written (<= n). */
 int tt_ctx_set_timing(tt_ctx_t ctx, int enable);
+/* Copy the context's device status words (after the last call) to out[0..n):
+ * [1] Householder fallback used, [2] zero sketch seen, [3] bit 1: Jacobi SVD hit
+ * its sweep limit; the others are per-QR route flags.
+ * Returns the number of words written. */
+int tt_ctx_flags(tt_ctx_t ctx, int* out, int n);
 int tt_ctx_last_timing(tt_ctx_t ctx, double* ms, int n);
 
 /* ---- kernel-level entry points (for the parity tests and bench) ---------- */
@@ -177,8 +183,10 @@ int tt_dgemm(tt_ctx_t ctx, int trans_a, int trans_b, int64_t m, int64_t n, int64
              double alpha, const double* A, int64_t lda, const double* B, int64_t ldb,
              double beta, double* C, int64_t ldc);
 /* Thin QR of the column-major m x n (m >= n) device matrix A: Q (m x n, ld m)
- * and, if R != NULL, R (n x n upper triangular, ld n).  Returns TT_OK and sets
- * *fallback = 1 if the Householder fallback ran. */
+ * and, if R != NULL, R (n x n upper triangular, ld n).  Q == NULL asks for R
+ * only (the truncation's use).  Routes: CholeskyQR2, shifted CholeskyQR3, then
+ * (R only) Householder TSQR or (with Q) single-CTA Householder; *fallback = 1
+ * if one of the two Householder fallbacks ran. */
 int tt_qr(tt_ctx_t ctx, int64_t m, int64_t n, const double* A, int64_t lda,
           double* Q, double* R, int* fallback);
 /* Singular values (descending) and right singular vectors of the column-major

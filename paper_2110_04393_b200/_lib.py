@@ -53,6 +53,7 @@ def load_library(path: str = LIB_PATH):
         "tt_ctx_destroy": (C.c_int, [P]),
         "tt_ctx_set_timing": (C.c_int, [P, C.c_int]),
         "tt_ctx_last_timing": (C.c_int, [P, C.POINTER(dbl), C.c_int]),
+        "tt_ctx_flags": (C.c_int, [P, C.POINTER(C.c_int), C.c_int]),
         "tt_sketch_create": (C.c_int, [P, i32, C.POINTER(i64), C.POINTER(i64), u64, C.c_uint32,
                                        C.POINTER(P)]),
         "tt_sketch_core": (C.c_int, [P, i32, C.POINTER(P)]),
@@ -213,13 +214,23 @@ class Sketch:
 
 
 class Context:
-    """tt_ctx_t: one CUDA device + stream (+ NCCL communicator when world > 1)."""
+    """tt_ctx_t: one CUDA device + stream (+ NCCL communicator when world > 1).
+
+    The stream defaults to torch's current stream of the device, so calls are
+    ordered with the torch kernels that produce the inputs."""
 
     def __init__(self, device: int = 0, stream: Optional[torch.cuda.Stream] = None,
                  nccl_id: Optional[bytes] = None, rank: int = 0, world: int = 1):
         L = load_library()
         self.device = torch.device("cuda", device)
-        sp = C.c_void_p(stream.cuda_stream) if stream is not None else None
+        if stream is None:
+            # order every library call after the torch work that produced its
+            # inputs (and before the torch work that consumes its outputs)
+            stream = torch.cuda.current_stream(self.device)
+        self.stream = stream
+        # handle 0 is torch's legacy default stream, but NULL means "library-owned
+        # stream" at the C-ABI: pass cudaStreamLegacy (0x1) for it explicitly
+        sp = C.c_void_p(stream.cuda_stream or 0x1)
         idbuf = (C.c_uint8 * 128)(*nccl_id) if nccl_id is not None else None
         h = C.c_void_p()
         _check(L.tt_ctx_create(device, sp, idbuf, rank, world, C.byref(h)))
@@ -240,6 +251,13 @@ class Context:
         buf = (C.c_double * 8)()
         n = load_library().tt_ctx_last_timing(self.handle, buf, 8)
         return [buf[i] for i in range(n)]
+
+    def status_words(self, n: int = 8) -> List[int]:
+        buf = (C.c_int * n)()
+        k = load_library().tt_ctx_flags(self.handle, buf, n)
+        if k < 0:
+            _check(k)
+        return [buf[i] for i in range(k)]
 
     # ---------------------------------------------------------------- sketch
     def tt_sketch_create(self, dims, ranks, seed: int, tag: int = 0) -> Sketch:
@@ -301,14 +319,15 @@ class Context:
                           C_out.data_ptr(), C_out.stride(1)))
         return C_out
 
-    def tt_qr(self, A: torch.Tensor, want_r: bool = False):
+    def tt_qr(self, A: torch.Tensor, want_r: bool = False, want_q: bool = True):
         L = load_library()
         m, n = A.shape
         assert A.stride(0) == 1
-        Q = torch.empty((n, m), dtype=torch.float64, device=A.device).t()
+        Q = torch.empty((n, m), dtype=torch.float64, device=A.device).t() if want_q else None
         R = torch.empty((n, n), dtype=torch.float64, device=A.device).t() if want_r else None
         fb = C.c_int()
-        _check(L.tt_qr(self.handle, m, n, A.data_ptr(), A.stride(1), Q.data_ptr(),
+        _check(L.tt_qr(self.handle, m, n, A.data_ptr(), A.stride(1),
+                       Q.data_ptr() if Q is not None else None,
                        R.data_ptr() if R is not None else None, C.byref(fb)))
         return Q, R, bool(fb.value)
 

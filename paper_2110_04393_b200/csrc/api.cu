@@ -442,25 +442,36 @@ int truncate(Ctx& c, tt_tensor& X, double tol, int64_t rmax, std::vector<int64_t
     const int64_t In = X.dims[n - 1];
     const int64_t r0 = r[n - 1];
     const int64_t mrow = In * r[n];
-    DBuf AV, V, sig, Q, R, Rt, newn, newp;
+    DBuf AV, V, sig, Q, R, Rt, Bk, newn, newp;
     int64_t k = 0;
     const int64_t rows_av = r0;
     const int64_t cols = std::min(r0, mrow);
     TTR_TRY(dalloc(AV, size_t(rows_av) * cols, s));
-    TTR_TRY(dalloc(V, size_t(cols) * cols, s));
     TTR_TRY(dalloc(sig, size_t(cols), s));
-    if (mrow >= r0) {
-      TTR_TRY(dalloc(Q, size_t(mrow) * r0, s));
+    // fast path: only R of the QR is needed, and the SVD of R^T does not form V
+    // (H(X_n) <- Sigma_k^{-2} (U Sigma)_k^T H(X_n) = V_k^T Q^T)
+    const bool fast = (mrow >= r0) && svd_nov_fits(r0, r0);
+    if (fast) {
       TTR_TRY(dalloc(R, size_t(r0) * r0, s));
       TTR_TRY(dalloc(Rt, size_t(r0) * r0, s));
-      // [Q, R] = qr(H(X_n)^T)
-      TTR_TRY(qr(c, mrow, r0, X.bufs[n - 1].p, r0, true, Q.p, R.p, s));
-      // [U, S, V] = svd(R^T)
+      TTR_TRY(qr(c, mrow, r0, X.bufs[n - 1].p, r0, true, nullptr, R.p, s));   // R of H(X_n)^T
       TTR_TRY(transpose(c, R.p, r0, r0, r0, Rt.p, r0, s));
-      TTR_TRY(svd_jacobi(c, r0, r0, Rt.p, r0, AV.p, V.p, sig.p, s));
+      TTR_TRY(svd_nov(c, r0, r0, Rt.p, r0, AV.p, sig.p, s));                 // svd(R^T)
     } else {
-      // wide unfolding (I_n r_n < r_{n-1}): SVD of H(X_n) directly
-      TTR_TRY(svd_jacobi(c, r0, mrow, X.bufs[n - 1].p, r0, AV.p, V.p, sig.p, s));
+      TTR_TRY(dalloc(V, size_t(cols) * cols, s));
+      if (mrow >= r0) {
+        TTR_TRY(dalloc(Q, size_t(mrow) * r0, s));
+        TTR_TRY(dalloc(R, size_t(r0) * r0, s));
+        TTR_TRY(dalloc(Rt, size_t(r0) * r0, s));
+        // [Q, R] = qr(H(X_n)^T)
+        TTR_TRY(qr(c, mrow, r0, X.bufs[n - 1].p, r0, true, Q.p, R.p, s));
+        // [U, S, V] = svd(R^T)
+        TTR_TRY(transpose(c, R.p, r0, r0, r0, Rt.p, r0, s));
+        TTR_TRY(svd_jacobi(c, r0, r0, Rt.p, r0, AV.p, V.p, sig.p, s));
+      } else {
+        // wide unfolding (I_n r_n < r_{n-1}): SVD of H(X_n) directly
+        TTR_TRY(svd_jacobi(c, r0, mrow, X.bufs[n - 1].p, r0, AV.p, V.p, sig.p, s));
+      }
     }
     if (tol > 0.0) {
       TTR_TRY(eps_rank_dev(c, sig.p, int(cols), nullptr, eps, int(rmax), kdev.p, s));
@@ -474,7 +485,12 @@ int truncate(Ctx& c, tt_tensor& X, double tol, int64_t rmax, std::vector<int64_t
     ks[n - 1] = k;
     // H(X_n) <- V_k^T Q^T  (or V_k^T)
     TTR_TRY(dalloc(newn, size_t(k) * mrow, s));
-    if (mrow >= r0) {
+    if (fast) {
+      TTR_TRY(dalloc(Bk, size_t(r0) * k, s));
+      TTR_TRY(scale_by_inv_sigma2(c, AV.p, r0, k, sig.p, Bk.p, s));
+      TTR_TRY(gemm1(c, true, false, int(k), int(mrow), int(r0), 1.0, Bk.p, int(r0),
+                    X.bufs[n - 1].p, int(r0), 0.0, newn.p, int(k), s));
+    } else if (mrow >= r0) {
       TTR_TRY(gemm1(c, true, true, int(k), int(mrow), int(r0), 1.0, V.p, int(cols), Q.p,
                     int(mrow), 0.0, newn.p, int(k), s));
     } else {
@@ -803,6 +819,14 @@ int tt_ctx_set_timing(tt_ctx_t c, int enable) {
   return TT_OK;
 }
 
+int tt_ctx_flags(tt_ctx_t c, int* out, int n) {
+  if (!c || !out) return TT_ERR_ARG;
+  const int k = std::min(n, c->nflags);
+  TTR_CUDA(cudaMemcpyAsync(out, c->flags.p, sizeof(int) * k, cudaMemcpyDeviceToHost, c->stream));
+  TTR_CUDA(cudaStreamSynchronize(c->stream));
+  return k;
+}
+
 int tt_ctx_last_timing(tt_ctx_t c, double* ms, int n) {
   if (!c || !ms) return TT_ERR_ARG;
   const int k = std::min(n, 8);
@@ -931,14 +955,14 @@ int tt_dgemm(tt_ctx_t c, int ta, int tb, int64_t m, int64_t n, int64_t k, double
 
 int tt_qr(tt_ctx_t c, int64_t m, int64_t n, const double* A, int64_t lda, double* Q, double* R,
           int* fallback) {
-  if (!c || !A || !Q) return TT_ERR_ARG;
+  if (!c || !A || (!Q && !R)) return TT_ERR_ARG;
   return guarded([&]() -> int {
     TTR_CUDA(cudaSetDevice(c->device));
     TTR_CUDA(cudaMemsetAsync(c->flags.p, 0, sizeof(int) * c->nflags, c->stream));
     TTR_TRY(qr(*c, m, n, A, lda, false, Q, R, c->stream));
-    int fl[4];
-    TTR_TRY(read_flags(*c, fl, 4));
-    if (fallback) *fallback = fl[1] ? 1 : 0;
+    int fl[16];
+    TTR_TRY(read_flags(*c, fl, 16));
+    if (fallback) *fallback = (fl[1] || fl[14]) ? 1 : 0;
     return TT_OK;
   });
 }

@@ -40,15 +40,16 @@ struct Status {
 
 // every kernel launch of the library goes through this counter (tt_launch_count)
 extern std::atomic<uint64_t> g_launches;
-inline int launched() {
+inline int launched_at(const char* file, int line) {
   g_launches.fetch_add(1, std::memory_order_relaxed);
   cudaError_t e = cudaPeekAtLastError();
   if (e != cudaSuccess) {
-    set_error("kernel launch failed: %s", cudaGetErrorString(e));
+    set_error("kernel launch failed at %s:%d: %s", file, line, cudaGetErrorString(e));
     return TT_ERR_CUDA;
   }
   return TT_OK;
 }
+#define launched() ::ttr::launched_at(__FILE__, __LINE__)
 
 // ---------------------------------------------------------------- device buffers
 // Stream-ordered allocations from the device's default memory pool (kept
@@ -105,7 +106,7 @@ struct Ctx {
   DBuf scratch;
   // split-K partials of the GEMMs
   DBuf gemm_ws;
-  // flags: [0] QR fallback used, [1] numeric breakdown, [2] zero sketch seen, [3..] ranks
+  // device status words, see linalg.cu (route flags 0/4/5, sticky 1-3, counters 8-13)
   IBuf flags;
   int nflags = 0;
 };
@@ -124,14 +125,17 @@ struct GemmDesc {
 };
 constexpr int kMaxGemmBatch = 64;
 
-// Batched FP64 DMMA GEMM (all entries share ta/tb/alpha/beta).
+// Batched FP64 DMMA GEMM (all entries share ta/tb/alpha/beta).  `gate`: optional
+// device flag; the launch is a no-op unless *gate == gate_val (device-side
+// branching of the QR without a host round trip).
 int gemm(Ctx& c, bool ta, bool tb, const GemmDesc* d, int nbatch, double alpha,
-         double beta, cudaStream_t s);
+         double beta, cudaStream_t s, const int* gate = nullptr, int gate_val = 0);
 inline int gemm1(Ctx& c, bool ta, bool tb, int M, int N, int K, double alpha,
                  const double* A, int lda, const double* B, int ldb, double beta,
-                 double* C, int ldc, cudaStream_t s) {
+                 double* C, int ldc, cudaStream_t s, const int* gate = nullptr,
+                 int gate_val = 0) {
   GemmDesc d{A, B, C, M, N, K, lda, ldb, ldc};
-  return gemm(c, ta, tb, &d, 1, alpha, beta, s);
+  return gemm(c, ta, tb, &d, 1, alpha, beta, s, gate, gate_val);
 }
 
 // ---------------------------------------------------------------- sketch
@@ -150,6 +154,15 @@ int qr(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, bool trans, d
 // (m x n, ld m), V (n x n, ld n), sigma (n) sorted descending.
 int svd_jacobi(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, double* AV,
                double* V, double* sigma, cudaStream_t s);
+// One-sided Jacobi of the m x n (m >= n, m <= 256, m n <= 26624) matrix A without
+// forming V: AV = U Sigma (m x n, ld m, sorted) and sigma.  svd_nov_fits() tells
+// whether the shape is supported.
+int svd_nov(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, double* AV,
+            double* sigma, cudaStream_t s);
+bool svd_nov_fits(int64_t m, int64_t n);
+// B(:, c) = AV(:, c) / sigma_c^2, c < k (0 for negligible sigma_c)
+int scale_by_inv_sigma2(Ctx& c, const double* AV, int64_t m, int64_t k, const double* sigma,
+                        double* B, cudaStream_t s);
 // k = eps-rank of sigma (n values, descending) given absolute eps and cap rmax
 // (0 = none), written to dst (device int).
 int eps_rank_dev(Ctx& c, const double* sigma, int n, const double* eps_dev, double eps_host,

@@ -49,6 +49,8 @@ struct GemmParams {
   int kchunk;        // K per slice (multiple of BK)
   double alpha, beta;
   double* ws;        // split-K partials (kslices > 1)
+  const int* gate;   // device-side predicate: run iff gate == nullptr || *gate == gate_val
+  int gate_val;
 };
 
 template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool TA, bool TB>
@@ -71,6 +73,7 @@ __global__ void __launch_bounds__(WM* WN * 32)
     dgemm_kernel(const __grid_constant__ GemmParams P) {
   using C = Cfg<BM, BN, BK, WM, WN, STAGES, TA, TB>;
   extern __shared__ __align__(16) double smem[];
+  if (P.gate && *P.gate != P.gate_val) return;
 
   const int tn = blockIdx.x, tm = blockIdx.y;
   const int b = blockIdx.z % P.nbatch;
@@ -203,6 +206,7 @@ __global__ void __launch_bounds__(WM* WN * 32)
 // deterministic split-K reduction: slices summed in index order
 template <int BM, int BN>
 __global__ void splitk_reduce(const __grid_constant__ GemmParams P) {
+  if (P.gate && *P.gate != P.gate_val) return;
   const int tn = blockIdx.x, tm = blockIdx.y, b = blockIdx.z;
   const GemmDesc& D = P.d[b];
   const int m0 = tm * BM, n0 = tn * BN;
@@ -303,7 +307,7 @@ int dispatch(Ctx& c, GemmParams& P, int maxM, int maxN, int maxK, cudaStream_t s
 }  // namespace
 
 int gemm(Ctx& c, bool ta, bool tb, const GemmDesc* d, int nbatch, double alpha, double beta,
-         cudaStream_t s) {
+         cudaStream_t s, const int* gate, int gate_val) {
   int done = 0;
   while (done < nbatch) {
     const int nb = std::min(kMaxGemmBatch, nbatch - done);
@@ -327,6 +331,8 @@ int gemm(Ctx& c, bool ta, bool tb, const GemmDesc* d, int nbatch, double alpha, 
     P.nbatch = live;
     P.alpha = alpha;
     P.beta = beta;
+    P.gate = gate;
+    P.gate_val = gate_val;
     int r;
     if (!ta && !tb) r = dispatch<false, false>(c, P, maxM, maxN, maxK, s);
     else if (!ta && tb) r = dispatch<false, true>(c, P, maxM, maxN, maxK, s);

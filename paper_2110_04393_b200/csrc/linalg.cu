@@ -5,6 +5,9 @@
 //  * one-sided Jacobi SVD (one CTA) for the truncation step (R3)
 //  * eps-rank, Frobenius norm, transpose, fill
 #include <math.h>
+#include <stdlib.h>
+
+#include <vector>
 
 #include "common.cuh"
 
@@ -74,24 +77,87 @@ namespace {
 constexpr int kCholThreads = 1024;
 constexpr int kSmemLimitDoubles = 26 * 1024;   // 208 KB of dynamic shared memory
 
-// flags layout (Ctx.flags): 0 = breakdown in current QR, 1 = fallback used (sticky),
-// 2 = zero sketch seen (sticky), 3 = numeric failure (sticky)
+// flags layout (Ctx.flags; see common.cuh):
+//  0 = route state of the current QR: 0 plain CholeskyQR2, 1 shifted CholeskyQR3,
+//      2 doubly shifted CholeskyQR4, 3 all failed (-> Householder / TSQR)
+//  1 = Householder fallback used (sticky)      2 = zero sketch seen (sticky)
+//  3 = numeric failure bits (sticky)
+//  8.. = counters: 8 CholQR2, 10 sCholQR3, 11 Householder, 12 Jacobi sweeps,
+//        13 Jacobi calls, 14 TSQR, 15 sCholQR4
+enum CholMode : int {
+  CH_FIRST = 0,    // route 0, pass 1 (input):  failure -> route 1
+  CH_SECOND = 1,   // route 0, pass 2:          failure or |diag R - 1| > kDevTol -> route 1
+  CH_THIRD = 2,    // (unused)
+  CH_SHIFT = 3,    // route 1, pass 1 (shifted): failure -> route 3
+  CH_SPLAIN = 4,   // route 1, pass 2:          failure -> route 2
+  CH_SLAST = 5,    // route 1, pass 3:          failure or deviation -> route 2
+  CH_SHIFT2 = 6,   // route 2, pass 2 (shifted again): failure -> route 3
+  CH_S2PLAIN = 7,  // route 2, pass 3:          failure -> route 3
+  CH_S2LAST = 8,   // route 2, pass 4:          failure or deviation -> route 3
+  CH_SHIFT1B = 9,  // route 2, pass 1 (shifted, on the input again): failure -> route 3
+};
+constexpr double kDevTol = 0.05;
+// mode bit of the R-only QR: a plain pass whose pivots spread by more than
+// 2^20 (kappa(Q1)^2 u no longer small) cannot give an accurate R -> next route
+constexpr int kStrict = 0x100;
+constexpr double kStrictRatio = 0x1p-20;
 
-// G (n x n, ld n, symmetric) -> Rinv (upper, ld n) with G + shift*I = R^T R,
-// optionally R.  mode: 0 = unshifted, 1 = shifted (sCholQR3 first pass, shift
-// 11(mn + n(n+1))u * trace(G)), 2 = unshifted + final-pass check ||diag R - 1||.
+// passes whose input should already be close to orthonormal (|diag R - 1| test);
+// the plain pass right after a shifted one legitimately is not
+__device__ __forceinline__ bool needs_dev(int mode) {
+  return mode == CH_SECOND || mode == CH_SLAST || mode == CH_S2LAST;
+}
+
+// route state machine of the CholeskyQR family (flags[0], see above)
+__device__ __forceinline__ void route_update(int* flags, int mode, bool bad, double dev) {
+  const bool fail = bad || (needs_dev(mode) && !(dev <= kDevTol));
+  switch (mode) {
+    case CH_FIRST:
+      if (bad) flags[0] = 1;
+      break;
+    case CH_SECOND:
+      if (fail) flags[0] = 1;
+      else flags[8] += 1;
+      break;
+    case CH_SHIFT:
+      if (bad) flags[0] = 3;
+      break;
+    case CH_SPLAIN:
+      if (fail) flags[0] = 2;
+      break;
+    case CH_SLAST:
+      if (fail) flags[0] = 2;
+      else flags[10] += 1;
+      break;
+    case CH_SHIFT1B:
+    case CH_SHIFT2:
+    case CH_S2PLAIN:
+      if (fail) flags[0] = 3;
+      break;
+    case CH_S2LAST:
+      if (fail) flags[0] = 3;
+      else flags[15] += 1;
+      break;
+  }
+}
+
+// G (n x n, ld n, symmetric) -> Rinv (upper, ld n) with G + shift*I = R^T R, and
+// optionally R.  Shift (CH_SHIFT only) = 11(mn + n(n+1))u * trace(G) (shifted
+// CholeskyQR3, Fukaya et al.).  Runs iff *gate == gate_val.
 template <int QN>
 __global__ void __launch_bounds__(kCholThreads)
     chol_inv_kernel(const double* __restrict__ G, int n, int64_t m, int mode,
                     double* __restrict__ Rinv, double* __restrict__ Rout,
-                    double* __restrict__ gwork, int* __restrict__ flags) {
+                    double* __restrict__ gwork, int* __restrict__ flags, const int* gate,
+                    int gate_val) {
+  if (gate && *gate != gate_val) return;
   extern __shared__ double sh[];
   const bool in_smem = (n * n <= kSmemLimitDoubles);
   double* L = in_smem ? sh : gwork;
   __shared__ double s_shift;
-  __shared__ int s_bad;
+  __shared__ int s_bad, s_zero;
   const int tid = threadIdx.x;
-  if (tid == 0) { s_bad = 0; }
+  if (tid == 0) { s_bad = 0; s_zero = 0; }
   // trace for the shift and the zero test
   if (tid < 32) {
     double tr = 0.0;
@@ -99,11 +165,13 @@ __global__ void __launch_bounds__(kCholThreads)
     for (int o = 16; o; o >>= 1) tr += __shfl_xor_sync(0xffffffffu, tr, o);
     if (tid == 0) {
       if (!(tr > 0.0)) {
-        if (tr == 0.0) atomicOr(&flags[2], 1);   // Y_n == 0: zero sum (R16)
+        if (tr == 0.0) { atomicOr(&flags[2], 1); s_zero = 1; }   // Y_n == 0: zero sum (R16)
         s_bad = 1;
       }
       const double u = 0x1p-53;
-      s_shift = (mode == 1) ? 11.0 * (double(m) * n + double(n) * (n + 1)) * u * tr : 0.0;
+      s_shift = ((mode & 0xff) == CH_SHIFT || (mode & 0xff) == CH_SHIFT2 ||
+                     (mode & 0xff) == CH_SHIFT1B)
+                    ? 11.0 * (double(m) * n + double(n) * (n + 1)) * u * tr : 0.0;
     }
   }
   __syncthreads();
@@ -172,19 +240,215 @@ __global__ void __launch_bounds__(kCholThreads)
     }
   }
   __syncthreads();
-  if (tid == 0) {
+  if (tid == 0 && !s_zero && !(flags[2] & 1)) {
     int bad = s_bad;
-    if (mode == 2 && !bad) {
-      double dev = 0.0;
-      for (int i = 0; i < n; ++i) dev = fmax(dev, fabs(L[i + i * n] - 1.0));
-      if (!(dev < 1e-6)) bad = 1;
+    double dev = 0.0, dmin = INFINITY, dmax = 0.0;
+    for (int i = 0; i < n; ++i) {
+      const double d = fabs(L[i + i * n]);
+      dmin = fmin(dmin, d);
+      dmax = fmax(dmax, d);
+      if (needs_dev(mode & 0xff)) dev = fmax(dev, fabs(L[i + i * n] - 1.0));
     }
-    if (bad && !(flags[2] & 1)) atomicOr(&flags[0], 1);
+    if ((mode & kStrict) && !(dmin >= dmax * kStrictRatio)) bad = 1;
+    route_update(flags, mode & 0xff, bad, dev);
   }
 }
 
+// Register-tiled Cholesky + triangular inverse for n <= 32*NA (one CTA of 1024
+// threads).  Thread (warp w, lane t) owns the entries (i, j) = (t + 32x, w + 32y)
+// of the working matrix; only the lower triangle is ever needed, i.e. y <= x
+// (x > y is always below the diagonal, x == y iff t >= w), so a thread keeps
+// NA(NA+1)/2 doubles in registers.  Each elimination step broadcasts one column
+// (Cholesky) or one row (inverse) through shared memory: one __syncthreads and
+// <= NA(NA+1)/2 FMAs per thread per step.  Same contract and flags as
+// chol_inv_kernel.
+template <int NA>
+__global__ void __launch_bounds__(1024, 1)
+    chol_reg_kernel(const double* __restrict__ G, int n, int64_t m, int mode,
+                    double* __restrict__ Rinv, double* __restrict__ Rout,
+                    int* __restrict__ flags, const int* gate, int gate_val) {
+  if (gate && *gate != gate_val) return;
+  extern __shared__ double sh[];                 // (n+1) x n padded, column-major
+  __shared__ double colbuf[2][32 * NA];
+  __shared__ double s_shift;
+  __shared__ int s_bad, s_zero;
+  constexpr int NT = NA * (NA + 1) / 2;
+  const int ldl = n + 1;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  if (tid == 0) { s_bad = 0; s_zero = 0; }
+  if (tid < 32) {
+    double tr = 0.0;
+    for (int i = tid; i < n; i += 32) tr += G[i + int64_t(i) * n];
+    for (int o = 16; o; o >>= 1) tr += __shfl_xor_sync(0xffffffffu, tr, o);
+    if (tid == 0) {
+      if (!(tr > 0.0)) {
+        if (tr == 0.0) { atomicOr(&flags[2], 1); s_zero = 1; }
+        s_bad = 1;
+      }
+      s_shift = ((mode & 0xff) == CH_SHIFT || (mode & 0xff) == CH_SHIFT2 ||
+                     (mode & 0xff) == CH_SHIFT1B)
+                    ? 11.0 * (double(m) * n + double(n) * (n + 1)) * 0x1p-53 * tr : 0.0;
+    }
+  }
+  __syncthreads();
+  const double shift = s_shift;
+  double a[NT];   // a[x(x+1)/2 + y], y <= x
+#pragma unroll
+  for (int x = 0; x < NA; ++x)
+#pragma unroll
+    for (int y = 0; y <= x; ++y) {
+      const int i = lane + 32 * x, j = w + 32 * y;
+      a[x * (x + 1) / 2 + y] =
+          (i < n && j < n && i >= j) ? G[i + int64_t(j) * n] + (i == j ? shift : 0.0) : 0.0;
+    }
+  // ---- right-looking Cholesky: after step k, column k holds L(:, k)
+  if (w == 0) {
+#pragma unroll
+    for (int x = 0; x < NA; ++x) colbuf[0][lane + 32 * x] = a[x * (x + 1) / 2];
+  }
+  __syncthreads();
+  bool bad = false;
+  for (int k = 0; k < n; ++k) {
+    const double* cb = colbuf[k & 1];
+    const double dkk = cb[k];
+    const bool okp = dkk > 0.0 && isfinite(dkk);
+    bad |= !okp;
+    const double dk = okp ? sqrt(dkk) : 1.0;
+    const double dinv = 1.0 / dk;
+    double li[NA];
+#pragma unroll
+    for (int x = 0; x < NA; ++x) {
+      const int i = lane + 32 * x;
+      li[x] = (i > k && i < n) ? cb[i] * dinv : 0.0;
+    }
+    const int yk = k >> 5;
+    if (w == (k & 31)) {   // finalise column k in its owner's registers
+#pragma unroll
+      for (int x = 0; x < NA; ++x)
+#pragma unroll
+        for (int y = 0; y <= x; ++y)
+          if (y == yk) {
+            const int i = lane + 32 * x;
+            a[x * (x + 1) / 2 + y] = (i > k) ? li[x] : (i == k ? dk : 0.0);
+          }
+    }
+    // trailing update A(i, j) -= l_i l_j for i >= j > k (l_j: warp-uniform broadcast)
+#pragma unroll
+    for (int y = 0; y < NA; ++y) {
+      const int j = w + 32 * y;
+      const double lj = (j > k && j < n) ? cb[j] * dinv : 0.0;
+#pragma unroll
+      for (int x = y; x < NA; ++x) a[x * (x + 1) / 2 + y] -= li[x] * lj;
+    }
+    // publish column k+1 (already updated by this step)
+    if (k + 1 < n && w == ((k + 1) & 31)) {
+      const int y1 = (k + 1) >> 5;
+#pragma unroll
+      for (int x = 0; x < NA; ++x)
+#pragma unroll
+        for (int y = 0; y <= x; ++y)
+          if (y == y1) colbuf[(k + 1) & 1][lane + 32 * x] = a[x * (x + 1) / 2 + y];
+    }
+    __syncthreads();
+  }
+  if (bad && lane == 0) s_bad = 1;
+  // L (lower) to shared memory
+#pragma unroll
+  for (int x = 0; x < NA; ++x)
+#pragma unroll
+    for (int y = 0; y < NA; ++y) {
+      const int i = lane + 32 * x, j = w + 32 * y;
+      if (i < n && j < n) sh[i + j * ldl] = (y <= x && i >= j) ? a[x * (x + 1) / 2 + (y <= x ? y : 0)] : 0.0;
+    }
+  __syncthreads();
+  // ---- X = L^{-1} (lower): step k scales row k of X by 1/L_kk and eliminates
+  // it from the rows i > k (all right-hand sides at once)
+#pragma unroll
+  for (int x = 0; x < NA; ++x)
+#pragma unroll
+    for (int y = 0; y <= x; ++y) a[x * (x + 1) / 2 + y] = ((lane + 32 * x) == (w + 32 * y)) ? 1.0 : 0.0;
+  double* rowbuf = &colbuf[0][0];   // reused: [2][32*NA]
+  for (int k = 0; k < n; ++k) {
+    double* rb = rowbuf + (k & 1) * (32 * NA);
+    if (lane == (k & 31)) {
+      const double inv = 1.0 / sh[k + k * ldl];
+      const int xk = k >> 5;
+#pragma unroll
+      for (int x = 0; x < NA; ++x)
+        if (x == xk) {
+#pragma unroll
+          for (int y = 0; y < NA; ++y) {
+            double v = 0.0;
+            if (y <= x) {
+              a[x * (x + 1) / 2 + (y <= x ? y : 0)] *= inv;
+              v = a[x * (x + 1) / 2 + (y <= x ? y : 0)];
+            }
+            rb[w + 32 * y] = v;
+          }
+        }
+    }
+    __syncthreads();
+    double lk[NA];
+#pragma unroll
+    for (int x = 0; x < NA; ++x) {
+      const int i = lane + 32 * x;
+      lk[x] = (i > k && i < n) ? sh[i + k * ldl] : 0.0;
+    }
+#pragma unroll
+    for (int y = 0; y < NA; ++y) {
+      const double xk = rb[w + 32 * y];
+#pragma unroll
+      for (int x = y; x < NA; ++x) a[x * (x + 1) / 2 + y] -= lk[x] * xk;
+    }
+  }
+  __syncthreads();
+  // R = L^T (upper) from shared memory, then X into shared memory for Rinv = X^T
+  if (Rout)
+    for (int e = tid; e < n * n; e += 1024) {
+      const int r = e % n, c = e / n;    // R(r, c) = L(c, r)
+      Rout[e] = (c >= r) ? sh[c + r * ldl] : 0.0;
+    }
+  __syncthreads();
+#pragma unroll
+  for (int x = 0; x < NA; ++x)
+#pragma unroll
+    for (int y = 0; y < NA; ++y) {
+      const int i = lane + 32 * x, j = w + 32 * y;
+      if (i < n && j < n) sh[i + j * ldl] = (y <= x && i >= j) ? a[x * (x + 1) / 2 + (y <= x ? y : 0)] : 0.0;
+    }
+  __syncthreads();
+  for (int e = tid; e < n * n; e += 1024) {
+    const int r = e % n, c = e / n;      // Rinv(r, c) = X(c, r)
+    Rinv[e] = sh[c + r * ldl];
+  }
+  if (tid == 0 && !s_zero && !(flags[2] & 1)) {
+    int bad2 = s_bad;
+    double dev = 0.0, dmin = INFINITY, dmax = 0.0;
+    for (int i = 0; i < n; ++i) {
+      const double d = fabs(1.0 / sh[i + i * ldl]);     // |L_ii|
+      dmin = fmin(dmin, d);
+      dmax = fmax(dmax, d);
+      if (needs_dev(mode & 0xff)) dev = fmax(dev, fabs(1.0 / sh[i + i * ldl] - 1.0));
+    }
+    if ((mode & kStrict) && !(dmin >= dmax * kStrictRatio)) bad2 = 1;
+    route_update(flags, mode & 0xff, bad2, dev);
+  }
+}
+
+__global__ void gated_set_kernel(int* flag, int from, int to) {
+  if (*flag == from) *flag = to;
+}
+
+__global__ void gated_copy_kernel(const double* __restrict__ src, double* __restrict__ dst,
+                                  int64_t n, const int* gate, int gate_val) {
+  if (gate && *gate != gate_val) return;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x)
+    dst[i] = src[i];
+}
+
 // ---------------------------------------------------------- Householder fallback
-// Single CTA; runs only if flags[0] is set (breakdown).  A (m x n) is copied to
+// Single CTA; runs only if every CholeskyQR route broke down (route state 3).  A (m x n) is copied to
 // the workspace, factored in place (LAPACK-style reflectors with v0 = 1), then
 // Q = H_0 ... H_{n-1} [I; 0] is formed by backward accumulation into Q.
 constexpr int kHhThreads = 1024;
@@ -211,7 +475,7 @@ __global__ void __launch_bounds__(kHhThreads)
     householder_kernel(const double* __restrict__ A, int64_t lda, bool trans, int64_t m, int n,
                        double* __restrict__ W, double* __restrict__ tau,
                        double* __restrict__ Q, double* __restrict__ R, int* flags) {
-  if (!(flags[0] & 1)) return;
+  if (flags[0] != 3) return;
   __shared__ double red[32];
   __shared__ double s_beta, s_tau;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -294,11 +558,219 @@ __global__ void __launch_bounds__(kHhThreads)
   }
   if (tid == 0) {
     atomicOr(&flags[1], 1);
-    flags[0] = 0;
+    flags[11] += 1;            // route counter: Householder
   }
 }
 
 }  // namespace
+
+// ---------------------------------------------------------- TSQR (R only)
+// Rank-deficiency-proof R factor of a tall m x n (n <= 160) matrix op(A): the
+// fallback of the R-only QR when both CholeskyQR routes fail (numerically rank-
+// deficient bond matrices of the truncation).  Householder on
+// row blocks (one CTA per block, block in shared memory), then a binary tree of
+// merges of two upper triangles [R1; R2] (packed, both in shared memory).
+// Packed upper triangle: element (r, c), r <= c, at c(c+1)/2 + r.
+__device__ __forceinline__ int pk(int r, int c) { return c * (c + 1) / 2 + r; }
+
+__global__ void __launch_bounds__(1024, 1)
+    tsqr_leaf_kernel(const double* __restrict__ A, int64_t lda, bool trans, int64_t m, int n,
+                     int br, double* __restrict__ Rp, const int* gate, int gate_val) {
+  if (gate && *gate != gate_val) return;
+  extern __shared__ double B[];        // rows x n, ld br
+  __shared__ double red[32];
+  __shared__ double s_tau;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t r0 = int64_t(blockIdx.x) * br;
+  const int rows = int((m - r0) < br ? (m - r0) : int64_t(br));
+  for (int e = tid; e < rows * n; e += 1024) {
+    int i, j;
+    if (trans) { j = e % n; i = e / n; } else { i = e % rows; j = e / rows; }
+    const int64_t gi = r0 + i;
+    B[i + j * br] = trans ? A[j + gi * lda] : A[gi + int64_t(j) * lda];
+  }
+  __syncthreads();
+  const int steps = min(rows, n);
+  for (int j = 0; j < steps; ++j) {
+    if (warp == 0) {
+      double ss = 0.0;
+      for (int i = j + 1 + lane; i < rows; i += 32) ss += B[i + j * br] * B[i + j * br];
+      for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+      const double alpha = B[j + j * br];
+      double tau = 0.0, beta = alpha, scal = 0.0;
+      if (ss > 0.0) {
+        const double nrm = sqrt(alpha * alpha + ss);
+        beta = (alpha >= 0.0) ? -nrm : nrm;
+        tau = (beta - alpha) / beta;
+        scal = 1.0 / (alpha - beta);
+      }
+      __syncwarp();
+      if (ss > 0.0)
+        for (int i = j + 1 + lane; i < rows; i += 32) B[i + j * br] *= scal;
+      if (lane == 0) {
+        s_tau = tau;
+        red[0] = beta;
+      }
+    }
+    __syncthreads();
+    const double tau = s_tau;
+    if (tau != 0.0) {
+      for (int k = j + 1 + warp; k < n; k += 32) {
+        double wsum = (lane == 0) ? B[j + k * br] : 0.0;
+        for (int i = j + 1 + lane; i < rows; i += 32) wsum += B[i + j * br] * B[i + k * br];
+        for (int o = 16; o; o >>= 1) wsum += __shfl_xor_sync(0xffffffffu, wsum, o);
+        wsum *= tau;
+        if (lane == 0) B[j + k * br] -= wsum;
+        for (int i = j + 1 + lane; i < rows; i += 32) B[i + k * br] -= wsum * B[i + j * br];
+      }
+    }
+    if (tid == 0) B[j + j * br] = red[0];
+    __syncthreads();
+  }
+  double* out = Rp + int64_t(blockIdx.x) * (int64_t(n) * (n + 1) / 2);
+  for (int c = warp; c < n; c += 32)
+    for (int r = lane; r <= c; r += 32) out[pk(r, c)] = (r < rows) ? B[r + c * br] : 0.0;
+}
+
+// out[q] = R of [in[2q]; in[2q+1]] (both n x n upper triangles, packed)
+__global__ void __launch_bounds__(1024, 1)
+    tsqr_merge_kernel(const double* __restrict__ in, int count, int n, double* __restrict__ out,
+                      const int* gate, int gate_val) {
+  if (gate && *gate != gate_val) return;
+  extern __shared__ double T[];        // two packed triangles
+  __shared__ double s_tau, s_beta;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t tri = int64_t(n) * (n + 1) / 2;
+  const int q = blockIdx.x;
+  double* T1 = T;
+  double* T2 = T + tri;
+  double* o = out + q * tri;
+  if (2 * q + 1 >= count) {              // odd one out: copy through
+    for (int64_t e = tid; e < tri; e += 1024) o[e] = in[(2 * q) * tri + e];
+    return;
+  }
+  for (int64_t e = tid; e < 2 * tri; e += 1024) T[e] = in[(2 * q) * tri + e];
+  __syncthreads();
+  for (int j = 0; j < n; ++j) {
+    // reflector on x = (T1(j,j), T2(0..j, j))
+    if (warp == 0) {
+      double ss = 0.0;
+      for (int r = lane; r <= j; r += 32) ss += T2[pk(r, j)] * T2[pk(r, j)];
+      for (int o2 = 16; o2; o2 >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o2);
+      const double alpha = T1[pk(j, j)];
+      double tau = 0.0, beta = alpha, scal = 0.0;
+      if (ss > 0.0) {
+        const double nrm = sqrt(alpha * alpha + ss);
+        beta = (alpha >= 0.0) ? -nrm : nrm;
+        tau = (beta - alpha) / beta;
+        scal = 1.0 / (alpha - beta);
+      }
+      __syncwarp();
+      if (ss > 0.0)
+        for (int r = lane; r <= j; r += 32) T2[pk(r, j)] *= scal;   // v (below the unit head)
+      if (lane == 0) { s_tau = tau; s_beta = beta; }
+    }
+    __syncthreads();
+    const double tau = s_tau;
+    if (tau != 0.0) {
+      for (int k = j + 1 + warp; k < n; k += 32) {
+        double wsum = (lane == 0) ? T1[pk(j, k)] : 0.0;
+        for (int r = lane; r <= j; r += 32) wsum += T2[pk(r, j)] * T2[pk(r, k)];
+        for (int o2 = 16; o2; o2 >>= 1) wsum += __shfl_xor_sync(0xffffffffu, wsum, o2);
+        wsum *= tau;
+        if (lane == 0) T1[pk(j, k)] -= wsum;
+        for (int r = lane; r <= j; r += 32) T2[pk(r, k)] -= wsum * T2[pk(r, j)];
+      }
+    }
+    __syncthreads();
+    if (tid == 0) T1[pk(j, j)] = s_beta;
+  }
+  __syncthreads();
+  for (int64_t e = tid; e < tri; e += 1024) o[e] = T1[e];
+}
+
+__global__ void unpack_upper_kernel(const double* __restrict__ P, int n, double* __restrict__ R,
+                                    const int* gate, int gate_val, int* flags) {
+  if (gate && *gate != gate_val) return;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n * n; e += gridDim.x * blockDim.x) {
+    const int r = e % n, c = e / n;
+    R[e] = (r <= c) ? P[pk(r, c)] : 0.0;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) flags[14] += 1;   // route counter: TSQR
+}
+
+// R (n x n, ld n) of op(A) by TSQR; gated like the other QR launches.
+static int tsqr_r(Ctx& c, int64_t m, int n, const double* A, int64_t lda, bool trans,
+                  double* R, const int* gate, int gv, cudaStream_t s) {
+  const int br = std::max(n, std::min<int>(int(m), kSmemLimitDoubles / n));
+  const int64_t P = (m + br - 1) / br;
+  const int64_t tri = int64_t(n) * (n + 1) / 2;
+  DBuf W0, W1;
+  TTR_TRY(dalloc(W0, size_t(P * tri), s));
+  TTR_TRY(dalloc(W1, size_t((P + 1) / 2 * tri), s));
+  static bool attr = false;
+  if (!attr) {
+    TTR_CUDA(cudaFuncSetAttribute(tsqr_leaf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  kSmemLimitDoubles * 8));
+    TTR_CUDA(cudaFuncSetAttribute(tsqr_merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  kSmemLimitDoubles * 8));
+    attr = true;
+  }
+  tsqr_leaf_kernel<<<unsigned(P), 1024, size_t(br) * n * 8, s>>>(A, lda, trans, m, n, br, W0.p,
+                                                                  gate, gv);
+  TTR_TRY(launched());
+  double* cur = W0.p;
+  double* nxt = W1.p;
+  int64_t cnt = P;
+  while (cnt > 1) {
+    const int64_t half = (cnt + 1) / 2;
+    tsqr_merge_kernel<<<unsigned(half), 1024, size_t(2 * tri) * 8, s>>>(cur, int(cnt), n, nxt,
+                                                                         gate, gv);
+    TTR_TRY(launched());
+    std::swap(cur, nxt);
+    cnt = half;
+  }
+  unpack_upper_kernel<<<std::max(1, (n * n + 255) / 256), 256, 0, s>>>(cur, n, R, gate, gv,
+                                                                      c.flags.p);
+  return launched();
+}
+
+bool tsqr_fits(int n) { return n >= 1 && 2 * (int64_t(n) * (n + 1) / 2) <= kSmemLimitDoubles; }
+
+// Launch one Cholesky(+inverse) of the n x n Gram Gm (see chol_reg_kernel).
+static int launch_chol(Ctx& c, const double* Gm, int n, int64_t m, int mode, double* Rinv,
+                       double* Rk, double* gw, const int* gate, int gv, cudaStream_t s) {
+  static bool attr_done = false;
+  if (!attr_done) {
+    TTR_CUDA(cudaFuncSetAttribute(chol_inv_kernel<32>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  kSmemLimitDoubles * 8));
+    TTR_CUDA(cudaFuncSetAttribute(chol_reg_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  200 * 1024));
+    TTR_CUDA(cudaFuncSetAttribute(chol_reg_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  200 * 1024));
+    TTR_CUDA(cudaFuncSetAttribute(chol_reg_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  200 * 1024));
+    TTR_CUDA(cudaFuncSetAttribute(chol_reg_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  220 * 1024));
+    attr_done = true;
+  }
+  const size_t shm = size_t(n + 1) * n * sizeof(double);
+  if (n <= 32) {
+    chol_reg_kernel<1><<<1, 1024, shm, s>>>(Gm, n, m, mode, Rinv, Rk, c.flags.p, gate, gv);
+  } else if (n <= 64) {
+    chol_reg_kernel<2><<<1, 1024, shm, s>>>(Gm, n, m, mode, Rinv, Rk, c.flags.p, gate, gv);
+  } else if (n <= 96) {
+    chol_reg_kernel<3><<<1, 1024, shm, s>>>(Gm, n, m, mode, Rinv, Rk, c.flags.p, gate, gv);
+  } else if (n <= 160) {
+    chol_reg_kernel<5><<<1, 1024, shm, s>>>(Gm, n, m, mode, Rinv, Rk, c.flags.p, gate, gv);
+  } else {
+    const bool big = n * n > kSmemLimitDoubles;
+    chol_inv_kernel<32><<<1, kCholThreads, big ? 0 : size_t(n) * n * 8, s>>>(
+        Gm, n, m, mode, Rinv, Rk, gw, c.flags.p, gate, gv);
+  }
+  return launched();
+}
 
 int qr(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, bool trans, double* Q,
        double* R, cudaStream_t s) {
@@ -310,74 +782,150 @@ int qr(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, bool trans, d
     set_error("qr: n = %lld > 1024 unsupported", (long long)n);
     return TT_ERR_ARG;
   }
-  const int ni = int(n);
+  if (!Q && !R) {
+    set_error("qr: nothing to compute");
+    return TT_ERR_ARG;
+  }
+  const int ni = int(n), mi = int(m);
+  const bool r_only = (Q == nullptr);
   DBuf T1, T2, Gm, Rinv, Rk, Racc, Rtmp, gw;
   TTR_TRY(dalloc(T1, size_t(m) * n, s));
   TTR_TRY(dalloc(T2, size_t(m) * n, s));
   TTR_TRY(dalloc(Gm, size_t(n) * n, s));
   TTR_TRY(dalloc(Rinv, size_t(n) * n, s));
-  const bool big = ni * ni > kSmemLimitDoubles;
-  if (big) TTR_TRY(dalloc(gw, size_t(n) * n, s));
+  if (ni > 160 && ni * ni > kSmemLimitDoubles) TTR_TRY(dalloc(gw, size_t(n) * n, s));
   if (R) {
     TTR_TRY(dalloc(Rk, size_t(n) * n, s));
     TTR_TRY(dalloc(Racc, size_t(n) * n, s));
     TTR_TRY(dalloc(Rtmp, size_t(n) * n, s));
   }
-  TTR_CUDA(cudaMemsetAsync(c.flags.p, 0, sizeof(int), s));  // flags[0]: this QR's breakdown
-  const size_t shm = big ? 0 : size_t(ni) * ni * sizeof(double);
-  static bool attr = false;
-  if (!attr) {
-    TTR_CUDA(cudaFuncSetAttribute(chol_inv_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  kSmemLimitDoubles * 8));
-    TTR_CUDA(cudaFuncSetAttribute(chol_inv_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  kSmemLimitDoubles * 8));
-    attr = true;
-  }
-  auto chol = ni <= 160 ? chol_inv_kernel<5> : chol_inv_kernel<32>;
-  const int mi = int(m);
-  const double* src = A;
-  double* bufs[3] = {T1.p, T2.p, Q};
-  for (int pass = 0; pass < 3; ++pass) {
-    // Gram G = op(src)^T op(src)
-    if (pass == 0 && trans) {
-      TTR_TRY(gemm1(c, false, true, ni, ni, mi, 1.0, src, int(lda), src, int(lda), 0.0, Gm.p,
-                    ni, s));
-    } else {
-      const int ld = pass == 0 ? int(lda) : mi;
-      TTR_TRY(gemm1(c, true, false, ni, ni, mi, 1.0, src, ld, src, ld, 0.0, Gm.p, ni, s));
-    }
-    chol<<<1, kCholThreads, shm, s>>>(Gm.p, ni, m, pass == 0 ? 1 : (pass == 2 ? 2 : 0),
-                                                 Rinv.p, R ? Rk.p : nullptr, gw.p, c.flags.p);
+  int* F = c.flags.p;
+  TTR_CUDA(cudaMemsetAsync(F, 0, sizeof(int), s));          // route state 0
+  const int copy_blocks = int(std::min<int64_t>((int64_t(m) * n + 255) / 256, c.sm_count * 8));
+  double* Rk_p = R ? Rk.p : nullptr;
+
+  // Gram of the input op(A) (A is m x n, or n x m when trans)
+  auto gram_of_input = [&](const int* gate, int gv) -> int {
+    if (trans)
+      return gemm1(c, false, true, ni, ni, mi, 1.0, A, int(lda), A, int(lda), 0.0, Gm.p, ni, s,
+                   gate, gv);
+    return gemm1(c, true, false, ni, ni, mi, 1.0, A, int(lda), A, int(lda), 0.0, Gm.p, ni, s,
+                 gate, gv);
+  };
+  auto input_times_rinv = [&](double* dst, const int* gate, int gv) -> int {
+    if (trans)
+      return gemm1(c, true, false, mi, ni, ni, 1.0, A, int(lda), Rinv.p, ni, 0.0, dst, mi, s,
+                   gate, gv);
+    return gemm1(c, false, false, mi, ni, ni, 1.0, A, int(lda), Rinv.p, ni, 0.0, dst, mi, s,
+                 gate, gv);
+  };
+  auto gram = [&](const double* src, const int* gate, int gv) -> int {
+    return gemm1(c, true, false, ni, ni, mi, 1.0, src, mi, src, mi, 0.0, Gm.p, ni, s, gate, gv);
+  };
+  auto times_rinv = [&](const double* src, double* dst, const int* gate, int gv) -> int {
+    return gemm1(c, false, false, mi, ni, ni, 1.0, src, mi, Rinv.p, ni, 0.0, dst, mi, s, gate,
+                 gv);
+  };
+  static const bool dbg = getenv("TTR_QR_DEBUG") != nullptr;
+  auto dump = [&](const char* what, const double* p, int64_t cnt) {
+    if (!dbg) return;
+    cudaStreamSynchronize(s);
+    std::vector<double> h(cnt);
+    cudaMemcpy(h.data(), p, cnt * 8, cudaMemcpyDeviceToHost);
+    int f[16];
+    cudaMemcpy(f, F, sizeof f, cudaMemcpyDeviceToHost);
+    double ss = 0;
+    for (double v : h) ss += v * v;
+    fprintf(stderr, "[qr %lldx%d] %s: norm %.6e  [0]=%.6e  route=%d\n", (long long)m, ni, what,
+            sqrt(ss), h[0], f[0]);
+  };
+  auto chol = [&](int mode, const int* gate, int gv) -> int {
+    dump("gram", Gm.p, int64_t(ni) * ni);
+    int r = launch_chol(c, Gm.p, ni, m, mode, Rinv.p, Rk_p, gw.p, gate, gv, s);
+    if (Rk_p) dump("Rk", Rk_p, int64_t(ni) * ni);
+    return r;
+  };
+  // Racc <- Rk Racc (gated)
+  auto accumulate_r = [&](const int* gate, int gv) -> int {
+    if (!R) return TT_OK;
+    TTR_TRY(gemm1(c, false, false, ni, ni, ni, 1.0, Rk.p, ni, Racc.p, ni, 0.0, Rtmp.p, ni, s,
+                  gate, gv));
+    gated_copy_kernel<<<std::max(1, (ni * ni + 255) / 256), 256, 0, s>>>(Rtmp.p, Racc.p,
+                                                                       int64_t(ni) * ni, gate, gv);
+    return launched();
+  };
+  auto copy_r_first = [&](const int* gate, int gv) -> int {
+    if (!R) return TT_OK;
+    gated_copy_kernel<<<std::max(1, (ni * ni + 255) / 256), 256, 0, s>>>(Rk.p, Racc.p,
+                                                                       int64_t(ni) * ni, gate, gv);
+    return launched();
+  };
+  auto gated_copy = [&](const double* src, double* dst, const int* gate, int gv) -> int {
+    gated_copy_kernel<<<copy_blocks, 256, 0, s>>>(src, dst, int64_t(m) * n, gate, gv);
+    return launched();
+  };
+
+  // ---- route 0: CholeskyQR2, accepted when pass 2 finds Q1 close to
+  // orthonormal (|diag R2 - 1| <= kDevTol).  The route state F[0] lives on the
+  // device; every launch of an inactive route is a no-op.
+  TTR_TRY(gram_of_input(nullptr, 0));                       // pass 1 on the input
+  TTR_TRY(chol(CH_FIRST, nullptr, 0));
+  TTR_TRY(copy_r_first(F, 0));
+  TTR_TRY(input_times_rinv(T1.p, F, 0));                    // Q1 -> T1
+  TTR_TRY(gram(T1.p, F, 0));                                // pass 2
+  TTR_TRY(chol(CH_SECOND, F, 0));
+  TTR_TRY(accumulate_r(F, 0));
+  if (!r_only) TTR_TRY(times_rinv(T1.p, Q, F, 0));        // Q = Q1 R2^{-1}
+  // ---- route 1: shifted CholeskyQR3 (kappa up to ~1e10)
+  TTR_TRY(gram_of_input(F, 1));
+  TTR_TRY(chol(CH_SHIFT, F, 1));
+  TTR_TRY(copy_r_first(F, 1));
+  TTR_TRY(input_times_rinv(T1.p, F, 1));                    // Q1 (shifted) -> T1
+  TTR_TRY(gram(T1.p, F, 1));
+  TTR_TRY(chol(CH_SPLAIN | (r_only ? kStrict : 0), F, 1));  // -> route 2 if Q1 is still too ill-conditioned
+  TTR_TRY(accumulate_r(F, 1));
+  TTR_TRY(times_rinv(T1.p, T2.p, F, 1));
+  TTR_TRY(gram(T2.p, F, 1));
+  TTR_TRY(chol(CH_SLAST, F, 1));
+  TTR_TRY(accumulate_r(F, 1));
+  if (!r_only) TTR_TRY(times_rinv(T2.p, Q, F, 1));
+  // ---- route 2: shifted pass on the input, a second shifted pass on its Q1
+  // (kappa up to ~1/u), then CholeskyQR2.  Skipped for R-only QRs, whose hard
+  // cases are exactly rank-deficient (TSQR).
+  if (!r_only) {
+    TTR_TRY(gram_of_input(F, 2));
+    TTR_TRY(chol(CH_SHIFT1B, F, 2));
+    TTR_TRY(copy_r_first(F, 2));
+    TTR_TRY(input_times_rinv(T1.p, F, 2));
+    TTR_TRY(gram(T1.p, F, 2));
+    TTR_TRY(chol(CH_SHIFT2, F, 2));
+    TTR_TRY(accumulate_r(F, 2));
+    TTR_TRY(times_rinv(T1.p, T2.p, F, 2));
+    TTR_TRY(gram(T2.p, F, 2));
+    TTR_TRY(chol(CH_S2PLAIN, F, 2));
+    TTR_TRY(accumulate_r(F, 2));
+    TTR_TRY(times_rinv(T2.p, T1.p, F, 2));
+    TTR_TRY(gram(T1.p, F, 2));
+    TTR_TRY(chol(CH_S2LAST, F, 2));
+    TTR_TRY(accumulate_r(F, 2));
+    TTR_TRY(times_rinv(T1.p, Q, F, 2));
+  } else {
+    gated_set_kernel<<<1, 1, 0, s>>>(F, 2, 3);              // route 2 -> 3 (TSQR)
     TTR_TRY(launched());
-    // Q_{pass} = op(src) * Rinv
-    if (pass == 0 && trans) {
-      TTR_TRY(gemm1(c, true, false, mi, ni, ni, 1.0, src, int(lda), Rinv.p, ni, 0.0, bufs[pass],
-                    mi, s));
-    } else {
-      const int ld = pass == 0 ? int(lda) : mi;
-      TTR_TRY(gemm1(c, false, false, mi, ni, ni, 1.0, src, ld, Rinv.p, ni, 0.0, bufs[pass], mi,
-                    s));
-    }
-    if (R) {
-      if (pass == 0) {
-        TTR_CUDA(cudaMemcpyAsync(Racc.p, Rk.p, sizeof(double) * n * n, cudaMemcpyDeviceToDevice,
-                                 s));
-      } else {
-        // Racc = Rk * Racc
-        TTR_TRY(gemm1(c, false, false, ni, ni, ni, 1.0, Rk.p, ni, Racc.p, ni, 0.0, Rtmp.p, ni, s));
-        std::swap(Racc, Rtmp);
-      }
-    }
-    src = bufs[pass];
   }
-  if (R) {
+  if (R)
     TTR_CUDA(cudaMemcpyAsync(R, Racc.p, sizeof(double) * n * n, cudaMemcpyDeviceToDevice, s));
+  // ---- route 3 (all CholeskyQR variants failed): R-only QRs of a numerically
+  // rank-deficient matrix go to the Householder TSQR; otherwise Householder
+  if (r_only && tsqr_fits(ni)) {
+    TTR_TRY(tsqr_r(c, m, ni, A, lda, trans, R, F, 3, s));
+    return TT_OK;
   }
-  // fallback (no-op unless flags[0] is set)
   DBuf hw, htau;
   TTR_TRY(dalloc(hw, size_t(m) * n, s));
   TTR_TRY(dalloc(htau, size_t(n), s));
-  householder_kernel<<<1, kHhThreads, 0, s>>>(A, lda, trans, m, ni, hw.p, htau.p, Q, R, c.flags.p);
+  householder_kernel<<<1, kHhThreads, 0, s>>>(A, lda, trans, m, ni, hw.p, htau.p,
+                                              r_only ? T1.p : Q, R, F);
   TTR_TRY(launched());
   return TT_OK;
 }
@@ -402,23 +950,25 @@ __global__ void __launch_bounds__(kJacThreads)
   double* W = (w_in_smem || wonly_smem) ? sh : Wg;
   double* V = w_in_smem ? sh + m * n : Vg;
   const int np = (n + 1) & ~1;          // even count (a dummy column when n is odd)
-  __shared__ int perm[1026];
   __shared__ int s_rot;
   for (int e = tid; e < m * n; e += kJacThreads) {
     const int i = e % m, j = e / m;
     W[e] = A[i + int64_t(j) * lda];
   }
   for (int e = tid; e < n * n; e += kJacThreads) V[e] = ((e % n) == (e / n)) ? 1.0 : 0.0;
-  for (int e = tid; e < np; e += kJacThreads) perm[e] = e;
   __syncthreads();
-  const double tol = 1e-15;
+  // convergence: all column pairs orthogonal to working precision (m eps; the
+  // computed cosine carries ~sqrt(m) eps of rounding noise, so a tighter bar
+  // would never be met)
+  const double tol = double(m) * 0x1p-52;
   for (int sweep = 0; sweep < max_sweeps; ++sweep) {
     if (tid == 0) s_rot = 0;
     __syncthreads();
     int rotated = 0;
     for (int round = 0; round < np - 1; ++round) {
       for (int pi = warp; pi < np / 2; pi += nw) {
-        int p = perm[pi], q = perm[np - 1 - pi];
+        int p = (pi == 0) ? 0 : ((pi - 1 + round) % (np - 1)) + 1;
+        int q = ((np - 2 - pi + round) % (np - 1)) + 1;
         if (p >= n || q >= n) continue;
         if (p > q) { const int t = p; p = q; q = t; }
         double* ap = W + int64_t(p) * m;
@@ -452,13 +1002,6 @@ __global__ void __launch_bounds__(kJacThreads)
         rotated = 1;
       }
       __syncthreads();
-      // rotate the tournament: keep perm[0], shift the rest
-      if (tid == 0) {
-        const int last = perm[np - 1];
-        for (int k = np - 1; k > 1; --k) perm[k] = perm[k - 1];
-        perm[1] = last;
-      }
-      __syncthreads();
     }
     if (rotated) atomicOr(&s_rot, 1);
     __syncthreads();
@@ -486,6 +1029,119 @@ __global__ void __launch_bounds__(kJacThreads)
     for (int i = lane; i < m; i += 32) AV[i + int64_t(rank) * m] = W[i + int64_t(j) * m];
     for (int i = lane; i < n; i += 32) Vout[i + int64_t(rank) * n] = V[i + int64_t(j) * n];
     if (lane == 0) sigma[rank] = sj;
+  }
+}
+
+// One-sided (Hestenes) Jacobi without accumulating V, for the truncation step
+// (R3): W = A (m x n, m <= 32*MT) lives in shared memory; each round of the
+// round-robin ("circle") ordering pairs all columns disjointly, one warp per
+// pair with the pair's two columns in registers; the pairing is arithmetic
+// (position 0 fixed, the others rotate by one per round).  Output: AV = U Sigma
+// (m x n, columns sorted by descending norm) and sigma.  V is not formed: the
+// truncation forms V_k^T Q^T as Sigma_k^{-2} (U Sigma)_k^T H(X_n), which needs only
+// R of the QR.
+template <int MT>
+__global__ void __launch_bounds__(1024, 1)
+    jacobi_nov_kernel(const double* __restrict__ A, int64_t lda, int m, int n,
+                      double* __restrict__ AV, double* __restrict__ sigma, int max_sweeps,
+                      int* flags) {
+  extern __shared__ double W[];   // m x n, ld m
+  __shared__ double nrm[1024];
+  __shared__ int s_rot;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  constexpr int NW = 32;
+  for (int e = tid; e < m * n; e += 1024) {
+    const int i = e % m, j = e / m;
+    W[e] = A[i + int64_t(j) * lda];
+  }
+  const int np = (n + 1) & ~1;
+  const int half = np / 2;
+  const double tol = double(m) * 0x1p-52;
+  __syncthreads();
+  int sweep = 0;
+  for (; sweep < max_sweeps; ++sweep) {
+    if (tid == 0) s_rot = 0;
+    int rotated = 0;
+    for (int r = 0; r < np - 1; ++r) {
+      __syncthreads();
+      for (int ps = warp; ps < half; ps += NW) {
+        int p = (ps == 0) ? 0 : ((ps - 1 + r) % (np - 1)) + 1;
+        int q = ((np - 2 - ps + r) % (np - 1)) + 1;
+        if (p >= n || q >= n) continue;
+        if (p > q) { const int t = p; p = q; q = t; }
+        double* wp = W + p * m;
+        double* wq = W + q * m;
+        double x[MT], y[MT];
+        double al = 0.0, be = 0.0, ga = 0.0;
+#pragma unroll
+        for (int t = 0; t < MT; ++t) {
+          const int i = lane + 32 * t;
+          x[t] = (i < m) ? wp[i] : 0.0;
+          y[t] = (i < m) ? wq[i] : 0.0;
+          al = fma(x[t], x[t], al);
+          be = fma(y[t], y[t], be);
+          ga = fma(x[t], y[t], ga);
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+          al += __shfl_xor_sync(0xffffffffu, al, o);
+          be += __shfl_xor_sync(0xffffffffu, be, o);
+          ga += __shfl_xor_sync(0xffffffffu, ga, o);
+        }
+        if (al == 0.0 || be == 0.0 || !(fabs(ga) > tol * sqrt(al) * sqrt(be))) continue;
+        const double zeta = (be - al) / (2.0 * ga);
+        const double tt = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+        const double cs = 1.0 / sqrt(1.0 + tt * tt), sn = cs * tt;
+#pragma unroll
+        for (int t = 0; t < MT; ++t) {
+          const int i = lane + 32 * t;
+          if (i < m) {
+            wp[i] = cs * x[t] - sn * y[t];
+            wq[i] = sn * x[t] + cs * y[t];
+          }
+        }
+        rotated = 1;
+      }
+    }
+    if (rotated) atomicOr(&s_rot, 1);
+    __syncthreads();
+    if (!s_rot) break;
+  }
+  if (tid == 0) {
+    if (sweep == max_sweeps) atomicOr(&flags[3], 2);
+    flags[12] += sweep + 1;    // Jacobi sweeps (counter)
+    flags[13] += 1;            // Jacobi calls (counter)
+  }
+  for (int j = warp; j < n; j += NW) {
+    double s2 = 0.0;
+    for (int i = lane; i < m; i += 32) s2 = fma(W[i + j * m], W[i + j * m], s2);
+    for (int o = 16; o; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+    if (lane == 0) nrm[j] = sqrt(s2);
+  }
+  __syncthreads();
+  for (int j = warp; j < n; j += NW) {
+    const double sj = nrm[j];
+    int rank = 0;
+    for (int k = lane; k < n; k += 32) {
+      const double sk = nrm[k];
+      rank += (sk > sj) || (sk == sj && k < j);
+    }
+    for (int o = 16; o; o >>= 1) rank += __shfl_xor_sync(0xffffffffu, rank, o);
+    for (int i = lane; i < m; i += 32) AV[i + int64_t(rank) * m] = W[i + j * m];
+    if (lane == 0) sigma[rank] = sj;
+  }
+}
+
+// B(:, c) = AV(:, c) / sigma_c^2 for c < k (0 when sigma_c is negligible), so that
+// B^T H(X_n) = V_k^T Q^T (see svd_nov).
+__global__ void scale_by_inv_sigma2_kernel(const double* __restrict__ AV, int m, int k,
+                                           const double* __restrict__ sigma,
+                                           double* __restrict__ B) {
+  const double s0 = sigma[0];
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < m * k; e += gridDim.x * blockDim.x) {
+    const int c = e / m;
+    const double sc = sigma[c];
+    B[e] = (sc > s0 * double(m) * 0x1p-52) ? AV[e] / (sc * sc) : 0.0;
   }
 }
 
@@ -565,6 +1221,49 @@ int svd_jacobi(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, doubl
   }
   jacobi_kernel<<<1, kJacThreads, shm, s>>>(A, lda, int(m), int(n), Wg.p, Vg.p, AV, V, sigma, 40,
                                            c.flags.p);
+  return launched();
+}
+
+int svd_nov(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, double* AV,
+            double* sigma, cudaStream_t s) {
+  if (m < n || n < 1 || m > 256 || m * n > kSmemLimitDoubles) {
+    set_error("svd_nov: unsupported shape m=%lld n=%lld", (long long)m, (long long)n);
+    return TT_ERR_ARG;
+  }
+  static bool attr = false;
+  if (!attr) {
+    TTR_CUDA(cudaFuncSetAttribute(jacobi_nov_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  kSmemLimitDoubles * 8));
+    TTR_CUDA(cudaFuncSetAttribute(jacobi_nov_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  kSmemLimitDoubles * 8));
+    TTR_CUDA(cudaFuncSetAttribute(jacobi_nov_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  kSmemLimitDoubles * 8));
+    TTR_CUDA(cudaFuncSetAttribute(jacobi_nov_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  kSmemLimitDoubles * 8));
+    TTR_CUDA(cudaFuncSetAttribute(jacobi_nov_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  kSmemLimitDoubles * 8));
+    attr = true;
+  }
+  const size_t shm = size_t(m) * n * 8;
+  if (m <= 32)
+    jacobi_nov_kernel<1><<<1, 1024, shm, s>>>(A, lda, int(m), int(n), AV, sigma, 40, c.flags.p);
+  else if (m <= 64)
+    jacobi_nov_kernel<2><<<1, 1024, shm, s>>>(A, lda, int(m), int(n), AV, sigma, 40, c.flags.p);
+  else if (m <= 96)
+    jacobi_nov_kernel<3><<<1, 1024, shm, s>>>(A, lda, int(m), int(n), AV, sigma, 40, c.flags.p);
+  else if (m <= 160)
+    jacobi_nov_kernel<5><<<1, 1024, shm, s>>>(A, lda, int(m), int(n), AV, sigma, 40, c.flags.p);
+  else
+    jacobi_nov_kernel<8><<<1, 1024, shm, s>>>(A, lda, int(m), int(n), AV, sigma, 40, c.flags.p);
+  return launched();
+}
+
+bool svd_nov_fits(int64_t m, int64_t n) { return m >= n && m <= 256 && m * n <= kSmemLimitDoubles; }
+
+int scale_by_inv_sigma2(Ctx& c, const double* AV, int64_t m, int64_t k, const double* sigma,
+                        double* B, cudaStream_t s) {
+  const int blocks = int(std::min<int64_t>((m * k + 255) / 256, c.sm_count * 4));
+  scale_by_inv_sigma2_kernel<<<std::max(1, blocks), 256, 0, s>>>(AV, int(m), int(k), sigma, B);
   return launched();
 }
 

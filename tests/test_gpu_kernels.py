@@ -77,7 +77,10 @@ def test_sketch_large_count_and_odd_tail(ctx):
 
 
 @pytest.mark.parametrize("m,n,cond", [(40, 7, 1e2), (2240, 35, 1e8), (7000, 70, 1e6),
-                                      (36864, 144, 1e4), (500, 1, 1.0), (100, 100, 10.0)])
+                                      (36864, 144, 1e4), (500, 1, 1.0), (100, 100, 10.0),
+                                      (1000, 32, 10.0), (1000, 33, 1e3), (3000, 96, 1e5),
+                                      (3000, 97, 1e2), (5000, 160, 1e6), (5000, 161, 1e3),
+                                      (6000, 250, 1e4)])
 def test_qr_orthogonality_and_factorization(ctx, m, n, cond):
     rng = np.random.default_rng(m + n)
     U, _ = np.linalg.qr(rng.standard_normal((m, n)))
@@ -94,6 +97,43 @@ def test_qr_orthogonality_and_factorization(ctx, m, n, cond):
     # same projector as LAPACK Householder (the oracle's thin_qr)
     Qo, _ = np.linalg.qr(A)
     assert np.linalg.norm(Qh @ (Qh.T @ A) - Qo @ (Qo.T @ A)) < 1e-13 * np.linalg.norm(A)
+
+
+@pytest.mark.parametrize("m,n,cond", [(36864, 144, 1e10), (10240, 80, 1e12), (2240, 35, 1e8),
+                                      (36864, 144, 1e13), (20000, 100, 1e14)])
+def test_qr_ill_conditioned_stays_on_cholesky_routes(ctx, m, n, cond):
+    """kappa up to ~1/u must be handled by CholeskyQR2/3 or shifted CholeskyQR3
+    (DMMA, all SMs), never by the single-CTA Householder fallback."""
+    g = torch.Generator(device="cuda").manual_seed(m + n)
+    U, _ = torch.linalg.qr(torch.randn(m, n, dtype=torch.float64, device="cuda", generator=g))
+    V, _ = torch.linalg.qr(torch.randn(n, n, dtype=torch.float64, device="cuda", generator=g))
+    s = torch.logspace(0, -math.log10(cond), n, dtype=torch.float64, device="cuda")
+    A = ((U * s) @ V.T).t().contiguous().t()
+    Q, R, fb = ctx.tt_qr(A, want_r=True)
+    assert not fb
+    eye = torch.eye(n, dtype=torch.float64, device="cuda")
+    assert (Q.T @ Q - eye).norm().item() < 1e-13 * math.sqrt(n)
+    assert ((Q @ R - A).norm() / A.norm()).item() < 1e-13 * math.log10(cond)
+    assert torch.allclose(torch.tril(R, -1), torch.zeros_like(R))
+
+
+@pytest.mark.parametrize("m,n,r", [(32768, 144, 128), (5000, 80, 3), (300, 33, 1)])
+def test_qr_r_only_rank_deficient_tsqr(ctx, m, n, r):
+    """R-only QR of a numerically rank-deficient matrix (the truncation's bond
+    matrices at depth): both CholeskyQR routes must fail over to
+    the Householder TSQR, whose R reproduces the singular values of A."""
+    g = torch.Generator(device="cuda").manual_seed(m + n + r)
+    A = (torch.randn(m, r, dtype=torch.float64, device="cuda", generator=g)
+         @ torch.randn(r, n, dtype=torch.float64, device="cuda", generator=g))
+    A = (A * torch.logspace(0, -9, n, dtype=torch.float64, device="cuda")).t().contiguous().t()
+    _, R, fb = ctx.tt_qr(A, want_r=True, want_q=False)
+    assert fb and ctx.status_words(16)[14] == 1
+    assert torch.allclose(torch.tril(R, -1), torch.zeros_like(R))
+    sA = torch.linalg.svdvals(A)
+    sR = torch.linalg.svdvals(R)
+    assert (sA - sR).abs().max().item() <= 1e-13 * sA[0].item() * math.sqrt(n)
+    G = A.T @ A
+    assert (R.T @ R - G).norm().item() <= 1e-13 * G.norm().item() * math.sqrt(n)
 
 
 def test_qr_rank_deficient_uses_valid_basis(ctx):
