@@ -95,6 +95,10 @@ enum CholMode : int {
   CH_S2PLAIN = 7,  // route 2, pass 3:          failure -> route 3
   CH_S2LAST = 8,   // route 2, pass 4:          failure or deviation -> route 3
   CH_SHIFT1B = 9,  // route 2, pass 1 (shifted, on the input again): failure -> route 3
+  // robust R-only QR (truncation): no routes, never fails on a finite input
+  CH_RSHIFT = 10,  // passes 1, 2: shifted (compress kappa)
+  CH_RCLAMP = 11,  // passes 3, 4: plain, pivots below tau = 64 n u max(diag G)
+                   // (numerically null directions only) clamped to tau
 };
 constexpr double kDevTol = 0.05;
 // mode bit of the R-only QR: a plain pass whose pivots spread by more than
@@ -138,6 +142,10 @@ __device__ __forceinline__ void route_update(int* flags, int mode, bool bad, dou
       if (fail) flags[0] = 3;
       else flags[15] += 1;
       break;
+    case CH_RSHIFT:
+    case CH_RCLAMP:
+      if (bad) atomicOr(&flags[3], 1);   // non-finite input even with the shift
+      break;
   }
 }
 
@@ -170,7 +178,7 @@ __global__ void __launch_bounds__(kCholThreads)
       }
       const double u = 0x1p-53;
       s_shift = ((mode & 0xff) == CH_SHIFT || (mode & 0xff) == CH_SHIFT2 ||
-                     (mode & 0xff) == CH_SHIFT1B)
+                     (mode & 0xff) == CH_SHIFT1B || (mode & 0xff) == CH_RSHIFT)
                     ? 11.0 * (double(m) * n + double(n) * (n + 1)) * u * tr : 0.0;
     }
   }
@@ -254,184 +262,314 @@ __global__ void __launch_bounds__(kCholThreads)
   }
 }
 
-// Register-tiled Cholesky + triangular inverse for n <= 32*NA (one CTA of 1024
-// threads).  Thread (warp w, lane t) owns the entries (i, j) = (t + 32x, w + 32y)
-// of the working matrix; only the lower triangle is ever needed, i.e. y <= x
-// (x > y is always below the diagonal, x == y iff t >= w), so a thread keeps
-// NA(NA+1)/2 doubles in registers.  Each elimination step broadcasts one column
-// (Cholesky) or one row (inverse) through shared memory: one __syncthreads and
-// <= NA(NA+1)/2 FMAs per thread per step.  Same contract and flags as
-// chol_inv_kernel.
-template <int NA>
-__global__ void __launch_bounds__(1024, 1)
-    chol_reg_kernel(const double* __restrict__ G, int n, int64_t m, int mode,
+// Blocked Cholesky + in-place triangular inverse for n <= 32*NB (one CTA of 256
+// threads).  Same contract and flags as chol_inv_kernel.  The n x n working
+// matrix S (ld odd) holds L in its lower triangle.  Per 32-column block k:
+//  C1  warp 0 factors the diagonal block in registers (lane i = row i, 496
+//      shuffles) and inverts it (X_kk = L_kk^{-1}); X_kk's strictly lower part
+//      is parked transposed in the (unused) upper triangle of the block;
+//  C2  panel L_ik = A_ik X_kk^T (register tiles: lane = row, warp = column);
+//  C3  trailing update A_ij -= L_ik L_jk^T.
+// Then X = L^{-1} in place, block columns right to left (LAPACK dtrtri order):
+//  I1  A21 <- X22 A21,  I2  A21 <- -A21 X11,  I3  X11 into the lower triangle.
+// Three __syncthreads per block and phase instead of one per column.
+constexpr int kBlkThreads = 256;
+
+template <int NB>
+__global__ void __launch_bounds__(kBlkThreads, 1)
+    chol_blk_kernel(const double* __restrict__ G, int n, int64_t m, int mode,
                     double* __restrict__ Rinv, double* __restrict__ Rout,
                     int* __restrict__ flags, const int* gate, int gate_val) {
   if (gate && *gate != gate_val) return;
-  extern __shared__ double sh[];                 // (n+1) x n padded, column-major
-  __shared__ double colbuf[2][32 * NA];
-  __shared__ double s_shift;
-  __shared__ int s_bad, s_zero;
-  constexpr int NT = NA * (NA + 1) / 2;
-  const int ldl = n + 1;
+  extern __shared__ double S[];
+  __shared__ double s_tr, s_dmax;
+  __shared__ int s_bad, s_zero, s_clamped;
+  const int ld = (n & 1) ? n : n + 1;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  if (tid == 0) { s_bad = 0; s_zero = 0; }
+  constexpr int NW = kBlkThreads / 32;
+  const int nb = (n + 31) / 32;
+  const int md = mode & 0xff;
+  if (tid == 0) { s_bad = 0; s_zero = 0; s_clamped = 0; }
   if (tid < 32) {
-    double tr = 0.0;
-    for (int i = tid; i < n; i += 32) tr += G[i + int64_t(i) * n];
-    for (int o = 16; o; o >>= 1) tr += __shfl_xor_sync(0xffffffffu, tr, o);
+    double tr = 0.0, dmax = 0.0;
+    for (int i = tid; i < n; i += 32) {
+      const double gi = G[i + int64_t(i) * n];
+      tr += gi;
+      dmax = fmax(dmax, gi);
+    }
+    for (int o = 16; o; o >>= 1) {
+      tr += __shfl_xor_sync(0xffffffffu, tr, o);
+      dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+    }
     if (tid == 0) {
       if (!(tr > 0.0)) {
-        if (tr == 0.0) { atomicOr(&flags[2], 1); s_zero = 1; }
+        if (tr == 0.0) { atomicOr(&flags[2], 1); s_zero = 1; }   // Y_n == 0: zero sum (R16)
         s_bad = 1;
       }
-      s_shift = ((mode & 0xff) == CH_SHIFT || (mode & 0xff) == CH_SHIFT2 ||
-                     (mode & 0xff) == CH_SHIFT1B)
-                    ? 11.0 * (double(m) * n + double(n) * (n + 1)) * 0x1p-53 * tr : 0.0;
+      s_tr = tr;
+      s_dmax = dmax;
     }
   }
   __syncthreads();
-  const double shift = s_shift;
-  double a[NT];   // a[x(x+1)/2 + y], y <= x
-#pragma unroll
-  for (int x = 0; x < NA; ++x)
-#pragma unroll
-    for (int y = 0; y <= x; ++y) {
-      const int i = lane + 32 * x, j = w + 32 * y;
-      a[x * (x + 1) / 2 + y] =
-          (i < n && j < n && i >= j) ? G[i + int64_t(j) * n] + (i == j ? shift : 0.0) : 0.0;
-    }
-  // ---- right-looking Cholesky: after step k, column k holds L(:, k)
-  if (w == 0) {
-#pragma unroll
-    for (int x = 0; x < NA; ++x) colbuf[0][lane + 32 * x] = a[x * (x + 1) / 2];
-  }
-  __syncthreads();
-  bool bad = false;
-  for (int k = 0; k < n; ++k) {
-    const double* cb = colbuf[k & 1];
-    const double dkk = cb[k];
-    const bool okp = dkk > 0.0 && isfinite(dkk);
-    bad |= !okp;
-    const double dk = okp ? sqrt(dkk) : 1.0;
-    const double dinv = 1.0 / dk;
-    double li[NA];
-#pragma unroll
-    for (int x = 0; x < NA; ++x) {
-      const int i = lane + 32 * x;
-      li[x] = (i > k && i < n) ? cb[i] * dinv : 0.0;
-    }
-    const int yk = k >> 5;
-    if (w == (k & 31)) {   // finalise column k in its owner's registers
-#pragma unroll
-      for (int x = 0; x < NA; ++x)
-#pragma unroll
-        for (int y = 0; y <= x; ++y)
-          if (y == yk) {
-            const int i = lane + 32 * x;
-            a[x * (x + 1) / 2 + y] = (i > k) ? li[x] : (i == k ? dk : 0.0);
-          }
-    }
-    // trailing update A(i, j) -= l_i l_j for i >= j > k (l_j: warp-uniform broadcast)
-#pragma unroll
-    for (int y = 0; y < NA; ++y) {
-      const int j = w + 32 * y;
-      const double lj = (j > k && j < n) ? cb[j] * dinv : 0.0;
-#pragma unroll
-      for (int x = y; x < NA; ++x) a[x * (x + 1) / 2 + y] -= li[x] * lj;
-    }
-    // publish column k+1 (already updated by this step)
-    if (k + 1 < n && w == ((k + 1) & 31)) {
-      const int y1 = (k + 1) >> 5;
-#pragma unroll
-      for (int x = 0; x < NA; ++x)
-#pragma unroll
-        for (int y = 0; y <= x; ++y)
-          if (y == y1) colbuf[(k + 1) & 1][lane + 32 * x] = a[x * (x + 1) / 2 + y];
+  const bool shifted = md == CH_SHIFT || md == CH_SHIFT2 || md == CH_SHIFT1B || md == CH_RSHIFT;
+  const double shift = shifted ? 11.0 * (double(m) * n + double(n) * (n + 1)) * 0x1p-53 * s_tr : 0.0;
+  const bool clamp = md == CH_RCLAMP;
+  const double tau = 64.0 * n * 0x1p-53 * s_dmax;
+  bool bad_final = s_bad;
+  {
+    __syncthreads();
+    for (int e = tid; e < n * n; e += kBlkThreads) {
+      const int i = e % n, j = e / n;
+      if (i >= j) S[i + j * ld] = G[e] + ((i == j) ? shift : 0.0);
     }
     __syncthreads();
-  }
-  if (bad && lane == 0) s_bad = 1;
-  // L (lower) to shared memory
+    for (int k = 0; k < nb; ++k) {
+      const int k0 = 32 * k, kb = min(32, n - k0);
+      // ---- C1: diagonal block (warp 0)
+      if (w == 0) {
+        double a[32], x[32];
+        const int i = lane;
 #pragma unroll
-  for (int x = 0; x < NA; ++x)
+        for (int j = 0; j < 32; ++j)
+          a[j] = (i < kb && j <= i) ? S[(k0 + i) + (k0 + j) * ld] : 0.0;
+        bool bad = false;
 #pragma unroll
-    for (int y = 0; y < NA; ++y) {
-      const int i = lane + 32 * x, j = w + 32 * y;
-      if (i < n && j < n) sh[i + j * ldl] = (y <= x && i >= j) ? a[x * (x + 1) / 2 + (y <= x ? y : 0)] : 0.0;
-    }
-  __syncthreads();
-  // ---- X = L^{-1} (lower): step k scales row k of X by 1/L_kk and eliminates
-  // it from the rows i > k (all right-hand sides at once)
-#pragma unroll
-  for (int x = 0; x < NA; ++x)
-#pragma unroll
-    for (int y = 0; y <= x; ++y) a[x * (x + 1) / 2 + y] = ((lane + 32 * x) == (w + 32 * y)) ? 1.0 : 0.0;
-  double* rowbuf = &colbuf[0][0];   // reused: [2][32*NA]
-  for (int k = 0; k < n; ++k) {
-    double* rb = rowbuf + (k & 1) * (32 * NA);
-    if (lane == (k & 31)) {
-      const double inv = 1.0 / sh[k + k * ldl];
-      const int xk = k >> 5;
-#pragma unroll
-      for (int x = 0; x < NA; ++x)
-        if (x == xk) {
-#pragma unroll
-          for (int y = 0; y < NA; ++y) {
-            double v = 0.0;
-            if (y <= x) {
-              a[x * (x + 1) / 2 + (y <= x ? y : 0)] *= inv;
-              v = a[x * (x + 1) / 2 + (y <= x ? y : 0)];
+        for (int j = 0; j < 32; ++j) {
+          if (j < kb) {
+            double piv = __shfl_sync(0xffffffffu, a[j], j);
+            if (clamp && !(piv > tau) && isfinite(piv)) {   // numerically null direction
+              piv = tau;
+              if (i == j) a[j] = tau;
+              if (lane == 0) s_clamped += 1;
             }
-            rb[w + 32 * y] = v;
+            const bool ok = piv > 0.0 && isfinite(piv);
+            bad |= !ok;
+            const double d = ok ? sqrt(piv) : 1.0;
+            if (i > j) a[j] *= 1.0 / d;
+            else if (i == j) a[j] = d;
+#pragma unroll
+            for (int q = j + 1; q < 32; ++q) {
+              const double lqj = __shfl_sync(0xffffffffu, a[j], q);
+              if (i >= q && q < kb) a[q] = fma(-a[j], lqj, a[q]);
+            }
           }
         }
-    }
-    __syncthreads();
-    double lk[NA];
 #pragma unroll
-    for (int x = 0; x < NA; ++x) {
-      const int i = lane + 32 * x;
-      lk[x] = (i > k && i < n) ? sh[i + k * ldl] : 0.0;
-    }
+        for (int j = 0; j < 32; ++j) x[j] = (i == j) ? 1.0 : 0.0;
 #pragma unroll
-    for (int y = 0; y < NA; ++y) {
-      const double xk = rb[w + 32 * y];
+        for (int q = 0; q < 32; ++q) {
+          if (q < kb) {
+            const double lqq = __shfl_sync(0xffffffffu, a[q], q);
+            if (i == q) {
 #pragma unroll
-      for (int x = y; x < NA; ++x) a[x * (x + 1) / 2 + y] -= lk[x] * xk;
+              for (int j = 0; j <= q; ++j) x[j] /= lqq;
+            }
+#pragma unroll
+            for (int j = 0; j <= q; ++j) {
+              const double xqj = __shfl_sync(0xffffffffu, x[j], q);
+              if (i > q) x[j] = fma(-a[q], xqj, x[j]);
+            }
+          }
+        }
+        if (i < kb) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            if (j <= i) S[(k0 + i) + (k0 + j) * ld] = a[j];
+            if (j < i) S[(k0 + j) + (k0 + i) * ld] = x[j];   // X(i, j) parked at (j, i)
+          }
+        }
+        if (bad && lane == 0) s_bad = 1;
+      }
+      __syncthreads();
+      if (s_bad) break;
+      const int r0 = k0 + kb;   // first row below the block
+      if (r0 >= n) break;
+      // ---- C2: panel L(r, c) = sum_{t <= c} A(r, t) X_kk(c, t)
+      {
+        double acc[4][4];
+#pragma unroll
+        for (int ii = 0; ii < 4; ++ii)
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj) acc[ii][jj] = 0.0;
+        for (int t = 0; t < kb; ++t) {
+          double av[4], xv[4];
+#pragma unroll
+          for (int ii = 0; ii < 4; ++ii) {
+            const int r = r0 + lane + 32 * ii;
+            av[ii] = (r < n) ? S[r + (k0 + t) * ld] : 0.0;
+          }
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj) {
+            const int c = w + NW * jj;   // column within the block
+            xv[jj] = (c >= kb || t > c) ? 0.0
+                     : (t == c ? 1.0 / S[(k0 + c) + (k0 + c) * ld] : S[(k0 + t) + (k0 + c) * ld]);
+          }
+#pragma unroll
+          for (int ii = 0; ii < 4; ++ii)
+#pragma unroll
+            for (int jj = 0; jj < 4; ++jj) acc[ii][jj] = fma(av[ii], xv[jj], acc[ii][jj]);
+        }
+        __syncthreads();
+#pragma unroll
+        for (int ii = 0; ii < 4; ++ii)
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj) {
+            const int r = r0 + lane + 32 * ii, c = w + NW * jj;
+            if (r < n && c < kb) S[r + (k0 + c) * ld] = acc[ii][jj];
+          }
+      }
+      __syncthreads();
+      // ---- C3: trailing A(r, c) -= sum_t L(r, t) L(c, t), block columns j > k
+      for (int j = k + 1; j < nb; ++j) {
+        const int j0 = 32 * j, jb = min(32, n - j0);
+        double acc[4][4];
+#pragma unroll
+        for (int ii = 0; ii < 4; ++ii)
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj) acc[ii][jj] = 0.0;
+        for (int t = 0; t < kb; ++t) {
+          double lv[4], cv[4];
+#pragma unroll
+          for (int ii = 0; ii < 4; ++ii) {
+            const int r = j0 + lane + 32 * ii;
+            lv[ii] = (r < n) ? S[r + (k0 + t) * ld] : 0.0;
+          }
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj) {
+            const int c = j0 + w + NW * jj;
+            cv[jj] = (c < j0 + jb) ? S[c + (k0 + t) * ld] : 0.0;
+          }
+#pragma unroll
+          for (int ii = 0; ii < 4; ++ii)
+#pragma unroll
+            for (int jj = 0; jj < 4; ++jj) acc[ii][jj] = fma(lv[ii], cv[jj], acc[ii][jj]);
+        }
+#pragma unroll
+        for (int ii = 0; ii < 4; ++ii)
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj) {
+            const int r = j0 + lane + 32 * ii, c = j0 + w + NW * jj;
+            if (r < n && c < j0 + jb && r >= c) S[r + c * ld] -= acc[ii][jj];
+          }
+      }
+      __syncthreads();
     }
+    bad_final = s_bad;
   }
   __syncthreads();
-  // R = L^T (upper) from shared memory, then X into shared memory for Rinv = X^T
-  if (Rout)
-    for (int e = tid; e < n * n; e += 1024) {
-      const int r = e % n, c = e / n;    // R(r, c) = L(c, r)
-      Rout[e] = (c >= r) ? sh[c + r * ldl] : 0.0;
-    }
-  __syncthreads();
-#pragma unroll
-  for (int x = 0; x < NA; ++x)
-#pragma unroll
-    for (int y = 0; y < NA; ++y) {
-      const int i = lane + 32 * x, j = w + 32 * y;
-      if (i < n && j < n) sh[i + j * ldl] = (y <= x && i >= j) ? a[x * (x + 1) / 2 + (y <= x ? y : 0)] : 0.0;
-    }
-  __syncthreads();
-  for (int e = tid; e < n * n; e += 1024) {
-    const int r = e % n, c = e / n;      // Rinv(r, c) = X(c, r)
-    Rinv[e] = sh[c + r * ldl];
-  }
+  // route checks on diag(L); R = L^T before L is overwritten by its inverse
   if (tid == 0 && !s_zero && !(flags[2] & 1)) {
-    int bad2 = s_bad;
+    int bad2 = bad_final;
     double dev = 0.0, dmin = INFINITY, dmax = 0.0;
     for (int i = 0; i < n; ++i) {
-      const double d = fabs(1.0 / sh[i + i * ldl]);     // |L_ii|
+      const double d = fabs(S[i + i * ld]);
       dmin = fmin(dmin, d);
       dmax = fmax(dmax, d);
-      if (needs_dev(mode & 0xff)) dev = fmax(dev, fabs(1.0 / sh[i + i * ldl] - 1.0));
+      if (needs_dev(md)) dev = fmax(dev, fabs(S[i + i * ld] - 1.0));
     }
     if ((mode & kStrict) && !(dmin >= dmax * kStrictRatio)) bad2 = 1;
-    route_update(flags, mode & 0xff, bad2, dev);
+    if (s_clamped) flags[16] += 1;   // counter: clamped (rank-deficient) passes
+    route_update(flags, md, bad2, dev);
+  }
+  if (bad_final) return;   // outputs are not used (the route moved on)
+  if (Rout)
+    for (int e = tid; e < n * n; e += kBlkThreads) {
+      const int r = e % n, c = e / n;   // R(r, c) = L(c, r)
+      Rout[e] = (c >= r) ? S[c + r * ld] : 0.0;
+    }
+  __syncthreads();
+  // ---- X = L^{-1} in place, block columns right to left
+  for (int k = nb - 1; k >= 0; --k) {
+    const int k0 = 32 * k, kb = min(32, n - k0);
+    const int r0 = k0 + kb;
+    if (r0 < n) {
+      // I1: A21 <- X22 A21  (X22 final lower triangle of rows/cols >= r0)
+      double acc[4][4];
+#pragma unroll
+      for (int ii = 0; ii < 4; ++ii)
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) acc[ii][jj] = 0.0;
+      for (int t = r0; t < n; ++t) {
+        double xv[4], av[4];
+#pragma unroll
+        for (int ii = 0; ii < 4; ++ii) {
+          const int r = r0 + lane + 32 * ii;
+          xv[ii] = (r < n && t <= r) ? S[r + t * ld] : 0.0;
+        }
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) {
+          const int c = w + NW * jj;
+          av[jj] = (c < kb) ? S[t + (k0 + c) * ld] : 0.0;
+        }
+#pragma unroll
+        for (int ii = 0; ii < 4; ++ii)
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj) acc[ii][jj] = fma(xv[ii], av[jj], acc[ii][jj]);
+      }
+      __syncthreads();
+#pragma unroll
+      for (int ii = 0; ii < 4; ++ii)
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) {
+          const int r = r0 + lane + 32 * ii, c = w + NW * jj;
+          if (r < n && c < kb) S[r + (k0 + c) * ld] = acc[ii][jj];
+        }
+      __syncthreads();
+      // I2: A21 <- -A21 X11, X11(t, c) (t > c) parked at (c, t), diag 1/L(c, c)
+#pragma unroll
+      for (int ii = 0; ii < 4; ++ii)
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) acc[ii][jj] = 0.0;
+      for (int t = 0; t < kb; ++t) {
+        double av[4], xv[4];
+#pragma unroll
+        for (int ii = 0; ii < 4; ++ii) {
+          const int r = r0 + lane + 32 * ii;
+          av[ii] = (r < n) ? S[r + (k0 + t) * ld] : 0.0;
+        }
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) {
+          const int c = w + NW * jj;
+          xv[jj] = (c >= kb || t < c) ? 0.0
+                   : (t == c ? 1.0 / S[(k0 + c) + (k0 + c) * ld] : S[(k0 + c) + (k0 + t) * ld]);
+        }
+#pragma unroll
+        for (int ii = 0; ii < 4; ++ii)
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj) acc[ii][jj] = fma(av[ii], xv[jj], acc[ii][jj]);
+      }
+      __syncthreads();
+#pragma unroll
+      for (int ii = 0; ii < 4; ++ii)
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) {
+          const int r = r0 + lane + 32 * ii, c = w + NW * jj;
+          if (r < n && c < kb) S[r + (k0 + c) * ld] = -acc[ii][jj];
+        }
+      __syncthreads();
+    }
+    // I3: X11 into the lower triangle of the diagonal block
+    double v[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int e = tid + kBlkThreads * q;   // 1024 = 32 x 32 slots
+      const int a = e % 32, b = e / 32;      // X(a, b), a >= b
+      v[q] = 0.0;
+      if (a < kb && b < kb && a >= b)
+        v[q] = (a == b) ? 1.0 / S[(k0 + a) + (k0 + a) * ld] : S[(k0 + b) + (k0 + a) * ld];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int e = tid + kBlkThreads * q;
+      const int a = e % 32, b = e / 32;
+      if (a < kb && b < kb && a >= b) S[(k0 + a) + (k0 + b) * ld] = v[q];
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < n * n; e += kBlkThreads) {
+    const int r = e % n, c = e / n;     // Rinv(r, c) = X(c, r), c >= r
+    Rinv[e] = (c >= r) ? S[c + r * ld] : 0.0;
   }
 }
 
@@ -737,7 +875,7 @@ static int tsqr_r(Ctx& c, int64_t m, int n, const double* A, int64_t lda, bool t
 
 bool tsqr_fits(int n) { return n >= 1 && 2 * (int64_t(n) * (n + 1) / 2) <= kSmemLimitDoubles; }
 
-// Launch one Cholesky(+inverse) of the n x n Gram Gm (see chol_reg_kernel).
+// Launch one Cholesky(+inverse) of the n x n Gram Gm (see chol_blk_kernel).
 static int launch_chol(Ctx& c, const double* Gm, int n, int64_t m, int mode, double* Rinv,
                        double* Rk, double* gw, const int* gate, int gv, cudaStream_t s) {
   static bool attr_done = false;
@@ -745,25 +883,22 @@ static int launch_chol(Ctx& c, const double* Gm, int n, int64_t m, int mode, dou
     TTR_CUDA(cudaFuncSetAttribute(chol_inv_kernel<32>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   kSmemLimitDoubles * 8));
-    TTR_CUDA(cudaFuncSetAttribute(chol_reg_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  200 * 1024));
-    TTR_CUDA(cudaFuncSetAttribute(chol_reg_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  200 * 1024));
-    TTR_CUDA(cudaFuncSetAttribute(chol_reg_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  200 * 1024));
-    TTR_CUDA(cudaFuncSetAttribute(chol_reg_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    TTR_CUDA(cudaFuncSetAttribute(chol_blk_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  220 * 1024));
+    TTR_CUDA(cudaFuncSetAttribute(chol_blk_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  220 * 1024));
+    TTR_CUDA(cudaFuncSetAttribute(chol_blk_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   220 * 1024));
     attr_done = true;
   }
-  const size_t shm = size_t(n + 1) * n * sizeof(double);
+  const int ldb = (n & 1) ? n : n + 1;
+  const size_t shm = size_t(ldb) * n * sizeof(double);
   if (n <= 32) {
-    chol_reg_kernel<1><<<1, 1024, shm, s>>>(Gm, n, m, mode, Rinv, Rk, c.flags.p, gate, gv);
+    chol_blk_kernel<1><<<1, kBlkThreads, shm, s>>>(Gm, n, m, mode, Rinv, Rk, c.flags.p, gate, gv);
   } else if (n <= 64) {
-    chol_reg_kernel<2><<<1, 1024, shm, s>>>(Gm, n, m, mode, Rinv, Rk, c.flags.p, gate, gv);
-  } else if (n <= 96) {
-    chol_reg_kernel<3><<<1, 1024, shm, s>>>(Gm, n, m, mode, Rinv, Rk, c.flags.p, gate, gv);
+    chol_blk_kernel<2><<<1, kBlkThreads, shm, s>>>(Gm, n, m, mode, Rinv, Rk, c.flags.p, gate, gv);
   } else if (n <= 160) {
-    chol_reg_kernel<5><<<1, 1024, shm, s>>>(Gm, n, m, mode, Rinv, Rk, c.flags.p, gate, gv);
+    chol_blk_kernel<5><<<1, kBlkThreads, shm, s>>>(Gm, n, m, mode, Rinv, Rk, c.flags.p, gate, gv);
   } else {
     const bool big = n * n > kSmemLimitDoubles;
     chol_inv_kernel<32><<<1, kCholThreads, big ? 0 : size_t(n) * n * 8, s>>>(
@@ -865,6 +1000,33 @@ int qr(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, bool trans, d
     return launched();
   };
 
+  // ---- R only, n <= 160 (the truncation): four CholeskyQR passes, no routes.
+  // Passes 1-2 are shifted (shift 11(mn + n(n+1)) u tr G, Fukaya et al.), which
+  // compresses kappa(op(A)) up to ~1/u; passes 3-4 are plain, so the final Q4
+  // is orthonormal and A = Q4 R carries no shift bias; a pivot below
+  // tau = 64 n u max(diag G) (a numerically null direction of a rank-deficient
+  // bond matrix) is clamped to tau instead of breaking down.  R^T R = A^T A +
+  // O(u ||A||^2): singular values/vectors of R are those of op(A) to O(u ||A||)
+  // (DESIGN.md §QR).
+  if (r_only && ni <= 160) {
+    TTR_TRY(gram_of_input(nullptr, 0));
+    TTR_TRY(chol(CH_RSHIFT, nullptr, 0));                   // R1 (shifted)
+    TTR_TRY(copy_r_first(nullptr, 0));
+    TTR_TRY(input_times_rinv(T1.p, nullptr, 0));            // Q1 = op(A) R1^{-1}
+    TTR_TRY(gram(T1.p, nullptr, 0));
+    TTR_TRY(chol(CH_RSHIFT, nullptr, 0));                   // R2 (shifted)
+    TTR_TRY(accumulate_r(nullptr, 0));
+    TTR_TRY(times_rinv(T1.p, T2.p, nullptr, 0));            // Q2 = Q1 R2^{-1}
+    TTR_TRY(gram(T2.p, nullptr, 0));
+    TTR_TRY(chol(CH_RCLAMP, nullptr, 0));                   // R3 (plain, clamped)
+    TTR_TRY(accumulate_r(nullptr, 0));
+    TTR_TRY(times_rinv(T2.p, T1.p, nullptr, 0));            // Q3 = Q2 R3^{-1}
+    TTR_TRY(gram(T1.p, nullptr, 0));
+    TTR_TRY(chol(CH_RCLAMP, nullptr, 0));                   // R4 (plain, clamped)
+    TTR_TRY(accumulate_r(nullptr, 0));
+    TTR_CUDA(cudaMemcpyAsync(R, Racc.p, sizeof(double) * n * n, cudaMemcpyDeviceToDevice, s));
+    return TT_OK;
+  }
   // ---- route 0: CholeskyQR2, accepted when pass 2 finds Q1 close to
   // orthonormal (|diag R2 - 1| <= kDevTol).  The route state F[0] lives on the
   // device; every launch of an inactive route is a no-op.
@@ -1032,106 +1194,6 @@ __global__ void __launch_bounds__(kJacThreads)
   }
 }
 
-// One-sided (Hestenes) Jacobi without accumulating V, for the truncation step
-// (R3): W = A (m x n, m <= 32*MT) lives in shared memory; each round of the
-// round-robin ("circle") ordering pairs all columns disjointly, one warp per
-// pair with the pair's two columns in registers; the pairing is arithmetic
-// (position 0 fixed, the others rotate by one per round).  Output: AV = U Sigma
-// (m x n, columns sorted by descending norm) and sigma.  V is not formed: the
-// truncation forms V_k^T Q^T as Sigma_k^{-2} (U Sigma)_k^T H(X_n), which needs only
-// R of the QR.
-template <int MT>
-__global__ void __launch_bounds__(1024, 1)
-    jacobi_nov_kernel(const double* __restrict__ A, int64_t lda, int m, int n,
-                      double* __restrict__ AV, double* __restrict__ sigma, int max_sweeps,
-                      int* flags) {
-  extern __shared__ double W[];   // m x n, ld m
-  __shared__ double nrm[1024];
-  __shared__ int s_rot;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  constexpr int NW = 32;
-  for (int e = tid; e < m * n; e += 1024) {
-    const int i = e % m, j = e / m;
-    W[e] = A[i + int64_t(j) * lda];
-  }
-  const int np = (n + 1) & ~1;
-  const int half = np / 2;
-  const double tol = double(m) * 0x1p-52;
-  __syncthreads();
-  int sweep = 0;
-  for (; sweep < max_sweeps; ++sweep) {
-    if (tid == 0) s_rot = 0;
-    int rotated = 0;
-    for (int r = 0; r < np - 1; ++r) {
-      __syncthreads();
-      for (int ps = warp; ps < half; ps += NW) {
-        int p = (ps == 0) ? 0 : ((ps - 1 + r) % (np - 1)) + 1;
-        int q = ((np - 2 - ps + r) % (np - 1)) + 1;
-        if (p >= n || q >= n) continue;
-        if (p > q) { const int t = p; p = q; q = t; }
-        double* wp = W + p * m;
-        double* wq = W + q * m;
-        double x[MT], y[MT];
-        double al = 0.0, be = 0.0, ga = 0.0;
-#pragma unroll
-        for (int t = 0; t < MT; ++t) {
-          const int i = lane + 32 * t;
-          x[t] = (i < m) ? wp[i] : 0.0;
-          y[t] = (i < m) ? wq[i] : 0.0;
-          al = fma(x[t], x[t], al);
-          be = fma(y[t], y[t], be);
-          ga = fma(x[t], y[t], ga);
-        }
-#pragma unroll
-        for (int o = 16; o; o >>= 1) {
-          al += __shfl_xor_sync(0xffffffffu, al, o);
-          be += __shfl_xor_sync(0xffffffffu, be, o);
-          ga += __shfl_xor_sync(0xffffffffu, ga, o);
-        }
-        if (al == 0.0 || be == 0.0 || !(fabs(ga) > tol * sqrt(al) * sqrt(be))) continue;
-        const double zeta = (be - al) / (2.0 * ga);
-        const double tt = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-        const double cs = 1.0 / sqrt(1.0 + tt * tt), sn = cs * tt;
-#pragma unroll
-        for (int t = 0; t < MT; ++t) {
-          const int i = lane + 32 * t;
-          if (i < m) {
-            wp[i] = cs * x[t] - sn * y[t];
-            wq[i] = sn * x[t] + cs * y[t];
-          }
-        }
-        rotated = 1;
-      }
-    }
-    if (rotated) atomicOr(&s_rot, 1);
-    __syncthreads();
-    if (!s_rot) break;
-  }
-  if (tid == 0) {
-    if (sweep == max_sweeps) atomicOr(&flags[3], 2);
-    flags[12] += sweep + 1;    // Jacobi sweeps (counter)
-    flags[13] += 1;            // Jacobi calls (counter)
-  }
-  for (int j = warp; j < n; j += NW) {
-    double s2 = 0.0;
-    for (int i = lane; i < m; i += 32) s2 = fma(W[i + j * m], W[i + j * m], s2);
-    for (int o = 16; o; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
-    if (lane == 0) nrm[j] = sqrt(s2);
-  }
-  __syncthreads();
-  for (int j = warp; j < n; j += NW) {
-    const double sj = nrm[j];
-    int rank = 0;
-    for (int k = lane; k < n; k += 32) {
-      const double sk = nrm[k];
-      rank += (sk > sj) || (sk == sj && k < j);
-    }
-    for (int o = 16; o; o >>= 1) rank += __shfl_xor_sync(0xffffffffu, rank, o);
-    for (int i = lane; i < m; i += 32) AV[i + int64_t(rank) * m] = W[i + j * m];
-    if (lane == 0) sigma[rank] = sj;
-  }
-}
-
 // B(:, c) = AV(:, c) / sigma_c^2 for c < k (0 when sigma_c is negligible), so that
 // B^T H(X_n) = V_k^T Q^T (see svd_nov).
 __global__ void scale_by_inv_sigma2_kernel(const double* __restrict__ AV, int m, int k,
@@ -1223,42 +1285,6 @@ int svd_jacobi(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, doubl
                                            c.flags.p);
   return launched();
 }
-
-int svd_nov(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, double* AV,
-            double* sigma, cudaStream_t s) {
-  if (m < n || n < 1 || m > 256 || m * n > kSmemLimitDoubles) {
-    set_error("svd_nov: unsupported shape m=%lld n=%lld", (long long)m, (long long)n);
-    return TT_ERR_ARG;
-  }
-  static bool attr = false;
-  if (!attr) {
-    TTR_CUDA(cudaFuncSetAttribute(jacobi_nov_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  kSmemLimitDoubles * 8));
-    TTR_CUDA(cudaFuncSetAttribute(jacobi_nov_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  kSmemLimitDoubles * 8));
-    TTR_CUDA(cudaFuncSetAttribute(jacobi_nov_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  kSmemLimitDoubles * 8));
-    TTR_CUDA(cudaFuncSetAttribute(jacobi_nov_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  kSmemLimitDoubles * 8));
-    TTR_CUDA(cudaFuncSetAttribute(jacobi_nov_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  kSmemLimitDoubles * 8));
-    attr = true;
-  }
-  const size_t shm = size_t(m) * n * 8;
-  if (m <= 32)
-    jacobi_nov_kernel<1><<<1, 1024, shm, s>>>(A, lda, int(m), int(n), AV, sigma, 40, c.flags.p);
-  else if (m <= 64)
-    jacobi_nov_kernel<2><<<1, 1024, shm, s>>>(A, lda, int(m), int(n), AV, sigma, 40, c.flags.p);
-  else if (m <= 96)
-    jacobi_nov_kernel<3><<<1, 1024, shm, s>>>(A, lda, int(m), int(n), AV, sigma, 40, c.flags.p);
-  else if (m <= 160)
-    jacobi_nov_kernel<5><<<1, 1024, shm, s>>>(A, lda, int(m), int(n), AV, sigma, 40, c.flags.p);
-  else
-    jacobi_nov_kernel<8><<<1, 1024, shm, s>>>(A, lda, int(m), int(n), AV, sigma, 40, c.flags.p);
-  return launched();
-}
-
-bool svd_nov_fits(int64_t m, int64_t n) { return m >= n && m <= 256 && m * n <= kSmemLimitDoubles; }
 
 int scale_by_inv_sigma2(Ctx& c, const double* AV, int64_t m, int64_t k, const double* sigma,
                         double* B, cudaStream_t s) {

@@ -117,23 +117,43 @@ def test_qr_ill_conditioned_stays_on_cholesky_routes(ctx, m, n, cond):
     assert torch.allclose(torch.tril(R, -1), torch.zeros_like(R))
 
 
-@pytest.mark.parametrize("m,n,r", [(32768, 144, 128), (5000, 80, 3), (300, 33, 1)])
-def test_qr_r_only_rank_deficient_tsqr(ctx, m, n, r):
+@pytest.mark.parametrize("m,n,r", [(32768, 144, 128), (5000, 80, 3), (300, 33, 1),
+                                   (32768, 144, 144), (4000, 160, 100)])
+def test_qr_r_only_rank_deficient_robust(ctx, m, n, r):
     """R-only QR of a numerically rank-deficient matrix (the truncation's bond
-    matrices at depth): both CholeskyQR routes must fail over to
-    the Householder TSQR, whose R reproduces the singular values of A."""
+    matrices at depth): two shifted + two clamped CholeskyQR
+    passes (no TSQR, no Householder) whose R reproduces the singular values of A
+    and R^T R = A^T A to O(u ||A||^2)."""
     g = torch.Generator(device="cuda").manual_seed(m + n + r)
     A = (torch.randn(m, r, dtype=torch.float64, device="cuda", generator=g)
          @ torch.randn(r, n, dtype=torch.float64, device="cuda", generator=g))
     A = (A * torch.logspace(0, -9, n, dtype=torch.float64, device="cuda")).t().contiguous().t()
     _, R, fb = ctx.tt_qr(A, want_r=True, want_q=False)
-    assert fb and ctx.status_words(16)[14] == 1
+    st = ctx.status_words(17)
+    assert not fb and st[14] == 0 and st[11] == 0      # no TSQR, no Householder
     assert torch.allclose(torch.tril(R, -1), torch.zeros_like(R))
     sA = torch.linalg.svdvals(A)
     sR = torch.linalg.svdvals(R)
     assert (sA - sR).abs().max().item() <= 1e-13 * sA[0].item() * math.sqrt(n)
     G = A.T @ A
     assert (R.T @ R - G).norm().item() <= 1e-13 * G.norm().item() * math.sqrt(n)
+
+
+@pytest.mark.parametrize("m,n,cond", [(32768, 144, 1e15), (10000, 100, 1e3), (500, 160, 1e8)])
+def test_qr_r_only_ill_conditioned(ctx, m, n, cond):
+    """Full-rank but ill-conditioned (kappa up to ~1/u): the same R-only path keeps
+    the small singular values to O(u ||A||) absolute."""
+    g = torch.Generator(device="cuda").manual_seed(m + n)
+    U, _ = torch.linalg.qr(torch.randn(m, n, dtype=torch.float64, device="cuda", generator=g))
+    V, _ = torch.linalg.qr(torch.randn(n, n, dtype=torch.float64, device="cuda", generator=g))
+    s = torch.logspace(0, -math.log10(cond), n, dtype=torch.float64, device="cuda")
+    A = ((U * s) @ V.T).t().contiguous().t()
+    _, R, fb = ctx.tt_qr(A, want_r=True, want_q=False)
+    assert not fb
+    sR = torch.linalg.svdvals(R)
+    assert (sR - s).abs().max().item() <= 1e-14 * math.sqrt(n)
+    G = A.T @ A
+    assert (R.T @ R - G).norm().item() <= 1e-14 * math.sqrt(n)
 
 
 def test_qr_rank_deficient_uses_valid_basis(ctx):

@@ -13,11 +13,11 @@ import ttsynth
 
 name = sys.argv[1]
 d = int(sys.argv[2]) if len(sys.argv) > 2 else None
-w = ttsynth.CONFIGS[name](device="cuda", **({"d": d} if d else {}))
+w = ttsynth.CONFIGS[name](device=os.environ.get("DEV", "cuda"), **({"d": d} if d else {}))
 terms = w.terms
 S, D = len(terms), len(terms[0])
 dims = [c.shape[1] for c in terms[0]]
-dev = "cuda"
+dev = os.environ.get("DEV", "cuda")
 g = torch.Generator(device=dev).manual_seed(1)
 sumR = [1] + [sum(t[n].shape[2] for t in terms) for n in range(D - 1)] + [1]
 ell = w.ell
