@@ -140,7 +140,7 @@ int launch_rr(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, double
   const size_t shm = size_t(n) * 8 * RPT * sizeof(double);
   if (!attr[c.device & 63]) {
     TTR_CUDA(cudaFuncSetAttribute(jacobi_rr_kernel<RPT>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, 222 * 1024));
     attr[c.device & 63] = true;
   }
   const int half = int((n + 1) / 2);
