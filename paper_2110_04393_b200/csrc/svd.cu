@@ -27,7 +27,7 @@ namespace {
 constexpr int kGroup = 8;   // threads per column pair
 
 template <int RPT>   // rows per thread (even); m <= 8 * RPT
-__global__ void __launch_bounds__(32 * RPT) __maxnreg__(RPT >= 20 ? 96 : (RPT >= 18 ? 112 : 128))
+__global__ void __launch_bounds__(32 * RPT) __maxnreg__(RPT >= 20 ? 96 : (RPT >= 18 ? 104 : (RPT >= 16 ? 120 : 128)))
     jacobi_rr_kernel(const double* __restrict__ A, int64_t lda, int m, int n,
                      double* __restrict__ AV, double* __restrict__ sigma, int max_sweeps,
                      int* __restrict__ flags) {
