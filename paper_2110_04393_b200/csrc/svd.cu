@@ -26,8 +26,10 @@ namespace {
 
 constexpr int kGroup = 8;   // threads per column pair
 
+// Register cap: a CTA of W warps puts ceil(W/4) warps on one SM sub-partition,
+// whose register file holds 16K registers -> <= 96 registers at 18-20 warps.
 template <int RPT>   // rows per thread (even); m <= 8 * RPT
-__global__ void __launch_bounds__(32 * RPT) __maxnreg__(RPT >= 20 ? 96 : (RPT >= 18 ? 104 : (RPT >= 16 ? 120 : 128)))
+__global__ void __launch_bounds__(32 * RPT) __maxnreg__(RPT >= 18 ? 96 : 128)
     jacobi_rr_kernel(const double* __restrict__ A, int64_t lda, int m, int n,
                      double* __restrict__ AV, double* __restrict__ sigma, int max_sweeps,
                      int* __restrict__ flags) {
@@ -147,7 +149,16 @@ int launch_rr(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, double
   const int threads = std::max(32, ((half * kGroup + 31) / 32) * 32);
   jacobi_rr_kernel<RPT><<<1, threads, shm, s>>>(A, lda, int(m), int(n), AV, sigma, 40,
                                                  c.flags.p);
-  return launched();
+  const int rc = launched();
+  if (rc != TT_OK) {
+    cudaFuncAttributes fa;
+    cudaFuncGetAttributes(&fa, jacobi_rr_kernel<RPT>);
+    set_error("jacobi_rr_kernel<%d> launch failed (%d threads, %zu B smem; kernel: %d regs, "
+              "max %d threads, %zu B static smem, max dyn %d B): %s", RPT, threads, shm,
+              fa.numRegs, fa.maxThreadsPerBlock, fa.sharedSizeBytes,
+              fa.maxDynamicSharedSizeBytes, last_error());
+  }
+  return rc;
 }
 
 }  // namespace
