@@ -323,60 +323,66 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
       if (i >= j) S[i + j * ld] = G[e] + ((i == j) ? shift : 0.0);
     }
     __syncthreads();
+    #pragma unroll 1
     for (int k = 0; k < nb; ++k) {
       const int k0 = 32 * k, kb = min(32, n - k0);
-      // ---- C1: diagonal block (warp 0)
+      // ---- C1: diagonal block (warp 0).  Lane i keeps the not yet eliminated
+      // part of row i in a[0..31] (a[0] = current column j; the array shifts
+      // left after every step), so every register index is static and the
+      // column loop stays rolled (a fully unrolled 32x32 elimination is ~100k
+      // instructions and thrashes the instruction cache).
       if (w == 0) {
-        double a[32], x[32];
         const int i = lane;
+        double a[32];
 #pragma unroll
-        for (int j = 0; j < 32; ++j)
-          a[j] = (i < kb && j <= i) ? S[(k0 + i) + (k0 + j) * ld] : 0.0;
+        for (int q = 0; q < 32; ++q)
+          a[q] = (i < kb && q <= i) ? S[(k0 + i) + (k0 + q) * ld] : 0.0;
         bool bad = false;
-#pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          if (j < kb) {
-            double piv = __shfl_sync(0xffffffffu, a[j], j);
-            if (clamp && !(piv > tau) && isfinite(piv)) {   // numerically null direction
-              piv = tau;
-              if (i == j) a[j] = tau;
-              if (lane == 0) s_clamped += 1;
-            }
-            const bool ok = piv > 0.0 && isfinite(piv);
-            bad |= !ok;
-            const double d = ok ? sqrt(piv) : 1.0;
-            if (i > j) a[j] *= 1.0 / d;
-            else if (i == j) a[j] = d;
-#pragma unroll
-            for (int q = j + 1; q < 32; ++q) {
-              const double lqj = __shfl_sync(0xffffffffu, a[j], q);
-              if (i >= q && q < kb) a[q] = fma(-a[j], lqj, a[q]);
-            }
+        #pragma unroll 1
+        for (int j = 0; j < kb; ++j) {
+          double piv = __shfl_sync(0xffffffffu, a[0], j);
+          if (clamp && !(piv > tau) && isfinite(piv)) {   // numerically null direction
+            piv = tau;
+            if (lane == 0) s_clamped += 1;
           }
+          const bool ok = piv > 0.0 && isfinite(piv);
+          bad |= !ok;
+          const double d = ok ? sqrt(piv) : 1.0;
+          const double lij = (i > j && i < kb) ? a[0] * (1.0 / d) : (i == j ? d : 0.0);
+          if (i >= j && i < kb) S[(k0 + i) + (k0 + j) * ld] = lij;
+#pragma unroll
+          for (int q = 1; q < 32; ++q) {
+            const double lqj = __shfl_sync(0xffffffffu, lij, (j + q) & 31);
+            a[q] = fma(-lij, lqj, a[q]);
+          }
+#pragma unroll
+          for (int q = 0; q < 31; ++q) a[q] = a[q + 1];
+          a[31] = 0.0;
         }
+        __syncwarp();
+        // X_kk = L_kk^{-1}: lane i keeps row i of X; step k finalises row k and
+        // eliminates it from the rows below
+        double x[32];
 #pragma unroll
-        for (int j = 0; j < 32; ++j) x[j] = (i == j) ? 1.0 : 0.0;
+        for (int q = 0; q < 32; ++q) x[q] = (i == q) ? 1.0 : 0.0;
+        #pragma unroll 1
+        for (int k = 0; k < kb; ++k) {
+          const double rk = 1.0 / S[(k0 + k) + (k0 + k) * ld];
+          if (i == k) {
 #pragma unroll
-        for (int q = 0; q < 32; ++q) {
-          if (q < kb) {
-            const double lqq = __shfl_sync(0xffffffffu, a[q], q);
-            if (i == q) {
+            for (int q = 0; q < 32; ++q) x[q] *= rk;
+          }
+          const double lik = (i > k && i < kb) ? S[(k0 + i) + (k0 + k) * ld] : 0.0;
 #pragma unroll
-              for (int j = 0; j <= q; ++j) x[j] /= lqq;
-            }
-#pragma unroll
-            for (int j = 0; j <= q; ++j) {
-              const double xqj = __shfl_sync(0xffffffffu, x[j], q);
-              if (i > q) x[j] = fma(-a[q], xqj, x[j]);
-            }
+          for (int q = 0; q < 32; ++q) {
+            const double xkq = __shfl_sync(0xffffffffu, x[q], k);
+            x[q] = fma(-lik, xkq, x[q]);
           }
         }
         if (i < kb) {
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            if (j <= i) S[(k0 + i) + (k0 + j) * ld] = a[j];
-            if (j < i) S[(k0 + j) + (k0 + i) * ld] = x[j];   // X(i, j) parked at (j, i)
-          }
+          for (int q = 0; q < 32; ++q)
+            if (q < i) S[(k0 + q) + (k0 + i) * ld] = x[q];   // X(i, q) parked at (q, i)
         }
         if (bad && lane == 0) s_bad = 1;
       }
@@ -391,7 +397,8 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
         for (int ii = 0; ii < 4; ++ii)
 #pragma unroll
           for (int jj = 0; jj < 4; ++jj) acc[ii][jj] = 0.0;
-        for (int t = 0; t < kb; ++t) {
+      #pragma unroll 1
+      for (int t = 0; t < kb; ++t) {
           double av[4], xv[4];
 #pragma unroll
           for (int ii = 0; ii < 4; ++ii) {
@@ -420,6 +427,7 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
       }
       __syncthreads();
       // ---- C3: trailing A(r, c) -= sum_t L(r, t) L(c, t), block columns j > k
+      #pragma unroll 1
       for (int j = k + 1; j < nb; ++j) {
         const int j0 = 32 * j, jb = min(32, n - j0);
         double acc[4][4];
@@ -427,7 +435,8 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
         for (int ii = 0; ii < 4; ++ii)
 #pragma unroll
           for (int jj = 0; jj < 4; ++jj) acc[ii][jj] = 0.0;
-        for (int t = 0; t < kb; ++t) {
+      #pragma unroll 1
+      for (int t = 0; t < kb; ++t) {
           double lv[4], cv[4];
 #pragma unroll
           for (int ii = 0; ii < 4; ++ii) {
@@ -479,6 +488,7 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
     }
   __syncthreads();
   // ---- X = L^{-1} in place, block columns right to left
+  #pragma unroll 1
   for (int k = nb - 1; k >= 0; --k) {
     const int k0 = 32 * k, kb = min(32, n - k0);
     const int r0 = k0 + kb;
@@ -489,6 +499,7 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
       for (int ii = 0; ii < 4; ++ii)
 #pragma unroll
         for (int jj = 0; jj < 4; ++jj) acc[ii][jj] = 0.0;
+      #pragma unroll 1
       for (int t = r0; t < n; ++t) {
         double xv[4], av[4];
 #pragma unroll
@@ -520,6 +531,7 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
       for (int ii = 0; ii < 4; ++ii)
 #pragma unroll
         for (int jj = 0; jj < 4; ++jj) acc[ii][jj] = 0.0;
+      #pragma unroll 1
       for (int t = 0; t < kb; ++t) {
         double av[4], xv[4];
 #pragma unroll
