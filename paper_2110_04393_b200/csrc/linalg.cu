@@ -262,19 +262,24 @@ __global__ void __launch_bounds__(kCholThreads)
   }
 }
 
-// Blocked Cholesky + in-place triangular inverse for n <= 32*NB (one CTA of 256
-// threads).  Same contract and flags as chol_inv_kernel.  The n x n working
-// matrix S (ld odd) holds L in its lower triangle.  Per 32-column block k:
-//  C1  warp 0 factors the diagonal block in registers (lane i = row i, 496
-//      shuffles) and inverts it (X_kk = L_kk^{-1}); X_kk's strictly lower part
-//      is parked transposed in the (unused) upper triangle of the block;
-//  C2  panel L_ik = A_ik X_kk^T (register tiles: lane = row, warp = column);
-//  C3  trailing update A_ij -= L_ik L_jk^T.
-// Then X = L^{-1} in place, block columns right to left (LAPACK dtrtri order):
-//  I1  A21 <- X22 A21,  I2  A21 <- -A21 X11,  I3  X11 into the lower triangle.
-// Three __syncthreads per block and phase instead of one per column.
-constexpr int kBlkThreads = 256;
+constexpr int kBlkThreads = 512;
 
+// Blocked Cholesky + in-place triangular inverse for n <= 32*NB (one CTA of
+// 512 threads, 16 warps).  Same contract and flags as chol_inv_kernel.  The
+// n x n working matrix S (odd ld) holds L in its lower triangle.  Per 32-column
+// block k:
+//  C1  warp 0 factors the diagonal block: lane i keeps the not yet eliminated
+//      part of row i in registers, shifted left after every pivot (static
+//      register indices in a rolled loop: fully unrolled elimination code is
+//      executed once per block and thrashes the instruction cache);
+//  C2  panel L_ik = A_ik L_kk^{-T} by forward substitution, 4 threads per row
+//      (8 columns each, quad shuffles between the quarters);
+//  C3  trailing update A_ij -= L_ik L_jk^T (register tiles: lane = row,
+//      warp = column).
+// Then X = L^{-1} in place: I0 all diagonal blocks X_kk at once (one warp per
+// block, column-wise forward substitution, parked in the unused upper triangle),
+// then block columns right to left (LAPACK dtrtri order): I1 A21 <- X22 A21,
+// I2 A21 <- -A21 X11, I3 X11 into the lower triangle.
 template <int NB>
 __global__ void __launch_bounds__(kBlkThreads, 1)
     chol_blk_kernel(const double* __restrict__ G, int n, int64_t m, int mode,
@@ -282,11 +287,12 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
                     int* __restrict__ flags, const int* gate, int gate_val) {
   if (gate && *gate != gate_val) return;
   extern __shared__ double S[];
+  __shared__ double rdiag[32 * NB];   // 1 / L(i, i)
   __shared__ double s_tr, s_dmax;
   __shared__ int s_bad, s_zero, s_clamped;
+  constexpr int NW = kBlkThreads / 32;   // 16 warps: tile columns w, w + 16
   const int ld = (n & 1) ? n : n + 1;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  constexpr int NW = kBlkThreads / 32;
   const int nb = (n + 31) / 32;
   const int md = mode & 0xff;
   if (tid == 0) { s_bad = 0; s_zero = 0; s_clamped = 0; }
@@ -315,157 +321,128 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
   const double shift = shifted ? 11.0 * (double(m) * n + double(n) * (n + 1)) * 0x1p-53 * s_tr : 0.0;
   const bool clamp = md == CH_RCLAMP;
   const double tau = 64.0 * n * 0x1p-53 * s_dmax;
-  bool bad_final = s_bad;
-  {
-    __syncthreads();
-    for (int e = tid; e < n * n; e += kBlkThreads) {
-      const int i = e % n, j = e / n;
-      if (i >= j) S[i + j * ld] = G[e] + ((i == j) ? shift : 0.0);
-    }
-    __syncthreads();
-    #pragma unroll 1
-    for (int k = 0; k < nb; ++k) {
-      const int k0 = 32 * k, kb = min(32, n - k0);
-      // ---- C1: diagonal block (warp 0).  Lane i keeps the not yet eliminated
-      // part of row i in a[0..31] (a[0] = current column j; the array shifts
-      // left after every step), so every register index is static and the
-      // column loop stays rolled (a fully unrolled 32x32 elimination is ~100k
-      // instructions and thrashes the instruction cache).
-      if (w == 0) {
-        const int i = lane;
-        double a[32];
-#pragma unroll
-        for (int q = 0; q < 32; ++q)
-          a[q] = (i < kb && q <= i) ? S[(k0 + i) + (k0 + q) * ld] : 0.0;
-        bool bad = false;
-        #pragma unroll 1
-        for (int j = 0; j < kb; ++j) {
-          double piv = __shfl_sync(0xffffffffu, a[0], j);
-          if (clamp && !(piv > tau) && isfinite(piv)) {   // numerically null direction
-            piv = tau;
-            if (lane == 0) s_clamped += 1;
-          }
-          const bool ok = piv > 0.0 && isfinite(piv);
-          bad |= !ok;
-          const double d = ok ? sqrt(piv) : 1.0;
-          const double lij = (i > j && i < kb) ? a[0] * (1.0 / d) : (i == j ? d : 0.0);
-          if (i >= j && i < kb) S[(k0 + i) + (k0 + j) * ld] = lij;
-#pragma unroll
-          for (int q = 1; q < 32; ++q) {
-            const double lqj = __shfl_sync(0xffffffffu, lij, (j + q) & 31);
-            a[q] = fma(-lij, lqj, a[q]);
-          }
-#pragma unroll
-          for (int q = 0; q < 31; ++q) a[q] = a[q + 1];
-          a[31] = 0.0;
-        }
-        __syncwarp();
-        // X_kk = L_kk^{-1}: lane i keeps row i of X; step k finalises row k and
-        // eliminates it from the rows below
-        double x[32];
-#pragma unroll
-        for (int q = 0; q < 32; ++q) x[q] = (i == q) ? 1.0 : 0.0;
-        #pragma unroll 1
-        for (int k = 0; k < kb; ++k) {
-          const double rk = 1.0 / S[(k0 + k) + (k0 + k) * ld];
-          if (i == k) {
-#pragma unroll
-            for (int q = 0; q < 32; ++q) x[q] *= rk;
-          }
-          const double lik = (i > k && i < kb) ? S[(k0 + i) + (k0 + k) * ld] : 0.0;
-#pragma unroll
-          for (int q = 0; q < 32; ++q) {
-            const double xkq = __shfl_sync(0xffffffffu, x[q], k);
-            x[q] = fma(-lik, xkq, x[q]);
-          }
-        }
-        if (i < kb) {
-#pragma unroll
-          for (int q = 0; q < 32; ++q)
-            if (q < i) S[(k0 + q) + (k0 + i) * ld] = x[q];   // X(i, q) parked at (q, i)
-        }
-        if (bad && lane == 0) s_bad = 1;
-      }
-      __syncthreads();
-      if (s_bad) break;
-      const int r0 = k0 + kb;   // first row below the block
-      if (r0 >= n) break;
-      // ---- C2: panel L(r, c) = sum_{t <= c} A(r, t) X_kk(c, t)
-      {
-        double acc[4][4];
-#pragma unroll
-        for (int ii = 0; ii < 4; ++ii)
-#pragma unroll
-          for (int jj = 0; jj < 4; ++jj) acc[ii][jj] = 0.0;
-      #pragma unroll 1
-      for (int t = 0; t < kb; ++t) {
-          double av[4], xv[4];
-#pragma unroll
-          for (int ii = 0; ii < 4; ++ii) {
-            const int r = r0 + lane + 32 * ii;
-            av[ii] = (r < n) ? S[r + (k0 + t) * ld] : 0.0;
-          }
-#pragma unroll
-          for (int jj = 0; jj < 4; ++jj) {
-            const int c = w + NW * jj;   // column within the block
-            xv[jj] = (c >= kb || t > c) ? 0.0
-                     : (t == c ? 1.0 / S[(k0 + c) + (k0 + c) * ld] : S[(k0 + t) + (k0 + c) * ld]);
-          }
-#pragma unroll
-          for (int ii = 0; ii < 4; ++ii)
-#pragma unroll
-            for (int jj = 0; jj < 4; ++jj) acc[ii][jj] = fma(av[ii], xv[jj], acc[ii][jj]);
-        }
-        __syncthreads();
-#pragma unroll
-        for (int ii = 0; ii < 4; ++ii)
-#pragma unroll
-          for (int jj = 0; jj < 4; ++jj) {
-            const int r = r0 + lane + 32 * ii, c = w + NW * jj;
-            if (r < n && c < kb) S[r + (k0 + c) * ld] = acc[ii][jj];
-          }
-      }
-      __syncthreads();
-      // ---- C3: trailing A(r, c) -= sum_t L(r, t) L(c, t), block columns j > k
-      #pragma unroll 1
-      for (int j = k + 1; j < nb; ++j) {
-        const int j0 = 32 * j, jb = min(32, n - j0);
-        double acc[4][4];
-#pragma unroll
-        for (int ii = 0; ii < 4; ++ii)
-#pragma unroll
-          for (int jj = 0; jj < 4; ++jj) acc[ii][jj] = 0.0;
-      #pragma unroll 1
-      for (int t = 0; t < kb; ++t) {
-          double lv[4], cv[4];
-#pragma unroll
-          for (int ii = 0; ii < 4; ++ii) {
-            const int r = j0 + lane + 32 * ii;
-            lv[ii] = (r < n) ? S[r + (k0 + t) * ld] : 0.0;
-          }
-#pragma unroll
-          for (int jj = 0; jj < 4; ++jj) {
-            const int c = j0 + w + NW * jj;
-            cv[jj] = (c < j0 + jb) ? S[c + (k0 + t) * ld] : 0.0;
-          }
-#pragma unroll
-          for (int ii = 0; ii < 4; ++ii)
-#pragma unroll
-            for (int jj = 0; jj < 4; ++jj) acc[ii][jj] = fma(lv[ii], cv[jj], acc[ii][jj]);
-        }
-#pragma unroll
-        for (int ii = 0; ii < 4; ++ii)
-#pragma unroll
-          for (int jj = 0; jj < 4; ++jj) {
-            const int r = j0 + lane + 32 * ii, c = j0 + w + NW * jj;
-            if (r < n && c < j0 + jb && r >= c) S[r + c * ld] -= acc[ii][jj];
-          }
-      }
-      __syncthreads();
-    }
-    bad_final = s_bad;
+  for (int e = tid; e < n * n; e += kBlkThreads) {
+    const int i = e % n, j = e / n;
+    if (i >= j) S[i + j * ld] = G[e] + ((i == j) ? shift : 0.0);
   }
   __syncthreads();
+#pragma unroll 1
+  for (int k = 0; k < nb; ++k) {
+    const int k0 = 32 * k, kb = min(32, n - k0);
+    // ---- C1 (warp 0)
+    if (w == 0) {
+      const int i = lane;
+      double a[32];
+#pragma unroll
+      for (int q = 0; q < 32; ++q)
+        a[q] = (i < kb && q <= i) ? S[(k0 + i) + (k0 + q) * ld] : 0.0;
+      bool bad = false;
+#pragma unroll 1
+      for (int j = 0; j < kb; ++j) {   // a[0] is column j of row i
+        double piv = __shfl_sync(0xffffffffu, a[0], j);
+        if (clamp && !(piv > tau) && isfinite(piv)) {   // numerically null direction
+          piv = tau;
+          if (lane == 0) s_clamped += 1;
+        }
+        const bool ok = piv > 0.0 && isfinite(piv);
+        bad |= !ok;
+        const double d = ok ? sqrt(piv) : 1.0;
+        const double rd = 1.0 / d;
+        const double lij = (i > j) ? a[0] * rd : (i == j ? d : 0.0);
+        if (i >= j && i < kb) S[(k0 + i) + (k0 + j) * ld] = lij;
+        if (i == j) rdiag[k0 + j] = rd;
+#pragma unroll
+        for (int q = 1; q < 32; ++q) {
+          const double lqj = __shfl_sync(0xffffffffu, lij, (j + q) & 31);
+          a[q] = fma(-lij, lqj, a[q]);
+        }
+#pragma unroll
+        for (int q = 0; q < 31; ++q) a[q] = a[q + 1];
+        a[31] = 0.0;
+      }
+      if (bad && lane == 0) s_bad = 1;
+    }
+    __syncthreads();
+    if (s_bad) break;
+    const int r0 = k0 + kb;   // first row below the block (kb == 32 if r0 < n)
+    if (r0 >= n) break;
+    // ---- C2: panel, row r by 4 threads (columns 8q .. 8q+7 of the block)
+    {
+      const int rho = tid >> 2, qt = tid & 3;
+      const int r = r0 + rho;
+      const bool live = r < n;
+      const unsigned qmask = 0xFu << (lane & 28);
+      double a[8];
+#pragma unroll
+      for (int jj = 0; jj < 8; ++jj) a[jj] = live ? S[r + (k0 + 8 * qt + jj) * ld] : 0.0;
+#pragma unroll
+      for (int qq = 0; qq < 4; ++qq) {
+        if (qt == qq) {
+#pragma unroll
+          for (int jj = 0; jj < 8; ++jj) {
+            const int c = 8 * qq + jj;
+            a[jj] *= rdiag[k0 + c];
+#pragma unroll
+            for (int j2 = jj + 1; j2 < 8; ++j2)
+              a[j2] = fma(-a[jj], S[(k0 + 8 * qq + j2) + (k0 + c) * ld], a[j2]);
+          }
+        }
+        double xq[8];
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj) xq[jj] = __shfl_sync(qmask, a[jj], (lane & 28) | qq);
+        if (qt > qq) {
+#pragma unroll
+          for (int j2 = 0; j2 < 8; ++j2) {
+            const int c2 = 8 * qt + j2;
+            double acc = a[j2];
+#pragma unroll
+            for (int jj = 0; jj < 8; ++jj)
+              acc = fma(-xq[jj], S[(k0 + c2) + (k0 + 8 * qq + jj) * ld], acc);
+            a[j2] = acc;
+          }
+        }
+      }
+      if (live) {
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj) S[r + (k0 + 8 * qt + jj) * ld] = a[jj];
+      }
+    }
+    __syncthreads();
+    // ---- C3: trailing A(r, c) -= sum_t L(r, t) L(c, t), block columns j > k
+#pragma unroll 1
+    for (int j = k + 1; j < nb; ++j) {
+      const int j0 = 32 * j, jb = min(32, n - j0);
+      double acc[4][2] = {};
+#pragma unroll 4
+      for (int t = 0; t < 32; ++t) {
+        double lv[4], cv[2];
+#pragma unroll
+        for (int ii = 0; ii < 4; ++ii) {
+          const int r = j0 + lane + 32 * ii;
+          lv[ii] = (r < n) ? S[r + (k0 + t) * ld] : 0.0;
+        }
+#pragma unroll
+        for (int jj = 0; jj < 2; ++jj) {
+          const int c = j0 + w + NW * jj;
+          cv[jj] = (c < j0 + jb) ? S[c + (k0 + t) * ld] : 0.0;
+        }
+#pragma unroll
+        for (int ii = 0; ii < 4; ++ii)
+#pragma unroll
+          for (int jj = 0; jj < 2; ++jj) acc[ii][jj] = fma(lv[ii], cv[jj], acc[ii][jj]);
+      }
+#pragma unroll
+      for (int ii = 0; ii < 4; ++ii)
+#pragma unroll
+        for (int jj = 0; jj < 2; ++jj) {
+          const int r = j0 + lane + 32 * ii, c = j0 + w + NW * jj;
+          if (r < n && c < j0 + jb && r >= c) S[r + c * ld] -= acc[ii][jj];
+        }
+    }
+    __syncthreads();
+  }
+  __syncthreads();
+  const bool bad_final = s_bad;
   // route checks on diag(L); R = L^T before L is overwritten by its inverse
   if (tid == 0 && !s_zero && !(flags[2] & 1)) {
     int bad2 = bad_final;
@@ -486,93 +463,105 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
       const int r = e % n, c = e / n;   // R(r, c) = L(c, r)
       Rout[e] = (c >= r) ? S[c + r * ld] : 0.0;
     }
+  // ---- I0: X_kk = L_kk^{-1} for every block at once (warp k), lane c = column
+  // c; X(r, c) (r > c) is parked at (c, r), the diagonal is rdiag
+  if (w < nb) {
+    const int k0 = 32 * w, kb = min(32, n - k0);
+    const int c = lane;
+    if (c < kb) {
+#pragma unroll 1
+      for (int r = c + 1; r < kb; ++r) {
+        double acc0 = -S[(k0 + r) + (k0 + c) * ld] * rdiag[k0 + c], acc1 = 0.0;
+        int t = c + 1;
+#pragma unroll 1
+        for (; t + 1 < r; t += 2) {
+          acc0 = fma(-S[(k0 + r) + (k0 + t) * ld], S[(k0 + c) + (k0 + t) * ld], acc0);
+          acc1 = fma(-S[(k0 + r) + (k0 + t + 1) * ld], S[(k0 + c) + (k0 + t + 1) * ld], acc1);
+        }
+        if (t < r) acc0 = fma(-S[(k0 + r) + (k0 + t) * ld], S[(k0 + c) + (k0 + t) * ld], acc0);
+        S[(k0 + c) + (k0 + r) * ld] = (acc0 + acc1) * rdiag[k0 + r];
+      }
+    }
+  }
   __syncthreads();
   // ---- X = L^{-1} in place, block columns right to left
-  #pragma unroll 1
+#pragma unroll 1
   for (int k = nb - 1; k >= 0; --k) {
     const int k0 = 32 * k, kb = min(32, n - k0);
     const int r0 = k0 + kb;
     if (r0 < n) {
-      // I1: A21 <- X22 A21  (X22 final lower triangle of rows/cols >= r0)
-      double acc[4][4];
-#pragma unroll
-      for (int ii = 0; ii < 4; ++ii)
-#pragma unroll
-        for (int jj = 0; jj < 4; ++jj) acc[ii][jj] = 0.0;
-      #pragma unroll 1
+      // I1: A21 <- X22 A21  (X22: final lower triangle of rows/cols >= r0)
+      double acc[4][2] = {};
+#pragma unroll 4
       for (int t = r0; t < n; ++t) {
-        double xv[4], av[4];
+        double xv[4], av[2];
 #pragma unroll
         for (int ii = 0; ii < 4; ++ii) {
           const int r = r0 + lane + 32 * ii;
           xv[ii] = (r < n && t <= r) ? S[r + t * ld] : 0.0;
         }
 #pragma unroll
-        for (int jj = 0; jj < 4; ++jj) {
-          const int c = w + NW * jj;
-          av[jj] = (c < kb) ? S[t + (k0 + c) * ld] : 0.0;
-        }
+        for (int jj = 0; jj < 2; ++jj) av[jj] = S[t + (k0 + w + NW * jj) * ld];
 #pragma unroll
         for (int ii = 0; ii < 4; ++ii)
 #pragma unroll
-          for (int jj = 0; jj < 4; ++jj) acc[ii][jj] = fma(xv[ii], av[jj], acc[ii][jj]);
+          for (int jj = 0; jj < 2; ++jj) acc[ii][jj] = fma(xv[ii], av[jj], acc[ii][jj]);
       }
       __syncthreads();
 #pragma unroll
       for (int ii = 0; ii < 4; ++ii)
 #pragma unroll
-        for (int jj = 0; jj < 4; ++jj) {
+        for (int jj = 0; jj < 2; ++jj) {
           const int r = r0 + lane + 32 * ii, c = w + NW * jj;
-          if (r < n && c < kb) S[r + (k0 + c) * ld] = acc[ii][jj];
+          if (r < n) S[r + (k0 + c) * ld] = acc[ii][jj];
         }
       __syncthreads();
-      // I2: A21 <- -A21 X11, X11(t, c) (t > c) parked at (c, t), diag 1/L(c, c)
+      // I2: A21 <- -A21 X11
 #pragma unroll
       for (int ii = 0; ii < 4; ++ii)
 #pragma unroll
-        for (int jj = 0; jj < 4; ++jj) acc[ii][jj] = 0.0;
-      #pragma unroll 1
-      for (int t = 0; t < kb; ++t) {
-        double av[4], xv[4];
+        for (int jj = 0; jj < 2; ++jj) acc[ii][jj] = 0.0;
+#pragma unroll 4
+      for (int t = 0; t < 32; ++t) {
+        double av[4], xv[2];
 #pragma unroll
         for (int ii = 0; ii < 4; ++ii) {
           const int r = r0 + lane + 32 * ii;
           av[ii] = (r < n) ? S[r + (k0 + t) * ld] : 0.0;
         }
 #pragma unroll
-        for (int jj = 0; jj < 4; ++jj) {
+        for (int jj = 0; jj < 2; ++jj) {
           const int c = w + NW * jj;
-          xv[jj] = (c >= kb || t < c) ? 0.0
-                   : (t == c ? 1.0 / S[(k0 + c) + (k0 + c) * ld] : S[(k0 + c) + (k0 + t) * ld]);
+          xv[jj] = (t < c) ? 0.0 : (t == c ? rdiag[k0 + c] : S[(k0 + c) + (k0 + t) * ld]);
         }
 #pragma unroll
         for (int ii = 0; ii < 4; ++ii)
 #pragma unroll
-          for (int jj = 0; jj < 4; ++jj) acc[ii][jj] = fma(av[ii], xv[jj], acc[ii][jj]);
+          for (int jj = 0; jj < 2; ++jj) acc[ii][jj] = fma(av[ii], xv[jj], acc[ii][jj]);
       }
       __syncthreads();
 #pragma unroll
       for (int ii = 0; ii < 4; ++ii)
 #pragma unroll
-        for (int jj = 0; jj < 4; ++jj) {
+        for (int jj = 0; jj < 2; ++jj) {
           const int r = r0 + lane + 32 * ii, c = w + NW * jj;
-          if (r < n && c < kb) S[r + (k0 + c) * ld] = -acc[ii][jj];
+          if (r < n) S[r + (k0 + c) * ld] = -acc[ii][jj];
         }
       __syncthreads();
     }
     // I3: X11 into the lower triangle of the diagonal block
-    double v[4];
+    double v[2];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
+    for (int q = 0; q < 2; ++q) {
       const int e = tid + kBlkThreads * q;   // 1024 = 32 x 32 slots
       const int a = e % 32, b = e / 32;      // X(a, b), a >= b
       v[q] = 0.0;
       if (a < kb && b < kb && a >= b)
-        v[q] = (a == b) ? 1.0 / S[(k0 + a) + (k0 + a) * ld] : S[(k0 + b) + (k0 + a) * ld];
+        v[q] = (a == b) ? rdiag[k0 + a] : S[(k0 + b) + (k0 + a) * ld];
     }
     __syncthreads();
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
+    for (int q = 0; q < 2; ++q) {
       const int e = tid + kBlkThreads * q;
       const int a = e % 32, b = e / 32;
       if (a < kb && b < kb && a >= b) S[(k0 + a) + (k0 + b) * ld] = v[q];
@@ -584,6 +573,8 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
     Rinv[e] = (c >= r) ? S[c + r * ld] : 0.0;
   }
 }
+
+__global__ void route_start_kernel(int* flags) { flags[0] = flags[0] >= 1 ? 1 : 0; }
 
 __global__ void gated_set_kernel(int* flag, int from, int to) {
   if (*flag == from) *flag = to;
@@ -947,7 +938,12 @@ int qr(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, bool trans, d
     TTR_TRY(dalloc(Rtmp, size_t(n) * n, s));
   }
   int* F = c.flags.p;
-  TTR_CUDA(cudaMemsetAsync(F, 0, sizeof(int), s));          // route state 0
+  // starting route: 0 (CholeskyQR2), or 1 when the previous QR of this call
+  // sequence needed a shifted route -- the sweep's sketches Y_n have similar
+  // conditioning from bond to bond, so a failed CholeskyQR2 attempt is not
+  // repeated at every step (flags are cleared at the start of every rounding)
+  route_start_kernel<<<1, 1, 0, s>>>(F);
+  TTR_TRY(launched());
   const int copy_blocks = int(std::min<int64_t>((int64_t(m) * n + 255) / 256, c.sm_count * 8));
   double* Rk_p = R ? Rk.p : nullptr;
 
@@ -1042,8 +1038,8 @@ int qr(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, bool trans, d
   // ---- route 0: CholeskyQR2, accepted when pass 2 finds Q1 close to
   // orthonormal (|diag R2 - 1| <= kDevTol).  The route state F[0] lives on the
   // device; every launch of an inactive route is a no-op.
-  TTR_TRY(gram_of_input(nullptr, 0));                       // pass 1 on the input
-  TTR_TRY(chol(CH_FIRST, nullptr, 0));
+  TTR_TRY(gram_of_input(F, 0));                             // pass 1 on the input
+  TTR_TRY(chol(CH_FIRST, F, 0));
   TTR_TRY(copy_r_first(F, 0));
   TTR_TRY(input_times_rinv(T1.p, F, 0));                    // Q1 -> T1
   TTR_TRY(gram(T1.p, F, 0));                                // pass 2
