@@ -264,22 +264,36 @@ __global__ void __launch_bounds__(kCholThreads)
 
 constexpr int kBlkThreads = 512;
 
+__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+// leading dimension of the Cholesky working matrix: >= round8(n) + 4 and
+// == 4 (mod 16) doubles, so DMMA fragment loads (8 rows x 4 columns) are
+// conflict-free
+__host__ __device__ __forceinline__ int chol_ld(int n) {
+  const int n8 = (n + 7) & ~7;
+  return n8 + ((20 - n8 % 16) % 16);
+}
+
 // Blocked Cholesky + in-place triangular inverse for n <= 32*NB (one CTA of
 // 512 threads, 16 warps).  Same contract and flags as chol_inv_kernel.  The
-// n x n working matrix S (odd ld) holds L in its lower triangle.  Per 32-column
-// block k:
+// working matrix S (ld = chol_ld(n), columns padded to a multiple of 8) holds L
+// in its lower triangle.  Per 32-column block k:
 //  C1  warp 0 factors the diagonal block: lane i keeps the not yet eliminated
 //      part of row i in registers, shifted left after every pivot (static
-//      register indices in a rolled loop: fully unrolled elimination code is
-//      executed once per block and thrashes the instruction cache);
+//      register indices in a rolled loop: fully unrolled elimination code runs
+//      once per block and thrashes the instruction cache);
 //  C2  panel L_ik = A_ik L_kk^{-T} by forward substitution, 4 threads per row
 //      (8 columns each, quad shuffles between the quarters);
-//  C3  trailing update A_ij -= L_ik L_jk^T (register tiles: lane = row,
-//      warp = column).
-// Then X = L^{-1} in place: I0 all diagonal blocks X_kk at once (one warp per
-// block, column-wise forward substitution, parked in the unused upper triangle),
-// then block columns right to left (LAPACK dtrtri order): I1 A21 <- X22 A21,
-// I2 A21 <- -A21 X11, I3 X11 into the lower triangle.
+//  C3  trailing update A_ij -= L_ik L_jk^T on 8x8 DMMA tiles (m8n8k4).
+// Then X = L^{-1} in place: I0 every diagonal block X_kk at once (one warp per
+// block, column-wise forward substitution, parked in the unused upper
+// triangle), then block columns right to left (LAPACK dtrtri order), both on
+// DMMA tiles: I1 A21 <- X22 A21, I2 A21 <- -A21 X11; I3 X11 into the lower
+// triangle.
 template <int NB>
 __global__ void __launch_bounds__(kBlkThreads, 1)
     chol_blk_kernel(const double* __restrict__ G, int n, int64_t m, int mode,
@@ -290,9 +304,11 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
   __shared__ double rdiag[32 * NB];   // 1 / L(i, i)
   __shared__ double s_tr, s_dmax;
   __shared__ int s_bad, s_zero, s_clamped;
-  constexpr int NW = kBlkThreads / 32;   // 16 warps: tile columns w, w + 16
-  const int ld = (n & 1) ? n : n + 1;
+  constexpr int NW = kBlkThreads / 32;
+  const int ld = chol_ld(n);
+  const int n8 = (n + 7) & ~7, nt8 = n8 / 8;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int g = lane >> 2, t4 = lane & 3;   // DMMA fragment coordinates
   const int nb = (n + 31) / 32;
   const int md = mode & 0xff;
   if (tid == 0) { s_bad = 0; s_zero = 0; s_clamped = 0; }
@@ -321,9 +337,9 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
   const double shift = shifted ? 11.0 * (double(m) * n + double(n) * (n + 1)) * 0x1p-53 * s_tr : 0.0;
   const bool clamp = md == CH_RCLAMP;
   const double tau = 64.0 * n * 0x1p-53 * s_dmax;
-  for (int e = tid; e < n * n; e += kBlkThreads) {
-    const int i = e % n, j = e / n;
-    if (i >= j) S[i + j * ld] = G[e] + ((i == j) ? shift : 0.0);
+  for (int e = tid; e < ld * n8; e += kBlkThreads) {   // lower triangle of G (+ shift); pads 0
+    const int i = e % ld, j = e / ld;
+    S[e] = (i < n && j < n && i >= j) ? G[i + int64_t(j) * n] + ((i == j) ? shift : 0.0) : 0.0;
   }
   __syncthreads();
 #pragma unroll 1
@@ -408,36 +424,29 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
       }
     }
     __syncthreads();
-    // ---- C3: trailing A(r, c) -= sum_t L(r, t) L(c, t), block columns j > k
+    // ---- C3: trailing A(r, c) -= sum_t L(r, t) L(c, t) on the lower 8x8 tiles
+    {
+      const int tb = r0 / 8, nrt = nt8 - tb;
+      const int ntiles = nrt * (nrt + 1) / 2;
 #pragma unroll 1
-    for (int j = k + 1; j < nb; ++j) {
-      const int j0 = 32 * j, jb = min(32, n - j0);
-      double acc[4][2] = {};
-#pragma unroll 4
-      for (int t = 0; t < 32; ++t) {
-        double lv[4], cv[2];
+      for (int tt = w; tt < ntiles; tt += NW) {
+        int tr = int((sqrtf(8.0f * tt + 1.0f) - 1.0f) * 0.5f);   // tt = tr(tr+1)/2 + tc
+        while ((tr + 1) * (tr + 2) / 2 <= tt) ++tr;
+        while (tr * (tr + 1) / 2 > tt) --tr;
+        const int tc = tt - tr * (tr + 1) / 2;
+        const int R = 8 * (tb + tr), C = 8 * (tb + tc);
+        double c0 = 0.0, c1 = 0.0;
 #pragma unroll
-        for (int ii = 0; ii < 4; ++ii) {
-          const int r = j0 + lane + 32 * ii;
-          lv[ii] = (r < n) ? S[r + (k0 + t) * ld] : 0.0;
+        for (int kk = 0; kk < 8; ++kk) {
+          const int tcol = k0 + 4 * kk + t4;
+          dmma884(c0, c1, S[(R + g) + tcol * ld], S[(C + g) + tcol * ld]);
         }
-#pragma unroll
-        for (int jj = 0; jj < 2; ++jj) {
-          const int c = j0 + w + NW * jj;
-          cv[jj] = (c < j0 + jb) ? S[c + (k0 + t) * ld] : 0.0;
+        const int r = R + g, cA = C + 2 * t4;
+        if (r < n) {
+          if (cA < n) S[r + cA * ld] -= c0;
+          if (cA + 1 < n) S[r + (cA + 1) * ld] -= c1;
         }
-#pragma unroll
-        for (int ii = 0; ii < 4; ++ii)
-#pragma unroll
-          for (int jj = 0; jj < 2; ++jj) acc[ii][jj] = fma(lv[ii], cv[jj], acc[ii][jj]);
       }
-#pragma unroll
-      for (int ii = 0; ii < 4; ++ii)
-#pragma unroll
-        for (int jj = 0; jj < 2; ++jj) {
-          const int r = j0 + lane + 32 * ii, c = j0 + w + NW * jj;
-          if (r < n && c < j0 + jb && r >= c) S[r + c * ld] -= acc[ii][jj];
-        }
     }
     __syncthreads();
   }
@@ -490,63 +499,71 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
     const int k0 = 32 * k, kb = min(32, n - k0);
     const int r0 = k0 + kb;
     if (r0 < n) {
-      // I1: A21 <- X22 A21  (X22: final lower triangle of rows/cols >= r0)
-      double acc[4][2] = {};
-#pragma unroll 4
-      for (int t = r0; t < n; ++t) {
-        double xv[4], av[2];
+      // tiles of A21: rows [r0, n8) x the 32 block columns; <= 4 per warp
+      const int tb = r0 / 8, nrt = nt8 - tb, ntiles = nrt * 4;
+      double acc[4][2];
+      // I1: A21 <- X22 A21, X22(r, t) = 0 for t > r (parked data is masked)
 #pragma unroll
-        for (int ii = 0; ii < 4; ++ii) {
-          const int r = r0 + lane + 32 * ii;
-          xv[ii] = (r < n && t <= r) ? S[r + t * ld] : 0.0;
+      for (int q = 0; q < 4; ++q) {
+        acc[q][0] = acc[q][1] = 0.0;
+        const int tt = w + NW * q;
+        if (tt < ntiles) {
+          const int R = 8 * (tb + tt / 4), C = k0 + 8 * (tt % 4);
+          const int kend = min(n8, R + 8);
+#pragma unroll 1
+          for (int t0 = r0; t0 < kend; t0 += 4) {
+            const int tcol = t0 + t4;
+            const double av = (tcol <= R + g) ? S[(R + g) + tcol * ld] : 0.0;
+            dmma884(acc[q][0], acc[q][1], av, S[tcol + (C + g) * ld]);
+          }
         }
-#pragma unroll
-        for (int jj = 0; jj < 2; ++jj) av[jj] = S[t + (k0 + w + NW * jj) * ld];
-#pragma unroll
-        for (int ii = 0; ii < 4; ++ii)
-#pragma unroll
-          for (int jj = 0; jj < 2; ++jj) acc[ii][jj] = fma(xv[ii], av[jj], acc[ii][jj]);
       }
       __syncthreads();
 #pragma unroll
-      for (int ii = 0; ii < 4; ++ii)
-#pragma unroll
-        for (int jj = 0; jj < 2; ++jj) {
-          const int r = r0 + lane + 32 * ii, c = w + NW * jj;
-          if (r < n) S[r + (k0 + c) * ld] = acc[ii][jj];
+      for (int q = 0; q < 4; ++q) {
+        const int tt = w + NW * q;
+        if (tt < ntiles) {
+          const int R = 8 * (tb + tt / 4), C = k0 + 8 * (tt % 4);
+          const int r = R + g, cA = C + 2 * t4;
+          if (r < n) {
+            S[r + cA * ld] = acc[q][0];
+            S[r + (cA + 1) * ld] = acc[q][1];
+          }
         }
+      }
       __syncthreads();
-      // I2: A21 <- -A21 X11
+      // I2: A21 <- -A21 X11, X11(t, c) = 0 for t < c, rdiag on the diagonal,
+      // parked at (c, t) below it
 #pragma unroll
-      for (int ii = 0; ii < 4; ++ii)
+      for (int q = 0; q < 4; ++q) {
+        acc[q][0] = acc[q][1] = 0.0;
+        const int tt = w + NW * q;
+        if (tt < ntiles) {
+          const int R = 8 * (tb + tt / 4), cb = 8 * (tt % 4);   // block-local columns
 #pragma unroll
-        for (int jj = 0; jj < 2; ++jj) acc[ii][jj] = 0.0;
-#pragma unroll 4
-      for (int t = 0; t < 32; ++t) {
-        double av[4], xv[2];
-#pragma unroll
-        for (int ii = 0; ii < 4; ++ii) {
-          const int r = r0 + lane + 32 * ii;
-          av[ii] = (r < n) ? S[r + (k0 + t) * ld] : 0.0;
+          for (int kk = 0; kk < 8; ++kk) {
+            const int tl = 4 * kk + t4;   // A fragment column (block-local t)
+            const double av = S[(R + g) + (k0 + tl) * ld];
+            const int cl = cb + g;   // B fragment: X11(tl, cl)
+            const double bv = (tl < cl) ? 0.0
+                              : (tl == cl ? rdiag[k0 + cl] : S[(k0 + cl) + (k0 + tl) * ld]);
+            dmma884(acc[q][0], acc[q][1], av, bv);
+          }
         }
-#pragma unroll
-        for (int jj = 0; jj < 2; ++jj) {
-          const int c = w + NW * jj;
-          xv[jj] = (t < c) ? 0.0 : (t == c ? rdiag[k0 + c] : S[(k0 + c) + (k0 + t) * ld]);
-        }
-#pragma unroll
-        for (int ii = 0; ii < 4; ++ii)
-#pragma unroll
-          for (int jj = 0; jj < 2; ++jj) acc[ii][jj] = fma(av[ii], xv[jj], acc[ii][jj]);
       }
       __syncthreads();
 #pragma unroll
-      for (int ii = 0; ii < 4; ++ii)
-#pragma unroll
-        for (int jj = 0; jj < 2; ++jj) {
-          const int r = r0 + lane + 32 * ii, c = w + NW * jj;
-          if (r < n) S[r + (k0 + c) * ld] = -acc[ii][jj];
+      for (int q = 0; q < 4; ++q) {
+        const int tt = w + NW * q;
+        if (tt < ntiles) {
+          const int R = 8 * (tb + tt / 4), C = k0 + 8 * (tt % 4);
+          const int r = R + g, cA = C + 2 * t4;
+          if (r < n) {
+            S[r + cA * ld] = -acc[q][0];
+            S[r + (cA + 1) * ld] = -acc[q][1];
+          }
         }
+      }
       __syncthreads();
     }
     // I3: X11 into the lower triangle of the diagonal block
@@ -894,8 +911,7 @@ static int launch_chol(Ctx& c, const double* Gm, int n, int64_t m, int mode, dou
                                   220 * 1024));
     attr_done = true;
   }
-  const int ldb = (n & 1) ? n : n + 1;
-  const size_t shm = size_t(ldb) * n * sizeof(double);
+  const size_t shm = size_t(chol_ld(n)) * ((n + 7) & ~7) * sizeof(double);
   if (n <= 32) {
     chol_blk_kernel<1><<<1, kBlkThreads, shm, s>>>(Gm, n, m, mode, Rinv, Rk, c.flags.p, gate, gv);
   } else if (n <= 64) {
