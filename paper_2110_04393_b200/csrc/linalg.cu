@@ -345,7 +345,9 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
 #pragma unroll 1
   for (int k = 0; k < nb; ++k) {
     const int k0 = 32 * k, kb = min(32, n - k0);
-    // ---- C1 (warp 0)
+    // ---- C1 (warp 0): lane i = row i in registers, fully unrolled pivots
+    // (static register indices; ~2k instructions, hot in the instruction
+    // cache from the second block on).  1/L_jj = rsqrt(pivot), L_jj = pivot/L_jj.
     if (w == 0) {
       const int i = lane;
       double a[32];
@@ -353,28 +355,31 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
       for (int q = 0; q < 32; ++q)
         a[q] = (i < kb && q <= i) ? S[(k0 + i) + (k0 + q) * ld] : 0.0;
       bool bad = false;
-#pragma unroll 1
-      for (int j = 0; j < kb; ++j) {   // a[0] is column j of row i
-        double piv = __shfl_sync(0xffffffffu, a[0], j);
-        if (clamp && !(piv > tau) && isfinite(piv)) {   // numerically null direction
-          piv = tau;
-          if (lane == 0) s_clamped += 1;
-        }
-        const bool ok = piv > 0.0 && isfinite(piv);
-        bad |= !ok;
-        const double d = ok ? sqrt(piv) : 1.0;
-        const double rd = 1.0 / d;
-        const double lij = (i > j) ? a[0] * rd : (i == j ? d : 0.0);
-        if (i >= j && i < kb) S[(k0 + i) + (k0 + j) * ld] = lij;
-        if (i == j) rdiag[k0 + j] = rd;
 #pragma unroll
-        for (int q = 1; q < 32; ++q) {
-          const double lqj = __shfl_sync(0xffffffffu, lij, (j + q) & 31);
-          a[q] = fma(-lij, lqj, a[q]);
-        }
+      for (int j = 0; j < 32; ++j) {
+        if (j < kb) {
+          double piv = __shfl_sync(0xffffffffu, a[j], j);
+          if (clamp && !(piv > tau) && isfinite(piv)) {   // numerically null direction
+            piv = tau;
+            if (lane == 0) s_clamped += 1;
+          }
+          const bool ok = piv > 0.0 && isfinite(piv);
+          bad |= !ok;
+          const double rd = ok ? rsqrt(piv) : 1.0;
+          const double lij = (i > j) ? a[j] * rd : (i == j ? piv * rd : 0.0);
+          a[j] = lij;
+          if (i == j) rdiag[k0 + j] = rd;
 #pragma unroll
-        for (int q = 0; q < 31; ++q) a[q] = a[q + 1];
-        a[31] = 0.0;
+          for (int q = j + 1; q < 32; ++q) {
+            const double lqj = __shfl_sync(0xffffffffu, lij, q);
+            if (i >= q) a[q] = fma(-lij, lqj, a[q]);
+          }
+        }
+      }
+      if (i < kb) {
+#pragma unroll
+        for (int q = 0; q < 32; ++q)
+          if (q <= i) S[(k0 + i) + (k0 + q) * ld] = a[q];
       }
       if (bad && lane == 0) s_bad = 1;
     }
