@@ -302,6 +302,7 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
   if (gate && *gate != gate_val) return;
   extern __shared__ double S[];
   __shared__ double rdiag[32 * NB];   // 1 / L(i, i)
+  __shared__ double colb[32];         // pivot column broadcast (C1)
   __shared__ double s_tr, s_dmax;
   __shared__ int s_bad, s_zero, s_clamped;
   constexpr int NW = kBlkThreads / 32;
@@ -345,9 +346,12 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
 #pragma unroll 1
   for (int k = 0; k < nb; ++k) {
     const int k0 = 32 * k, kb = min(32, n - k0);
-    // ---- C1 (warp 0): lane i = row i in registers, fully unrolled pivots
-    // (static register indices; ~2k instructions, hot in the instruction
-    // cache from the second block on).  1/L_jj = rsqrt(pivot), L_jj = pivot/L_jj.
+    // ---- C1 (warp 0): lane i keeps the not yet eliminated part of row i in
+    // registers, a[q] = A(i, j0 + q); pivots in groups of 4 with static
+    // register offsets, then a shift by 4 (a fully unrolled elimination is ~15k
+    // instructions run once per block: instruction-cache bound).  The pivot
+    // column is broadcast through shared memory (colb), 1/L_jj = rsqrt(pivot).
+    // Updates of the upper slots (column > row) are harmless garbage.
     if (w == 0) {
       const int i = lane;
       double a[32];
@@ -355,31 +359,36 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
       for (int q = 0; q < 32; ++q)
         a[q] = (i < kb && q <= i) ? S[(k0 + i) + (k0 + q) * ld] : 0.0;
       bool bad = false;
+      const int kb4 = (kb + 3) & ~3;
+#pragma unroll 1
+      for (int j0 = 0; j0 < kb4; j0 += 4) {
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        if (j < kb) {
-          double piv = __shfl_sync(0xffffffffu, a[j], j);
-          if (clamp && !(piv > tau) && isfinite(piv)) {   // numerically null direction
+        for (int sft = 0; sft < 4; ++sft) {
+          const int j = j0 + sft;
+          double piv = __shfl_sync(0xffffffffu, a[sft], j);
+          if (j >= kb) piv = 1.0;                            // padding pivot
+          if (clamp && !(piv > tau) && isfinite(piv)) {     // numerically null direction
             piv = tau;
             if (lane == 0) s_clamped += 1;
           }
           const bool ok = piv > 0.0 && isfinite(piv);
           bad |= !ok;
           const double rd = ok ? rsqrt(piv) : 1.0;
-          const double lij = (i > j) ? a[j] * rd : (i == j ? piv * rd : 0.0);
-          a[j] = lij;
-          if (i == j) rdiag[k0 + j] = rd;
-#pragma unroll
-          for (int q = j + 1; q < 32; ++q) {
-            const double lqj = __shfl_sync(0xffffffffu, lij, q);
-            if (i >= q) a[q] = fma(-lij, lqj, a[q]);
+          const double lij = (i > j) ? a[sft] * rd : (i == j ? piv * rd : 0.0);
+          if (j < kb) {
+            if (i >= j && i < kb) S[(k0 + i) + (k0 + j) * ld] = lij;
+            if (i == j) rdiag[k0 + j] = rd;
           }
-        }
-      }
-      if (i < kb) {
+          colb[i] = lij;
+          __syncwarp();
 #pragma unroll
-        for (int q = 0; q < 32; ++q)
-          if (q <= i) S[(k0 + i) + (k0 + q) * ld] = a[q];
+          for (int qq = 1; qq < 32 - sft; ++qq)
+            a[sft + qq] = fma(-lij, colb[(j + qq) & 31], a[sft + qq]);
+          __syncwarp();
+        }
+#pragma unroll
+        for (int q = 0; q < 28; ++q) a[q] = a[q + 4];
+        a[28] = a[29] = a[30] = a[31] = 0.0;
       }
       if (bad && lane == 0) s_bad = 1;
     }
