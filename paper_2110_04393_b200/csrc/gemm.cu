@@ -283,25 +283,38 @@ int launch_cfg(Ctx& c, GemmParams& P, int maxM, int maxN, int maxK, cudaStream_t
 
 // tile shapes (DESIGN.md §Kernels / K2): BM, BN, BK, warps_m, warps_n, stages
 using TallS = Shape<128, 48, 16, 4, 2, 4>;   // M >> N ~ l (phase-1 Z, Y_n, Q = Y R^-1)
-using WideS = Shape<48, 128, 16, 2, 4, 4>;   // N >> M ~ l (carry M^(j) H(T))
+using WideS = Shape<48, 128, 16, 2, 4, 4>;   // N >> M ~ l (carry M^(j) H(T), projection)
 using SqS = Shape<64, 64, 16, 2, 2, 4>;      // general / split-K
+using RowS = Shape<64, 48, 16, 4, 2, 4>;     // M = R = 64, N = l = 144 (phase-1 W, split-K)
+using GramS = Shape<48, 48, 16, 2, 2, 4>;    // l x l Grams (split-K)
 using SmallS = Shape<32, 32, 16, 2, 2, 3>;   // tiny problems
 
 template <bool TA, bool TB>
 int dispatch(Ctx& c, GemmParams& P, int maxM, int maxN, int maxK, cudaStream_t s) {
-  // pick the shape that wastes least on ragged edges, preferring big tiles
+  // the shape that wastes least on ragged edges; ties go to the larger tile
+  struct Cand { int bm, bn, id; };
+  static constexpr Cand cands[] = {{128, 48, 0}, {48, 128, 1}, {64, 64, 2}, {64, 48, 3},
+                                   {48, 48, 4}, {32, 32, 5}};
   auto waste = [&](int bm, int bn) {
     const double tm = double((maxM + bm - 1) / bm) * bm, tn = double((maxN + bn - 1) / bn) * bn;
     return (tm * tn) / (double(maxM) * maxN);
   };
-  if (maxM <= 32 && maxN <= 32) return launch_cfg<SmallS, TA, TB>(c, P, maxM, maxN, maxK, s);
-  if (maxM >= 4 * maxN && maxN <= 160 && waste(128, 48) <= 1.35)
-    return launch_cfg<TallS, TA, TB>(c, P, maxM, maxN, maxK, s);
-  if (maxN >= 4 * maxM && maxM <= 160 && waste(48, 128) <= 1.35)
-    return launch_cfg<WideS, TA, TB>(c, P, maxM, maxN, maxK, s);
-  if (waste(64, 64) > 1.6 && waste(32, 32) < waste(64, 64))
-    return launch_cfg<SmallS, TA, TB>(c, P, maxM, maxN, maxK, s);
-  return launch_cfg<SqS, TA, TB>(c, P, maxM, maxN, maxK, s);
+  int best = 5;
+  double bw = 1e30;
+  for (const Cand& x : cands) {
+    // big tiles only where the problem has at least one full tile in each dimension
+    if (x.bm > 32 && (maxM < x.bm / 2 || maxN < x.bn / 2)) continue;
+    const double wv = waste(x.bm, x.bn) * (1.0 - 1e-3 * (x.bm * x.bn) / 6144.0);
+    if (wv < bw) { bw = wv; best = x.id; }
+  }
+  switch (best) {
+    case 0: return launch_cfg<TallS, TA, TB>(c, P, maxM, maxN, maxK, s);
+    case 1: return launch_cfg<WideS, TA, TB>(c, P, maxM, maxN, maxK, s);
+    case 2: return launch_cfg<SqS, TA, TB>(c, P, maxM, maxN, maxK, s);
+    case 3: return launch_cfg<RowS, TA, TB>(c, P, maxM, maxN, maxK, s);
+    case 4: return launch_cfg<GramS, TA, TB>(c, P, maxM, maxN, maxK, s);
+    default: return launch_cfg<SmallS, TA, TB>(c, P, maxM, maxN, maxK, s);
+  }
 }
 
 }  // namespace

@@ -38,6 +38,7 @@ __global__ void __launch_bounds__(32 * RPT) __maxnreg__(RPT >= 18 ? 96 : 128)
   extern __shared__ __align__(16) double W[];   // n x LDW
   __shared__ double red[32];
   __shared__ double nrm[256];
+  __shared__ double cn[256];   // squared column norms
   const int tid = threadIdx.x, nt = blockDim.x;
   const int lane = tid & 31, warp = tid >> 5;
   const int grp = tid / kGroup, t8 = tid % kGroup;
@@ -62,43 +63,58 @@ __global__ void __launch_bounds__(32 * RPT) __maxnreg__(RPT >= 18 ? 96 : 128)
   const int np = (n + 1) & ~1;
   const int half = np / 2;
   const unsigned gmask = 0xFFu << (lane & 24);
+  const int nw = nt / 32;
 
   int sweep = 0;
   bool conv = false;
   for (; sweep < max_sweeps; ++sweep) {
+    // squared column norms, recomputed every sweep and updated analytically
+    // after each rotation (alpha' = alpha - t gamma, beta' = beta + t gamma), so
+    // a round only forms the cross products gamma; a sweep without rotations
+    // (the convergence test) sees exact norms
+    for (int j = warp; j < n; j += nw) {
+      double s2 = 0.0;
+      for (int i = lane; i < m; i += 32) s2 = fma(W[i + j * LDW], W[i + j * LDW], s2);
+      for (int o = 16; o; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+      if (lane == 0) cn[j] = s2;
+    }
     int rot = 0;
+    // circle ordering: group grp pairs (p, q) = (0 or 1 + (grp-1+r) mod (np-1),
+    // 1 + (np-2-grp+r) mod (np-1)), advanced incrementally
+    int pp = grp - 1, qq = np - 2 - grp;
     for (int r = 0; r < np - 1; ++r) {
       __syncthreads();
+      const int p0 = (grp == 0) ? 0 : pp + 1, q0 = qq + 1;
+      pp = (pp + 1 == np - 1) ? 0 : pp + 1;
+      qq = (qq + 1 == np - 1) ? 0 : qq + 1;
       if (grp >= half) continue;
-      int p = (grp == 0) ? 0 : ((grp - 1 + r) % (np - 1)) + 1;
-      int q = ((np - 2 - grp + r) % (np - 1)) + 1;
-      if (p >= n || q >= n) continue;                   // dummy column (odd n)
+      const int p = min(p0, q0), q = max(p0, q0);
+      if (q >= n) continue;                             // dummy column (odd n)
       double2* wp = reinterpret_cast<double2*>(W + p * LDW) + t8;
       double2* wq = reinterpret_cast<double2*>(W + q * LDW) + t8;
       double2 x[S2], y[S2];
-      double al = 0.0, be = 0.0, ga = 0.0;
+      double ga = 0.0;
 #pragma unroll
       for (int s = 0; s < S2; ++s) {
         x[s] = wp[s * kGroup];
         y[s] = wq[s * kGroup];
-        al = fma(x[s].x, x[s].x, fma(x[s].y, x[s].y, al));
-        be = fma(y[s].x, y[s].x, fma(y[s].y, y[s].y, be));
         ga = fma(x[s].x, y[s].x, fma(x[s].y, y[s].y, ga));
       }
 #pragma unroll
-      for (int o = 4; o; o >>= 1) {
-        al += __shfl_xor_sync(gmask, al, o, kGroup);
-        be += __shfl_xor_sync(gmask, be, o, kGroup);
-        ga += __shfl_xor_sync(gmask, ga, o, kGroup);
-      }
-      if (!(fmin(al, be) > small) || !(fabs(ga) > tol * sqrt(al) * sqrt(be))) continue;
+      for (int o = 4; o; o >>= 1) ga += __shfl_xor_sync(gmask, ga, o, kGroup);
+      const double al = cn[p], be = cn[q];
+      if (!(fmin(al, be) > small) || !(fabs(ga) > tol * sqrt(al * be))) continue;
       const double zeta = (be - al) / (2.0 * ga);
       const double tt = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
-      const double cs = 1.0 / sqrt(fma(tt, tt, 1.0)), sn = cs * tt;
+      const double cs = rsqrt(fma(tt, tt, 1.0)), sn = cs * tt;
 #pragma unroll
       for (int s = 0; s < S2; ++s) {
-        wp[s * kGroup] = make_double2(cs * x[s].x - sn * y[s].x, cs * x[s].y - sn * y[s].y);
-        wq[s * kGroup] = make_double2(sn * x[s].x + cs * y[s].x, sn * x[s].y + cs * y[s].y);
+        wp[s * kGroup] = make_double2(fma(cs, x[s].x, -sn * y[s].x), fma(cs, x[s].y, -sn * y[s].y));
+        wq[s * kGroup] = make_double2(fma(sn, x[s].x, cs * y[s].x), fma(sn, x[s].y, cs * y[s].y));
+      }
+      if (t8 == 0) {
+        cn[p] = al - tt * ga;
+        cn[q] = be + tt * ga;
       }
       rot = 1;
     }
@@ -114,7 +130,6 @@ __global__ void __launch_bounds__(32 * RPT) __maxnreg__(RPT >= 18 ? 96 : 128)
   }
   __syncthreads();
   // sigma_j = ||w_j||, then columns sorted by descending norm (ties by index)
-  const int nw = nt / 32;
   for (int j = warp; j < n; j += nw) {
     double s2 = 0.0;
     for (int i = lane; i < m; i += 32) s2 = fma(W[i + j * LDW], W[i + j * LDW], s2);
