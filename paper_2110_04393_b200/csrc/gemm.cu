@@ -203,27 +203,34 @@ __global__ void __launch_bounds__(WM* WN * 32)
   }
 }
 
-// deterministic split-K reduction: slices summed in index order
+// deterministic split-K reduction: slices summed in index order, one output
+// element per thread (grid: tiles x element chunks), slice loads issued ahead
 template <int BM, int BN>
-__global__ void splitk_reduce(const __grid_constant__ GemmParams P) {
+__global__ void __launch_bounds__(256) splitk_reduce(const __grid_constant__ GemmParams P) {
   if (P.gate && *P.gate != P.gate_val) return;
-  const int tn = blockIdx.x, tm = blockIdx.y, b = blockIdx.z;
+  const int tile_id = blockIdx.x;             // (b, tm, tn)
+  const int tn = tile_id % P.tiles_n, tm = (tile_id / P.tiles_n) % P.tiles_m;
+  const int b = tile_id / (P.tiles_n * P.tiles_m);
   const GemmDesc& D = P.d[b];
-  const int m0 = tm * BM, n0 = tn * BN;
-  if (m0 >= D.M || n0 >= D.N) return;
+  const int e = blockIdx.y * 256 + threadIdx.x;
+  if (e >= BM * BN) return;
+  const int ml = e % BM, nl = e / BM;
+  const int m = tm * BM + ml, n = tn * BN + nl;
+  if (m >= D.M || n >= D.N) return;
   const size_t stride = size_t(P.nbatch) * P.tiles_m * P.tiles_n * (BM * BN);
-  const size_t tile = ((size_t(b) * P.tiles_m + tm) * P.tiles_n + tn) * (BM * BN);
-  for (int e = threadIdx.x; e < BM * BN; e += blockDim.x) {
-    const int ml = e % BM, nl = e / BM;
-    const int m = m0 + ml, n = n0 + nl;
-    if (m >= D.M || n >= D.N) continue;
-    double s = 0.0;
-    for (int k = 0; k < P.kslices; ++k) s += P.ws[tile + k * stride + e];
-    double* cp = D.C + m + int64_t(n) * D.ldc;
-    double v = P.alpha * s;
-    if (P.beta != 0.0) v += P.beta * *cp;
-    *cp = v;
+  const double* src = P.ws + ((size_t(b) * P.tiles_m + tm) * P.tiles_n + tn) * (BM * BN) + e;
+  double s = 0.0;
+  int k = 0;
+  for (; k + 4 <= P.kslices; k += 4) {
+    const double v0 = src[k * stride], v1 = src[(k + 1) * stride];
+    const double v2 = src[(k + 2) * stride], v3 = src[(k + 3) * stride];
+    s = (((s + v0) + v1) + v2) + v3;
   }
+  for (; k < P.kslices; ++k) s += src[k * stride];
+  double* cp = D.C + m + int64_t(n) * D.ldc;
+  double v = P.alpha * s;
+  if (P.beta != 0.0) v += P.beta * *cp;
+  *cp = v;
 }
 
 template <int BM, int BN, int BK, int WM, int WN, int STAGES>
@@ -275,7 +282,8 @@ int launch_cfg(Ctx& c, GemmParams& P, int maxM, int maxN, int maxK, cudaStream_t
   kern<<<grid, C::NT, C::SMEM, s>>>(P);
   TTR_TRY(launched());
   if (ksl > 1) {
-    splitk_reduce<S::bm, S::bn><<<dim3(P.tiles_n, P.tiles_m, P.nbatch), 256, 0, s>>>(P);
+    splitk_reduce<S::bm, S::bn><<<dim3(P.tiles_n * P.tiles_m * P.nbatch,
+                                       (S::bm * S::bn + 255) / 256), 256, 0, s>>>(P);
     TTR_TRY(launched());
   }
   return TT_OK;

@@ -16,9 +16,12 @@
 // against a large column re-randomises them) and contribute < 16 m u ||A|| to
 // the tensor; without this test the sweep never stops on the numerically
 // rank-deficient bond matrices of config 5.
+#include <cooperative_groups.h>
 #include <math.h>
 
 #include "common.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace ttr {
 
@@ -181,6 +184,9 @@ int launch_rr(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, double
 // m <= 160: W (n x 8 RPT doubles) fits in shared memory and 8 ceil(n/2) <= 32 RPT
 // threads (the launch bound) for every n <= m
 bool svd_nov_fits(int64_t m, int64_t n) { return n >= 1 && m >= n && m <= 160; }
+bool svd_cluster_fits(int64_t m, int64_t n);
+int svd_nov_cluster(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, double* AV,
+                    double* sigma, cudaStream_t s);
 
 int svd_nov(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, double* AV,
             double* sigma, cudaStream_t s) {
@@ -188,6 +194,7 @@ int svd_nov(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, double* 
     set_error("svd_nov: unsupported shape m=%lld n=%lld", (long long)m, (long long)n);
     return TT_ERR_ARG;
   }
+  if (svd_cluster_fits(m, n)) return svd_nov_cluster(c, m, n, A, lda, AV, sigma, s);
   if (m <= 16) return launch_rr<2>(c, m, n, A, lda, AV, sigma, s);
   if (m <= 32) return launch_rr<4>(c, m, n, A, lda, AV, sigma, s);
   if (m <= 64) return launch_rr<8>(c, m, n, A, lda, AV, sigma, s);
@@ -195,6 +202,237 @@ int svd_nov(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, double* 
   if (m <= 128) return launch_rr<16>(c, m, n, A, lda, AV, sigma, s);
   if (m <= 144) return launch_rr<18>(c, m, n, A, lda, AV, sigma, s);
   return launch_rr<20>(c, m, n, A, lda, AV, sigma, s);
+}
+
+}  // namespace ttr
+
+// ============================================================================
+// Cluster version for 64 <= n <= 160: the same one-sided Jacobi (same rotation
+// formulas, thresholds and convergence test) spread over a cluster of 8 CTAs.
+//
+// Column pairs are "groups" of 16 threads (row t + 16 s of a column per
+// thread); group g of the circle ordering lives in CTA g / GPC_G.  A group
+// keeps its two columns in registers for the round, rotates them and writes
+// them straight into the slots of the groups that own them next round
+// (top row shifts right, bottom row shifts left, position 0 fixed), so the
+// move IS the write-back; only the two columns crossing a CTA boundary go
+// through distributed shared memory.  One cluster barrier per round.
+// ============================================================================
+namespace ttr {
+namespace {
+
+constexpr int kCl = 8;          // CTAs per cluster
+constexpr int kGpc = 9;         // groups per CTA (n <= 144 -> 72 groups)
+constexpr int kG16 = 16;        // threads per group
+constexpr int kRps = 10;        // rows per thread (m <= 160)
+constexpr int kSlot = kG16 * kRps + 2;   // 160 rows + [norm^2, column id]
+
+struct JcShared {
+  double slot[2][kGpc + 2][2][kSlot];   // [buffer][local group][top/bottom][rows, a, id]
+  double norms[kCl * kGpc * 2];         // final column norms (all columns, by id)
+  double red[8];
+  int rot;
+};
+
+__global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kGpc * kG16)
+    jacobi_cluster_kernel(const double* __restrict__ A, int64_t lda, int m, int n, int gpc,
+                          double* __restrict__ AV, double* __restrict__ sigma, int max_sweeps,
+                          int* __restrict__ flags) {
+  extern __shared__ __align__(16) unsigned char jc_raw[];
+  JcShared& sh = *reinterpret_cast<JcShared*>(jc_raw);
+  cg::cluster_group cl = cg::this_cluster();
+  const int crank = int(cl.block_rank());
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int lg = tid / kG16, t16 = tid % kG16;
+  const int np = (n + 1) & ~1, half = np / 2;
+  const int g = crank * gpc + lg;                 // global group index
+  const bool live = lg < gpc && g < half;
+  const unsigned gmask = 0xFFFFu << (lane & 16);
+
+  // initial placement (circle ordering, round 0): group g holds top = column
+  // (g == 0 ? 0 : g), bottom = column np - 1 - g ... expressed through the same
+  // index formulas as the single-CTA kernel: p = 0 or 1 + (g - 1), q = 1 + (np - 2 - g)
+  if (live) {
+    const int colt = (g == 0) ? 0 : g, colb = np - 1 - g;
+    for (int which = 0; which < 2; ++which) {
+      const int col = which ? colb : colt;
+      double* sl = sh.slot[0][lg][which];
+      for (int i = t16; i < kG16 * kRps; i += kG16)
+        sl[i] = (col < n && i < m) ? A[i + int64_t(col) * lda] : 0.0;
+      if (t16 == 0) sl[kG16 * kRps + 1] = double(col);
+    }
+  }
+  // ||A||_F^2 over the cluster
+  double part = 0.0;
+  if (live)
+    for (int which = 0; which < 2; ++which)
+      for (int i = t16; i < kG16 * kRps; i += kG16) {
+        const double v = sh.slot[0][lg][which][i];
+        part = fma(v, v, part);
+      }
+  for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+  if (lane == 0) sh.red[warp] = part;
+  __syncthreads();
+  if (tid == 0) {
+    double s = 0.0;
+    for (int w = 0; w < (blockDim.x + 31) / 32; ++w) s += sh.red[w];
+    for (int r = 0; r < kCl; ++r) cl.map_shared_rank(&sh, r)->norms[crank] = s;   // scratch
+  }
+  cl.sync();
+  double fro2 = 0.0;
+  for (int r = 0; r < kCl; ++r) fro2 += sh.norms[r];
+  cl.sync();
+
+  const double u = 0x1p-53;
+  const double tol = 2.0 * m * u;
+  const double negl = 16.0 * m * u;
+  const double small = negl * negl * fro2;
+
+  // destinations of this group's columns after a round
+  // top:    g == 0 -> (0, top); g < half-1 -> (g+1, top); g == half-1 -> (g, bottom)
+  // bottom: g == 0 -> (1, top); g >= 1 -> (g-1, bottom)
+  auto dest = [&](int gg, int which, int buf) -> double* {
+    const int dc = gg / gpc, dl = gg % gpc;
+    JcShared* dsh = (dc == crank) ? &sh : cl.map_shared_rank(&sh, dc);
+    return dsh->slot[buf][dl][which];
+  };
+  int buf = 0, sweep = 0;
+  bool conv = false;
+  for (; sweep < max_sweeps; ++sweep) {
+    if (tid == 0) sh.rot = 0;
+    int rot = 0;
+    for (int r = 0; r < np - 1; ++r) {
+      if (live) {
+        double* st = sh.slot[buf][lg][0];
+        double* sb = sh.slot[buf][lg][1];
+        double x[kRps], y[kRps];
+        double ga = 0.0, al = 0.0, be = 0.0;
+#pragma unroll
+        for (int s = 0; s < kRps; ++s) {
+          x[s] = st[t16 + kG16 * s];
+          y[s] = sb[t16 + kG16 * s];
+          ga = fma(x[s], y[s], ga);
+        }
+        const int colt = int(st[kG16 * kRps + 1]), colb = int(sb[kG16 * kRps + 1]);
+        if (r == 0) {   // exact squared norms at the start of every sweep
+#pragma unroll
+          for (int s = 0; s < kRps; ++s) {
+            al = fma(x[s], x[s], al);
+            be = fma(y[s], y[s], be);
+          }
+#pragma unroll
+          for (int o = 8; o; o >>= 1) {
+            al += __shfl_xor_sync(gmask, al, o, kG16);
+            be += __shfl_xor_sync(gmask, be, o, kG16);
+          }
+        } else {
+          al = st[kG16 * kRps];
+          be = sb[kG16 * kRps];
+        }
+#pragma unroll
+        for (int o = 8; o; o >>= 1) ga += __shfl_xor_sync(gmask, ga, o, kG16);
+        // (p, q) = (min, max) column index as in the single-CTA kernel
+        const bool swp = colt > colb;
+        const double ap = swp ? be : al, aq = swp ? al : be;
+        double cs = 1.0, sn = 0.0, tt = 0.0;
+        if (colt < n && colb < n && fmin(ap, aq) > small && fabs(ga) > tol * sqrt(ap * aq)) {
+          const double zeta = (aq - ap) / (2.0 * ga);
+          tt = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
+          cs = rsqrt(fma(tt, tt, 1.0));
+          sn = cs * tt;
+          rot = 1;
+        }
+        // xp = column p, xq = column q
+        const int nb = buf ^ 1;
+        double* dt = (g == 0) ? dest(0, 0, nb) : (g < half - 1 ? dest(g + 1, 0, nb) : dest(g, 1, nb));
+        double* db = (g == 0) ? dest(1, 0, nb) : dest(g - 1, 1, nb);
+        const double anew_p = ap - tt * ga, anew_q = aq + tt * ga;
+#pragma unroll
+        for (int s = 0; s < kRps; ++s) {
+          const double xp = swp ? y[s] : x[s], xq = swp ? x[s] : y[s];
+          const double np_ = fma(cs, xp, -sn * xq), nq_ = fma(sn, xp, cs * xq);
+          dt[t16 + kG16 * s] = swp ? nq_ : np_;   // the top column stays the same column
+          db[t16 + kG16 * s] = swp ? np_ : nq_;
+        }
+        if (t16 == 0) {
+          dt[kG16 * kRps] = swp ? anew_q : anew_p;
+          db[kG16 * kRps] = swp ? anew_p : anew_q;
+          dt[kG16 * kRps + 1] = double(colt);
+          db[kG16 * kRps + 1] = double(colb);
+        }
+      }
+      buf ^= 1;
+      cl.sync();
+    }
+    // cluster-wide OR of "rotated in this sweep"
+    if (rot) atomicOr(&cl.map_shared_rank(&sh, 0)->rot, 1);
+    cl.sync();
+    const int any = cl.map_shared_rank(&sh, 0)->rot;
+    cl.sync();
+    if (!any) {
+      conv = true;
+      break;
+    }
+  }
+  if (crank == 0 && tid == 0) {
+    if (!conv) atomicOr(&flags[3], 2);
+    flags[12] += conv ? sweep + 1 : sweep;
+    flags[13] += 1;
+  }
+  // norms of every column into every CTA (by column id), then sort by rank
+  if (live) {
+    for (int which = 0; which < 2; ++which) {
+      const double* sl = sh.slot[buf][lg][which];
+      double s2 = 0.0;
+#pragma unroll
+      for (int s = 0; s < kRps; ++s) s2 = fma(sl[t16 + kG16 * s], sl[t16 + kG16 * s], s2);
+#pragma unroll
+      for (int o = 8; o; o >>= 1) s2 += __shfl_xor_sync(gmask, s2, o, kG16);
+      const int col = int(sl[kG16 * kRps + 1]);
+      if (t16 == 0 && col < n)
+        for (int rr = 0; rr < kCl; ++rr) cl.map_shared_rank(&sh, rr)->norms[col] = sqrt(s2);
+    }
+  }
+  cl.sync();
+  if (live) {
+    for (int which = 0; which < 2; ++which) {
+      const double* sl = sh.slot[buf][lg][which];
+      const int col = int(sl[kG16 * kRps + 1]);
+      if (col >= n) continue;
+      const double sj = sh.norms[col];
+      int rank = 0;
+      for (int k = t16; k < n; k += kG16) {
+        const double sk = sh.norms[k];
+        rank += (sk > sj) || (sk == sj && k < col);
+      }
+#pragma unroll
+      for (int o = 8; o; o >>= 1) rank += __shfl_xor_sync(gmask, rank, o, kG16);
+      for (int i = t16; i < m; i += kG16) AV[i + int64_t(rank) * m] = sl[i];
+      if (t16 == 0) sigma[rank] = sj;
+    }
+  }
+}
+
+}  // namespace
+
+bool svd_cluster_fits(int64_t m, int64_t n) {
+  return n >= 64 && m >= n && m <= kG16 * kRps && (n + 1) / 2 <= kCl * kGpc;
+}
+
+int svd_nov_cluster(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, double* AV,
+                    double* sigma, cudaStream_t s) {
+  static bool attr[64] = {false};
+  const size_t shm = sizeof(JcShared);
+  if (!attr[c.device & 63]) {
+    TTR_CUDA(cudaFuncSetAttribute(jacobi_cluster_kernel,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, int(shm)));
+    attr[c.device & 63] = true;
+  }
+  const int half = int((n + 1) / 2);
+  const int gpc = (half + kCl - 1) / kCl;
+  jacobi_cluster_kernel<<<kCl, kGpc * kG16, shm, s>>>(A, lda, int(m), int(n), gpc, AV, sigma,
+                                                       40, c.flags.p);
+  return launched();
 }
 
 }  // namespace ttr
