@@ -225,16 +225,20 @@ constexpr int kCl = 8;          // CTAs per cluster
 constexpr int kGpc = 9;         // groups per CTA (n <= 144 -> 72 groups)
 constexpr int kG16 = 16;        // threads per group
 constexpr int kRps = 10;        // rows per thread (m <= 160)
-constexpr int kSlot = kG16 * kRps + 2;   // 160 rows + [norm^2, column id]
+constexpr int kRows = kG16 * kRps;       // 160 rows per column slot
 
 struct JcShared {
-  double slot[2][kGpc + 2][2][kSlot];   // [buffer][local group][top/bottom][rows, a, id]
-  double norms[kCl * kGpc * 2];         // final column norms (all columns, by id)
+  double slot[2][kGpc][2][kRows];   // [buffer][local group][top/bottom][rows]
+  double alpha[2][kGpc][2];         // squared norms travelling with the columns
+  int col[2][kGpc][2];              // column ids travelling with the columns
+  double norms[kCl * kGpc * 2];     // final column norms (all columns, by id)
   double red[8];
   int rot;
 };
 
-__global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kGpc * kG16)
+constexpr int kJcThreads = ((kGpc * kG16 + 31) / 32) * 32;   // 160: whole warps
+
+__global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kJcThreads)
     jacobi_cluster_kernel(const double* __restrict__ A, int64_t lda, int m, int n, int gpc,
                           double* __restrict__ AV, double* __restrict__ sigma, int max_sweeps,
                           int* __restrict__ flags) {
@@ -246,27 +250,27 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kGpc * kG16)
   const int lg = tid / kG16, t16 = tid % kG16;
   const int np = (n + 1) & ~1, half = np / 2;
   const int g = crank * gpc + lg;                 // global group index
-  const bool live = lg < gpc && g < half;
-  const unsigned gmask = 0xFFFFu << (lane & 16);
+  const bool live = lg < gpc && lg < kGpc && g < half;
 
-  // initial placement (circle ordering, round 0): group g holds top = column
-  // (g == 0 ? 0 : g), bottom = column np - 1 - g ... expressed through the same
-  // index formulas as the single-CTA kernel: p = 0 or 1 + (g - 1), q = 1 + (np - 2 - g)
-  if (live) {
-    const int colt = (g == 0) ? 0 : g, colb = np - 1 - g;
+  // round 0 of the circle ordering: group g holds top = column g (0 for g = 0)
+  // and bottom = column np - 1 - g (index n is the dummy column of an odd n)
+  if (lg < kGpc) {
     for (int which = 0; which < 2; ++which) {
-      const int col = which ? colb : colt;
+      const int c0 = live ? (which ? np - 1 - g : g) : n;
       double* sl = sh.slot[0][lg][which];
-      for (int i = t16; i < kG16 * kRps; i += kG16)
-        sl[i] = (col < n && i < m) ? A[i + int64_t(col) * lda] : 0.0;
-      if (t16 == 0) sl[kG16 * kRps + 1] = double(col);
+      for (int i = t16; i < kRows; i += kG16)
+        sl[i] = (c0 < n && i < m) ? A[i + int64_t(c0) * lda] : 0.0;
+      if (t16 == 0) {
+        sh.col[0][lg][which] = c0;
+        sh.alpha[0][lg][which] = 0.0;
+      }
     }
   }
   // ||A||_F^2 over the cluster
   double part = 0.0;
-  if (live)
+  if (lg < kGpc)
     for (int which = 0; which < 2; ++which)
-      for (int i = t16; i < kG16 * kRps; i += kG16) {
+      for (int i = t16; i < kRows; i += kG16) {
         const double v = sh.slot[0][lg][which][i];
         part = fma(v, v, part);
       }
@@ -288,23 +292,25 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kGpc * kG16)
   const double negl = 16.0 * m * u;
   const double small = negl * negl * fro2;
 
-  // destinations of this group's columns after a round
+  // where this group's columns go after a round (fixed for the whole run):
   // top:    g == 0 -> (0, top); g < half-1 -> (g+1, top); g == half-1 -> (g, bottom)
   // bottom: g == 0 -> (1, top); g >= 1 -> (g-1, bottom)
-  auto dest = [&](int gg, int which, int buf) -> double* {
-    const int dc = gg / gpc, dl = gg % gpc;
-    JcShared* dsh = (dc == crank) ? &sh : cl.map_shared_rank(&sh, dc);
-    return dsh->slot[buf][dl][which];
-  };
+  const int gt = (g == 0) ? 0 : (g < half - 1 ? g + 1 : g), wt = (g == 0 || g < half - 1) ? 0 : 1;
+  const int gb = (g == 0) ? 1 : g - 1, wb = (g == 0) ? 0 : 1;
+  JcShared* sht = (gt / gpc == crank) ? &sh : cl.map_shared_rank(&sh, gt / gpc);
+  JcShared* shb = (gb / gpc == crank) ? &sh : cl.map_shared_rank(&sh, gb / gpc);
+  const int lt = gt % gpc, lb = gb % gpc;
+  const int lgc = live ? lg : 0;   // non-live groups compute on slot 0 and write nothing
+
   int buf = 0, sweep = 0;
   bool conv = false;
   for (; sweep < max_sweeps; ++sweep) {
     if (tid == 0) sh.rot = 0;
     int rot = 0;
     for (int r = 0; r < np - 1; ++r) {
-      if (live) {
-        double* st = sh.slot[buf][lg][0];
-        double* sb = sh.slot[buf][lg][1];
+      {   // every thread of the CTA (5 full warps) runs this: full-warp shuffles
+        const double* st = sh.slot[buf][lgc][0];
+        const double* sb = sh.slot[buf][lgc][1];
         double x[kRps], y[kRps];
         double ga = 0.0, al = 0.0, be = 0.0;
 #pragma unroll
@@ -313,7 +319,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kGpc * kG16)
           y[s] = sb[t16 + kG16 * s];
           ga = fma(x[s], y[s], ga);
         }
-        const int colt = int(st[kG16 * kRps + 1]), colb = int(sb[kG16 * kRps + 1]);
+        const int colt = sh.col[buf][lgc][0], colb = sh.col[buf][lgc][1];
         if (r == 0) {   // exact squared norms at the start of every sweep
 #pragma unroll
           for (int s = 0; s < kRps; ++s) {
@@ -322,43 +328,44 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kGpc * kG16)
           }
 #pragma unroll
           for (int o = 8; o; o >>= 1) {
-            al += __shfl_xor_sync(gmask, al, o, kG16);
-            be += __shfl_xor_sync(gmask, be, o, kG16);
+            al += __shfl_xor_sync(0xffffffffu, al, o);
+            be += __shfl_xor_sync(0xffffffffu, be, o);
           }
         } else {
-          al = st[kG16 * kRps];
-          be = sb[kG16 * kRps];
+          al = sh.alpha[buf][lgc][0];
+          be = sh.alpha[buf][lgc][1];
         }
 #pragma unroll
-        for (int o = 8; o; o >>= 1) ga += __shfl_xor_sync(gmask, ga, o, kG16);
-        // (p, q) = (min, max) column index as in the single-CTA kernel
+        for (int o = 8; o; o >>= 1) ga += __shfl_xor_sync(0xffffffffu, ga, o);
+        // rotation of (p, q) = (min, max) column ids, applied as T' = c T - s' B,
+        // B' = s' T + c B with s' = -s when the top column is q
         const bool swp = colt > colb;
         const double ap = swp ? be : al, aq = swp ? al : be;
         double cs = 1.0, sn = 0.0, tt = 0.0;
-        if (colt < n && colb < n && fmin(ap, aq) > small && fabs(ga) > tol * sqrt(ap * aq)) {
+        if (live && colt < n && colb < n && fmin(ap, aq) > small &&
+            fabs(ga) > tol * sqrt(ap * aq)) {
           const double zeta = (aq - ap) / (2.0 * ga);
           tt = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
           cs = rsqrt(fma(tt, tt, 1.0));
           sn = cs * tt;
           rot = 1;
         }
-        // xp = column p, xq = column q
-        const int nb = buf ^ 1;
-        double* dt = (g == 0) ? dest(0, 0, nb) : (g < half - 1 ? dest(g + 1, 0, nb) : dest(g, 1, nb));
-        double* db = (g == 0) ? dest(1, 0, nb) : dest(g - 1, 1, nb);
-        const double anew_p = ap - tt * ga, anew_q = aq + tt * ga;
+        if (swp) { sn = -sn; tt = -tt; }
+        if (live) {
+          const int nb = buf ^ 1;
+          double* dt = sht->slot[nb][lt][wt];
+          double* db = shb->slot[nb][lb][wb];
 #pragma unroll
-        for (int s = 0; s < kRps; ++s) {
-          const double xp = swp ? y[s] : x[s], xq = swp ? x[s] : y[s];
-          const double np_ = fma(cs, xp, -sn * xq), nq_ = fma(sn, xp, cs * xq);
-          dt[t16 + kG16 * s] = swp ? nq_ : np_;   // the top column stays the same column
-          db[t16 + kG16 * s] = swp ? np_ : nq_;
-        }
-        if (t16 == 0) {
-          dt[kG16 * kRps] = swp ? anew_q : anew_p;
-          db[kG16 * kRps] = swp ? anew_p : anew_q;
-          dt[kG16 * kRps + 1] = double(colt);
-          db[kG16 * kRps + 1] = double(colb);
+          for (int s = 0; s < kRps; ++s) {
+            dt[t16 + kG16 * s] = fma(cs, x[s], -sn * y[s]);
+            db[t16 + kG16 * s] = fma(sn, x[s], cs * y[s]);
+          }
+          if (t16 == 0) {
+            sht->alpha[nb][lt][wt] = al - tt * ga;
+            shb->alpha[nb][lb][wb] = be + tt * ga;
+            sht->col[nb][lt][wt] = colt;
+            shb->col[nb][lb][wb] = colb;
+          }
         }
       }
       buf ^= 1;
@@ -380,16 +387,16 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kGpc * kG16)
     flags[13] += 1;
   }
   // norms of every column into every CTA (by column id), then sort by rank
-  if (live) {
+  {
     for (int which = 0; which < 2; ++which) {
-      const double* sl = sh.slot[buf][lg][which];
+      const double* sl = sh.slot[buf][lgc][which];
       double s2 = 0.0;
 #pragma unroll
       for (int s = 0; s < kRps; ++s) s2 = fma(sl[t16 + kG16 * s], sl[t16 + kG16 * s], s2);
 #pragma unroll
-      for (int o = 8; o; o >>= 1) s2 += __shfl_xor_sync(gmask, s2, o, kG16);
-      const int col = int(sl[kG16 * kRps + 1]);
-      if (t16 == 0 && col < n)
+      for (int o = 8; o; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+      const int col = sh.col[buf][lgc][which];
+      if (live && t16 == 0 && col < n)
         for (int rr = 0; rr < kCl; ++rr) cl.map_shared_rank(&sh, rr)->norms[col] = sqrt(s2);
     }
   }
@@ -397,7 +404,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kGpc * kG16)
   if (live) {
     for (int which = 0; which < 2; ++which) {
       const double* sl = sh.slot[buf][lg][which];
-      const int col = int(sl[kG16 * kRps + 1]);
+      const int col = sh.col[buf][lg][which];
       if (col >= n) continue;
       const double sj = sh.norms[col];
       int rank = 0;
@@ -406,7 +413,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kGpc * kG16)
         rank += (sk > sj) || (sk == sj && k < col);
       }
 #pragma unroll
-      for (int o = 8; o; o >>= 1) rank += __shfl_xor_sync(gmask, rank, o, kG16);
+      for (int o = 8; o; o >>= 1) rank += __shfl_xor_sync(0xffffu << (lane & 16), rank, o);
       for (int i = t16; i < m; i += kG16) AV[i + int64_t(rank) * m] = sl[i];
       if (t16 == 0) sigma[rank] = sj;
     }
@@ -430,7 +437,7 @@ int svd_nov_cluster(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, 
   }
   const int half = int((n + 1) / 2);
   const int gpc = (half + kCl - 1) / kCl;
-  jacobi_cluster_kernel<<<kCl, kGpc * kG16, shm, s>>>(A, lda, int(m), int(n), gpc, AV, sigma,
+  jacobi_cluster_kernel<<<kCl, kJcThreads, shm, s>>>(A, lda, int(m), int(n), gpc, AV, sigma,
                                                        40, c.flags.p);
   return launched();
 }
