@@ -243,23 +243,35 @@ int launch_cfg(Ctx& c, GemmParams& P, int maxM, int maxN, int maxK, cudaStream_t
   using C = Cfg<S::bm, S::bn, S::bk, S::wm, S::wn, S::st, TA, TB>;
   auto kern = dgemm_kernel<S::bm, S::bn, S::bk, S::wm, S::wn, S::st, TA, TB>;
   static bool attr_set[64] = {false};
+  static int resident[64] = {0};   // CTAs of this configuration per SM
   int dev = c.device;
   if (!attr_set[dev & 63]) {
     TTR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   int(C::SMEM)));
+    int nb = 1;
+    TTR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, C::NT, C::SMEM));
+    resident[dev & 63] = std::max(1, nb);
     attr_set[dev & 63] = true;
   }
   P.tiles_m = (maxM + S::bm - 1) / S::bm;
   P.tiles_n = (maxN + S::bn - 1) / S::bn;
-  // split-K: fill ~2 waves of SMs when the tile grid alone cannot
-  const int ctas_per_sm = std::max(1, int((200 * 1024) / C::SMEM));
+  // split-K, wave-aware: pick the slice count whose grid fills the resident CTA
+  // slots (SMs x CTAs per SM) best -- a grid of 1.13 waves runs at 57% -- with
+  // a small penalty per slice for the extra partial traffic and reduction
+  const long slots = long(c.sm_count) * resident[dev & 63];
   const long tiles = long(P.tiles_m) * P.tiles_n * P.nbatch;
-  const long target = 2L * c.sm_count * ctas_per_sm;
   const int ktiles = (maxK + S::bk - 1) / S::bk;
   int ksl = 1;
-  if (tiles < target) {
-    ksl = int(std::min<long>((target + tiles - 1) / tiles, std::max(1, ktiles / 4)));
-    ksl = std::max(1, std::min(ksl, 64));
+  if (tiles < 3 * slots) {
+    const int kmax = std::max(1, std::min(64, ktiles / 4));
+    double best = -1.0;
+    for (int k = 1; k <= kmax; ++k) {
+      const long ctas = tiles * k;
+      const long waves = (ctas + slots - 1) / slots;
+      const double eff = double(ctas) / double(waves * slots);
+      const double score = eff - 0.004 * k;
+      if (score > best + 1e-12) { best = score; ksl = k; }
+    }
   }
   const int kchunk_tiles = (ktiles + ksl - 1) / ksl;
   ksl = std::max(1, (ktiles + kchunk_tiles - 1) / std::max(1, kchunk_tiles));
