@@ -194,7 +194,8 @@ def main():
 
     wl = make_workload(args.workload, dev)
     S = len(wl.terms)
-    lo, hi = (rank * S) // world, ((rank + 1) * S) // world
+    from paper_2110_04393_b200.shard import shard_bounds
+    lo, hi = shard_bounds(S, world, rank)
     local_terms = wl.terms[lo:hi]
     for t in wl.terms[:lo] + wl.terms[hi:]:
         t.clear()

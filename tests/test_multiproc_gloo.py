@@ -1,0 +1,109 @@
+"""World-size-2 check of the summand-sharded sweep on CPU with gloo.
+
+The CUDA path shards summands over ranks: phase 1 (Alg. 3) and the carries stay
+local, every sweep step all-reduces the partial sketched core Y_n and
+the last core, and the QR of Y_n is replicated.  This test runs that
+exact decomposition with the oracle's primitives on two gloo processes and
+checks it against the unsharded oracle Alg. 7 (oracle.round_sum_rand_orth),
+plus the contiguous shard bounds that bench.py uses."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle
+import ttsynth
+from paper_2110_04393_b200.shard import shard_bounds
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def sharded_alg7(local_terms, G, allreduce):
+    """Alg. 7 with the summands split over ranks: Y_n and the last
+    core are sums over summands, so each rank forms its partial
+    sum and one all-reduce completes it; Q_n is then identical on every rank."""
+    N = len(local_terms[0])
+    Gc = [g if g is not None else np.zeros((1, 1, 1)) for g in G]
+    Wj = [oracle.partial_contractions_rl(t, Gc) for t in local_terms]
+    Xn = np.concatenate([t[0] for t in local_terms], axis=2)
+    X = [None] * N
+    for n in range(1, N):
+        I = Xn.shape[1]
+        Zn = oracle.V(Xn)
+        Yn = allreduce(Zn @ np.concatenate([w[n] for w in Wj], axis=0))
+        Q, _ = oracle.thin_qr(Yn)
+        X[n - 1] = oracle.fold_V(Q, I)
+        M = Q.T @ Zn
+        offs = np.cumsum([0] + [t[n - 1].shape[2] for t in local_terms])
+        Mj = [M[:, offs[j]:offs[j + 1]] for j in range(len(local_terms))]
+        if n < N - 1:
+            Xn = np.concatenate([oracle.fold_H(Mj[j] @ oracle.H(t[n]), t[n].shape[1])
+                                 for j, t in enumerate(local_terms)], axis=2)
+        else:
+            last = sum(Mj[j] @ oracle.H(t[N - 1]) for j, t in enumerate(local_terms))
+            X[N - 1] = oracle.fold_H(allreduce(last), local_terms[0][N - 1].shape[1])
+    return X
+
+
+def _worker(rank, world, port, out_q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        w = ttsynth.config3_sum10(d=5, I=12, S=5)
+        terms = [ttsynth.to_numpy(t) for t in w.terms]
+        lo, hi = shard_bounds(len(terms), world, rank)
+        dims = oracle.dims_of(terms[0])
+        sumR = [1] + [sum(t[n].shape[2] for t in terms) for n in range(len(dims) - 1)] + [1]
+        G = oracle.gaussian_sketch(dims, oracle.rank_caps(dims, sumR, 9), seed=1)
+
+        def allreduce(a):
+            t = torch.from_numpy(np.ascontiguousarray(a))
+            dist.all_reduce(t)          # fp64 sum, as ncclAllReduce in the CUDA path
+            return t.numpy()
+
+        X = sharded_alg7(terms[lo:hi], G, allreduce)
+        out_q.put((rank, [c.copy() for c in X]))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_shard_bounds_cover_contiguously():
+    for S in (1, 5, 10, 32):
+        for world in (1, 2, 3, 8):
+            b = [shard_bounds(S, world, r) for r in range(world)]
+            assert b[0][0] == 0 and b[-1][1] == S
+            assert all(b[r][1] == b[r + 1][0] for r in range(world - 1))
+            assert max(h - l for l, h in b) - min(h - l for l, h in b) <= 1
+
+
+def test_sharded_sweep_world2_matches_unsharded_oracle():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=240) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    w = ttsynth.config3_sum10(d=5, I=12, S=5)
+    terms = [ttsynth.to_numpy(t) for t in w.terms]
+    dims = oracle.dims_of(terms[0])
+    sumR = [1] + [sum(t[n].shape[2] for t in terms) for n in range(len(dims) - 1)] + [1]
+    G = oracle.gaussian_sketch(dims, oracle.rank_caps(dims, sumR, 9), seed=1)
+    ref = oracle.round_sum_rand_orth(terms, G)
+    for r in (0, 1):
+        assert oracle.rel_diff(res[r], ref) <= 1e-12
+    # replicated QR on identical all-reduced inputs: ranks agree bit for bit
+    for a, b in zip(res[0], res[1]):
+        assert np.array_equal(a, b)
+    assert oracle.left_orth_residual(res[0]) < 1e-12
