@@ -274,10 +274,11 @@ def main():
                "sample": desc}
 
     if rank == 0:
-        traffic = None
+        traffic = traffic_kernel = None
         prof = os.path.join(ROOT, "profiles", "traffic.json")
         try:
-            traffic = json.load(open(prof)).get(args.workload)
+            tr = json.load(open(prof)).get(args.workload)
+            traffic, traffic_kernel = tr["bytes_per_launch"], tr["kernel"]
         except Exception:
             pass
         line = {
@@ -298,7 +299,8 @@ def main():
             "roofline": {"bound": "tensor", "kernel": "dgemm_kernel (phase-1 Alg. 3 contractions, DMMA.8x8x4)",
                          "achieved": p1_achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": (p1_achieved / peak) if p1_achieved else None,
-                         "traffic": traffic,
+                         "traffic": traffic, "traffic_kernel": traffic_kernel,
+                         "traffic_source": "profiles/traffic.json (ncu --set full, DRAM bytes per launch)",
                          "algorithmic": "phase-1 flops = sum_j [2 R I l + sum_n (2 R^2 I l + 2 R I l^2)] (SURVEY 8d)"},
             "gpu_launches": launches,
             "ranks_out": ranks_out,
