@@ -51,6 +51,7 @@ struct GemmParams {
   double* ws;        // split-K partials (kslices > 1)
   const int* gate;   // device-side predicate: run iff gate == nullptr || *gate == gate_val
   int gate_val;
+  int vec;           // 1: every A/B 16-byte aligned with even leading dimensions
 };
 
 template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool TA, bool TB>
@@ -122,6 +123,71 @@ __global__ void __launch_bounds__(WM* WN * 32)
     }
   };
 
+  // 16-byte path (P.vec): each thread's cp.async sources are computed once and
+  // advanced by one k-tile per load; vectors run along the contiguous dimension
+  // of each operand (m or k for A, k or n for B); a vector straddling the M/N
+  // edge or the end of the K slice copies 8 bytes and zero-fills the rest
+  constexpr int AVn = BM * BK / 2, BVn = BN * BK / 2;
+  constexpr int NAL = (AVn + C::NT - 1) / C::NT, NBL = (BVn + C::NT - 1) / C::NT;
+  const double* a_ptr[NAL];
+  const double* b_ptr[NAL > NBL ? NAL : NBL];
+  int a_dst[NAL], b_dst[NBL], a_k[NAL], b_k[NBL];
+  bool a_ok[NAL], b_ok[NBL];
+  int a_full[NAL], b_full[NBL];
+  if (P.vec) {
+#pragma unroll
+    for (int i = 0; i < NAL; ++i) {
+      const int v = tid + i * C::NT;
+      int m, k;
+      if (TA) { k = 2 * (v % (BK / 2)); m = v / (BK / 2); }
+      else { m = 2 * (v % (BM / 2)); k = v / (BM / 2); }
+      const bool in = v < AVn;
+      a_ok[i] = in && (m0 + m < D.M);
+      a_full[i] = TA ? 16 : ((m0 + m + 1 < D.M) ? 16 : 8);
+      a_k[i] = k;
+      a_dst[i] = TA ? m * C::LDA + k : k * C::LDA + m;
+      a_ptr[i] = a_ok[i] ? (TA ? A + (kbeg + k) + int64_t(m0 + m) * lda
+                               : A + (m0 + m) + int64_t(kbeg + k) * lda) : A;
+    }
+#pragma unroll
+    for (int i = 0; i < NBL; ++i) {
+      const int v = tid + i * C::NT;
+      int n, k;
+      if (TB) { n = 2 * (v % (BN / 2)); k = v / (BN / 2); }
+      else { k = 2 * (v % (BK / 2)); n = v / (BK / 2); }
+      const bool in = v < BVn;
+      b_ok[i] = in && (n0 + n < D.N);
+      b_full[i] = TB ? ((n0 + n + 1 < D.N) ? 16 : 8) : 16;
+      b_k[i] = k;
+      b_dst[i] = TB ? k * C::LDB + n : n * C::LDB + k;
+      b_ptr[i] = b_ok[i] ? (TB ? B + (n0 + n) + int64_t(kbeg + k) * ldb
+                               : B + (kbeg + k) + int64_t(n0 + n) * ldb) : B;
+    }
+  }
+  auto load_tile_vec = [&](int slot, int kt) {
+    double* sA = smem + slot * C::SEL;
+    double* sB = sA + C::AEL;
+    const int k0 = kbeg + kt * BK;
+#pragma unroll
+    for (int i = 0; i < NAL; ++i) {
+      if (tid + i * C::NT < AVn) {
+        const int rem = kend - (k0 + a_k[i]);   // K left from this vector's first k
+        int bytes = a_ok[i] ? (TA ? (rem >= 2 ? 16 : (rem == 1 ? 8 : 0)) : (rem >= 1 ? a_full[i] : 0)) : 0;
+        const double* src = a_ptr[i] + (TA ? int64_t(kt) * BK : int64_t(kt) * BK * lda);
+        cp_async16(sA + a_dst[i], bytes ? src : A, bytes);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < NBL; ++i) {
+      if (tid + i * C::NT < BVn) {
+        const int rem = kend - (k0 + b_k[i]);
+        int bytes = b_ok[i] ? (TB ? (rem >= 1 ? b_full[i] : 0) : (rem >= 2 ? 16 : (rem == 1 ? 8 : 0))) : 0;
+        const double* src = b_ptr[i] + (TB ? int64_t(kt) * BK * ldb : int64_t(kt) * BK);
+        cp_async16(sB + b_dst[i], bytes ? src : B, bytes);
+      }
+    }
+  };
+
   double acc[C::FM][C::FN][2];
 #pragma unroll
   for (int i = 0; i < C::FM; ++i)
@@ -130,7 +196,10 @@ __global__ void __launch_bounds__(WM* WN * 32)
 
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < KT) load_tile(s, kbeg + s * BK);
+    if (s < KT) {
+      if (P.vec) load_tile_vec(s, s);
+      else load_tile(s, kbeg + s * BK);
+    }
     cp_async_commit();
   }
 
@@ -138,7 +207,10 @@ __global__ void __launch_bounds__(WM* WN * 32)
     cp_async_wait<STAGES - 2>();
     __syncthreads();
     const int nk = kt + STAGES - 1;
-    if (nk < KT) load_tile(nk % STAGES, kbeg + nk * BK);
+    if (nk < KT) {
+      if (P.vec) load_tile_vec(nk % STAGES, nk);
+      else load_tile(nk % STAGES, kbeg + nk * BK);
+    }
     cp_async_commit();
 
     const double* sA = smem + (kt % STAGES) * C::SEL;
@@ -362,6 +434,13 @@ int gemm(Ctx& c, bool ta, bool tb, const GemmDesc* d, int nbatch, double alpha, 
     done += nb;
     if (live == 0) continue;
     P.nbatch = live;
+    P.vec = 1;
+    for (int i = 0; i < live; ++i) {
+      const GemmDesc& x = P.d[i];
+      if ((reinterpret_cast<uintptr_t>(x.A) & 15) || (reinterpret_cast<uintptr_t>(x.B) & 15) ||
+          (x.lda & 1) || (x.ldb & 1))
+        P.vec = 0;
+    }
     P.alpha = alpha;
     P.beta = beta;
     P.gate = gate;
