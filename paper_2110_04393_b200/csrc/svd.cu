@@ -208,35 +208,66 @@ int svd_nov(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, double* 
 
 // ============================================================================
 // Cluster version for 64 <= n <= 160: the same one-sided Jacobi (same rotation
-// formulas, thresholds and convergence test) spread over a cluster of 8 CTAs.
+// formulas, thresholds and convergence test) on a cluster of 8 CTAs, over
+// UNITS of two columns (block-cyclic ordering).
 //
-// Column pairs are "groups" of 16 threads (row t + 16 s of a column per
-// thread); group g of the circle ordering lives in CTA g / GPC_G.  A group
-// keeps its two columns in registers for the round, rotates them and writes
-// them straight into the slots of the groups that own them next round
-// (top row shifts right, bottom row shifts left, position 0 fixed), so the
-// move IS the write-back; only the two columns crossing a CTA boundary go
-// through distributed shared memory.  One cluster barrier per round.
+// Units u = (2u, 2u+1) take part in a circle ordering; a "group" (one warp)
+// holds a top and a bottom unit.  Round 0 of a sweep first rotates the two
+// intra-unit pairs; every round then rotates the four cross pairs in two
+// sub-rounds ((t0,b0),(t1,b1)) and ((t0,b1),(t1,b0)), one pair per half-warp
+// (16 threads, rows t + 16 s).  The second sub-round writes its rotated columns
+// straight into the slots of the groups that own the units next round (top row
+// shifts right, bottom row left, unit 0 fixed), so the move is the write-back;
+// only the units crossing a CTA boundary go through distributed shared memory.
+// One cluster barrier per round, half as many rounds as column pairs.
 // ============================================================================
 namespace ttr {
 namespace {
 
 constexpr int kCl = 8;          // CTAs per cluster
-constexpr int kGpc = 9;         // groups per CTA (n <= 144 -> 72 groups)
-constexpr int kG16 = 16;        // threads per group
+constexpr int kGpc = 5;         // groups (warps) per CTA: n <= 160 -> <= 40 groups
+constexpr int kG16 = 16;        // threads per pair
 constexpr int kRps = 10;        // rows per thread (m <= 160)
-constexpr int kRows = kG16 * kRps;       // 160 rows per column slot
+constexpr int kRows = kG16 * kRps;
 
 struct JcShared {
-  double slot[2][kGpc][2][kRows];   // [buffer][local group][top/bottom][rows]
-  double alpha[2][kGpc][2];         // squared norms travelling with the columns
-  int col[2][kGpc][2];              // column ids travelling with the columns
-  double norms[kCl * kGpc * 2];     // final column norms (all columns, by id)
+  double slot[2][kGpc][4][kRows];   // [buffer][group][t0, t1, b0, b1][rows]
+  double alpha[2][kGpc][4];         // squared norms travelling with the columns
+  int col[2][kGpc][4];              // column ids travelling with the columns
+  double norms[kCl * kGpc * 4];     // final column norms (all columns, by id)
   double red[8];
   int rot;
 };
 
-constexpr int kJcThreads = ((kGpc * kG16 + 31) / 32) * 32;   // 160: whole warps
+constexpr int kJcThreads = kGpc * 32;
+
+// rotate the pair (X, Y) held by this half-warp (ids cx, cy, squared norms ax,
+// ay); p = min(id) is rotated as column p of the single-CTA kernel
+__device__ __forceinline__ bool jc_rotate(double (&x)[kRps], double (&y)[kRps], int cx, int cy,
+                                          double& ax, double& ay, int n, double small, double tol) {
+  double ga = 0.0;
+#pragma unroll
+  for (int s = 0; s < kRps; ++s) ga = fma(x[s], y[s], ga);
+#pragma unroll
+  for (int o = 8; o; o >>= 1) ga += __shfl_xor_sync(0xffffffffu, ga, o);
+  const bool swp = cx > cy;
+  const double ap = swp ? ay : ax, aq = swp ? ax : ay;
+  if (!(cx < n && cy < n && fmin(ap, aq) > small && fabs(ga) > tol * sqrt(ap * aq))) return false;
+  const double zeta = (aq - ap) / (2.0 * ga);
+  double tt = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
+  const double cs = rsqrt(fma(tt, tt, 1.0));
+  double sn = cs * tt;
+  if (swp) { sn = -sn; tt = -tt; }
+#pragma unroll
+  for (int s = 0; s < kRps; ++s) {
+    const double xs = x[s], ys = y[s];
+    x[s] = fma(cs, xs, -sn * ys);
+    y[s] = fma(sn, xs, cs * ys);
+  }
+  ax -= tt * ga;
+  ay += tt * ga;
+  return true;
+}
 
 __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kJcThreads)
     jacobi_cluster_kernel(const double* __restrict__ A, int64_t lda, int m, int n, int gpc,
@@ -247,39 +278,41 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kJcThreads)
   cg::cluster_group cl = cg::this_cluster();
   const int crank = int(cl.block_rank());
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int lg = tid / kG16, t16 = tid % kG16;
-  const int np = (n + 1) & ~1, half = np / 2;
-  const int g = crank * gpc + lg;                 // global group index
-  const bool live = lg < gpc && lg < kGpc && g < half;
+  const int lg = warp, h = lane >> 4, t16 = lane & 15;    // group, half, thread in half
+  const int U = (n + 1) / 2, UP = U + (U & 1), halfU = UP / 2;
+  const int g = crank * gpc + lg;
+  const bool live = lg < gpc && g < halfU;
+  const int lgc = live ? lg : 0;
 
-  // round 0 of the circle ordering: group g holds top = column g (0 for g = 0)
-  // and bottom = column np - 1 - g (index n is the dummy column of an odd n)
-  if (lg < kGpc) {
-    for (int which = 0; which < 2; ++which) {
-      const int c0 = live ? (which ? np - 1 - g : g) : n;
-      double* sl = sh.slot[0][lg][which];
-      for (int i = t16; i < kRows; i += kG16)
-        sl[i] = (c0 < n && i < m) ? A[i + int64_t(c0) * lda] : 0.0;
-      if (t16 == 0) {
-        sh.col[0][lg][which] = c0;
-        sh.alpha[0][lg][which] = 0.0;
+  // round 0: group g holds top unit (g == 0 ? 0 : g) and bottom unit UP - 1 - g
+  {
+    const int ut = live ? g : -1, ub = live ? UP - 1 - g : -1;
+    for (int c4 = 0; c4 < 4; ++c4) {
+      const int unit = c4 < 2 ? ut : ub;
+      const int c0 = unit < 0 ? n : 2 * unit + (c4 & 1);
+      const int cid = c0 < n ? c0 : n;
+      double* sl = sh.slot[0][lg][c4];
+      for (int i = lane; i < kRows; i += 32)
+        sl[i] = (cid < n && i < m) ? A[i + int64_t(cid) * lda] : 0.0;
+      if (lane == 0) {
+        sh.col[0][lg][c4] = cid;
+        sh.alpha[0][lg][c4] = 0.0;
       }
     }
   }
-  // ||A||_F^2 over the cluster
+  __syncthreads();
   double part = 0.0;
-  if (lg < kGpc)
-    for (int which = 0; which < 2; ++which)
-      for (int i = t16; i < kRows; i += kG16) {
-        const double v = sh.slot[0][lg][which][i];
-        part = fma(v, v, part);
-      }
+  for (int c4 = 0; c4 < 4; ++c4)
+    for (int i = lane; i < kRows; i += 32) {
+      const double v = sh.slot[0][lg][c4][i];
+      part = fma(v, v, part);
+    }
   for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
   if (lane == 0) sh.red[warp] = part;
   __syncthreads();
   if (tid == 0) {
     double s = 0.0;
-    for (int w = 0; w < (blockDim.x + 31) / 32; ++w) s += sh.red[w];
+    for (int w = 0; w < kGpc; ++w) s += sh.red[w];
     for (int r = 0; r < kCl; ++r) cl.map_shared_rank(&sh, r)->norms[crank] = s;   // scratch
   }
   cl.sync();
@@ -292,86 +325,109 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kJcThreads)
   const double negl = 16.0 * m * u;
   const double small = negl * negl * fro2;
 
-  // where this group's columns go after a round (fixed for the whole run):
-  // top:    g == 0 -> (0, top); g < half-1 -> (g+1, top); g == half-1 -> (g, bottom)
+  // destinations of this group's units after a round (fixed for the run):
+  // top:    g == 0 -> (0, top); g < halfU-1 -> (g+1, top); g == halfU-1 -> (g, bottom)
   // bottom: g == 0 -> (1, top); g >= 1 -> (g-1, bottom)
-  const int gt = (g == 0) ? 0 : (g < half - 1 ? g + 1 : g), wt = (g == 0 || g < half - 1) ? 0 : 1;
-  const int gb = (g == 0) ? 1 : g - 1, wb = (g == 0) ? 0 : 1;
+  const int gt = (g == 0) ? 0 : (g < halfU - 1 ? g + 1 : g);
+  const int wt = (g == 0 || g < halfU - 1) ? 0 : 2;
+  const int gb = (g == 0) ? 1 : g - 1, wb = (g == 0) ? 0 : 2;
   JcShared* sht = (gt / gpc == crank) ? &sh : cl.map_shared_rank(&sh, gt / gpc);
   JcShared* shb = (gb / gpc == crank) ? &sh : cl.map_shared_rank(&sh, gb / gpc);
   const int lt = gt % gpc, lb = gb % gpc;
-  const int lgc = live ? lg : 0;   // non-live groups compute on slot 0 and write nothing
 
   int buf = 0, sweep = 0;
   bool conv = false;
   for (; sweep < max_sweeps; ++sweep) {
     if (tid == 0) sh.rot = 0;
     int rot = 0;
-    for (int r = 0; r < np - 1; ++r) {
-      {   // every thread of the CTA (5 full warps) runs this: full-warp shuffles
-        const double* st = sh.slot[buf][lgc][0];
-        const double* sb = sh.slot[buf][lgc][1];
-        double x[kRps], y[kRps];
-        double ga = 0.0, al = 0.0, be = 0.0;
+    for (int r = 0; r < UP - 1; ++r) {
+      double (*sl)[kRows] = sh.slot[buf][lgc];
+      double* al = sh.alpha[buf][lgc];
+      const int* cid = sh.col[buf][lgc];
+      double x[kRps], y[kRps];
+      if (r == 0) {
+        // exact squared norms, then the intra-unit pairs (t0,t1) | (b0,b1)
+        const int cx = 2 * h, cy = 2 * h + 1;
 #pragma unroll
         for (int s = 0; s < kRps; ++s) {
-          x[s] = st[t16 + kG16 * s];
-          y[s] = sb[t16 + kG16 * s];
-          ga = fma(x[s], y[s], ga);
+          x[s] = sl[cx][t16 + kG16 * s];
+          y[s] = sl[cy][t16 + kG16 * s];
         }
-        const int colt = sh.col[buf][lgc][0], colb = sh.col[buf][lgc][1];
-        if (r == 0) {   // exact squared norms at the start of every sweep
+        double ax = 0.0, ay = 0.0;
+#pragma unroll
+        for (int s = 0; s < kRps; ++s) {
+          ax = fma(x[s], x[s], ax);
+          ay = fma(y[s], y[s], ay);
+        }
+#pragma unroll
+        for (int o = 8; o; o >>= 1) {
+          ax += __shfl_xor_sync(0xffffffffu, ax, o);
+          ay += __shfl_xor_sync(0xffffffffu, ay, o);
+        }
+        if (live && jc_rotate(x, y, cid[cx], cid[cy], ax, ay, n, small, tol)) rot = 1;
+        if (live) {   // (non-live warps alias group 0's slots: read only)
 #pragma unroll
           for (int s = 0; s < kRps; ++s) {
-            al = fma(x[s], x[s], al);
-            be = fma(y[s], y[s], be);
+            sl[cx][t16 + kG16 * s] = x[s];
+            sl[cy][t16 + kG16 * s] = y[s];
           }
+        }
+        __syncwarp();
+        if (live && t16 == 0) { al[cx] = ax; al[cy] = ay; }
+        __syncwarp();
+      }
+      // sub-round 1: (t0, b0) | (t1, b1), in place
+      {
+        const int cx = h, cy = 2 + h;
 #pragma unroll
-          for (int o = 8; o; o >>= 1) {
-            al += __shfl_xor_sync(0xffffffffu, al, o);
-            be += __shfl_xor_sync(0xffffffffu, be, o);
+        for (int s = 0; s < kRps; ++s) {
+          x[s] = sl[cx][t16 + kG16 * s];
+          y[s] = sl[cy][t16 + kG16 * s];
+        }
+        double ax = al[cx], ay = al[cy];
+        if (live && jc_rotate(x, y, cid[cx], cid[cy], ax, ay, n, small, tol)) rot = 1;
+        if (live) {   // (non-live warps alias group 0's slots: read only)
+#pragma unroll
+          for (int s = 0; s < kRps; ++s) {
+            sl[cx][t16 + kG16 * s] = x[s];
+            sl[cy][t16 + kG16 * s] = y[s];
           }
-        } else {
-          al = sh.alpha[buf][lgc][0];
-          be = sh.alpha[buf][lgc][1];
         }
+        __syncwarp();
+        if (live && t16 == 0) { al[cx] = ax; al[cy] = ay; }
+        __syncwarp();
+      }
+      // sub-round 2: (t0, b1) | (t1, b0), written to the next owners
+      {
+        const int cx = h, cy = 3 - h;
 #pragma unroll
-        for (int o = 8; o; o >>= 1) ga += __shfl_xor_sync(0xffffffffu, ga, o);
-        // rotation of (p, q) = (min, max) column ids, applied as T' = c T - s' B,
-        // B' = s' T + c B with s' = -s when the top column is q
-        const bool swp = colt > colb;
-        const double ap = swp ? be : al, aq = swp ? al : be;
-        double cs = 1.0, sn = 0.0, tt = 0.0;
-        if (live && colt < n && colb < n && fmin(ap, aq) > small &&
-            fabs(ga) > tol * sqrt(ap * aq)) {
-          const double zeta = (aq - ap) / (2.0 * ga);
-          tt = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
-          cs = rsqrt(fma(tt, tt, 1.0));
-          sn = cs * tt;
-          rot = 1;
+        for (int s = 0; s < kRps; ++s) {
+          x[s] = sl[cx][t16 + kG16 * s];
+          y[s] = sl[cy][t16 + kG16 * s];
         }
-        if (swp) { sn = -sn; tt = -tt; }
+        double ax = al[cx], ay = al[cy];
+        const int idx = cid[cx], idy = cid[cy];
+        if (live && jc_rotate(x, y, idx, idy, ax, ay, n, small, tol)) rot = 1;
         if (live) {
           const int nb = buf ^ 1;
-          double* dt = sht->slot[nb][lt][wt];
-          double* db = shb->slot[nb][lb][wb];
+          double* dx = sht->slot[nb][lt][wt + h];          // top unit column h
+          double* dy = shb->slot[nb][lb][wb + (1 - h)];    // bottom unit column 1-h
 #pragma unroll
           for (int s = 0; s < kRps; ++s) {
-            dt[t16 + kG16 * s] = fma(cs, x[s], -sn * y[s]);
-            db[t16 + kG16 * s] = fma(sn, x[s], cs * y[s]);
+            dx[t16 + kG16 * s] = x[s];
+            dy[t16 + kG16 * s] = y[s];
           }
           if (t16 == 0) {
-            sht->alpha[nb][lt][wt] = al - tt * ga;
-            shb->alpha[nb][lb][wb] = be + tt * ga;
-            sht->col[nb][lt][wt] = colt;
-            shb->col[nb][lb][wb] = colb;
+            sht->alpha[nb][lt][wt + h] = ax;
+            shb->alpha[nb][lb][wb + 1 - h] = ay;
+            sht->col[nb][lt][wt + h] = idx;
+            shb->col[nb][lb][wb + 1 - h] = idy;
           }
         }
       }
       buf ^= 1;
       cl.sync();
     }
-    // cluster-wide OR of "rotated in this sweep"
     if (rot) atomicOr(&cl.map_shared_rank(&sh, 0)->rot, 1);
     cl.sync();
     const int any = cl.map_shared_rank(&sh, 0)->rot;
@@ -387,35 +443,30 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kJcThreads)
     flags[13] += 1;
   }
   // norms of every column into every CTA (by column id), then sort by rank
-  {
-    for (int which = 0; which < 2; ++which) {
-      const double* sl = sh.slot[buf][lgc][which];
-      double s2 = 0.0;
-#pragma unroll
-      for (int s = 0; s < kRps; ++s) s2 = fma(sl[t16 + kG16 * s], sl[t16 + kG16 * s], s2);
-#pragma unroll
-      for (int o = 8; o; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
-      const int col = sh.col[buf][lgc][which];
-      if (live && t16 == 0 && col < n)
-        for (int rr = 0; rr < kCl; ++rr) cl.map_shared_rank(&sh, rr)->norms[col] = sqrt(s2);
-    }
+  for (int c4 = 0; c4 < 4; ++c4) {
+    const double* sl = sh.slot[buf][lgc][c4];
+    double s2 = 0.0;
+    for (int i = lane; i < kRows; i += 32) s2 = fma(sl[i], sl[i], s2);
+    for (int o = 16; o; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+    const int col = sh.col[buf][lgc][c4];
+    if (live && lane == 0 && col < n)
+      for (int rr = 0; rr < kCl; ++rr) cl.map_shared_rank(&sh, rr)->norms[col] = sqrt(s2);
   }
   cl.sync();
   if (live) {
-    for (int which = 0; which < 2; ++which) {
-      const double* sl = sh.slot[buf][lg][which];
-      const int col = sh.col[buf][lg][which];
+    for (int c4 = 0; c4 < 4; ++c4) {
+      const double* sl = sh.slot[buf][lg][c4];
+      const int col = sh.col[buf][lg][c4];
       if (col >= n) continue;
       const double sj = sh.norms[col];
       int rank = 0;
-      for (int k = t16; k < n; k += kG16) {
+      for (int k = lane; k < n; k += 32) {
         const double sk = sh.norms[k];
         rank += (sk > sj) || (sk == sj && k < col);
       }
-#pragma unroll
-      for (int o = 8; o; o >>= 1) rank += __shfl_xor_sync(0xffffu << (lane & 16), rank, o);
-      for (int i = t16; i < m; i += kG16) AV[i + int64_t(rank) * m] = sl[i];
-      if (t16 == 0) sigma[rank] = sj;
+      for (int o = 16; o; o >>= 1) rank += __shfl_xor_sync(0xffffffffu, rank, o);
+      for (int i = lane; i < m; i += 32) AV[i + int64_t(rank) * m] = sl[i];
+      if (lane == 0) sigma[rank] = sj;
     }
   }
 }
@@ -423,7 +474,8 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kJcThreads)
 }  // namespace
 
 bool svd_cluster_fits(int64_t m, int64_t n) {
-  return n >= 64 && m >= n && m <= kG16 * kRps && (n + 1) / 2 <= kCl * kGpc;
+  const int64_t U = (n + 1) / 2, UP = U + (U & 1);
+  return n >= 64 && m >= n && m <= kRows && UP / 2 <= kCl * kGpc;
 }
 
 int svd_nov_cluster(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, double* AV,
@@ -435,8 +487,8 @@ int svd_nov_cluster(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, 
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, int(shm)));
     attr[c.device & 63] = true;
   }
-  const int half = int((n + 1) / 2);
-  const int gpc = (half + kCl - 1) / kCl;
+  const int64_t U = (n + 1) / 2, UP = U + (U & 1);
+  const int gpc = int((UP / 2 + kCl - 1) / kCl);
   jacobi_cluster_kernel<<<kCl, kJcThreads, shm, s>>>(A, lda, int(m), int(n), gpc, AV, sigma,
                                                        40, c.flags.p);
   return launched();
