@@ -209,47 +209,53 @@ int svd_nov(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, double* 
 // ============================================================================
 // Cluster version for 64 <= n <= 160: the same one-sided Jacobi (same rotation
 // formulas, thresholds and convergence test) on a cluster of 8 CTAs, over
-// UNITS of two columns (block-cyclic ordering).
+// UNITS of four columns (block-cyclic ordering).
 //
-// Units u = (2u, 2u+1) take part in a circle ordering; a "group" (one warp)
-// holds a top and a bottom unit.  Round 0 of a sweep first rotates the two
-// intra-unit pairs; every round then rotates the four cross pairs in two
-// sub-rounds ((t0,b0),(t1,b1)) and ((t0,b1),(t1,b0)), one pair per half-warp
-// (16 threads, rows t + 16 s).  The second sub-round writes its rotated columns
+// Units u = (4u .. 4u+3) take part in a circle ordering; a "group" (one warp)
+// holds a top and a bottom unit (8 columns in shared memory).  Round 0 of a
+// sweep first rotates the 12 intra-unit pairs (3 sub-rounds of 4 disjoint
+// pairs); every round then rotates the 16 cross pairs in 4 sub-rounds
+// (t_i, b_{(i+s) mod 4}), one pair per 8-lane subgroup (rows t + 8 s), with only
+// __syncwarp between sub-rounds.  The last sub-round writes its rotated columns
 // straight into the slots of the groups that own the units next round (top row
-// shifts right, bottom row left, unit 0 fixed), so the move is the write-back;
+// shifts right, bottom row left, unit 0 fixed): the move is the write-back, and
 // only the units crossing a CTA boundary go through distributed shared memory.
-// One cluster barrier per round, half as many rounds as column pairs.
+// One cluster barrier per round: 35 per sweep for n = 144 instead of 143.
 // ============================================================================
 namespace ttr {
 namespace {
 
 constexpr int kCl = 8;          // CTAs per cluster
-constexpr int kGpc = 5;         // groups (warps) per CTA: n <= 160 -> <= 40 groups
-constexpr int kG16 = 16;        // threads per pair
-constexpr int kRps = 10;        // rows per thread (m <= 160)
-constexpr int kRows = kG16 * kRps;
+constexpr int kUw = 4;          // columns per unit
+constexpr int kGpc = 3;         // groups (warps) per CTA: n <= 160 -> <= 20 groups
+constexpr int kG8 = 8;          // threads per pair
+constexpr int kRps = 20;        // rows per thread (m <= 160)
+constexpr int kRows = kG8 * kRps;
 
 struct JcShared {
-  double slot[2][kGpc][4][kRows];   // [buffer][group][t0, t1, b0, b1][rows]
-  double alpha[2][kGpc][4];         // squared norms travelling with the columns
-  int col[2][kGpc][4];              // column ids travelling with the columns
-  double norms[kCl * kGpc * 4];     // final column norms (all columns, by id)
+  double slot[2][kGpc][2 * kUw][kRows];   // [buffer][group][t0..t3, b0..b3][rows]
+  double alpha[2][kGpc][2 * kUw];         // squared norms travelling with the columns
+  int col[2][kGpc][2 * kUw];              // column ids travelling with the columns
+  double norms[kCl * kGpc * 2 * kUw];     // final column norms (all columns, by id)
   double red[8];
   int rot;
 };
 
 constexpr int kJcThreads = kGpc * 32;
 
-// rotate the pair (X, Y) held by this half-warp (ids cx, cy, squared norms ax,
-// ay); p = min(id) is rotated as column p of the single-CTA kernel
+// rotate the pair (X, Y) held by this 8-lane subgroup (ids cx, cy, squared
+// norms ax, ay); p = min(id) is rotated as column p of the single-CTA kernel
 __device__ __forceinline__ bool jc_rotate(double (&x)[kRps], double (&y)[kRps], int cx, int cy,
                                           double& ax, double& ay, int n, double small, double tol) {
-  double ga = 0.0;
+  double ga0 = 0.0, ga1 = 0.0;
 #pragma unroll
-  for (int s = 0; s < kRps; ++s) ga = fma(x[s], y[s], ga);
+  for (int s = 0; s < kRps; s += 2) {
+    ga0 = fma(x[s], y[s], ga0);
+    ga1 = fma(x[s + 1], y[s + 1], ga1);
+  }
+  double ga = ga0 + ga1;
 #pragma unroll
-  for (int o = 8; o; o >>= 1) ga += __shfl_xor_sync(0xffffffffu, ga, o);
+  for (int o = 4; o; o >>= 1) ga += __shfl_xor_sync(0xffffffffu, ga, o);
   const bool swp = cx > cy;
   const double ap = swp ? ay : ax, aq = swp ? ax : ay;
   if (!(cx < n && cy < n && fmin(ap, aq) > small && fabs(ga) > tol * sqrt(ap * aq))) return false;
@@ -278,8 +284,8 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kJcThreads)
   cg::cluster_group cl = cg::this_cluster();
   const int crank = int(cl.block_rank());
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int lg = warp, h = lane >> 4, t16 = lane & 15;    // group, half, thread in half
-  const int U = (n + 1) / 2, UP = U + (U & 1), halfU = UP / 2;
+  const int lg = warp, rho = lane >> 3, t8 = lane & 7;    // group, pair slot, thread in pair
+  const int U = (n + kUw - 1) / kUw, UP = U + (U & 1), halfU = UP / 2;
   const int g = crank * gpc + lg;
   const bool live = lg < gpc && g < halfU;
   const int lgc = live ? lg : 0;
@@ -287,24 +293,24 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kJcThreads)
   // round 0: group g holds top unit (g == 0 ? 0 : g) and bottom unit UP - 1 - g
   {
     const int ut = live ? g : -1, ub = live ? UP - 1 - g : -1;
-    for (int c4 = 0; c4 < 4; ++c4) {
-      const int unit = c4 < 2 ? ut : ub;
-      const int c0 = unit < 0 ? n : 2 * unit + (c4 & 1);
+    for (int c8 = 0; c8 < 2 * kUw; ++c8) {
+      const int unit = c8 < kUw ? ut : ub;
+      const int c0 = unit < 0 ? n : kUw * unit + (c8 % kUw);
       const int cid = c0 < n ? c0 : n;
-      double* sl = sh.slot[0][lg][c4];
+      double* sl = sh.slot[0][lg][c8];
       for (int i = lane; i < kRows; i += 32)
         sl[i] = (cid < n && i < m) ? A[i + int64_t(cid) * lda] : 0.0;
       if (lane == 0) {
-        sh.col[0][lg][c4] = cid;
-        sh.alpha[0][lg][c4] = 0.0;
+        sh.col[0][lg][c8] = cid;
+        sh.alpha[0][lg][c8] = 0.0;
       }
     }
   }
   __syncthreads();
   double part = 0.0;
-  for (int c4 = 0; c4 < 4; ++c4)
+  for (int c8 = 0; c8 < 2 * kUw; ++c8)
     for (int i = lane; i < kRows; i += 32) {
-      const double v = sh.slot[0][lg][c4][i];
+      const double v = sh.slot[0][lg][c8][i];
       part = fma(v, v, part);
     }
   for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
@@ -329,11 +335,33 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kJcThreads)
   // top:    g == 0 -> (0, top); g < halfU-1 -> (g+1, top); g == halfU-1 -> (g, bottom)
   // bottom: g == 0 -> (1, top); g >= 1 -> (g-1, bottom)
   const int gt = (g == 0) ? 0 : (g < halfU - 1 ? g + 1 : g);
-  const int wt = (g == 0 || g < halfU - 1) ? 0 : 2;
-  const int gb = (g == 0) ? 1 : g - 1, wb = (g == 0) ? 0 : 2;
+  const int wt = (g == 0 || g < halfU - 1) ? 0 : kUw;
+  const int gb = (g == 0) ? 1 : g - 1, wb = (g == 0) ? 0 : kUw;
   JcShared* sht = (gt / gpc == crank) ? &sh : cl.map_shared_rank(&sh, gt / gpc);
   JcShared* shb = (gb / gpc == crank) ? &sh : cl.map_shared_rank(&sh, gb / gpc);
   const int lt = gt % gpc, lb = gb % gpc;
+
+  // rotate slots (cx, cy) of the current buffer in place
+  auto in_place = [&](double (*sl)[kRows], double* al, const int* cid, int cx, int cy,
+                      int& rot) {
+    double x[kRps], y[kRps];
+#pragma unroll
+    for (int s = 0; s < kRps; ++s) {
+      x[s] = sl[cx][t8 + kG8 * s];
+      y[s] = sl[cy][t8 + kG8 * s];
+    }
+    double ax = al[cx], ay = al[cy];
+    if (live && jc_rotate(x, y, cid[cx], cid[cy], ax, ay, n, small, tol)) {
+      rot = 1;
+#pragma unroll
+      for (int s = 0; s < kRps; ++s) {
+        sl[cx][t8 + kG8 * s] = x[s];
+        sl[cy][t8 + kG8 * s] = y[s];
+      }
+      if (t8 == 0) { al[cx] = ax; al[cy] = ay; }
+    }
+    __syncwarp();
+  };
 
   int buf = 0, sweep = 0;
   bool conv = false;
@@ -344,84 +372,56 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kJcThreads)
       double (*sl)[kRows] = sh.slot[buf][lgc];
       double* al = sh.alpha[buf][lgc];
       const int* cid = sh.col[buf][lgc];
-      double x[kRps], y[kRps];
       if (r == 0) {
-        // exact squared norms, then the intra-unit pairs (t0,t1) | (b0,b1)
-        const int cx = 2 * h, cy = 2 * h + 1;
+        // exact squared norms (subgroup rho: columns rho and 4 + rho) ...
+        for (int c = rho; c < 2 * kUw; c += kUw) {
+          double a2 = 0.0;
 #pragma unroll
-        for (int s = 0; s < kRps; ++s) {
-          x[s] = sl[cx][t16 + kG16 * s];
-          y[s] = sl[cy][t16 + kG16 * s];
-        }
-        double ax = 0.0, ay = 0.0;
+          for (int s = 0; s < kRps; ++s) a2 = fma(sl[c][t8 + kG8 * s], sl[c][t8 + kG8 * s], a2);
 #pragma unroll
-        for (int s = 0; s < kRps; ++s) {
-          ax = fma(x[s], x[s], ax);
-          ay = fma(y[s], y[s], ay);
-        }
-#pragma unroll
-        for (int o = 8; o; o >>= 1) {
-          ax += __shfl_xor_sync(0xffffffffu, ax, o);
-          ay += __shfl_xor_sync(0xffffffffu, ay, o);
-        }
-        if (live && jc_rotate(x, y, cid[cx], cid[cy], ax, ay, n, small, tol)) rot = 1;
-        if (live) {   // (non-live warps alias group 0's slots: read only)
-#pragma unroll
-          for (int s = 0; s < kRps; ++s) {
-            sl[cx][t16 + kG16 * s] = x[s];
-            sl[cy][t16 + kG16 * s] = y[s];
-          }
+          for (int o = 4; o; o >>= 1) a2 += __shfl_xor_sync(0xffffffffu, a2, o);
+          if (live && t8 == 0) al[c] = a2;
         }
         __syncwarp();
-        if (live && t16 == 0) { al[cx] = ax; al[cy] = ay; }
-        __syncwarp();
+        // ... then the intra-unit pairs: {(0,1),(2,3)}, {(0,2),(1,3)}, {(0,3),(1,2)}
+        // in both units (subgroup rho: unit rho >> 1, pair rho & 1)
+#pragma unroll 1
+        for (int k = 0; k < 3; ++k) {
+          const int base = kUw * (rho >> 1), pr = rho & 1;
+          const int a0 = (k == 0) ? 2 * pr : (k == 1 ? pr : (pr ? 1 : 0));
+          const int b0 = (k == 0) ? 2 * pr + 1 : (k == 1 ? pr + 2 : (pr ? 2 : 3));
+          in_place(sl, al, cid, base + a0, base + b0, rot);
+        }
       }
-      // sub-round 1: (t0, b0) | (t1, b1), in place
+      // cross pairs (t_i, b_{(i+s) mod 4}), s = 0..2 in place
+#pragma unroll 1
+      for (int sr = 0; sr < kUw - 1; ++sr) in_place(sl, al, cid, rho, kUw + ((rho + sr) & 3), rot);
+      // s = 3: rotated columns go to the next owners
       {
-        const int cx = h, cy = 2 + h;
+        const int cx = rho, cy = kUw + ((rho + kUw - 1) & 3);
+        double x[kRps], y[kRps];
 #pragma unroll
         for (int s = 0; s < kRps; ++s) {
-          x[s] = sl[cx][t16 + kG16 * s];
-          y[s] = sl[cy][t16 + kG16 * s];
-        }
-        double ax = al[cx], ay = al[cy];
-        if (live && jc_rotate(x, y, cid[cx], cid[cy], ax, ay, n, small, tol)) rot = 1;
-        if (live) {   // (non-live warps alias group 0's slots: read only)
-#pragma unroll
-          for (int s = 0; s < kRps; ++s) {
-            sl[cx][t16 + kG16 * s] = x[s];
-            sl[cy][t16 + kG16 * s] = y[s];
-          }
-        }
-        __syncwarp();
-        if (live && t16 == 0) { al[cx] = ax; al[cy] = ay; }
-        __syncwarp();
-      }
-      // sub-round 2: (t0, b1) | (t1, b0), written to the next owners
-      {
-        const int cx = h, cy = 3 - h;
-#pragma unroll
-        for (int s = 0; s < kRps; ++s) {
-          x[s] = sl[cx][t16 + kG16 * s];
-          y[s] = sl[cy][t16 + kG16 * s];
+          x[s] = sl[cx][t8 + kG8 * s];
+          y[s] = sl[cy][t8 + kG8 * s];
         }
         double ax = al[cx], ay = al[cy];
         const int idx = cid[cx], idy = cid[cy];
         if (live && jc_rotate(x, y, idx, idy, ax, ay, n, small, tol)) rot = 1;
         if (live) {
           const int nb = buf ^ 1;
-          double* dx = sht->slot[nb][lt][wt + h];          // top unit column h
-          double* dy = shb->slot[nb][lb][wb + (1 - h)];    // bottom unit column 1-h
+          double* dx = sht->slot[nb][lt][wt + cx];
+          double* dy = shb->slot[nb][lb][wb + (cy - kUw)];
 #pragma unroll
           for (int s = 0; s < kRps; ++s) {
-            dx[t16 + kG16 * s] = x[s];
-            dy[t16 + kG16 * s] = y[s];
+            dx[t8 + kG8 * s] = x[s];
+            dy[t8 + kG8 * s] = y[s];
           }
-          if (t16 == 0) {
-            sht->alpha[nb][lt][wt + h] = ax;
-            shb->alpha[nb][lb][wb + 1 - h] = ay;
-            sht->col[nb][lt][wt + h] = idx;
-            shb->col[nb][lb][wb + 1 - h] = idy;
+          if (t8 == 0) {
+            sht->alpha[nb][lt][wt + cx] = ax;
+            shb->alpha[nb][lb][wb + cy - kUw] = ay;
+            sht->col[nb][lt][wt + cx] = idx;
+            shb->col[nb][lb][wb + cy - kUw] = idy;
           }
         }
       }
@@ -443,20 +443,20 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kJcThreads)
     flags[13] += 1;
   }
   // norms of every column into every CTA (by column id), then sort by rank
-  for (int c4 = 0; c4 < 4; ++c4) {
-    const double* sl = sh.slot[buf][lgc][c4];
+  for (int c8 = 0; c8 < 2 * kUw; ++c8) {
+    const double* sl = sh.slot[buf][lgc][c8];
     double s2 = 0.0;
     for (int i = lane; i < kRows; i += 32) s2 = fma(sl[i], sl[i], s2);
     for (int o = 16; o; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
-    const int col = sh.col[buf][lgc][c4];
+    const int col = sh.col[buf][lgc][c8];
     if (live && lane == 0 && col < n)
       for (int rr = 0; rr < kCl; ++rr) cl.map_shared_rank(&sh, rr)->norms[col] = sqrt(s2);
   }
   cl.sync();
   if (live) {
-    for (int c4 = 0; c4 < 4; ++c4) {
-      const double* sl = sh.slot[buf][lg][c4];
-      const int col = sh.col[buf][lg][c4];
+    for (int c8 = 0; c8 < 2 * kUw; ++c8) {
+      const double* sl = sh.slot[buf][lg][c8];
+      const int col = sh.col[buf][lg][c8];
       if (col >= n) continue;
       const double sj = sh.norms[col];
       int rank = 0;
@@ -474,7 +474,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kJcThreads)
 }  // namespace
 
 bool svd_cluster_fits(int64_t m, int64_t n) {
-  const int64_t U = (n + 1) / 2, UP = U + (U & 1);
+  const int64_t U = (n + kUw - 1) / kUw, UP = U + (U & 1);
   return n >= 64 && m >= n && m <= kRows && UP / 2 <= kCl * kGpc;
 }
 
@@ -487,7 +487,7 @@ int svd_nov_cluster(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, 
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, int(shm)));
     attr[c.device & 63] = true;
   }
-  const int64_t U = (n + 1) / 2, UP = U + (U & 1);
+  const int64_t U = (n + kUw - 1) / kUw, UP = U + (U & 1);
   const int gpc = int((UP / 2 + kCl - 1) / kCl);
   jacobi_cluster_kernel<<<kCl, kJcThreads, shm, s>>>(A, lda, int(m), int(n), gpc, AV, sigma,
                                                        40, c.flags.p);
