@@ -233,7 +233,7 @@ constexpr int kRps = 20;        // rows per thread (m <= 160)
 constexpr int kRows = kG8 * kRps;
 
 struct JcShared {
-  double slot[2][kGpc][2 * kUw][kRows];   // [buffer][group][t0..t3, b0..b3][rows]
+  alignas(16) double slot[2][kGpc][2 * kUw][kRows];   // [buffer][group][t0..t3, b0..b3][rows]
   double alpha[2][kGpc][2 * kUw];         // squared norms travelling with the columns
   int col[2][kGpc][2 * kUw];              // column ids travelling with the columns
   double norms[kCl * kGpc * 2 * kUw];     // final column norms (all columns, by id)
@@ -244,14 +244,21 @@ struct JcShared {
 constexpr int kJcThreads = kGpc * 32;
 
 // rotate the pair (X, Y) held by this 8-lane subgroup (ids cx, cy, squared
-// norms ax, ay); p = min(id) is rotated as column p of the single-CTA kernel
-__device__ __forceinline__ bool jc_rotate(double (&x)[kRps], double (&y)[kRps], int cx, int cy,
+// norms ax, ay); p = min(id) is rotated as column p of the single-CTA kernel.
+// Rows are held as double2 (rows 2 t + 16 s, +1).  The angle
+//   t = sign(d) e / (|d| + sqrt(d^2 + e^2)),  d = a_q - a_p, e = 2 gamma
+// (= sign(zeta)/(|zeta| + sqrt(1 + zeta^2)), zeta = d/e) is computed in fp32 after
+// an exact power-of-two scaling: its error only changes how much of gamma one
+// rotation removes; the rotation stays orthogonal to working precision because
+// cs = rsqrt(1 + t^2) and sn = cs t are formed in fp64.
+constexpr int kR2 = kRps / 2;
+__device__ __forceinline__ bool jc_rotate(double2 (&x)[kR2], double2 (&y)[kR2], int cx, int cy,
                                           double& ax, double& ay, int n, double small, double tol) {
   double ga0 = 0.0, ga1 = 0.0;
 #pragma unroll
-  for (int s = 0; s < kRps; s += 2) {
-    ga0 = fma(x[s], y[s], ga0);
-    ga1 = fma(x[s + 1], y[s + 1], ga1);
+  for (int s = 0; s < kR2; ++s) {
+    ga0 = fma(x[s].x, y[s].x, ga0);
+    ga1 = fma(x[s].y, y[s].y, ga1);
   }
   double ga = ga0 + ga1;
 #pragma unroll
@@ -259,16 +266,20 @@ __device__ __forceinline__ bool jc_rotate(double (&x)[kRps], double (&y)[kRps], 
   const bool swp = cx > cy;
   const double ap = swp ? ay : ax, aq = swp ? ax : ay;
   if (!(cx < n && cy < n && fmin(ap, aq) > small && fabs(ga) > tol * sqrt(ap * aq))) return false;
-  const double zeta = (aq - ap) / (2.0 * ga);
-  double tt = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
+  const double d = aq - ap, e = 2.0 * ga;
+  int ex;
+  frexp(fmax(fabs(d), fabs(e)), &ex);
+  const float df = float(ldexp(d, -ex)), ef = float(ldexp(e, -ex));
+  const float tf = copysignf(1.0f, df) * ef / (fabsf(df) + sqrtf(fmaf(df, df, ef * ef)));
+  double tt = double(tf);
   const double cs = rsqrt(fma(tt, tt, 1.0));
   double sn = cs * tt;
   if (swp) { sn = -sn; tt = -tt; }
 #pragma unroll
-  for (int s = 0; s < kRps; ++s) {
-    const double xs = x[s], ys = y[s];
-    x[s] = fma(cs, xs, -sn * ys);
-    y[s] = fma(sn, xs, cs * ys);
+  for (int s = 0; s < kR2; ++s) {
+    const double2 xs = x[s], ys = y[s];
+    x[s] = make_double2(fma(cs, xs.x, -sn * ys.x), fma(cs, xs.y, -sn * ys.y));
+    y[s] = make_double2(fma(sn, xs.x, cs * ys.x), fma(sn, xs.y, cs * ys.y));
   }
   ax -= tt * ga;
   ay += tt * ga;
@@ -344,19 +355,23 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kJcThreads)
   // rotate slots (cx, cy) of the current buffer in place
   auto in_place = [&](double (*sl)[kRows], double* al, const int* cid, int cx, int cy,
                       int& rot) {
-    double x[kRps], y[kRps];
+    double2 x[kR2], y[kR2];
+    const double2* px = reinterpret_cast<const double2*>(sl[cx]) + t8;
+    const double2* py = reinterpret_cast<const double2*>(sl[cy]) + t8;
 #pragma unroll
-    for (int s = 0; s < kRps; ++s) {
-      x[s] = sl[cx][t8 + kG8 * s];
-      y[s] = sl[cy][t8 + kG8 * s];
+    for (int s = 0; s < kR2; ++s) {
+      x[s] = px[kG8 * s];
+      y[s] = py[kG8 * s];
     }
     double ax = al[cx], ay = al[cy];
     if (live && jc_rotate(x, y, cid[cx], cid[cy], ax, ay, n, small, tol)) {
       rot = 1;
+      double2* wx = reinterpret_cast<double2*>(sl[cx]) + t8;
+      double2* wy = reinterpret_cast<double2*>(sl[cy]) + t8;
 #pragma unroll
-      for (int s = 0; s < kRps; ++s) {
-        sl[cx][t8 + kG8 * s] = x[s];
-        sl[cy][t8 + kG8 * s] = y[s];
+      for (int s = 0; s < kR2; ++s) {
+        wx[kG8 * s] = x[s];
+        wy[kG8 * s] = y[s];
       }
       if (t8 == 0) { al[cx] = ax; al[cy] = ay; }
     }
@@ -399,23 +414,25 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kJcThreads)
       // s = 3: rotated columns go to the next owners
       {
         const int cx = rho, cy = kUw + ((rho + kUw - 1) & 3);
-        double x[kRps], y[kRps];
+        double2 x[kR2], y[kR2];
+        const double2* px = reinterpret_cast<const double2*>(sl[cx]) + t8;
+        const double2* py = reinterpret_cast<const double2*>(sl[cy]) + t8;
 #pragma unroll
-        for (int s = 0; s < kRps; ++s) {
-          x[s] = sl[cx][t8 + kG8 * s];
-          y[s] = sl[cy][t8 + kG8 * s];
+        for (int s = 0; s < kR2; ++s) {
+          x[s] = px[kG8 * s];
+          y[s] = py[kG8 * s];
         }
         double ax = al[cx], ay = al[cy];
         const int idx = cid[cx], idy = cid[cy];
         if (live && jc_rotate(x, y, idx, idy, ax, ay, n, small, tol)) rot = 1;
         if (live) {
           const int nb = buf ^ 1;
-          double* dx = sht->slot[nb][lt][wt + cx];
-          double* dy = shb->slot[nb][lb][wb + (cy - kUw)];
+          double2* dx = reinterpret_cast<double2*>(sht->slot[nb][lt][wt + cx]) + t8;
+          double2* dy = reinterpret_cast<double2*>(shb->slot[nb][lb][wb + (cy - kUw)]) + t8;
 #pragma unroll
-          for (int s = 0; s < kRps; ++s) {
-            dx[t8 + kG8 * s] = x[s];
-            dy[t8 + kG8 * s] = y[s];
+          for (int s = 0; s < kR2; ++s) {
+            dx[kG8 * s] = x[s];
+            dy[kG8 * s] = y[s];
           }
           if (t8 == 0) {
             sht->alpha[nb][lt][wt + cx] = ax;
