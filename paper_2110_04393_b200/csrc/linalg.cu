@@ -264,6 +264,21 @@ __global__ void __launch_bounds__(kCholThreads)
 
 constexpr int kBlkThreads = 512;
 
+// optional phase timing of chol_blk_kernel (build with -DTTR_CHOL_PROF): thread 0
+// adds clock64 deltas / 64 of C1, C2, C3, I0, I-phase to flags[32..36]
+#ifdef TTR_CHOL_PROF
+#define CHOL_PROF(slot)                                              \
+  do {                                                               \
+    if (threadIdx.x == 0) {                                          \
+      const long long t__ = clock64();                               \
+      atomicAdd(&flags[32 + (slot)], int((t__ - prof_t) >> 6));     \
+      prof_t = t__;                                                  \
+    }                                                                \
+  } while (0)
+#else
+#define CHOL_PROF(slot) do { } while (0)
+#endif
+
 __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(c0), "+d"(c1)
@@ -338,6 +353,9 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
   const double shift = shifted ? 11.0 * (double(m) * n + double(n) * (n + 1)) * 0x1p-53 * s_tr : 0.0;
   const bool clamp = md == CH_RCLAMP;
   const double tau = 64.0 * n * 0x1p-53 * s_dmax;
+#ifdef TTR_CHOL_PROF
+  long long prof_t = clock64();
+#endif
   for (int e = tid; e < ld * n8; e += kBlkThreads) {   // lower triangle of G (+ shift); pads 0
     const int i = e % ld, j = e / ld;
     S[e] = (i < n && j < n && i >= j) ? G[i + int64_t(j) * n] + ((i == j) ? shift : 0.0) : 0.0;
@@ -350,15 +368,18 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
     // registers, a[q] = A(i, j0 + q); pivots in groups of 4 with static
     // register offsets, then a shift by 4 (a fully unrolled elimination is ~15k
     // instructions run once per block: instruction-cache bound).  The pivot
-    // column is broadcast through shared memory (colb), 1/L_jj = rsqrt(pivot).
-    // Updates of the upper slots (column > row) are harmless garbage.
+    // column is broadcast through shared memory (colb).  The pivot step is
+    // branch-free: clamping and the finiteness test are selects, and
+    // 1/L_jj = rsqrt(pivot) is MUFU.RSQ64H + two Newton steps (no slow path:
+    // pivots are normal numbers here).  Updates of the upper slots (column >
+    // row) are harmless garbage.
     if (w == 0) {
       const int i = lane;
       double a[32];
 #pragma unroll
       for (int q = 0; q < 32; ++q)
         a[q] = (i < kb && q <= i) ? S[(k0 + i) + (k0 + q) * ld] : 0.0;
-      bool bad = false;
+      int bad = 0, nclamp = 0;
       const int kb4 = (kb + 3) & ~3;
 #pragma unroll 1
       for (int j0 = 0; j0 < kb4; j0 += 4) {
@@ -366,19 +387,21 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
         for (int sft = 0; sft < 4; ++sft) {
           const int j = j0 + sft;
           double piv = __shfl_sync(0xffffffffu, a[sft], j);
-          if (j >= kb) piv = 1.0;                            // padding pivot
-          if (clamp && !(piv > tau) && isfinite(piv)) {     // numerically null direction
-            piv = tau;
-            if (lane == 0) s_clamped += 1;
-          }
-          const bool ok = piv > 0.0 && isfinite(piv);
+          piv = (j < kb) ? piv : 1.0;                       // padding pivot
+          const bool fin = fabs(piv) <= 1.79e308;           // false for inf / nan
+          const bool cl = clamp && fin && !(piv > tau);     // numerically null direction
+          piv = cl ? tau : piv;
+          nclamp += cl;
+          const bool ok = fin && piv > 0.0;
           bad |= !ok;
-          const double rd = ok ? rsqrt(piv) : 1.0;
-          const double lij = (i > j) ? a[sft] * rd : (i == j ? piv * rd : 0.0);
-          if (j < kb) {
-            if (i >= j && i < kb) S[(k0 + i) + (k0 + j) * ld] = lij;
-            if (i == j) rdiag[k0 + j] = rd;
-          }
+          const double pv = ok ? piv : 1.0;
+          double rd;
+          asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(rd) : "d"(pv));
+          rd = rd * fma(-0.5 * pv * rd, rd, 1.5);           // Newton steps for 1/sqrt
+          rd = rd * fma(-0.5 * pv * rd, rd, 1.5);
+          const double lij = (i > j) ? a[sft] * rd : (i == j ? pv * rd : 0.0);
+          if (j < kb && i >= j && i < kb) S[(k0 + i) + (k0 + j) * ld] = lij;
+          if (i == j && j < kb) rdiag[k0 + j] = rd;
           colb[i] = lij;
           __syncwarp();
 #pragma unroll
@@ -390,9 +413,13 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
         for (int q = 0; q < 28; ++q) a[q] = a[q + 4];
         a[28] = a[29] = a[30] = a[31] = 0.0;
       }
-      if (bad && lane == 0) s_bad = 1;
+      if (lane == 0) {
+        if (bad) s_bad = 1;
+        if (nclamp) s_clamped += nclamp;
+      }
     }
     __syncthreads();
+    CHOL_PROF(0);
     if (s_bad) break;
     const int r0 = k0 + kb;   // first row below the block (kb == 32 if r0 < n)
     if (r0 >= n) break;
@@ -438,6 +465,7 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
       }
     }
     __syncthreads();
+    CHOL_PROF(1);
     // ---- C3: trailing A(r, c) -= sum_t L(r, t) L(c, t) on the lower 8x8 tiles
     {
       const int tb = r0 / 8, nrt = nt8 - tb;
@@ -463,6 +491,7 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
       }
     }
     __syncthreads();
+    CHOL_PROF(2);
   }
   __syncthreads();
   const bool bad_final = s_bad;
@@ -507,6 +536,7 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
     }
   }
   __syncthreads();
+  CHOL_PROF(3);
   // ---- X = L^{-1} in place, block columns right to left
 #pragma unroll 1
   for (int k = nb - 1; k >= 0; --k) {
@@ -603,6 +633,7 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
     const int r = e % n, c = e / n;     // Rinv(r, c) = X(c, r), c >= r
     Rinv[e] = (c >= r) ? S[c + r * ld] : 0.0;
   }
+  CHOL_PROF(4);
 }
 
 __global__ void route_start_kernel(int* flags) { flags[0] = flags[0] >= 1 ? 1 : 0; }
