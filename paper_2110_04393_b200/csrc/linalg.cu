@@ -356,11 +356,15 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
 #ifdef TTR_CHOL_PROF
   long long prof_t = clock64();
 #endif
-  for (int e = tid; e < ld * n8; e += kBlkThreads) {   // lower triangle of G (+ shift); pads 0
+  // lower triangle of G (+ shift) into S, pads 0; loads batched 8 deep (the
+  // loop is latency bound: one L2 round trip per batch, not per element)
+#pragma unroll 8
+  for (int e = tid; e < ld * n8; e += kBlkThreads) {
     const int i = e % ld, j = e / ld;
     S[e] = (i < n && j < n && i >= j) ? G[i + int64_t(j) * n] + ((i == j) ? shift : 0.0) : 0.0;
   }
   __syncthreads();
+  CHOL_PROF(5);
 #pragma unroll 1
   for (int k = 0; k < nb; ++k) {
     const int k0 = 32 * k, kb = min(32, n - k0);
