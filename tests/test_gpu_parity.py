@@ -191,3 +191,19 @@ def test_errors_are_reported(ctx):
     assert e.value.code == -2
     with pytest.raises(P.TTError):
         ctx.tt_round_sum(gpu_terms(terms), mode="tol", tol=0.0, oversample=3)
+
+
+def test_config5_full_size_in_bench_launch_configuration():
+    """Config 5 at BASELINE.json's full size (S=32, d=50, I=256, rank 64 per
+    summand, sketch 144 -> rank 128), rounded through the C-ABI in the launch
+    configuration bench.py times (library bound to torch's current stream), and
+    compared with the oracle on the host (NumPy, ~2-3 min) in TT arithmetic."""
+    import paper_2110_04393_b200 as P
+    w = ttsynth.config5_large()
+    c = P.Context(0, stream=torch.cuda.current_stream())
+    res = c.tt_round_sum(gpu_terms(w.terms), mode="rank", rank=w.rank,
+                         oversample=w.ell - w.rank, seed=1)
+    ref = oracle.round_sum([ttsynth.to_numpy(t) for t in w.terms], ell=w.ell, seed=1,
+                           rank=w.rank)
+    r, X = check(res, ref)
+    assert res.ranks == [1] + [w.rank] * (w.d - 1) + [1]
