@@ -141,7 +141,11 @@ int tt_round_sum(tt_ctx_t ctx, int32_t S_local, const tt_view* terms,
 
 /* Deterministic TT-rounding of the assembled sum: Alg. 1 + Alg. 2
  * with eps0 = opts->tol (and opts->rank as an optional rank cap).
- * Not yet implemented in this build: returns TT_ERR_ARG with a message. */
+ * Assembles the sum, orthogonalises right to left (Alg. 1, economy
+ * QR; a wide H(X_n)^T shrinks its bond) and truncates left to right with QR +
+ * one-sided Jacobi SVD (Alg. 2, R5, R13).  Single GPU.  Ranks above 160 use the
+ * generic (slow) Cholesky and the Jacobi that accumulates V.  Output ranks
+ * (1, k_1..k_{d-1}, 1), left-orthogonal. */
 int tt_round_deterministic(tt_ctx_t ctx, int32_t S, const tt_view* terms,
                            const tt_round_opts* opts, tt_tensor_t* out);
 

@@ -487,7 +487,7 @@ int truncate(Ctx& c, tt_tensor& X, double tol, int64_t rmax, std::vector<int64_t
     TTR_TRY(dalloc(newn, size_t(k) * mrow, s));
     if (fast) {
       TTR_TRY(dalloc(Bk, size_t(r0) * k, s));
-      TTR_TRY(scale_by_inv_sigma2(c, AV.p, r0, k, sig.p, Bk.p, s));
+      TTR_TRY(scale_by_inv_sigma(c, AV.p, r0, k, sig.p, Bk.p, 2, s));
       TTR_TRY(gemm1(c, true, false, int(k), int(mrow), int(r0), 1.0, Bk.p, int(r0),
                     X.bufs[n - 1].p, int(r0), 0.0, newn.p, int(k), s));
     } else if (mrow >= r0) {
@@ -667,6 +667,193 @@ int round_sum_impl(tt_ctx* c, int S, const tt_view* terms, const tt_round_opts* 
     return TT_ERR_NUMERIC;
   }
   *outp = out.release();
+  return TT_OK;
+}
+
+// ------------------------------------------------------------------ Alg. 1 + 2
+// Deterministic TT-rounding of the assembled sum (NEXT-1; the
+// baseline the paper compares with), on the same kernels.
+//  * assembly: first cores concatenated along the right rank, last
+//    cores along the left rank, middle cores block-diagonal (one strided copy per
+//    summand and core);
+//  * Alg. 1 OrthogonalizeRL: [Q,R] = qr(H(X_n)^T), H(X_n) <- Q^T,
+//    V(X_{n-1}) <- V(X_{n-1}) R^T.  When H(X_n)^T is wide (I_n r_n < r_{n-1}, e.g.
+//    the last core of a sum) the economy QR shrinks the bond to I_n r_n; any
+//    orthogonal Q of that square factor gives the same tensor (R11), and Q = I is
+//    taken: H(X_n) <- I, V(X_{n-1}) <- V(X_{n-1}) H(X_n);
+//  * eps = ||X_1||_F eps0 / sqrt(d-1) (Alg. 2 line 3);
+//  * Alg. 2 lines 5-9: [Q,R] = qr(V(X_n)), [U,S,V] = svd(R) (one-sided
+//    Jacobi: R V = U S), k = eps-rank (R5, capped by opts->rank), V(X_n) <- Q U_k
+//    (R13), H(X_{n+1}) <- (U_k^T R) H(X_{n+1}).  A wide V(X_n) (r_{n-1} I_n < r_n)
+//    is factored directly: Jacobi on V(X_n)^T gives its left singular vectors W
+//    (the accumulated rotations) and (S U^T) rows, V(X_n) <- W_k,
+//    H(X_{n+1}) <- (V(X_n)^T W)_k^T H(X_{n+1}).
+int deterministic_impl(tt_ctx* c, int S, const tt_view* terms, const tt_round_opts* o,
+                       tt_tensor** outp) {
+  std::vector<int64_t> dims;
+  TTR_TRY(validate(terms, S, dims));
+  if (!o || o->tol < 0.0 || o->rank < 0) {
+    set_error("tt_round_deterministic: need opts with tol >= 0 and rank >= 0");
+    return TT_ERR_ARG;
+  }
+  if (c->world > 1) {
+    set_error("tt_round_deterministic runs on one GPU (world size %d)", c->world);
+    return TT_ERR_ARG;
+  }
+  const int d = int(dims.size());
+  TTR_CUDA(cudaSetDevice(c->device));
+  cudaStream_t s = c->stream;
+  PhaseTimer tm(*c);
+  tm.begin(6);
+  Terms T;
+  TTR_TRY(stage_terms(*c, terms, S, T));
+  for (int n = 0; n < d; ++n) TTR_TRY(wait_core(*c, T, n));
+  std::vector<int64_t> r(d + 1, 0);
+  r[0] = r[d] = 1;
+  for (int n = 1; n < d; ++n)
+    for (int j = 0; j < S; ++j) r[n] += T.R[j][n];
+  std::unique_ptr<tt_tensor> X(new tt_tensor);
+  X->stream = s;
+  X->d = d;
+  X->dims = dims;
+  X->ranks = r;
+  X->bufs.resize(d);
+  X->ptrs.resize(d);
+  // ---- assembly
+  for (int n = 1; n <= d; ++n) {
+    const int64_t r0 = r[n - 1], In = dims[n - 1], r1 = r[n];
+    TTR_TRY(dalloc(X->bufs[n - 1], size_t(r0) * In * r1, s));
+    if (S > 1 && n > 1 && n < d)
+      TTR_CUDA(cudaMemsetAsync(X->bufs[n - 1].p, 0, sizeof(double) * r0 * In * r1, s));
+    int64_t A0 = 0, B0 = 0;
+    for (int j = 0; j < S; ++j) {
+      const int64_t ra = T.R[j][n - 1], rb = T.R[j][n];
+      // element (A0 + a, i, B0 + b) at (A0 + a) + r0 (i + In (B0 + b)); rows of
+      // (a) contiguous, (i, b) a uniform stride r0 (dst) / ra (src)
+      double* dst = X->bufs[n - 1].p + (n == 1 ? 0 : A0) + r0 * In * (n == d ? 0 : B0);
+      TTR_CUDA(cudaMemcpy2DAsync(dst, sizeof(double) * r0, T.core[j][n - 1], sizeof(double) * ra,
+                                 sizeof(double) * ra, size_t(In * rb), cudaMemcpyDeviceToDevice,
+                                 s));
+      if (n > 1) A0 += ra;
+      if (n < d) B0 += rb;
+    }
+  }
+  // ---- Alg. 1, n = d .. 2
+  tm.begin(3);
+  for (int n = d; n >= 2; --n) {
+    const int64_t r0 = r[n - 1], In = dims[n - 1], r1 = r[n], mrow = In * r1;
+    const int64_t mp = r[n - 2] * dims[n - 2];
+    DBuf newn, newp;
+    if (mrow >= r0) {
+      DBuf Q, R;
+      TTR_TRY(dalloc(Q, size_t(mrow) * r0, s));
+      TTR_TRY(dalloc(R, size_t(r0) * r0, s));
+      TTR_TRY(qr(*c, mrow, r0, X->bufs[n - 1].p, r0, true, Q.p, R.p, s));   // qr(H(X_n)^T)
+      TTR_TRY(dalloc(newn, size_t(r0) * mrow, s));
+      TTR_TRY(transpose(*c, Q.p, mrow, r0, mrow, newn.p, r0, s));           // H(X_n) = Q^T
+      TTR_TRY(dalloc(newp, size_t(mp) * r0, s));
+      TTR_TRY(gemm1(*c, false, true, int(mp), int(r0), int(r0), 1.0, X->bufs[n - 2].p, int(mp),
+                    R.p, int(r0), 0.0, newp.p, int(mp), s));                 // V(X_{n-1}) R^T
+    } else {
+      // wide: bond shrinks to mrow; H(X_n) <- I, V(X_{n-1}) <- V(X_{n-1}) H(X_n)
+      TTR_TRY(dalloc(newp, size_t(mp) * mrow, s));
+      TTR_TRY(gemm1(*c, false, false, int(mp), int(mrow), int(r0), 1.0, X->bufs[n - 2].p,
+                    int(mp), X->bufs[n - 1].p, int(r0), 0.0, newp.p, int(mp), s));
+      TTR_TRY(dalloc(newn, size_t(mrow) * mrow, s));
+      TTR_TRY(fill_zero(*c, newn.p, mrow * mrow, s));
+      TTR_TRY(set_identity(*c, newn.p, mrow, s));
+      r[n - 1] = mrow;
+    }
+    X->bufs[n - 1] = std::move(newn);
+    X->bufs[n - 2] = std::move(newp);
+  }
+  tm.end(3);
+  // ---- eps (Alg. 2 line 3)
+  double eps = 0.0;
+  if (o->tol > 0.0) {
+    DBuf nrm;
+    TTR_TRY(dalloc(nrm, 1, s));
+    TTR_TRY(fro_norm(*c, X->bufs[0].p, r[1] * dims[0], nrm.p, s));
+    double h = 0.0;
+    TTR_CUDA(cudaMemcpyAsync(&h, nrm.p, sizeof(double), cudaMemcpyDeviceToHost, s));
+    TTR_CUDA(cudaStreamSynchronize(s));
+    eps = h * o->tol / sqrt(double(d - 1));
+  }
+  // ---- Alg. 2, n = 1 .. d-1
+  tm.begin(5);
+  IBuf kdev;
+  TTR_TRY(ialloc(kdev, 1, s));
+  for (int n = 1; n <= d - 1; ++n) {
+    const int64_t r0 = r[n - 1], In = dims[n - 1], r1 = r[n], m = r0 * In;
+    const int64_t In1 = dims[n], r2 = r[n + 1];
+    const bool wide = m < r1;
+    const int64_t cols = wide ? m : r1;      // number of singular values
+    DBuf AV, V, sig, Q, R, Uk, B, newn, newq;
+    TTR_TRY(dalloc(sig, size_t(cols), s));
+    if (!wide) {
+      TTR_TRY(dalloc(Q, size_t(m) * r1, s));
+      TTR_TRY(dalloc(R, size_t(r1) * r1, s));
+      TTR_TRY(qr(*c, m, r1, X->bufs[n - 1].p, m, false, Q.p, R.p, s));     // line 6
+      TTR_TRY(dalloc(AV, size_t(r1) * r1, s));
+      if (svd_nov_fits(r1, r1)) {
+        TTR_TRY(svd_nov(*c, r1, r1, R.p, r1, AV.p, sig.p, s));              // line 7: R V = U S
+      } else {
+        TTR_TRY(dalloc(V, size_t(r1) * r1, s));
+        TTR_TRY(svd_jacobi(*c, r1, r1, R.p, r1, AV.p, V.p, sig.p, s));
+      }
+    } else {
+      DBuf Vt;
+      TTR_TRY(dalloc(Vt, size_t(r1) * m, s));
+      TTR_TRY(transpose(*c, X->bufs[n - 1].p, m, r1, m, Vt.p, r1, s));      // V(X_n)^T
+      TTR_TRY(dalloc(AV, size_t(r1) * m, s));
+      TTR_TRY(dalloc(V, size_t(m) * m, s));
+      TTR_TRY(svd_jacobi(*c, r1, m, Vt.p, r1, AV.p, V.p, sig.p, s));        // V^T W = U S
+    }
+    int64_t k;
+    TTR_TRY(eps_rank_dev(*c, sig.p, int(cols), nullptr, eps, int(o->rank), kdev.p, s));
+    {
+      int kh = 0;
+      TTR_CUDA(cudaMemcpyAsync(&kh, kdev.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+      TTR_CUDA(cudaStreamSynchronize(s));
+      k = kh;
+    }
+    TTR_TRY(dalloc(newn, size_t(m) * k, s));
+    TTR_TRY(dalloc(B, size_t(k) * r1, s));
+    if (!wide) {
+      TTR_TRY(dalloc(Uk, size_t(r1) * k, s));
+      TTR_TRY(scale_by_inv_sigma(*c, AV.p, r1, k, sig.p, Uk.p, 1, s));       // U_k
+      TTR_TRY(gemm1(*c, false, false, int(m), int(k), int(r1), 1.0, Q.p, int(m), Uk.p,
+                    int(r1), 0.0, newn.p, int(m), s));                        // line 8: Q U_k
+      TTR_TRY(gemm1(*c, true, false, int(k), int(r1), int(r1), 1.0, Uk.p, int(r1), R.p,
+                    int(r1), 0.0, B.p, int(k), s));                           // U_k^T R = S_k V_k^T
+    } else {
+      TTR_CUDA(cudaMemcpyAsync(newn.p, V.p, sizeof(double) * m * k, cudaMemcpyDeviceToDevice,
+                               s));                                          // W_k
+      TTR_TRY(transpose(*c, AV.p, r1, k, r1, B.p, k, s));                   // (S U^T)_k
+    }
+    // line 9: H(X_{n+1}) <- B H(X_{n+1})
+    TTR_TRY(dalloc(newq, size_t(k) * In1 * r2, s));
+    TTR_TRY(gemm1(*c, false, false, int(k), int(In1 * r2), int(r1), 1.0, B.p, int(k),
+                  X->bufs[n].p, int(r1), 0.0, newq.p, int(k), s));
+    X->bufs[n - 1] = std::move(newn);
+    X->bufs[n] = std::move(newq);
+    r[n] = k;
+  }
+  tm.end(5);
+  X->ranks = r;
+  for (int n = 0; n < d; ++n) X->ptrs[n] = X->bufs[n].p;
+  int fl[4];
+  TTR_TRY(read_flags(*c, fl, 4));
+  X->flags = TT_FLAG_LEFT_ORTH | (fl[1] ? TT_FLAG_QR_FALLBACK : 0);
+  X->passes = 1;
+  tm.end(6);
+  TTR_CUDA(cudaStreamSynchronize(s));
+  tm.finish();
+  if (fl[3] & 1) {
+    set_error("QR breakdown even after the Householder fallback");
+    return TT_ERR_NUMERIC;
+  }
+  *outp = X.release();
   return TT_OK;
 }
 
@@ -886,10 +1073,16 @@ int tt_round_sum(tt_ctx_t c, int32_t S_local, const tt_view* terms, const tt_rou
   return guarded([&] { return round_sum_impl(c, S_local, terms, opts, sketch, out); });
 }
 
-int tt_round_deterministic(tt_ctx_t, int32_t, const tt_view*, const tt_round_opts*,
-                           tt_tensor_t*) {
-  set_error("tt_round_deterministic is not implemented in this build (SURVEY §8f NEXT-1)");
-  return TT_ERR_ARG;
+int tt_round_deterministic(tt_ctx_t c, int32_t S, const tt_view* terms, const tt_round_opts* opts,
+                           tt_tensor_t* out) {
+  if (!c || !out) {
+    set_error("tt_round_deterministic: null ctx/out");
+    return TT_ERR_ARG;
+  }
+  return guarded([&] {
+    TTR_CUDA(cudaMemsetAsync(c->flags.p, 0, sizeof(int) * c->nflags, c->stream));
+    return deterministic_impl(c, S, terms, opts, out);
+  });
 }
 
 int tt_inner(tt_ctx_t c, const tt_view* x, const tt_view* y, double* out) {

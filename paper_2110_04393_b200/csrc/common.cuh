@@ -160,9 +160,9 @@ int svd_jacobi(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, doubl
 int svd_nov(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, double* AV,
             double* sigma, cudaStream_t s);
 bool svd_nov_fits(int64_t m, int64_t n);
-// B(:, c) = AV(:, c) / sigma_c^2, c < k (0 for negligible sigma_c)
-int scale_by_inv_sigma2(Ctx& c, const double* AV, int64_t m, int64_t k, const double* sigma,
-                        double* B, cudaStream_t s);
+// B(:, c) = AV(:, c) / sigma_c^pw, c < k, pw in {1, 2} (0 for negligible sigma_c)
+int scale_by_inv_sigma(Ctx& c, const double* AV, int64_t m, int64_t k, const double* sigma,
+                       double* B, int pw, cudaStream_t s);
 // k = eps-rank of sigma (n values, descending) given absolute eps and cap rmax
 // (0 = none), written to dst (device int).
 int eps_rank_dev(Ctx& c, const double* sigma, int n, const double* eps_dev, double eps_host,
@@ -173,6 +173,8 @@ int fro_norm(Ctx& c, const double* x, int64_t n, double* out, cudaStream_t s);
 int transpose(Ctx& c, const double* src, int64_t rows, int64_t cols, int64_t lds,
               double* dst, int64_t ldd, cudaStream_t s);
 int fill_zero(Ctx& c, double* p, int64_t n, cudaStream_t s);
+// diagonal of the n x n matrix p (ld n) set to 1 (other entries untouched)
+int set_identity(Ctx& c, double* p, int64_t n, cudaStream_t s);
 // dst[i] = (flag && *flag) ? 0 : src? (helper for degenerate cases)
 int max_abs_is_zero(Ctx& c, const double* x, int64_t n, int* flag_dst, cudaStream_t s);
 

@@ -1267,16 +1267,16 @@ __global__ void __launch_bounds__(kJacThreads)
   }
 }
 
-// B(:, c) = AV(:, c) / sigma_c^2 for c < k (0 when sigma_c is negligible), so that
-// B^T H(X_n) = V_k^T Q^T (see svd_nov).
-__global__ void scale_by_inv_sigma2_kernel(const double* __restrict__ AV, int m, int k,
-                                           const double* __restrict__ sigma,
-                                           double* __restrict__ B) {
+// B(:, c) = AV(:, c) / sigma_c^pw for c < k (0 when sigma_c is negligible), so that
+// B^T H(X_n) = V_k^T Q^T (pw = 2, see svd_nov) or B = U_k (pw = 1).
+__global__ void scale_by_inv_sigma_kernel(const double* __restrict__ AV, int m, int k,
+                                          const double* __restrict__ sigma,
+                                          double* __restrict__ B, int pw) {
   const double s0 = sigma[0];
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < m * k; e += gridDim.x * blockDim.x) {
     const int c = e / m;
     const double sc = sigma[c];
-    B[e] = (sc > s0 * double(m) * 0x1p-52) ? AV[e] / (sc * sc) : 0.0;
+    B[e] = (sc > s0 * double(m) * 0x1p-52) ? AV[e] / (pw == 2 ? sc * sc : sc) : 0.0;
   }
 }
 
@@ -1321,6 +1321,12 @@ __global__ void transpose_kernel(const double* __restrict__ src, int64_t rows, i
   }
 }
 
+__global__ void set_identity_kernel(double* p, int64_t n) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x)
+    p[i + i * n] = 1.0;
+}
+
 __global__ void fill_zero_kernel(double* p, int64_t n) {
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
        i += int64_t(gridDim.x) * blockDim.x)
@@ -1359,10 +1365,10 @@ int svd_jacobi(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, doubl
   return launched();
 }
 
-int scale_by_inv_sigma2(Ctx& c, const double* AV, int64_t m, int64_t k, const double* sigma,
-                        double* B, cudaStream_t s) {
+int scale_by_inv_sigma(Ctx& c, const double* AV, int64_t m, int64_t k, const double* sigma,
+                       double* B, int pw, cudaStream_t s) {
   const int blocks = int(std::min<int64_t>((m * k + 255) / 256, c.sm_count * 4));
-  scale_by_inv_sigma2_kernel<<<std::max(1, blocks), 256, 0, s>>>(AV, int(m), int(k), sigma, B);
+  scale_by_inv_sigma_kernel<<<std::max(1, blocks), 256, 0, s>>>(AV, int(m), int(k), sigma, B, pw);
   return launched();
 }
 
@@ -1381,6 +1387,11 @@ int transpose(Ctx& c, const double* src, int64_t rows, int64_t cols, int64_t lds
               int64_t ldd, cudaStream_t s) {
   dim3 grid(unsigned((rows + 31) / 32), unsigned((cols + 31) / 32));
   transpose_kernel<<<grid, dim3(32, 8), 0, s>>>(src, rows, cols, lds, dst, ldd);
+  return launched();
+}
+
+int set_identity(Ctx& c, double* p, int64_t n, cudaStream_t s) {
+  set_identity_kernel<<<std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 64)), 256, 0, s>>>(p, n);
   return launched();
 }
 

@@ -207,3 +207,53 @@ def test_config5_full_size_in_bench_launch_configuration():
                            rank=w.rank)
     r, X = check(res, ref)
     assert res.ranks == [1] + [w.rank] * (w.d - 1) + [1]
+
+
+# ------------------------------------------------------------------ deterministic (NEXT-1)
+def run_det(ctx, terms, tol=0.0, rank=0):
+    np_terms = [ttsynth.to_numpy(t) for t in terms]
+    ref = oracle.tt_round(oracle.tt_add(np_terms), tol, rank)
+    res = ctx.tt_round_deterministic(gpu_terms(terms), tol=tol, rank=rank)
+    X = res.numpy()
+    assert res.ranks == oracle.ranks_of(ref), (res.ranks, oracle.ranks_of(ref))
+    r = oracle.rel_diff(X, ref)
+    assert r <= TOL, r
+    return X, ref
+
+
+@pytest.mark.parametrize("tol,rank", [(0.0, 4), (1e-8, 0), (1e-2, 0), (0.0, 0)])
+def test_deterministic_config1(ctx, tol, rank):
+    w = ttsynth.config1_tiny()
+    X, ref = run_det(ctx, w.terms, tol, rank)
+    assert oracle.left_orth_residual(X) < 1e-12
+
+
+def test_deterministic_single_term_rank50(ctx):
+    w = ttsynth.config2_single(d=6)
+    run_det(ctx, w.terms, tol=1e-6)
+    run_det(ctx, w.terms, rank=25)
+
+
+@pytest.mark.parametrize("seed", [3, 4])
+def test_deterministic_ragged(ctx, seed):
+    dims = [3, 7, 5, 6, 2]
+    rng = np.random.default_rng(seed)
+    tr = [[1] + [int(x) for x in rng.integers(1, 7, size=len(dims) - 1)] + [1] for _ in range(4)]
+    terms = ttsynth.random_terms(seed, dims, tr)
+    run_det(ctx, terms, tol=1e-10)
+    run_det(ctx, terms, rank=3)
+
+
+def test_deterministic_sum_large_ranks(ctx):
+    # assembled ranks 180 > 160: the generic Cholesky and the Jacobi with V
+    w = ttsynth.config3_sum10(d=5, I=10, S=3)
+    run_det(ctx, w.terms, tol=1e-9)
+
+
+def test_deterministic_matches_randomized_when_sketch_is_exact(ctx):
+    # rank-r truncation of an exactly low-rank sum: both roundings give the best
+    # approximation (P:653-663 with l >= true rank), hence the same tensor
+    terms = ttsynth.random_terms(41, [5, 6, 4, 5], [[1, 2, 3, 2, 1], [1, 3, 2, 2, 1]])
+    a = ctx.tt_round_deterministic(gpu_terms(terms), tol=1e-12).numpy()
+    b = ctx.tt_round_sum(gpu_terms(terms), mode="tol", tol=1e-12, oversample=12, seed=2).numpy()
+    assert oracle.rel_diff(a, b) < 1e-10
