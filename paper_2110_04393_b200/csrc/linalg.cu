@@ -432,7 +432,6 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
       const int rho = tid >> 2, qt = tid & 3;
       const int r = r0 + rho;
       const bool live = r < n;
-      const unsigned qmask = 0xFu << (lane & 28);
       double a[8];
 #pragma unroll
       for (int jj = 0; jj < 8; ++jj) a[jj] = live ? S[r + (k0 + 8 * qt + jj) * ld] : 0.0;
@@ -450,7 +449,8 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
         }
         double xq[8];
 #pragma unroll
-        for (int jj = 0; jj < 8; ++jj) xq[jj] = __shfl_sync(qmask, a[jj], (lane & 28) | qq);
+        for (int jj = 0; jj < 8; ++jj)   // every lane reaches this: full mask, no divergence checks
+          xq[jj] = __shfl_sync(0xffffffffu, a[jj], (lane & 28) | qq);
         if (qt > qq) {
 #pragma unroll
           for (int j2 = 0; j2 < 8; ++j2) {

@@ -65,7 +65,6 @@ __global__ void __launch_bounds__(32 * RPT) __maxnreg__(RPT >= 18 ? 96 : 128)
   const double small = neg * neg * fro2;                // negligible squared norm
   const int np = (n + 1) & ~1;
   const int half = np / 2;
-  const unsigned gmask = 0xFFu << (lane & 24);
   const int nw = nt / 32;
 
   int sweep = 0;
@@ -90,9 +89,10 @@ __global__ void __launch_bounds__(32 * RPT) __maxnreg__(RPT >= 18 ? 96 : 128)
       const int p0 = (grp == 0) ? 0 : pp + 1, q0 = qq + 1;
       pp = (pp + 1 == np - 1) ? 0 : pp + 1;
       qq = (qq + 1 == np - 1) ? 0 : qq + 1;
-      if (grp >= half) continue;
-      const int p = min(p0, q0), q = max(p0, q0);
-      if (q >= n) continue;                             // dummy column (odd n)
+      // every thread takes part in the shuffles (full mask: no divergence
+      // checks); groups without a pair work on column 0 and write nothing
+      const bool act = grp < half && max(p0, q0) < n;
+      const int p = act ? min(p0, q0) : 0, q = act ? max(p0, q0) : 0;
       double2* wp = reinterpret_cast<double2*>(W + p * LDW) + t8;
       double2* wq = reinterpret_cast<double2*>(W + q * LDW) + t8;
       double2 x[S2], y[S2];
@@ -104,9 +104,9 @@ __global__ void __launch_bounds__(32 * RPT) __maxnreg__(RPT >= 18 ? 96 : 128)
         ga = fma(x[s].x, y[s].x, fma(x[s].y, y[s].y, ga));
       }
 #pragma unroll
-      for (int o = 4; o; o >>= 1) ga += __shfl_xor_sync(gmask, ga, o, kGroup);
+      for (int o = 4; o; o >>= 1) ga += __shfl_xor_sync(0xffffffffu, ga, o);
       const double al = cn[p], be = cn[q];
-      if (!(fmin(al, be) > small) || !(fabs(ga) > tol * sqrt(al * be))) continue;
+      if (!act || !(fmin(al, be) > small) || !(fabs(ga) > tol * sqrt(al * be))) continue;
       const double zeta = (be - al) / (2.0 * ga);
       const double tt = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
       const double cs = rsqrt(fma(tt, tt, 1.0)), sn = cs * tt;
