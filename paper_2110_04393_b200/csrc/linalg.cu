@@ -525,17 +525,21 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
     const int k0 = 32 * w, kb = min(32, n - k0);
     const int c = lane;
     if (c < kb) {
+      const double* Lr = S + k0 + k0 * ld;         // L(k0 + r, k0 + t) = Lr[r + t ld]
+      double* Xc = S + (k0 + c) + k0 * ld;         // X(t, c) parked at Xc[t ld]
 #pragma unroll 1
       for (int r = c + 1; r < kb; ++r) {
-        double acc0 = -S[(k0 + r) + (k0 + c) * ld] * rdiag[k0 + c], acc1 = 0.0;
+        double a0 = -Lr[r + c * ld] * rdiag[k0 + c], a1 = 0.0, a2 = 0.0, a3 = 0.0;
         int t = c + 1;
 #pragma unroll 1
-        for (; t + 1 < r; t += 2) {
-          acc0 = fma(-S[(k0 + r) + (k0 + t) * ld], S[(k0 + c) + (k0 + t) * ld], acc0);
-          acc1 = fma(-S[(k0 + r) + (k0 + t + 1) * ld], S[(k0 + c) + (k0 + t + 1) * ld], acc1);
+        for (; t + 3 < r; t += 4) {
+          a0 = fma(-Lr[r + t * ld], Xc[t * ld], a0);
+          a1 = fma(-Lr[r + (t + 1) * ld], Xc[(t + 1) * ld], a1);
+          a2 = fma(-Lr[r + (t + 2) * ld], Xc[(t + 2) * ld], a2);
+          a3 = fma(-Lr[r + (t + 3) * ld], Xc[(t + 3) * ld], a3);
         }
-        if (t < r) acc0 = fma(-S[(k0 + r) + (k0 + t) * ld], S[(k0 + c) + (k0 + t) * ld], acc0);
-        S[(k0 + c) + (k0 + r) * ld] = (acc0 + acc1) * rdiag[k0 + r];
+        for (; t < r; ++t) a0 = fma(-Lr[r + t * ld], Xc[t * ld], a0);
+        Xc[r * ld] = ((a0 + a1) + (a2 + a3)) * rdiag[k0 + r];
       }
     }
   }
