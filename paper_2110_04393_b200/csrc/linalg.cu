@@ -358,10 +358,12 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
 #endif
   // lower triangle of G (+ shift) into S, pads 0; loads batched 8 deep (the
   // loop is latency bound: one L2 round trip per batch, not per element)
-#pragma unroll 8
-  for (int e = tid; e < ld * n8; e += kBlkThreads) {
-    const int i = e % ld, j = e / ld;
-    S[e] = (i < n && j < n && i >= j) ? G[i + int64_t(j) * n] + ((i == j) ? shift : 0.0) : 0.0;
+  // (2-D loops: no integer division by the runtime n / ld per element)
+  for (int j = w; j < n8; j += NW) {
+#pragma unroll 4
+    for (int i = lane; i < ld; i += 32)
+      S[i + j * ld] = (i < n && j < n && i >= j) ? G[i + int64_t(j) * n] + ((i == j) ? shift : 0.0)
+                                                 : 0.0;
   }
   __syncthreads();
   CHOL_PROF(5);
@@ -500,25 +502,31 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
   __syncthreads();
   const bool bad_final = s_bad;
   // route checks on diag(L); R = L^T before L is overwritten by its inverse
-  if (tid == 0 && !s_zero && !(flags[2] & 1)) {
-    int bad2 = bad_final;
+  if (w == 0 && !s_zero) {   // route checks on diag(L), warp-parallel
     double dev = 0.0, dmin = INFINITY, dmax = 0.0;
-    for (int i = 0; i < n; ++i) {
+    for (int i = lane; i < n; i += 32) {
       const double d = fabs(S[i + i * ld]);
       dmin = fmin(dmin, d);
       dmax = fmax(dmax, d);
-      if (needs_dev(md)) dev = fmax(dev, fabs(S[i + i * ld] - 1.0));
+      dev = fmax(dev, fabs(S[i + i * ld] - 1.0));
     }
-    if ((mode & kStrict) && !(dmin >= dmax * kStrictRatio)) bad2 = 1;
-    if (s_clamped) flags[16] += 1;   // counter: clamped (rank-deficient) passes
-    route_update(flags, md, bad2, dev);
+    for (int o = 16; o; o >>= 1) {
+      dmin = fmin(dmin, __shfl_xor_sync(0xffffffffu, dmin, o));
+      dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+      dev = fmax(dev, __shfl_xor_sync(0xffffffffu, dev, o));
+    }
+    if (lane == 0 && !(flags[2] & 1)) {
+      int bad2 = bad_final;
+      if ((mode & kStrict) && !(dmin >= dmax * kStrictRatio)) bad2 = 1;
+      if (s_clamped) flags[16] += 1;   // counter: clamped (rank-deficient) passes
+      route_update(flags, md, bad2, needs_dev(md) ? dev : 0.0);
+    }
   }
   if (bad_final) return;   // outputs are not used (the route moved on)
   if (Rout)
-    for (int e = tid; e < n * n; e += kBlkThreads) {
-      const int r = e % n, c = e / n;   // R(r, c) = L(c, r)
-      Rout[e] = (c >= r) ? S[c + r * ld] : 0.0;
-    }
+    for (int c = w; c < n; c += NW)
+      for (int r = lane; r < n; r += 32)   // R(r, c) = L(c, r)
+        Rout[r + int64_t(c) * n] = (c >= r) ? S[c + r * ld] : 0.0;
   // ---- I0: X_kk = L_kk^{-1} for every block at once (warp k), lane c = column
   // c; X(r, c) (r > c) is parked at (c, r), the diagonal is rdiag
   if (w < nb) {
@@ -637,10 +645,9 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
     }
     __syncthreads();
   }
-  for (int e = tid; e < n * n; e += kBlkThreads) {
-    const int r = e % n, c = e / n;     // Rinv(r, c) = X(c, r), c >= r
-    Rinv[e] = (c >= r) ? S[c + r * ld] : 0.0;
-  }
+  for (int c = w; c < n; c += NW)
+    for (int r = lane; r < n; r += 32)   // Rinv(r, c) = X(c, r), c >= r
+      Rinv[r + int64_t(c) * n] = (c >= r) ? S[c + r * ld] : 0.0;
   CHOL_PROF(4);
 }
 
