@@ -409,141 +409,6 @@ int dispatch(Ctx& c, GemmParams& P, int maxM, int maxN, int maxK, cudaStream_t s
   }
 }
 
-// ---------------------------------------------------------------------------
-// B-stationary persistent GEMM for short K (K <= 64) and narrow N (N <= 144),
-// non-transposed operands: phase 1's Z = V(Y_n) W_n (Alg. 3 line 4; C5: 32 x
-// [16384 x 64] x [64 x 144]).  The generic kernel spends most of such a tile's
-// life in its prologue and epilogue (4 k-tiles) and re-reads A for each of the
-// three 48-wide N tiles; here a CTA keeps one summand's B (K x 144) in shared
-// memory, streams 128-row A tiles through a double buffer (one barrier per
-// tile) and writes each 128 x N tile straight from registers while the next
-// tile's loads and DMMAs proceed.  Warp tile 32 x 72 (4 x 9 m8n8k4 fragments):
-// 13 fragment loads per 36 DMMAs.  Work items (summand, 128-row tile) are split
-// into contiguous runs per CTA so B changes rarely.
-namespace bstat {
-constexpr int BM = 128, BN = 144, KMAX = 64;
-constexpr int LDA = BM + 4;        // A tile [k][m]
-constexpr int LDB = KMAX + 4;      // B tile [n][k]
-constexpr int NT = 256;
-constexpr size_t SMEM = (size_t(2) * KMAX * LDA + size_t(BN) * LDB) * sizeof(double);
-}  // namespace bstat
-
-__global__ void __launch_bounds__(bstat::NT, 1)
-    dgemm_bstat_kernel(const __grid_constant__ GemmParams P, int tiles_per_b, int items) {
-  using namespace bstat;
-  extern __shared__ __align__(16) double smem[];
-  double* sA0 = smem;
-  double* sB = smem + 2 * KMAX * LDA;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int g = lane >> 2, t = lane & 3;
-  const int wm0 = (warp & 3) * 32, wn0 = (warp >> 2) * 72;
-  const int per = (items + gridDim.x - 1) / gridDim.x;
-  const int it0 = blockIdx.x * per, it1 = min(items, it0 + per);
-  if (it0 >= it1) return;
-
-  auto load_A = [&](int item, int buf) {
-    const int b = item / tiles_per_b, tm = item % tiles_per_b;
-    const GemmDesc& D = P.d[b];
-    const int m0 = tm * BM, K = D.K;
-    double* sA = sA0 + buf * KMAX * LDA;
-    // 128 x K tile as 16-byte vectors along m (rows contiguous in a column)
-    for (int v = tid; v < (BM / 2) * KMAX; v += NT) {
-      const int m = 2 * (v % (BM / 2)), k = v / (BM / 2);
-      const int gm = m0 + m;
-      const int bytes = (k < K) ? ((gm + 1 < D.M) ? 16 : (gm < D.M ? 8 : 0)) : 0;
-      const double* src = bytes ? D.A + gm + int64_t(k) * D.lda : D.A;
-      cp_async16(sA + k * LDA + m, src, bytes);
-    }
-  };
-  auto load_B = [&](int b) {
-    const GemmDesc& D = P.d[b];
-    for (int v = tid; v < BN * (KMAX / 2); v += NT) {
-      const int k = 2 * (v % (KMAX / 2)), n = v / (KMAX / 2);
-      const int bytes = (n < D.N) ? ((k + 1 < D.K) ? 16 : (k < D.K ? 8 : 0)) : 0;
-      const double* src = bytes ? D.B + k + int64_t(n) * D.ldb : D.B;
-      cp_async16(sB + n * LDB + k, src, bytes);
-    }
-  };
-
-  int cur_b = -1, buf = 0;
-  load_A(it0, 0);
-  cp_async_commit();
-  for (int it = it0; it < it1; ++it) {
-    const int b = it / tiles_per_b, tm = it % tiles_per_b;
-    const GemmDesc& D = P.d[b];
-    if (b != cur_b) {   // new summand: its B (the previous tile's DMMAs are done)
-      __syncthreads();
-      load_B(b);
-      cp_async_commit();
-      cur_b = b;
-    }
-    if (it + 1 < it1 && (it + 1) / tiles_per_b == b) load_A(it + 1, buf ^ 1);
-    cp_async_commit();
-    cp_async_wait<1>();                  // this tile's A (and B) have landed
-    __syncthreads();
-    const double* sA = sA0 + buf * KMAX * LDA;
-    double acc[4][9][2];
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int j = 0; j < 9; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-    const int kend = (D.K + 3) & ~3;
-    for (int kk = 0; kk < kend; kk += 4) {
-      double af[4], bf[9];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) af[i] = sA[(kk + t) * LDA + wm0 + i * 8 + g];
-#pragma unroll
-      for (int j = 0; j < 9; ++j) bf[j] = sB[(wn0 + j * 8 + g) * LDB + kk + t];
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 9; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
-    }
-    // epilogue straight from registers (alpha / beta as in the generic kernel)
-    const int m0 = tm * BM;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int m = m0 + wm0 + i * 8 + g;
-      if (m >= D.M) continue;
-#pragma unroll
-      for (int j = 0; j < 9; ++j)
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int n = wn0 + j * 8 + 2 * t + e;
-          if (n < D.N) {
-            double* cp = D.C + m + int64_t(n) * D.ldc;
-            double v = P.alpha * acc[i][j][e];
-            if (P.beta != 0.0) v += P.beta * *cp;
-            *cp = v;
-          }
-        }
-    }
-    // the next tile's A was prefetched into buf ^ 1; make sure every warp has
-    // finished reading buf before it is refilled (two tiles ahead)
-    __syncthreads();
-    if (it + 1 < it1 && (it + 1) / tiles_per_b != b) {
-      load_A(it + 1, buf ^ 1);           // new summand: A was not prefetched
-      cp_async_commit();
-    }
-    buf ^= 1;
-  }
-  cp_async_wait<0>();
-}
-
-int launch_bstat(Ctx& c, GemmParams& P, int maxM, cudaStream_t s) {
-  static bool attr[64] = {false};
-  if (!attr[c.device & 63]) {
-    TTR_CUDA(cudaFuncSetAttribute(dgemm_bstat_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  int(bstat::SMEM)));
-    attr[c.device & 63] = true;
-  }
-  const int tiles_per_b = (maxM + bstat::BM - 1) / bstat::BM;
-  const int items = tiles_per_b * P.nbatch;
-  const int grid = std::min(items, c.sm_count);
-  dgemm_bstat_kernel<<<grid, bstat::NT, bstat::SMEM, s>>>(P, tiles_per_b, items);
-  return launched();
-}
-
 }  // namespace
 
 int gemm(Ctx& c, bool ta, bool tb, const GemmDesc* d, int nbatch, double alpha, double beta,
@@ -581,12 +446,7 @@ int gemm(Ctx& c, bool ta, bool tb, const GemmDesc* d, int nbatch, double alpha, 
     P.gate = gate;
     P.gate_val = gate_val;
     int r;
-    // short-K, narrow-N, many-row products (phase-1 Z): B-stationary persistent kernel
-    const bool bstat_ok = !ta && !tb && P.vec && gate == nullptr && maxK <= bstat::KMAX &&
-                          maxN <= bstat::BN && maxN > 96 &&
-                          long(maxM) * live >= 16L * bstat::BM * c.sm_count;
-    if (bstat_ok) r = launch_bstat(c, P, maxM, s);
-    else if (!ta && !tb) r = dispatch<false, false>(c, P, maxM, maxN, maxK, s);
+    if (!ta && !tb) r = dispatch<false, false>(c, P, maxM, maxN, maxK, s);
     else if (!ta && tb) r = dispatch<false, true>(c, P, maxM, maxN, maxK, s);
     else if (ta && !tb) r = dispatch<true, false>(c, P, maxM, maxN, maxK, s);
     else r = dispatch<true, true>(c, P, maxM, maxN, maxK, s);
