@@ -257,3 +257,50 @@ def test_deterministic_matches_randomized_when_sketch_is_exact(ctx):
     a = ctx.tt_round_deterministic(gpu_terms(terms), tol=1e-12).numpy()
     b = ctx.tt_round_sum(gpu_terms(terms), mode="tol", tol=1e-12, oversample=12, seed=2).numpy()
     assert oracle.rel_diff(a, b) < 1e-10
+
+
+# ------------------------------------------------------------------ more edge cases
+def test_unit_mode_and_rank_one_summands(ctx):
+    dims = [4, 1, 6, 1, 3]
+    terms = ttsynth.random_terms(51, dims, [[1, 1, 1, 1, 1, 1]] * 3)
+    res, ref = run_both(ctx, terms, 5, rank=2)
+    check(res, ref)
+    res, ref = run_both(ctx, terms, 5, sketch_only=True)
+    check(res, ref)
+
+
+def test_more_summands_than_one_gemm_batch(ctx):
+    # S = 70 > kMaxGemmBatch = 64: the batched GEMMs split into several launches
+    dims = [6, 5, 7, 4]
+    terms = ttsynth.random_terms(52, dims, [[1, 2, 3, 2, 1]] * 70)
+    res, ref = run_both(ctx, terms, 12, rank=8)
+    check(res, ref)
+
+
+def test_sketch_rank_above_structural_caps_is_flagged_and_exact(ctx):
+    import paper_2110_04393_b200 as P
+    terms = ttsynth.random_terms(53, [3, 4, 5], [[1, 2, 2, 1], [1, 3, 1, 1]])
+    res, ref = run_both(ctx, terms, 50, sketch_only=True)
+    check(res, ref)
+    assert res.flags & P.FLAG_RANK_CAPPED
+    S = oracle.tt_add([ttsynth.to_numpy(t) for t in terms])
+    assert oracle.rel_diff(res.numpy(), S) < 1e-12
+
+
+def test_partially_zero_summands(ctx):
+    terms = ttsynth.random_terms(54, [5, 6, 5, 4], [[1, 3, 3, 3, 1]] * 3)
+    terms[1] = [torch.zeros_like(c) for c in terms[1]]
+    res, ref = run_both(ctx, terms, 6, rank=3)
+    check(res, ref)
+
+
+def test_tolerance_bound_holds(ctx):
+    # truncation error of the returned TT against the input sum: the deterministic
+    # part obeys eps0 ||X||; the sketch adds its own (small) error on this
+    # exactly low-rank sum (l >= true rank)
+    terms = ttsynth.random_terms(55, [6, 7, 6, 5], [[1, 3, 4, 3, 1], [1, 2, 2, 2, 1]])
+    tol = 1e-3
+    res, ref = run_both(ctx, terms, 10, tol=tol)
+    check(res, ref)
+    S = oracle.tt_add([ttsynth.to_numpy(t) for t in terms])
+    assert oracle.rel_diff(res.numpy(), S) <= tol * (1 + 1e-10)
