@@ -227,11 +227,10 @@ namespace {
 
 constexpr int kCl = 8;          // CTAs per cluster
 constexpr int kUw = 4;          // columns per unit
-constexpr int kGpc = 3;         // groups per CTA: n <= 160 -> <= 20 groups
-constexpr int kTP = 16;         // threads per pair
-constexpr int kGT = kUw * kTP;  // threads per group (2 warps)
-constexpr int kRps = 10;        // rows per thread (m <= 160)
-constexpr int kRows = kTP * kRps;
+constexpr int kGpc = 3;         // groups (warps) per CTA: n <= 160 -> <= 20 groups
+constexpr int kG8 = 8;          // threads per pair
+constexpr int kRps = 20;        // rows per thread (m <= 160)
+constexpr int kRows = kG8 * kRps;
 
 struct JcShared {
   alignas(16) double slot[2][kGpc][2 * kUw][kRows];   // [buffer][group][t0..t3, b0..b3][rows]
@@ -242,11 +241,11 @@ struct JcShared {
   int rot;
 };
 
-constexpr int kJcThreads = kGpc * kGT;
+constexpr int kJcThreads = kGpc * 32;
 
-// rotate the pair (X, Y) held by this 16-lane subgroup (ids cx, cy, squared
+// rotate the pair (X, Y) held by this 8-lane subgroup (ids cx, cy, squared
 // norms ax, ay); p = min(id) is rotated as column p of the single-CTA kernel.
-// Rows are held as double2 (rows 2 t + 32 s, +1).  The angle
+// Rows are held as double2 (rows 2 t + 16 s, +1).  The angle
 //   t = sign(d) e / (|d| + sqrt(d^2 + e^2)),  d = a_q - a_p, e = 2 gamma
 // (= sign(zeta)/(|zeta| + sqrt(1 + zeta^2)), zeta = d/e) is computed in fp32 after
 // an exact power-of-two scaling: its error only changes how much of gamma one
@@ -263,7 +262,7 @@ __device__ __forceinline__ bool jc_rotate(double2 (&x)[kR2], double2 (&y)[kR2], 
   }
   double ga = ga0 + ga1;
 #pragma unroll
-  for (int o = kTP / 2; o; o >>= 1) ga += __shfl_xor_sync(0xffffffffu, ga, o);
+  for (int o = 4; o; o >>= 1) ga += __shfl_xor_sync(0xffffffffu, ga, o);
   const bool swp = cx > cy;
   const double ap = swp ? ay : ax, aq = swp ? ax : ay;
   if (!(cx < n && cy < n && fmin(ap, aq) > small && fabs(ga) > tol * sqrt(ap * aq))) return false;
@@ -287,10 +286,6 @@ __device__ __forceinline__ bool jc_rotate(double2 (&x)[kR2], double2 (&y)[kR2], 
   return true;
 }
 
-__device__ __forceinline__ void group_sync(int lg) {
-  asm volatile("bar.sync %0, %1;" ::"r"(1 + lg), "r"(kGT) : "memory");
-}
-
 __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kJcThreads)
     jacobi_cluster_kernel(const double* __restrict__ A, int64_t lda, int m, int n, int gpc,
                           double* __restrict__ AV, double* __restrict__ sigma, int max_sweeps,
@@ -300,8 +295,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kJcThreads)
   cg::cluster_group cl = cg::this_cluster();
   const int crank = int(cl.block_rank());
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int lg = tid / kGT, gtid = tid % kGT;              // group, thread in group
-  const int rho = gtid / kTP, tp = gtid % kTP;             // pair slot, thread in pair
+  const int lg = warp, rho = lane >> 3, t8 = lane & 7;    // group, pair slot, thread in pair
   const int U = (n + kUw - 1) / kUw, UP = U + (U & 1), halfU = UP / 2;
   const int g = crank * gpc + lg;
   const bool live = lg < gpc && g < halfU;
@@ -315,9 +309,9 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kJcThreads)
       const int c0 = unit < 0 ? n : kUw * unit + (c8 % kUw);
       const int cid = c0 < n ? c0 : n;
       double* sl = sh.slot[0][lg][c8];
-      for (int i = gtid; i < kRows; i += kGT)
+      for (int i = lane; i < kRows; i += 32)
         sl[i] = (cid < n && i < m) ? A[i + int64_t(cid) * lda] : 0.0;
-      if (gtid == 0) {
+      if (lane == 0) {
         sh.col[0][lg][c8] = cid;
         sh.alpha[0][lg][c8] = 0.0;
       }
@@ -326,7 +320,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kJcThreads)
   __syncthreads();
   double part = 0.0;
   for (int c8 = 0; c8 < 2 * kUw; ++c8)
-    for (int i = gtid; i < kRows; i += kGT) {
+    for (int i = lane; i < kRows; i += 32) {
       const double v = sh.slot[0][lg][c8][i];
       part = fma(v, v, part);
     }
@@ -335,7 +329,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kJcThreads)
   __syncthreads();
   if (tid == 0) {
     double s = 0.0;
-    for (int w = 0; w < kJcThreads / 32; ++w) s += sh.red[w];
+    for (int w = 0; w < kGpc; ++w) s += sh.red[w];
     for (int r = 0; r < kCl; ++r) cl.map_shared_rank(&sh, r)->norms[crank] = s;   // scratch
   }
   cl.sync();
@@ -362,26 +356,26 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kJcThreads)
   auto in_place = [&](double (*sl)[kRows], double* al, const int* cid, int cx, int cy,
                       int& rot) {
     double2 x[kR2], y[kR2];
-    const double2* px = reinterpret_cast<const double2*>(sl[cx]) + tp;
-    const double2* py = reinterpret_cast<const double2*>(sl[cy]) + tp;
+    const double2* px = reinterpret_cast<const double2*>(sl[cx]) + t8;
+    const double2* py = reinterpret_cast<const double2*>(sl[cy]) + t8;
 #pragma unroll
     for (int s = 0; s < kR2; ++s) {
-      x[s] = px[kTP * s];
-      y[s] = py[kTP * s];
+      x[s] = px[kG8 * s];
+      y[s] = py[kG8 * s];
     }
     double ax = al[cx], ay = al[cy];
     if (live && jc_rotate(x, y, cid[cx], cid[cy], ax, ay, n, small, tol)) {
       rot = 1;
-      double2* wx = reinterpret_cast<double2*>(sl[cx]) + tp;
-      double2* wy = reinterpret_cast<double2*>(sl[cy]) + tp;
+      double2* wx = reinterpret_cast<double2*>(sl[cx]) + t8;
+      double2* wy = reinterpret_cast<double2*>(sl[cy]) + t8;
 #pragma unroll
       for (int s = 0; s < kR2; ++s) {
-        wx[kTP * s] = x[s];
-        wy[kTP * s] = y[s];
+        wx[kG8 * s] = x[s];
+        wy[kG8 * s] = y[s];
       }
-      if (tp == 0) { al[cx] = ax; al[cy] = ay; }
+      if (t8 == 0) { al[cx] = ax; al[cy] = ay; }
     }
-    group_sync(lg);
+    __syncwarp();
   };
 
   int buf = 0, sweep = 0;
@@ -397,17 +391,13 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kJcThreads)
         // exact squared norms (subgroup rho: columns rho and 4 + rho) ...
         for (int c = rho; c < 2 * kUw; c += kUw) {
           double a2 = 0.0;
-          const double2* pc = reinterpret_cast<const double2*>(sl[c]) + tp;
 #pragma unroll
-          for (int s = 0; s < kR2; ++s) {
-            const double2 v = pc[kTP * s];
-            a2 = fma(v.x, v.x, fma(v.y, v.y, a2));
-          }
+          for (int s = 0; s < kRps; ++s) a2 = fma(sl[c][t8 + kG8 * s], sl[c][t8 + kG8 * s], a2);
 #pragma unroll
-          for (int o = kTP / 2; o; o >>= 1) a2 += __shfl_xor_sync(0xffffffffu, a2, o);
-          if (live && tp == 0) al[c] = a2;
+          for (int o = 4; o; o >>= 1) a2 += __shfl_xor_sync(0xffffffffu, a2, o);
+          if (live && t8 == 0) al[c] = a2;
         }
-        group_sync(lg);
+        __syncwarp();
         // ... then the intra-unit pairs: {(0,1),(2,3)}, {(0,2),(1,3)}, {(0,3),(1,2)}
         // in both units (subgroup rho: unit rho >> 1, pair rho & 1)
 #pragma unroll 1
@@ -425,26 +415,26 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kJcThreads)
       {
         const int cx = rho, cy = kUw + ((rho + kUw - 1) & 3);
         double2 x[kR2], y[kR2];
-        const double2* px = reinterpret_cast<const double2*>(sl[cx]) + tp;
-        const double2* py = reinterpret_cast<const double2*>(sl[cy]) + tp;
+        const double2* px = reinterpret_cast<const double2*>(sl[cx]) + t8;
+        const double2* py = reinterpret_cast<const double2*>(sl[cy]) + t8;
 #pragma unroll
         for (int s = 0; s < kR2; ++s) {
-          x[s] = px[kTP * s];
-          y[s] = py[kTP * s];
+          x[s] = px[kG8 * s];
+          y[s] = py[kG8 * s];
         }
         double ax = al[cx], ay = al[cy];
         const int idx = cid[cx], idy = cid[cy];
         if (live && jc_rotate(x, y, idx, idy, ax, ay, n, small, tol)) rot = 1;
         if (live) {
           const int nb = buf ^ 1;
-          double2* dx = reinterpret_cast<double2*>(sht->slot[nb][lt][wt + cx]) + tp;
-          double2* dy = reinterpret_cast<double2*>(shb->slot[nb][lb][wb + (cy - kUw)]) + tp;
+          double2* dx = reinterpret_cast<double2*>(sht->slot[nb][lt][wt + cx]) + t8;
+          double2* dy = reinterpret_cast<double2*>(shb->slot[nb][lb][wb + (cy - kUw)]) + t8;
 #pragma unroll
           for (int s = 0; s < kR2; ++s) {
-            dx[kTP * s] = x[s];
-            dy[kTP * s] = y[s];
+            dx[kG8 * s] = x[s];
+            dy[kG8 * s] = y[s];
           }
-          if (tp == 0) {
+          if (t8 == 0) {
             sht->alpha[nb][lt][wt + cx] = ax;
             shb->alpha[nb][lb][wb + cy - kUw] = ay;
             sht->col[nb][lt][wt + cx] = idx;
@@ -469,22 +459,18 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kJcThreads)
     flags[12] += conv ? sweep + 1 : sweep;
     flags[13] += 1;
   }
-  // norms of every column into every CTA (by column id), then sort by rank;
-  // the first warp of each group does this
-  const bool w0 = (gtid < 32);
-  if (w0) {
-    for (int c8 = 0; c8 < 2 * kUw; ++c8) {
-      const double* sl = sh.slot[buf][lgc][c8];
-      double s2 = 0.0;
-      for (int i = lane; i < kRows; i += 32) s2 = fma(sl[i], sl[i], s2);
-      for (int o = 16; o; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
-      const int col = sh.col[buf][lgc][c8];
-      if (live && lane == 0 && col < n)
-        for (int rr = 0; rr < kCl; ++rr) cl.map_shared_rank(&sh, rr)->norms[col] = sqrt(s2);
-    }
+  // norms of every column into every CTA (by column id), then sort by rank
+  for (int c8 = 0; c8 < 2 * kUw; ++c8) {
+    const double* sl = sh.slot[buf][lgc][c8];
+    double s2 = 0.0;
+    for (int i = lane; i < kRows; i += 32) s2 = fma(sl[i], sl[i], s2);
+    for (int o = 16; o; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+    const int col = sh.col[buf][lgc][c8];
+    if (live && lane == 0 && col < n)
+      for (int rr = 0; rr < kCl; ++rr) cl.map_shared_rank(&sh, rr)->norms[col] = sqrt(s2);
   }
   cl.sync();
-  if (live && w0) {
+  if (live) {
     for (int c8 = 0; c8 < 2 * kUw; ++c8) {
       const double* sl = sh.slot[buf][lg][c8];
       const int col = sh.col[buf][lg][c8];
