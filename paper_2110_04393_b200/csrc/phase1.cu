@@ -144,18 +144,16 @@ __global__ void __launch_bounds__(NT, 1) phase1_fused_kernel(const __grid_consta
     // Zc = Y_i W(:, chunk): warp w -> rows 8w..8w+7, 16 columns
     const double* Yb = sY + (item & 1) * SM_Y;
     const double* Gb = sG + (s & 1) * SM_G;
-    // (two k halves with separate accumulators: 4 independent DMMA chains)
-    double z0[2] = {0.0, 0.0}, z1[2] = {0.0, 0.0}, z2[2] = {0.0, 0.0}, z3[2] = {0.0, 0.0};
-#pragma unroll
-    for (int kk = 0; kk < KB / 2; kk += 4) {
+    double z0[2] = {0.0, 0.0}, z1[2] = {0.0, 0.0};
+    const int kend = (P.R1[j] + 3) & ~3;
+#pragma unroll 4
+    for (int kk = 0; kk < kend; kk += 4) {
       const double a = Yb[(kk + t) * LDY + 8 * warp + g];
-      const double a2 = Yb[(kk + KB / 2 + t) * LDY + 8 * warp + g];
-      dmma(z0[0], z0[1], a, sW[(ec * EC + g) * LDW + kk + t]);
-      dmma(z1[0], z1[1], a, sW[(ec * EC + 8 + g) * LDW + kk + t]);
-      dmma(z2[0], z2[1], a2, sW[(ec * EC + g) * LDW + kk + KB / 2 + t]);
-      dmma(z3[0], z3[1], a2, sW[(ec * EC + 8 + g) * LDW + kk + KB / 2 + t]);
+      const double b0 = sW[(ec * EC + g) * LDW + kk + t];
+      const double b1 = sW[(ec * EC + 8 + g) * LDW + kk + t];
+      dmma(z0[0], z0[1], a, b0);
+      dmma(z1[0], z1[1], a, b1);
     }
-    z0[0] += z2[0]; z0[1] += z2[1]; z1[0] += z3[0]; z1[1] += z3[1];
     // C fragment (row g, cols 2t, 2t+1) -> sZ[e_local][a]
     sZ[(2 * t) * LDZ + 8 * warp + g] = z0[0];
     sZ[(2 * t + 1) * LDZ + 8 * warp + g] = z0[1];
