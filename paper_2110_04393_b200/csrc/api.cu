@@ -315,6 +315,7 @@ int alg7(Ctx& c, const Terms& T, const std::vector<int64_t>& dims, const std::ve
   }
   DBuf Wst, Z, Xa, Xb, Yb, Mb, Stk;
   TTR_TRY(dalloc(Wst, wtot, s));
+  if (d > 2) TTR_TRY(dalloc(Z, zmax, s));
   TTR_TRY(dalloc(Xa, xmax, s));
   TTR_TRY(dalloc(Xb, xmax, s));
   TTR_TRY(dalloc(Yb, ymax, s));
@@ -340,25 +341,9 @@ int alg7(Ctx& c, const Terms& T, const std::vector<int64_t>& dims, const std::ve
                        int(T.R[j][d - 1]), int(l[d - 1]), int(dims[d - 1]),
                        int(T.R[j][d - 1]), int(l[d - 1]), int(sumR[d - 1])};
     TTR_TRY(gemm(c, false, true, gd.data(), S, 1.0, 0.0, s));
-    std::vector<const double*> yp(S);
-    std::vector<int64_t> r0(S), r1(S), wo(S), oo(S);
     for (int n = d - 1; n >= 2; --n) {     // lines 3-6
       TTR_TRY(wait_core(c, T, n - 1));
       const int64_t In = dims[n - 1];
-      // fused lines 4-5 (phase1.cu): Z never goes to HBM
-      for (int j = 0; j < S; ++j) {
-        yp[j] = T.core[j][n - 1];
-        r0[j] = T.R[j][n - 1];
-        r1[j] = T.R[j][n];
-        wo[j] = off[n][j];
-        oo[j] = off[n - 1][j];
-      }
-      const int fr = phase1_fused_step(c, S, yp.data(), r0.data(), r1.data(), In, Wst.p + woff[n],
-                                       sumR[n], wo.data(), sk.cores[n - 1].p, l[n - 1], l[n],
-                                       Wst.p + woff[n - 1], sumR[n - 1], oo.data(), s);
-      if (fr < 0) return fr;
-      if (fr == 0) continue;
-      if (!Z.p) TTR_TRY(dalloc(Z, zmax, s));
       std::vector<size_t> zoff(S + 1, 0);
       for (int j = 0; j < S; ++j) zoff[j + 1] = zoff[j] + size_t(T.R[j][n - 1]) * In * l[n];
       for (int j = 0; j < S; ++j)          // line 4: V(Z_n) = V(Y_n) W_n
@@ -1004,7 +989,6 @@ int tt_ctx_destroy(tt_ctx_t c) {
     cudaStreamSynchronize(c->stream);
     nccl_comm_destroy(*c);
     c->gemm_ws.release();
-    c->p1_ws.release();
     c->scratch.release();
     if (c->flags.p) cudaFreeAsync(c->flags.p, c->stream);
     c->flags.p = nullptr;

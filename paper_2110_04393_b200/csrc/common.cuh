@@ -106,8 +106,6 @@ struct Ctx {
   DBuf scratch;
   // split-K partials of the GEMMs
   DBuf gemm_ws;
-  // per-CTA partial tiles of the fused phase-1 kernel
-  DBuf p1_ws;
   // device status words, see linalg.cu (route flags 0/4/5, sticky 1-3, counters 8-13)
   IBuf flags;
   int nflags = 0;
@@ -139,15 +137,6 @@ inline int gemm1(Ctx& c, bool ta, bool tb, int M, int N, int K, double alpha,
   GemmDesc d{A, B, C, M, N, K, lda, ldb, ldc};
   return gemm(c, ta, tb, &d, 1, alpha, beta, s, gate, gate_val);
 }
-
-// ---------------------------------------------------------------- fused phase 1
-// One Alg. 3 step (lines 4-5) for S summands without materialising Z
-// (phase1.cu).  Returns TT_OK, a negative error, or 1 when the shapes are
-// outside the kernel's envelope (caller falls back to the two GEMMs).
-int phase1_fused_step(Ctx& c, int S, const double* const* Y, const int64_t* R0,
-                      const int64_t* R1, int64_t I, const double* W, int64_t ldw,
-                      const int64_t* woff, const double* G, int64_t l0, int64_t l1,
-                      double* O, int64_t ldo, const int64_t* ooff, cudaStream_t s);
 
 // ---------------------------------------------------------------- sketch
 int philox_fill(Ctx& c, double* out, int64_t count, uint64_t seed, uint32_t n,
