@@ -474,42 +474,25 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
     CHOL_PROF(1);
     // ---- C3: trailing A(r, c) -= sum_t L(r, t) L(c, t) on the lower 8x8 tiles
     {
-      // up to 4 tiles per warp at a time, k-steps outer: 4 independent DMMA
-      // chains instead of one 8-deep chain per tile
       const int tb = r0 / 8, nrt = nt8 - tb;
       const int ntiles = nrt * (nrt + 1) / 2;
 #pragma unroll 1
-      for (int base = w; base < ntiles; base += 4 * NW) {
-        int Rq[4], Cq[4];
-        bool okq[4];
-        double cq[4][2];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int tt = base + NW * q;
-          okq[q] = tt < ntiles;
-          int tr = int((sqrtf(8.0f * tt + 1.0f) - 1.0f) * 0.5f);   // tt = tr(tr+1)/2 + tc
-          while ((tr + 1) * (tr + 2) / 2 <= tt) ++tr;
-          while (tr * (tr + 1) / 2 > tt) --tr;
-          const int tc = tt - tr * (tr + 1) / 2;
-          Rq[q] = 8 * (tb + tr);
-          Cq[q] = 8 * (tb + tc);
-          cq[q][0] = cq[q][1] = 0.0;
-        }
+      for (int tt = w; tt < ntiles; tt += NW) {
+        int tr = int((sqrtf(8.0f * tt + 1.0f) - 1.0f) * 0.5f);   // tt = tr(tr+1)/2 + tc
+        while ((tr + 1) * (tr + 2) / 2 <= tt) ++tr;
+        while (tr * (tr + 1) / 2 > tt) --tr;
+        const int tc = tt - tr * (tr + 1) / 2;
+        const int R = 8 * (tb + tr), C = 8 * (tb + tc);
+        double c0 = 0.0, c1 = 0.0;
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
           const int tcol = k0 + 4 * kk + t4;
-#pragma unroll
-          for (int q = 0; q < 4; ++q)
-            if (okq[q])
-              dmma884(cq[q][0], cq[q][1], S[(Rq[q] + g) + tcol * ld], S[(Cq[q] + g) + tcol * ld]);
+          dmma884(c0, c1, S[(R + g) + tcol * ld], S[(C + g) + tcol * ld]);
         }
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int r = Rq[q] + g, cA = Cq[q] + 2 * t4;
-          if (okq[q] && r < n) {
-            if (cA < n) S[r + cA * ld] -= cq[q][0];
-            if (cA + 1 < n) S[r + (cA + 1) * ld] -= cq[q][1];
-          }
+        const int r = R + g, cA = C + 2 * t4;
+        if (r < n) {
+          if (cA < n) S[r + cA * ld] -= c0;
+          if (cA + 1 < n) S[r + (cA + 1) * ld] -= c1;
         }
       }
     }
@@ -579,23 +562,17 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
       // tiles of A21: rows [r0, n8) x the 32 block columns; <= 4 per warp
       const int tb = r0 / 8, nrt = nt8 - tb, ntiles = nrt * 4;
       double acc[4][2];
-      // I1: A21 <- X22 A21, X22(r, t) = 0 for t > r (parked data is masked);
-      // k-steps outer, the (<= 4) tiles of the warp inner: independent chains
-      int kmax = r0;
+      // I1: A21 <- X22 A21, X22(r, t) = 0 for t > r (parked data is masked)
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         acc[q][0] = acc[q][1] = 0.0;
         const int tt = w + NW * q;
-        if (tt < ntiles) kmax = max(kmax, min(n8, 8 * (tb + tt / 4) + 8));
-      }
-#pragma unroll 1
-      for (int t0 = r0; t0 < kmax; t0 += 4) {
-        const int tcol = t0 + t4;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int tt = w + NW * q;
+        if (tt < ntiles) {
           const int R = 8 * (tb + tt / 4), C = k0 + 8 * (tt % 4);
-          if (tt < ntiles && t0 < R + 8) {
+          const int kend = min(n8, R + 8);
+#pragma unroll 1
+          for (int t0 = r0; t0 < kend; t0 += 4) {
+            const int tcol = t0 + t4;
             const double av = (tcol <= R + g) ? S[(R + g) + tcol * ld] : 0.0;
             dmma884(acc[q][0], acc[q][1], av, S[tcol + (C + g) * ld]);
           }
@@ -616,17 +593,16 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
       }
       __syncthreads();
       // I2: A21 <- -A21 X11, X11(t, c) = 0 for t < c, rdiag on the diagonal,
-      // parked at (c, t) below it (k-steps outer, tiles inner)
+      // parked at (c, t) below it
 #pragma unroll
-      for (int q = 0; q < 4; ++q) acc[q][0] = acc[q][1] = 0.0;
+      for (int q = 0; q < 4; ++q) {
+        acc[q][0] = acc[q][1] = 0.0;
+        const int tt = w + NW * q;
+        if (tt < ntiles) {
+          const int R = 8 * (tb + tt / 4), cb = 8 * (tt % 4);   // block-local columns
 #pragma unroll
-      for (int kk = 0; kk < 8; ++kk) {
-        const int tl = 4 * kk + t4;   // A fragment column (block-local t)
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int tt = w + NW * q;
-          if (tt < ntiles) {
-            const int R = 8 * (tb + tt / 4), cb = 8 * (tt % 4);   // block-local columns
+          for (int kk = 0; kk < 8; ++kk) {
+            const int tl = 4 * kk + t4;   // A fragment column (block-local t)
             const double av = S[(R + g) + (k0 + tl) * ld];
             const int cl = cb + g;   // B fragment: X11(tl, cl)
             const double bv = (tl < cl) ? 0.0
