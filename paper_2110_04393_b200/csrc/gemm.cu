@@ -336,13 +336,18 @@ int launch_cfg(Ctx& c, GemmParams& P, int maxM, int maxN, int maxK, cudaStream_t
   int ksl = 1;
   if (tiles < 3 * slots) {
     const int kmax = std::max(1, std::min(64, ktiles / 4));
-    double best = -1.0;
-    for (int k = 1; k <= kmax; ++k) {
-      const long ctas = tiles * k;
-      const long waves = (ctas + slots - 1) / slots;
-      const double eff = double(ctas) / double(waves * slots);
-      const double score = eff - 0.004 * k;
-      if (score > best + 1e-12) { best = score; ksl = k; }
+    if (tiles * kmax <= slots) {
+      ksl = kmax;   // cannot fill one wave: as many slices as allowed (>= 4 k-tiles each)
+    } else {
+      double best = -1.0;
+      for (int k = 1; k <= kmax; ++k) {
+        const long ctas = tiles * k;
+        if (ctas < slots && k < kmax) continue;   // at least one full wave
+        const long waves = (ctas + slots - 1) / slots;
+        const double eff = double(ctas) / double(waves * slots);
+        const double score = eff - 0.004 * k;
+        if (score > best + 1e-12) { best = score; ksl = k; }
+      }
     }
   }
   const int kchunk_tiles = (ktiles + ksl - 1) / ksl;
