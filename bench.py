@@ -174,6 +174,10 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--batch", type=int, default=1,
+                    help="B independent roundings per step (distinct sketch seeds), spread "
+                         "over --streams contexts (SURVEY 8d batched throughput of C1/C2)")
+    ap.add_argument("--streams", type=int, default=8)
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -182,6 +186,8 @@ def main():
 
     if args.impl == "reference":
         return reference_arm(args, world, rank)
+    if args.batch > 1:
+        return batched_run(args, world, rank, local)
 
     import torch
     import torch.distributed as dist
@@ -311,6 +317,82 @@ def main():
         if cpu is not None:
             line["cpu_baseline"] = cpu
         print(json.dumps(line))
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def batched_run(args, world, rank, local):
+    """B independent roundings per step on one GPU (replicas across GPUs): the
+    same input sum rounded with sketch seeds 1..B by `--streams` library
+    contexts (one CUDA stream each) driven from host threads, so latency-bound
+    kernels of one rounding overlap with the others.  Timed by the host clock
+    between device-wide synchronisations (several streams)."""
+    import concurrent.futures as cf
+    import torch
+    import torch.distributed as dist
+    import paper_2110_04393_b200 as P
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    wl = make_workload(args.workload, dev)
+    ns = max(1, min(args.streams, args.batch))
+    ctxs = [P.Context(local) for _ in range(ns)]
+    if wl.tol > 0:
+        kw = dict(mode="tol", tol=wl.tol, oversample=wl.ell, adaptive=wl.adaptive, rank=wl.rank)
+    else:
+        kw = dict(mode="rank", rank=wl.rank, oversample=wl.ell - wl.rank)
+    B = args.batch
+    n0 = P.tt_launch_count()
+    ex = cf.ThreadPoolExecutor(ns)
+
+    def lane(t):
+        r = None
+        for b in range(t, B, ns):
+            r = ctxs[t].tt_round_sum(wl.terms, seed=1 + b, **kw)
+        return r.ranks
+
+    def step():
+        return list(ex.map(lane, range(ns)))
+
+    for _ in range(max(3, args.warmup)):
+        ranks_out = step()[0]
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    n0 = P.tt_launch_count()
+    with ClockSampler(local) as clk:
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            step()
+        torch.cuda.synchronize()
+        dt = (time.perf_counter() - t0) / args.steps
+    launches = P.tt_launch_count() - n0
+    if world > 1:
+        tt = torch.tensor([dt], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        dt = float(tt.item())
+    fl, _ = flops_of(wl, ranks_out)
+    peak, peak_src = fp64_peak()
+    value = B * world / dt
+    tf = fl["total"] * B * world / dt / 1e12
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "value": value, "unit": "roundings/s", "n_gpus": world,
+            "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": dt * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (ttsynth, seeded; DESIGN.md input recipe)",
+            "config": {"workload": args.workload, "desc": WORKLOADS[args.workload]["desc"],
+                       "batch_per_gpu": B, "streams": ns, "parallelism": f"replicas/{world}",
+                       "timing": "host clock between device synchronisations (several streams)"},
+            "tflops": tf, "fp64_peak_tflops": peak, "fp64_peak_source": peak_src,
+            "roofline": {"bound": "tensor", "kernel": "whole path (batched, latency-bound)",
+                         "achieved": tf, "peak": peak, "unit": "TFLOP/s", "frac": tf / peak,
+                         "traffic": None},
+            "gpu_launches": launches, "ranks_out": ranks_out, "clocks": clk.summary(),
+        }))
+    ex.shutdown()
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
