@@ -128,14 +128,19 @@ constexpr int kMaxGemmBatch = 64;
 // Batched FP64 DMMA GEMM (all entries share ta/tb/alpha/beta).  `gate`: optional
 // device flag; the launch is a no-op unless *gate == gate_val (device-side
 // branching of the QR without a host round trip).
+// flags: kGemmTriB -- op(B) is upper triangular (zero below the diagonal), the
+// K range of a column tile stops at its last column; kGemmLower -- only the
+// tiles meeting the lower triangle of C are computed (Grams feeding a Cholesky).
+constexpr unsigned kGemmTriB = 1u, kGemmLower = 2u;
 int gemm(Ctx& c, bool ta, bool tb, const GemmDesc* d, int nbatch, double alpha,
-         double beta, cudaStream_t s, const int* gate = nullptr, int gate_val = 0);
+         double beta, cudaStream_t s, const int* gate = nullptr, int gate_val = 0,
+         unsigned flags = 0);
 inline int gemm1(Ctx& c, bool ta, bool tb, int M, int N, int K, double alpha,
                  const double* A, int lda, const double* B, int ldb, double beta,
                  double* C, int ldc, cudaStream_t s, const int* gate = nullptr,
-                 int gate_val = 0) {
+                 int gate_val = 0, unsigned flags = 0) {
   GemmDesc d{A, B, C, M, N, K, lda, ldb, ldc};
-  return gemm(c, ta, tb, &d, 1, alpha, beta, s, gate, gate_val);
+  return gemm(c, ta, tb, &d, 1, alpha, beta, s, gate, gate_val, flags);
 }
 
 // ---------------------------------------------------------------- sketch

@@ -52,6 +52,7 @@ struct GemmParams {
   const int* gate;   // device-side predicate: run iff gate == nullptr || *gate == gate_val
   int gate_val;
   int vec;           // 1: every A/B 16-byte aligned with even leading dimensions
+  int flags;         // kGemmTriB / kGemmLower (common.cuh)
 };
 
 template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool TA, bool TB>
@@ -81,6 +82,8 @@ __global__ void __launch_bounds__(WM* WN * 32)
   const int ks = blockIdx.z / P.nbatch;
   const GemmDesc& D = P.d[b];
   const int m0 = tm * BM, n0 = tn * BN;
+  // kGemmLower: only tiles meeting the lower triangle (the Cholesky reads no more)
+  if ((P.flags & kGemmLower) && m0 + BM <= n0) return;
   const bool tile_live = (m0 < D.M) && (n0 < D.N);
   if (!tile_live && P.kslices == 1) return;
 
@@ -91,7 +94,9 @@ __global__ void __launch_bounds__(WM* WN * 32)
   const int wn0 = (warp / WM) * C::TN;
 
   const int kbeg = ks * P.kchunk;
-  const int kend = min(D.K, kbeg + P.kchunk);
+  // kGemmTriB: B upper triangular (B(k, n) = 0 for k > n): columns < n0 + BN
+  // need k < n0 + BN only
+  const int kend = min(min(D.K, kbeg + P.kchunk), (P.flags & kGemmTriB) ? n0 + BN : D.K);
   const int KT = (tile_live && kend > kbeg) ? (kend - kbeg + BK - 1) / BK : 0;
 
   const double* __restrict__ A = D.A;
@@ -287,6 +292,7 @@ __global__ void __launch_bounds__(256) splitk_reduce(const __grid_constant__ Gem
   const int e = blockIdx.y * 256 + threadIdx.x;
   if (e >= BM * BN) return;
   const int ml = e % BM, nl = e / BM;
+  if ((P.flags & kGemmLower) && tm * BM + BM <= tn * BN) return;
   const int m = tm * BM + ml, n = tn * BN + nl;
   if (m >= D.M || n >= D.N) return;
   const size_t stride = size_t(P.nbatch) * P.tiles_m * P.tiles_n * (BM * BN);
@@ -417,7 +423,7 @@ int dispatch(Ctx& c, GemmParams& P, int maxM, int maxN, int maxK, cudaStream_t s
 }  // namespace
 
 int gemm(Ctx& c, bool ta, bool tb, const GemmDesc* d, int nbatch, double alpha, double beta,
-         cudaStream_t s, const int* gate, int gate_val) {
+         cudaStream_t s, const int* gate, int gate_val, unsigned flags) {
   int done = 0;
   while (done < nbatch) {
     const int nb = std::min(kMaxGemmBatch, nbatch - done);
@@ -439,6 +445,7 @@ int gemm(Ctx& c, bool ta, bool tb, const GemmDesc* d, int nbatch, double alpha, 
     done += nb;
     if (live == 0) continue;
     P.nbatch = live;
+    P.flags = int(flags);
     P.vec = 1;
     for (int i = 0; i < live; ++i) {
       const GemmDesc& x = P.d[i];

@@ -1027,23 +1027,24 @@ int qr(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, bool trans, d
   auto gram_of_input = [&](const int* gate, int gv) -> int {
     if (trans)
       return gemm1(c, false, true, ni, ni, mi, 1.0, A, int(lda), A, int(lda), 0.0, Gm.p, ni, s,
-                   gate, gv);
+                   gate, gv, kGemmLower);
     return gemm1(c, true, false, ni, ni, mi, 1.0, A, int(lda), A, int(lda), 0.0, Gm.p, ni, s,
-                 gate, gv);
+                 gate, gv, kGemmLower);
   };
   auto input_times_rinv = [&](double* dst, const int* gate, int gv) -> int {
     if (trans)
       return gemm1(c, true, false, mi, ni, ni, 1.0, A, int(lda), Rinv.p, ni, 0.0, dst, mi, s,
-                   gate, gv);
+                   gate, gv, kGemmTriB);
     return gemm1(c, false, false, mi, ni, ni, 1.0, A, int(lda), Rinv.p, ni, 0.0, dst, mi, s,
-                 gate, gv);
+                 gate, gv, kGemmTriB);
   };
   auto gram = [&](const double* src, const int* gate, int gv) -> int {
-    return gemm1(c, true, false, ni, ni, mi, 1.0, src, mi, src, mi, 0.0, Gm.p, ni, s, gate, gv);
+    return gemm1(c, true, false, ni, ni, mi, 1.0, src, mi, src, mi, 0.0, Gm.p, ni, s, gate, gv,
+                 kGemmLower);
   };
   auto times_rinv = [&](const double* src, double* dst, const int* gate, int gv) -> int {
     return gemm1(c, false, false, mi, ni, ni, 1.0, src, mi, Rinv.p, ni, 0.0, dst, mi, s, gate,
-                 gv);
+                 gv, kGemmTriB);
   };
   static const bool dbg = getenv("TTR_QR_DEBUG") != nullptr;
   auto dump = [&](const char* what, const double* p, int64_t cnt) {
