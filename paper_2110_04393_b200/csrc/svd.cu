@@ -446,6 +446,9 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kJcThreads)
       cl.sync();
     }
     if (rot) atomicOr(&cl.map_shared_rank(&sh, 0)->rot, 1);
+#ifdef TTR_JAC_PROF
+    if (live && rot && (tid & 31) == 0) atomicAdd(&flags[40 + min(sweep, 23)], 1);
+#endif
     cl.sync();
     const int any = cl.map_shared_rank(&sh, 0)->rot;
     cl.sync();

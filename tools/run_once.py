@@ -24,4 +24,4 @@ else:
 for _ in range(reps):
     r = ctx.tt_round_sum(w.terms, seed=1, **kw)
     print(name, d, "ranks", r.ranks[:4], "passes", r.passes, "flags", r.flags, "timing",
-          [round(x, 3) for x in ctx.last_timing()], "status", ctx.status_words(40), flush=True)
+          [round(x, 3) for x in ctx.last_timing()], "status", ctx.status_words(64), flush=True)
