@@ -106,10 +106,19 @@ __global__ void __launch_bounds__(32 * RPT) __maxnreg__(RPT >= 18 ? 96 : 128)
 #pragma unroll
       for (int o = 4; o; o >>= 1) ga += __shfl_xor_sync(0xffffffffu, ga, o);
       const double al = cn[p], be = cn[q];
-      if (!act || !(fmin(al, be) > small) || !(fabs(ga) > tol * sqrt(al * be))) continue;
-      const double zeta = (be - al) / (2.0 * ga);
-      const double tt = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
-      const double cs = rsqrt(fma(tt, tt, 1.0)), sn = cs * tt;
+      if (!act || !(fmin(al, be) > small) || !(ga * ga > tol * tol * (al * be))) continue;
+      // angle as in the cluster kernel: MUFU-approximate t, Newton-exact cosine
+      const double d = be - al, e = 2.0 * ga;
+      const double r2 = fma(d, d, e * e);
+      double rs, rc, cs;
+      asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(rs) : "d"(r2));
+      asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(rc) : "d"(fabs(d) + r2 * rs));
+      const double tt = copysign(1.0, d) * e * rc;
+      const double qq1 = fma(tt, tt, 1.0);
+      asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(cs) : "d"(qq1));
+      cs = cs * fma(-0.5 * qq1 * cs, cs, 1.5);
+      cs = cs * fma(-0.5 * qq1 * cs, cs, 1.5);
+      const double sn = cs * tt;
 #pragma unroll
       for (int s = 0; s < S2; ++s) {
         wp[s * kGroup] = make_double2(fma(cs, x[s].x, -sn * y[s].x), fma(cs, x[s].y, -sn * y[s].y));
@@ -254,13 +263,15 @@ constexpr int kJcThreads = kGpc * 32;
 constexpr int kR2 = kRps / 2;
 __device__ __forceinline__ bool jc_rotate(double2 (&x)[kR2], double2 (&y)[kR2], int cx, int cy,
                                           double& ax, double& ay, int n, double small, double tol) {
-  double ga0 = 0.0, ga1 = 0.0;
+  double ga0 = 0.0, ga1 = 0.0, ga2 = 0.0, ga3 = 0.0;   // 4 short FMA chains
 #pragma unroll
-  for (int s = 0; s < kR2; ++s) {
+  for (int s = 0; s < kR2; s += 2) {
     ga0 = fma(x[s].x, y[s].x, ga0);
     ga1 = fma(x[s].y, y[s].y, ga1);
+    ga2 = fma(x[s + 1].x, y[s + 1].x, ga2);
+    ga3 = fma(x[s + 1].y, y[s + 1].y, ga3);
   }
-  double ga = ga0 + ga1;
+  double ga = (ga0 + ga1) + (ga2 + ga3);
 #pragma unroll
   for (int o = 4; o; o >>= 1) ga += __shfl_xor_sync(0xffffffffu, ga, o);
   const bool swp = cx > cy;
