@@ -317,7 +317,7 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
   if (gate && *gate != gate_val) return;
   extern __shared__ double S[];
   __shared__ double rdiag[32 * NB];   // 1 / L(i, i)
-  __shared__ double colb[32];         // pivot column broadcast (C1)
+  __shared__ double colb[64];         // pivot column broadcast (C1), doubled
   __shared__ double s_tr, s_dmax;
   __shared__ int s_bad, s_zero, s_clamped;
   constexpr int NW = kBlkThreads / 32;
@@ -408,11 +408,12 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
           const double lij = (i > j) ? a[sft] * rd : (i == j ? pv * rd : 0.0);
           if (j < kb && i >= j && i < kb) S[(k0 + i) + (k0 + j) * ld] = lij;
           if (i == j && j < kb) rdiag[k0 + j] = rd;
-          colb[i] = lij;
+          colb[i] = lij;          // doubled buffer: colb[j + qq] needs no wrap,
+          colb[i + 32] = lij;     // so every load is [base + constant]
           __syncwarp();
+          const double* cb = colb + j;
 #pragma unroll
-          for (int qq = 1; qq < 32 - sft; ++qq)
-            a[sft + qq] = fma(-lij, colb[(j + qq) & 31], a[sft + qq]);
+          for (int qq = 1; qq < 32 - sft; ++qq) a[sft + qq] = fma(-lij, cb[qq], a[sft + qq]);
           __syncwarp();
         }
 #pragma unroll
