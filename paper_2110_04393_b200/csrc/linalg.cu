@@ -571,12 +571,24 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
         if (tt < ntiles) {
           const int R = 8 * (tb + tt / 4), C = k0 + 8 * (tt % 4);
           const int kend = min(n8, R + 8);
+          // two accumulators (k-steps alternate): half the dependent DMMA chain
+          double e0 = 0.0, e1 = 0.0;
+          int t0 = r0;
 #pragma unroll 1
-          for (int t0 = r0; t0 < kend; t0 += 4) {
-            const int tcol = t0 + t4;
-            const double av = (tcol <= R + g) ? S[(R + g) + tcol * ld] : 0.0;
-            dmma884(acc[q][0], acc[q][1], av, S[tcol + (C + g) * ld]);
+          for (; t0 + 4 < kend; t0 += 8) {
+            const int tc0 = t0 + t4, tc1 = t0 + 4 + t4;
+            const double a0 = (tc0 <= R + g) ? S[(R + g) + tc0 * ld] : 0.0;
+            const double a1 = (tc1 <= R + g) ? S[(R + g) + tc1 * ld] : 0.0;
+            dmma884(acc[q][0], acc[q][1], a0, S[tc0 + (C + g) * ld]);
+            dmma884(e0, e1, a1, S[tc1 + (C + g) * ld]);
           }
+          if (t0 < kend) {
+            const int tc0 = t0 + t4;
+            const double a0 = (tc0 <= R + g) ? S[(R + g) + tc0 * ld] : 0.0;
+            dmma884(acc[q][0], acc[q][1], a0, S[tc0 + (C + g) * ld]);
+          }
+          acc[q][0] += e0;
+          acc[q][1] += e1;
         }
       }
       __syncthreads();
