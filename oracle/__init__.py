@@ -1,7 +1,7 @@
 """CPU ORACLE — TEST INFRASTRUCTURE ONLY.
 
 Plain, slow, obviously-correct fp64 NumPy implementation of what the hot path
-computes (Alg. 1, 2, 3, 5, 7 and the truncation recipe of P:667-670),
+computes (Alg. 1, 2, 3, 5, 6, 7 and the truncation recipe of P:667-670),
 written step by step in the paper's order and notation.  Library primitives
 (``numpy.matmul``, ``numpy.linalg.qr`` = LAPACK Householder, ``numpy.linalg.svd``)
 serve as single steps; there is no blocking, fusion or reordering beyond the

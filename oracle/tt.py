@@ -24,7 +24,9 @@ __all__ = [
     "partial_contractions_rl", "tt_round", "thin_qr", "eps_rank", "rank_caps",
     "structural_caps", "gaussian_sketch", "round_rand_orth", "round_sum_rand_orth",
     "truncate_left_orthogonal", "round_sum", "RoundResult", "left_orth_residual",
-    "right_orth_residual",
+    "right_orth_residual", "partial_contractions_lr", "gaussian_sketch_left", "pinv_rtol",
+    "round_two_sided", "round_sum_two_sided", "round_sum_2s", "two_sided_ranks",
+    "TAG_2S_L", "TAG_2S_R",
 ]
 
 Core = np.ndarray
@@ -431,3 +433,150 @@ def round_sum(terms: Sequence[TT], ell: int, seed: int = 1, rank: int = 0,
         if nxt <= cur:
             return RoundResult(Xt, ks, caps, passes, capped)
         cur = nxt
+
+
+# ---------------------------------------------------------------- Alg. 6
+# Two-Sided-Randomization (generalized Nyström), P:755-783 and its derivation
+# P:786-830.  Readings (R18-R21): PartialContractionsLR is the
+# left-to-right mirror of Alg. 3 (the paper names it, line 4, without a listing);
+# ρ = ⌈1.5ℓ⌉ by default; Σ† is the pseudo-inverse with numpy's
+# cutoff σ_i > max(ℓ_n, ρ_n)·ε·σ_1; on a sum the block structure of P:388-391
+# makes W^L_n = [W^L_n(Y^(1)) ⋯ W^L_n(Y^(s))] and W^R_n = [W^R_n(Y^(1)); ⋯], the
+# stacking identity of P:884-890 applied to Alg. 6.
+
+TAG_2S_L = 0x10001   # Philox tag of the left sketch 𝓛 (R21)
+TAG_2S_R = 0x10002   # Philox tag of the right sketch 𝓡
+
+
+def partial_contractions_lr(X: TT, Y: TT) -> Dict[int, np.ndarray]:
+    """PartialContractionsLR (Alg. 6 line 4), the mirror of Alg. 3:
+    {n: W_n}, n = 1..N-1, W_n = V(X^{1:n})ᵀ V(Y^{1:n}) (R^X_n × R^Y_n), so that
+    with X = 𝓛, W_n = Ψ_n V(Y^{1:n}).
+      W_1 = V(X_1)ᵀ V(Y_1);  n = 2..N-1: Z_n = Y_n ×₁ W_{n-1}, W_n = V(X_n)ᵀ V(Z_n)."""
+    N = len(X)
+    W: Dict[int, np.ndarray] = {}
+    if N < 2:
+        return W
+    W[1] = V(np.asarray(X[0])).T @ V(np.asarray(Y[0]))
+    for n in range(2, N):
+        Yn = np.asarray(Y[n - 1])
+        Z = fold_H(W[n - 1] @ H(Yn), Yn.shape[1])           # H(Z_n) = W_{n-1} H(Y_n)
+        W[n] = V(np.asarray(X[n - 1])).T @ V(Z)
+    return W
+
+
+def gaussian_sketch_left(dims: Sequence[int], ell_caps: Sequence[int], seed: int,
+                         tag: int = TAG_2S_L) -> List[Optional[Core]]:
+    """Random Gaussian TT 𝓛 of Def. 3.1 with ranks (1, ℓ_1..ℓ_{N-1}, 1)
+    for the left side of Alg. 6.  Only 𝓛^{1:N-1} enter Ψ_n: core N is None."""
+    N = len(dims)
+    l = [1] + list(ell_caps) + [1]
+    L: List[Optional[Core]] = []
+    for n in range(1, N):
+        L.append(sketch_core(seed, n, l[n - 1], dims[n - 1], l[n], tag))
+    L.append(None)
+    return L
+
+
+def pinv_rtol(shape: Tuple[int, int]) -> float:
+    """Relative cutoff of Σ† (R20): numpy.linalg.pinv's default max(M, N)·ε."""
+    return max(shape) * float(np.finfo(np.float64).eps)
+
+
+def _two_sided_factors(WL: np.ndarray, WR: np.ndarray):
+    """Alg. 6 lines 7-10 for one bond: SVD of W^L W^R, then
+    L_n = W^R V (Σ†)^{1/2} and R_n = (Σ†)^{1/2} Uᵀ W^L (eq. (3.3)).
+    Returns (L_n, R_n, σ)."""
+    P = WL @ WR                                             # ℓ_n × ρ_n
+    U, s, Vt = np.linalg.svd(P, full_matrices=False)        # line 8
+    keep = s > pinv_rtol(P.shape) * (s[0] if s.size else 0.0)
+    sih = np.zeros_like(s)
+    sih[keep] = 1.0 / np.sqrt(s[keep])                      # (Σ†)^{1/2}
+    Ln = (WR @ Vt.T) * sih[None, :]                         # line 9
+    Rn = sih[:, None] * (U.T @ WL)                          # line 10
+    return Ln, Rn, s
+
+
+def round_two_sided(Y: TT, L: List[Optional[Core]], R: List[Optional[Core]]) -> TT:
+    """Alg. 6 TT-Rounding two-sided on one (possibly assembled) TT,
+    line by line.  L has ranks ℓ, R ranks ρ (cores 1 of R / N of L unused)."""
+    N = len(Y)
+    Y = [np.asarray(c, dtype=np.float64) for c in Y]
+    Lc = [g if g is not None else np.zeros((1, 1, 1)) for g in L]
+    Rc = [g if g is not None else np.zeros((1, 1, 1)) for g in R]
+    WLd = partial_contractions_lr(Lc, Y)                    # line 4
+    WRd = partial_contractions_rl(Y, Rc)                    # line 5
+    Lf, Rf = {}, {}
+    for n in range(1, N):                                   # lines 6-11
+        Lf[n], Rf[n], s = _two_sided_factors(WLd[n], WRd[n])
+        if not s.size or s[0] == 0.0:
+            return [np.zeros((1, d, 1)) for d in dims_of(Y)]   # zero tensor (R16)
+    X: TT = [None] * N
+    X[0] = fold_V(V(Y[0]) @ Lf[1], Y[0].shape[1])           # line 12
+    for n in range(2, N):                                   # lines 13-15
+        I = Y[n - 1].shape[1]
+        T = fold_V(V(Y[n - 1]) @ Lf[n], I)
+        X[n - 1] = fold_H(Rf[n - 1] @ H(T), I)
+    X[N - 1] = fold_H(Rf[N - 1] @ H(Y[N - 1]), Y[N - 1].shape[1])   # line 16
+    return X
+
+
+def round_sum_two_sided(terms: Sequence[TT], L: List[Optional[Core]],
+                        R: List[Optional[Core]]) -> TT:
+    """Alg. 6 on Σ_j Y^(j) without forming the block cores (R19): per-summand
+    partial contractions, W^L_n = [W^L_n(Y^(j))]_j (ℓ_n × ΣR_n), W^R_n stacked
+    (ΣR_n × ρ_n); L_n / R_n split into the summands' row / column blocks and
+    X_n = Σ_j Y^(j)_n ×₁ R^(j)_{n-1} ×₃ L^(j)_n."""
+    s = len(terms)
+    N = len(terms[0])
+    if N < 2:
+        raise ValueError("a TT-tensor to round needs N >= 2 modes")
+    terms = [[np.asarray(c, dtype=np.float64) for c in t] for t in terms]
+    Lc = [g if g is not None else np.zeros((1, 1, 1)) for g in L]
+    Rc = [g if g is not None else np.zeros((1, 1, 1)) for g in R]
+    WLj = [partial_contractions_lr(Lc, t) for t in terms]   # line 4, per summand
+    WRj = [partial_contractions_rl(t, Rc) for t in terms]   # line 5, per summand
+    Lb, Rb = {}, {}
+    for n in range(1, N):
+        offs = np.cumsum([0] + [t[n - 1].shape[2] for t in terms])
+        WL = np.concatenate([WLj[j][n] for j in range(s)], axis=1)
+        WR = np.concatenate([WRj[j][n] for j in range(s)], axis=0)
+        Ln, Rn, sv = _two_sided_factors(WL, WR)
+        if not sv.size or sv[0] == 0.0:
+            return [np.zeros((1, d, 1)) for d in dims_of(terms[0])]
+        Lb[n] = [Ln[offs[j]:offs[j + 1], :] for j in range(s)]
+        Rb[n] = [Rn[:, offs[j]:offs[j + 1]] for j in range(s)]
+    X: TT = [None] * N
+    I1 = terms[0][0].shape[1]
+    X[0] = fold_V(sum(V(t[0]) @ Lb[1][j] for j, t in enumerate(terms)), I1)
+    for n in range(2, N):
+        I = terms[0][n - 1].shape[1]
+        X[n - 1] = sum(fold_H(Rb[n - 1][j] @ H(fold_V(V(t[n - 1]) @ Lb[n][j], I)), I)
+                       for j, t in enumerate(terms))
+    IN = terms[0][N - 1].shape[1]
+    X[N - 1] = fold_H(sum(Rb[N - 1][j] @ H(t[N - 1]) for j, t in enumerate(terms)), IN)
+    return X
+
+
+def two_sided_ranks(dims: Sequence[int], sumR: Sequence[int], ell: int,
+                    rho: int = 0) -> Tuple[List[int], List[int]]:
+    """Capped (ℓ_n, ρ_n), n = 1..N-1: R7's caps applied to ℓ and to
+    ρ = ⌈1.5ℓ⌉ when rho = 0; ℓ_n ≤ ρ_n follows."""
+    rho = int(rho) if rho > 0 else int(math.ceil(1.5 * int(ell)))
+    if rho < ell:
+        raise ValueError("Alg. 6 needs rho >= ell (P:763)")
+    return rank_caps(dims, sumR, ell), rank_caps(dims, sumR, rho)
+
+
+def round_sum_2s(terms: Sequence[TT], ell: int, rho: int = 0, seed: int = 1):
+    """The operation behind ``tt_round_sum_two_sided``: caps → 𝓛 (tag TAG_2S_L)
+    and 𝓡 (tag TAG_2S_R) from the seed → Alg. 6 on the sum.  Returns
+    (X, ℓ caps, ρ caps)."""
+    terms = [[np.asarray(c, dtype=np.float64) for c in t] for t in terms]
+    dims = dims_of(terms[0])
+    N = len(dims)
+    sumR = [1] + [sum(t[n].shape[2] for t in terms) for n in range(N - 1)] + [1]
+    lc, rc = two_sided_ranks(dims, sumR, ell, rho)
+    L = gaussian_sketch_left(dims, lc, seed)
+    R = gaussian_sketch(dims, rc, seed, tag=TAG_2S_R)
+    return round_sum_two_sided(terms, L, R), lc, rc
