@@ -4,7 +4,10 @@ truncation to rank r) on BASELINE.json's large config (config 5, reading "C":
 S=32 summands, d=50, I=256, summand rank 64, sketch rank 144 -> rank 128).
 
   python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference]
-                  [--workload large|sum10|gmres|single|tiny]
+                  [--workload large|sum10|gmres|single|tiny] [--algo rand_orth|two_sided]
+
+--algo two_sided times tt_round_sum_two_sided (Alg. 6) on the
+same inputs with l = the config's target rank and rho = ceil(1.5 l).
 
 N>1 runs under torchrun, one process per GPU; the summands are sharded across
 ranks and each sweep step allreduces the partial sketched core Y_n over NCCL
@@ -106,17 +109,26 @@ def make_workload(name, device, seed_offset=0):
     return fn(device=device, **w["args"])
 
 
-def flops_of(wl, ranks_out):
+def two_sided_ell(wl):
+    """Alg. 6's target rank for a workload: the config's rank (else its sketch rank)."""
+    return int(wl.rank) if wl.rank else int(wl.ell)
+
+
+def flops_of(wl, ranks_out, algo="rand_orth"):
     from paper_2110_04393_b200 import cost
     dims = wl.dims
     tr = [[int(t[0].shape[0])] + [int(c.shape[2]) for c in t] for t in wl.terms]
     sumR = [sum(r[n] for r in tr) for n in range(len(dims) + 1)]
+    if algo == "two_sided":
+        ell = two_sided_ell(wl)
+        l = cost.caps(dims, sumR, ell)
+        return cost.two_sided_flops(dims, tr, l, cost.caps(dims, sumR, (3 * ell + 1) // 2)), l
     l = cost.caps(dims, sumR, wl.ell)
     kept = ranks_out if (wl.tol > 0 or (wl.rank and any(x > wl.rank for x in l[1:-1]))) else None
     return cost.rounding_flops(dims, tr, l, kept), l
 
 
-def cpu_oracle_sample(name, budget_s=20.0):
+def cpu_oracle_sample(name, budget_s=20.0, algo="rand_orth"):
     """Time the oracle (as it stands) on a bounded sample of the workload: the same
     S, I, ranks, sketch rank at reduced order d, scaled to the full config by the
     exact flop ratio.  Returns (roundings/s for the full config, description, cores)."""
@@ -134,22 +146,32 @@ def cpu_oracle_sample(name, budget_s=20.0):
     t0 = time.perf_counter()
     reps = 0
     while True:
-        r = oracle.round_sum(terms, ell=sample.ell, seed=1, rank=sample.rank, tol=sample.tol,
-                             adaptive=sample.adaptive)
+        if algo == "two_sided":
+            X2, lc, _ = oracle.round_sum_2s(terms, ell=two_sided_ell(sample), seed=1)
+            ranks_s = lc
+        else:
+            r = oracle.round_sum(terms, ell=sample.ell, seed=1, rank=sample.rank, tol=sample.tol,
+                                 adaptive=sample.adaptive)
+            ranks_s = list(r.ranks)
         reps += 1
         if time.perf_counter() - t0 > budget_s or reps >= 50:
             break
     dt = (time.perf_counter() - t0) / reps
-    fs, _ = flops_of(sample, [1] + list(r.ranks) + [1])
+    fs, _ = flops_of(sample, [1] + ranks_s + [1], algo)
     # flops of the full config (ranks after truncation taken as the target rank)
     fw = sample if d_s == d_full else None
     if fw is None:
         dims = [sample.dims[0]] * d_full
         tr = [[1] + [int(sample.terms[0][1].shape[0])] * (d_full - 1) + [1]] * len(sample.terms)
         sumR = [sum(x[n] for x in tr) for n in range(d_full + 1)]
-        l = cost.caps(dims, sumR, sample.ell)
-        kept = [1] + [min(sample.rank, x) for x in l[1:-1]] + [1]
-        ff = cost.rounding_flops(dims, tr, l, kept)["total"]
+        if algo == "two_sided":
+            e2 = two_sided_ell(sample)
+            ff = cost.two_sided_flops(dims, tr, cost.caps(dims, sumR, e2),
+                                      cost.caps(dims, sumR, (3 * e2 + 1) // 2))["total"]
+        else:
+            l = cost.caps(dims, sumR, sample.ell)
+            kept = [1] + [min(sample.rank, x) for x in l[1:-1]] + [1]
+            ff = cost.rounding_flops(dims, tr, l, kept)["total"]
     else:
         ff = fs["total"]
     rate = 1.0 / (dt * ff / fs["total"])
@@ -158,7 +180,7 @@ def cpu_oracle_sample(name, budget_s=20.0):
         cores = max([x.get("num_threads", 1) for x in threadpool_info()] + [1])
     except Exception:
         cores = os.cpu_count()
-    desc = (f"oracle (NumPy fp64, BLAS/LAPACK steps) on {w['desc']} at d={d_s} "
+    desc = (f"oracle{' Alg. 6' if algo == 'two_sided' else ''} (NumPy fp64, BLAS/LAPACK steps) on {w['desc']} at d={d_s} "
             f"({reps} run(s), {dt:.2f} s each, {fs['total'] / dt / 1e9:.2f} GFLOP/s), "
             f"scaled to d={d_full} by the exact flop ratio")
     return rate, desc, cores, fs["total"] / dt
@@ -178,6 +200,9 @@ def main():
                     help="B independent roundings per step (distinct sketch seeds), spread "
                          "over --streams contexts (SURVEY 8d batched throughput of C1/C2)")
     ap.add_argument("--streams", type=int, default=8)
+    ap.add_argument("--algo", default="rand_orth", choices=["rand_orth", "two_sided"],
+                    help="rand_orth: tt_round_sum (Alg. 7 + truncation, the headline); "
+                         "two_sided: tt_round_sum_two_sided (Alg. 6)")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -220,8 +245,15 @@ def main():
     else:
         kw = dict(mode="rank", rank=wl.rank, oversample=wl.ell - wl.rank)
 
+    two_sided = args.algo == "two_sided"
+
+    def call(terms):
+        if two_sided:
+            return ctx.tt_round_sum_two_sided(terms, ell=two_sided_ell(wl), rho=0, seed=1)
+        return ctx.tt_round_sum(terms, seed=1, **kw)
+
     def step():
-        return ctx.tt_round_sum(local_terms, seed=1, **kw)
+        return call(local_terms)
 
     def barrier():
         if world > 1:
@@ -260,7 +292,7 @@ def main():
         phase = ph.tolist()
     phase = [p / args.steps for p in phase]
 
-    fl, l = flops_of(wl, ranks_out)
+    fl, l = flops_of(wl, ranks_out, args.algo)
     peak, peak_src = fp64_peak()
     value = 1000.0 / ms                       # roundings/s (one rounding per step, all ranks)
     tflops = fl["total"] / (ms * 1e-3) / 1e12
@@ -271,11 +303,11 @@ def main():
 
     e2e = None
     if not args.no_e2e:
-        e2e = e2e_run(args, ctx, local_terms, kw, dev, world, dist if world > 1 else None)
+        e2e = e2e_run(args, call, local_terms, dev, world, dist if world > 1 else None)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        rate, desc, cores, gfs = cpu_oracle_sample(args.workload)
+        rate, desc, cores, gfs = cpu_oracle_sample(args.workload, algo=args.algo)
         cpu = {"value": rate, "unit": "roundings/s", "cores": cores, "kind": "oracle",
                "sample": desc}
 
@@ -283,7 +315,7 @@ def main():
         traffic = traffic_kernel = None
         prof = os.path.join(ROOT, "profiles", "traffic.json")
         try:
-            tr = json.load(open(prof)).get(args.workload)
+            tr = json.load(open(prof)).get(args.workload + ("_two_sided" if two_sided else ""))
             traffic, traffic_kernel = tr["bytes_per_launch"], tr["kernel"]
         except Exception:
             pass
@@ -295,14 +327,22 @@ def main():
             "config": {"workload": args.workload, "desc": WORKLOADS[args.workload]["desc"],
                        "summands": S, "d": wl.d, "I": wl.dims[0], "sketch_rank": wl.ell,
                        "rank": wl.rank, "tol": wl.tol, "parallelism": f"summands/{world}",
+                       "algo": ("two_sided (Alg. 6): l = %d, rho = %d" % (
+                           two_sided_ell(wl), (3 * two_sided_ell(wl) + 1) // 2))
+                       if two_sided else "rand_orth (Alg. 7 + truncation)",
                        "l2": "inputs (12.9 GB) larger than L2 (126 MB); no flush"},
             "tflops": tflops, "fp64_peak_tflops": peak, "fp64_peak_source": peak_src,
             "frac_of_fp64_peak": tflops / peak,
             "flops_per_rounding": fl,
-            "phase_ms": {"sketch": phase[0], "phase1_contractions": phase[1],
-                         "sweep_gemms": phase[2], "qr": phase[3], "collectives": phase[4],
-                         "truncation": phase[5], "total": phase[6]},
-            "roofline": {"bound": "tensor", "kernel": "dgemm_kernel (phase-1 Alg. 3 contractions, DMMA.8x8x4)",
+            "phase_ms": ({"sketches": phase[0], "right_contractions": phase[1],
+                          "left_contraction_and_assembly": phase[2], "bond_qr_svd": phase[3],
+                          "collectives": phase[4], "bond_factors": phase[5], "total": phase[6]}
+                         if two_sided else
+                         {"sketch": phase[0], "phase1_contractions": phase[1],
+                          "sweep_gemms": phase[2], "qr": phase[3], "collectives": phase[4],
+                          "truncation": phase[5], "total": phase[6]}),
+            "roofline": {"bound": "tensor", "kernel": "dgemm_kernel (phase-1 Alg. 3 contractions, DMMA.8x8x4)"
+                         + (" with the right sketch (rho)" if two_sided else ""),
                          "achieved": p1_achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": (p1_achieved / peak) if p1_achieved else None,
                          "traffic": traffic, "traffic_kernel": traffic_kernel,
@@ -398,7 +438,7 @@ def batched_run(args, world, rank, local):
         dist.destroy_process_group()
 
 
-def e2e_run(args, ctx, local_terms, kw, dev, world, dist):
+def e2e_run(args, call, local_terms, dev, world, dist):
     """Same metric through the C-ABI with HOST (pinned) buffers: the H2D copies of
     the inputs happen inside the call (overlapped with phase 1) and the result is
     read back D2H into pinned memory, both inside the timed region."""
@@ -406,7 +446,7 @@ def e2e_run(args, ctx, local_terms, kw, dev, world, dist):
     host = [[c.permute(2, 1, 0).contiguous().cpu().pin_memory().permute(2, 1, 0) for c in t]
             for t in local_terms]
     h2d = sum(c.numel() * 8 for t in host for c in t)
-    r = ctx.tt_round_sum(host, seed=1, **kw)
+    r = call(host)
     outs = [torch.empty((r.ranks[n + 1], r.dims[n], r.ranks[n]), dtype=torch.float64).pin_memory()
             for n in range(r.d)]
     d2h = sum(o.numel() * 8 for o in outs)
@@ -419,7 +459,7 @@ def e2e_run(args, ctx, local_terms, kw, dev, world, dist):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     for _ in range(args.e2e_steps):
-        r = ctx.tt_round_sum(host, seed=1, **kw)
+        r = call(host)
         for n in range(r.d):
             _lib._check(L.tt_tensor_copy_core(r._h.ptr, n + 1, ctypes.c_void_p(outs[n].data_ptr())))
         del r
@@ -442,9 +482,9 @@ def reference_arm(args, world, rank):
     steps = []
     desc = cores = None
     for _ in range(args.warmup):
-        cpu_oracle_sample(args.workload, budget_s=2.0)
+        cpu_oracle_sample(args.workload, budget_s=2.0, algo=args.algo)
     for _ in range(args.steps):
-        rate, desc, cores, _ = cpu_oracle_sample(args.workload, budget_s=10.0)
+        rate, desc, cores, _ = cpu_oracle_sample(args.workload, budget_s=10.0, algo=args.algo)
         steps.append(1.0 / rate)
     ms = 1000.0 * statistics.mean(steps)
     value = 1000.0 / ms
@@ -453,7 +493,8 @@ def reference_arm(args, world, rank):
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": {"workload": args.workload,
-                                        "desc": WORKLOADS[args.workload]["desc"]},
+                                        "desc": WORKLOADS[args.workload]["desc"],
+                                        "algo": args.algo},
         "cpu_baseline": {"value": value, "unit": "roundings/s", "cores": cores,
                          "kind": "oracle", "sample": desc},
         "e2e": {"value": value, "unit": "roundings/s", "h2d_bytes_per_step": 0,

@@ -149,6 +149,23 @@ int tt_round_sum(tt_ctx_t ctx, int32_t S_local, const tt_view* terms,
 int tt_round_deterministic(tt_ctx_t ctx, int32_t S, const tt_view* terms,
                            const tt_round_opts* opts, tt_tensor_t* out);
 
+/* Two-Sided-Randomization (generalized Nystrom), Alg. 6, of the sum
+ * Y = sum_j Y^(j) of S_local summands (R18-R21).
+ *  - ell: target ranks l (>= 1); rho: right sketch rank (>= ell), 0 = ceil(1.5 l)
+ *    (P:944); both capped per bond by R7, so l_n <= rho_n.
+ *  - seed: Philox key of the left sketch L (tag 0x10001, cores 1..d-1) and the
+ *    right sketch R (tag 0x10002, cores 2..d), Def. 3.1.
+ *  - W^L_n = PartialContractionsLR(Y^(j), L) (R18), W^R_n = Alg. 3 with R, per
+ *    summand; P_n = W^L_n W^R_n (sum over summands, all-reduced over ranks);
+ *    SVD P_n = U S V^T; L_n = W^R_n V S^{-1/2}, R_n = S^{-1/2} U^T W^L_n with the
+ *    pseudo-inverse cutoff s_i > max(l_n, rho_n) eps s_1 (R20);
+ *    X_n = sum_j Y^(j)_n x1 R^(j)_{n-1} x3 L^(j)_n (R19).
+ * Output ranks (1, l_1..l_{d-1}, 1), not orthogonal; an exactly zero
+ * sum gives a zero TT of ranks 1 (TT_FLAG_ZERO).  Errors as tt_round_sum;
+ * TT_ERR_NUMERIC for a non-finite singular value. */
+int tt_round_sum_two_sided(tt_ctx_t ctx, int32_t S_local, const tt_view* terms,
+                           int64_t ell, int64_t rho, uint64_t seed, tt_tensor_t* out);
+
 /* <x, y> by the full right-to-left contraction (App. A); *out is a
  * host double.  x and y must have equal dims. */
 int tt_inner(tt_ctx_t ctx, const tt_view* x, const tt_view* y, double* out);
@@ -171,7 +188,9 @@ uint64_t tt_launch_count(void);
 /* Per-phase device times (ms) of the last tt_round_sum on ctx, measured with
  * CUDA events on the context stream when timing is enabled:
  * [0] sketch, [1] phase 1 (Alg. 3), [2] sweep GEMMs, [3] QR, [4] collectives,
- * [5] truncation, [6] total.  Returns the number of entries written (<= n). */
+ * [5] truncation, [6] total.  Returns the number of entries written (<= n).
+ * tt_round_sum_two_sided: [0] sketches, [1] Alg. 3 with R, [2] left contraction
+ * and assembly GEMMs, [3] bond QR + SVD, [4] collectives, [5] bond factors. */
 int tt_ctx_set_timing(tt_ctx_t ctx, int enable);
 /* Copy the context's device status words (after the last call) to out[0..n):
  * [1] Householder fallback used, [2] zero sketch seen, [3] bit 1: Jacobi SVD hit

@@ -62,6 +62,8 @@ def load_library(path: str = LIB_PATH):
                                    C.POINTER(P)]),
         "tt_round_deterministic": (C.c_int, [P, i32, C.POINTER(tt_view),
                                              C.POINTER(tt_round_opts), C.POINTER(P)]),
+        "tt_round_sum_two_sided": (C.c_int, [P, i32, C.POINTER(tt_view), i64, i64, u64,
+                                             C.POINTER(P)]),
         "tt_inner": (C.c_int, [P, C.POINTER(tt_view), C.POINTER(tt_view), C.POINTER(dbl)]),
         "tt_tensor_info": (C.c_int, [P, C.POINTER(i32), C.POINTER(C.POINTER(i64)),
                                      C.POINTER(C.POINTER(i64)), C.POINTER(C.POINTER(P)),
@@ -299,6 +301,17 @@ class Context:
         opts = tt_round_opts(TOL, 0, int(rank), 0, float(tol), 0, 0)
         h = C.c_void_p()
         _check(L.tt_round_deterministic(self.handle, len(views), arr, C.byref(opts), C.byref(h)))
+        return TTResult(h.value, self.device)
+
+    def tt_round_sum_two_sided(self, terms, ell: int, rho: int = 0, seed: int = 1) -> TTResult:
+        """Round sum_j terms[j] with Alg. 6 (two-sided randomization); rho = 0 means
+        ceil(1.5 ell).  See include/ttround.h."""
+        L = load_library()
+        views = [_View(t) for t in terms]
+        arr = (tt_view * len(views))(*[v.view for v in views])
+        h = C.c_void_p()
+        _check(L.tt_round_sum_two_sided(self.handle, len(views), arr, int(ell), int(rho),
+                                        C.c_uint64(seed).value, C.byref(h)))
         return TTResult(h.value, self.device)
 
     # ---------------------------------------------------------------- kernels

@@ -61,6 +61,44 @@ def rounding_flops(dims: Sequence[int], term_ranks: Sequence[Sequence[int]], l: 
             "total": total}
 
 
+def two_sided_flops(dims: Sequence[int], term_ranks: Sequence[Sequence[int]],
+                    l: Sequence[int], rho: Sequence[int]) -> Dict[str, float]:
+    """Exact per-step counts of Alg. 6 on a sum (R18-R20): l = (l_0..l_N) left /
+    output ranks, rho = (rho_0..rho_N) right sketch ranks.  The bond SVD of the
+    l x rho matrix W^L W^R is credited at the Householder QR count of its
+    transpose, the SVD of the l x l factor is not credited."""
+    N = len(dims)
+    I = list(dims)
+    sumR = [sum(r[n] for r in term_ranks) for n in range(N + 1)]
+    right = rounding_flops(dims, term_ranks, rho)["phase1"]              # line 5 (Alg. 3)
+    left = 0.0
+    for R in term_ranks:                                                  # line 4 (R18)
+        left += 2.0 * I[0] * l[1] * R[1]
+        for n in range(2, N):
+            left += 2.0 * l[n - 1] * R[n - 1] * I[n - 1] * R[n]
+            left += 2.0 * l[n] * l[n - 1] * I[n - 1] * R[n]
+    bond = 0.0
+    for n in range(1, N):                                                 # lines 7-10
+        bond += 2.0 * l[n] * sumR[n] * rho[n]                             # W^L W^R
+        bond += 4.0 * rho[n] * l[n] ** 2 - 4.0 * l[n] ** 3 / 3.0          # QR of its transpose
+        bond += 2.0 * sumR[n] * rho[n] * l[n] + 2.0 * l[n] * l[n] * sumR[n]   # L_n, R_n
+    asm = 2.0 * I[0] * sumR[1] * l[1]                                     # lines 12-16
+    for n in range(2, N):
+        asm += sum(2.0 * l[n - 1] * R[n - 1] * I[n - 1] * R[n] for R in term_ranks)
+        asm += 2.0 * l[n - 1] * I[n - 1] * sumR[n] * l[n]
+    asm += 2.0 * l[N - 1] * sumR[N - 1] * I[N - 1]
+    total = right + left + bond + asm
+    return {"phase1": right, "left": left, "bond": bond, "assembly": asm, "total": total}
+
+
+def paper_two_sided(N: int, I: int, R: int, ell: int, rho: int) -> float:
+    """Leading-order cost of Alg. 6 on one TT: (N-2)I(2R²ρ + 2Rρ²)
+    for the right contraction + (N-2)I(2R²l + 2Rl²) left + (N-2)I(2R²l + 2Rl²)
+    assembly; with rho = 1.5 l this is P:944's I(N-2)(7R²l + 8.5Rl²)."""
+    return I * (N - 2) * (2.0 * R * R * rho + 2.0 * R * rho * rho
+                          + 4.0 * R * R * ell + 4.0 * R * ell * ell)
+
+
 def paper_rto_sum(N: int, I: int, R: int, ell: int, s: int) -> float:
     """Leading-order cost of Alg. 7 printed at P:985-987 (last term read 4l³, R14)."""
     return I * (N - 2) * (4.0 * s * R * R * ell + 6.0 * s * R * ell * ell + 4.0 * ell ** 3)

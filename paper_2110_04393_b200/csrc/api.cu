@@ -262,9 +262,12 @@ inline int wait_core(Ctx& c, const Terms& T, int n /*0-based*/) {
   return TT_OK;
 }
 
+// Def. 3.1 Gaussian TT cores n = first..last (1-based; default 2..d, the cores
+// Alg. 3 reads) from the R9 Philox stream (seed, n, tag).
 int make_sketch(Ctx& c, const std::vector<int64_t>& dims, const std::vector<int64_t>& l,
-                uint64_t seed, uint32_t tag, tt_sketch& sk) {
+                uint64_t seed, uint32_t tag, tt_sketch& sk, int first = 2, int last = 0) {
   const int d = int(dims.size());
+  if (last <= 0) last = d;
   sk.d = d;
   sk.dims = dims;
   sk.ranks = l;
@@ -272,7 +275,7 @@ int make_sketch(Ctx& c, const std::vector<int64_t>& dims, const std::vector<int6
   sk.tag = tag;
   sk.cores.clear();
   sk.cores.resize(d);
-  for (int n = 2; n <= d; ++n) {
+  for (int n = first; n <= last; ++n) {
     const int64_t cnt = l[n - 1] * dims[n - 1] * l[n];
     TTR_TRY(dalloc(sk.cores[n - 1], size_t(cnt), c.stream));
     TTR_TRY(philox_fill(c, sk.cores[n - 1].p, cnt, seed, uint32_t(n), tag,
@@ -281,58 +284,34 @@ int make_sketch(Ctx& c, const std::vector<int64_t>& dims, const std::vector<int6
   return TT_OK;
 }
 
-// ------------------------------------------------------------------ Alg. 7
-// X (output cores, ranks l) from the staged summands and the sketch.
-int alg7(Ctx& c, const Terms& T, const std::vector<int64_t>& dims, const std::vector<int64_t>& l,
-         const tt_sketch& sk, tt_tensor& out, PhaseTimer& tm) {
+// ------------------------------------------------------------------ Alg. 3
+// PartialContractionsRL(Y^(j), sk) for every local summand, batched per step
+// (one launch per Alg. 3 line for all summands).  W stack per bond n = 1..d-1:
+// sumR[n] x l[n] (ld sumR[n]) at Wst + woff[n], summand j in rows off[n][j]..
+int partial_contractions_rl(Ctx& c, const Terms& T, const std::vector<int64_t>& dims,
+                            const std::vector<int64_t>& l, const tt_sketch& sk,
+                            const std::vector<std::vector<int64_t>>& off,
+                            const std::vector<int64_t>& sumR, DBuf& Wst,
+                            std::vector<size_t>& woff) {
   const int S = T.S, d = T.d;
   cudaStream_t s = c.stream;
-  // local summed ranks and per-summand offsets
-  std::vector<int64_t> sumR(d + 1, 0);
-  std::vector<std::vector<int64_t>> off(d + 1, std::vector<int64_t>(S + 1, 0));
-  for (int n = 0; n <= d; ++n)
-    for (int j = 0; j < S; ++j) {
-      off[n][j + 1] = off[n][j] + T.R[j][n];
-      sumR[n] = off[n][j + 1];
-    }
-  // W stack per bond n = 1..d-1: sumR[n] x l[n] (ld sumR[n])
-  std::vector<size_t> woff(d + 1, 0);
+  woff.assign(d + 1, 0);
   size_t wtot = 0;
   for (int n = 1; n < d; ++n) {
     woff[n] = wtot;
     wtot += size_t(sumR[n]) * l[n];
   }
-  size_t zmax = 1, xmax = 1, ymax = 1, mmax = 1;
+  size_t zmax = 1;
   for (int n = 2; n < d; ++n) {
     size_t z = 0;
     for (int j = 0; j < S; ++j) z += size_t(T.R[j][n - 1]) * dims[n - 1] * l[n];
     zmax = std::max(zmax, z);
   }
-  for (int n = 1; n < d; ++n) {
-    xmax = std::max(xmax, size_t(l[n - 1]) * dims[n - 1] * sumR[n]);
-    ymax = std::max(ymax, size_t(l[n - 1]) * dims[n - 1] * l[n]);
-    mmax = std::max(mmax, size_t(l[n]) * sumR[n]);
-  }
-  DBuf Wst, Z, Xa, Xb, Yb, Mb, Stk;
+  DBuf Z;
   TTR_TRY(dalloc(Wst, wtot, s));
   if (d > 2) TTR_TRY(dalloc(Z, zmax, s));
-  TTR_TRY(dalloc(Xa, xmax, s));
-  TTR_TRY(dalloc(Xb, xmax, s));
-  TTR_TRY(dalloc(Yb, ymax, s));
-  TTR_TRY(dalloc(Mb, mmax, s));
-  TTR_TRY(dalloc(Stk, size_t(sumR[d - 1]) * dims[d - 1], s));
-
-  out.d = d;
-  out.dims = dims;
-  out.ranks = l;
-  out.bufs.clear();
-  out.bufs.resize(d);
-  for (int n = 1; n <= d; ++n)
-    TTR_TRY(dalloc(out.bufs[n - 1], size_t(l[n - 1]) * dims[n - 1] * l[n], s));
-
   std::vector<GemmDesc> gd(S);
   // ---------------- phase 1: Alg. 3 for every summand (batched), n = d .. 2
-  tm.begin(1);
   {
     TTR_TRY(wait_core(c, T, d - 1));
     const double* G = sk.cores[d - 1].p;   // H(G_d): l_{d-1} x I_d (ld l_{d-1})
@@ -359,7 +338,50 @@ int alg7(Ctx& c, const Terms& T, const std::vector<int64_t>& dims, const std::ve
       TTR_TRY(gemm(c, false, true, gd.data(), S, 1.0, 0.0, s));
     }
   }
+  return TT_OK;
+}
+
+// ------------------------------------------------------------------ Alg. 7
+// X (output cores, ranks l) from the staged summands and the sketch.
+int alg7(Ctx& c, const Terms& T, const std::vector<int64_t>& dims, const std::vector<int64_t>& l,
+         const tt_sketch& sk, tt_tensor& out, PhaseTimer& tm) {
+  const int S = T.S, d = T.d;
+  cudaStream_t s = c.stream;
+  // local summed ranks and per-summand offsets
+  std::vector<int64_t> sumR(d + 1, 0);
+  std::vector<std::vector<int64_t>> off(d + 1, std::vector<int64_t>(S + 1, 0));
+  for (int n = 0; n <= d; ++n)
+    for (int j = 0; j < S; ++j) {
+      off[n][j + 1] = off[n][j] + T.R[j][n];
+      sumR[n] = off[n][j + 1];
+    }
+  std::vector<size_t> woff;
+  DBuf Wst;
+  tm.begin(1);
+  TTR_TRY(partial_contractions_rl(c, T, dims, l, sk, off, sumR, Wst, woff));
   tm.end(1);
+  size_t xmax = 1, ymax = 1, mmax = 1;
+  for (int n = 1; n < d; ++n) {
+    xmax = std::max(xmax, size_t(l[n - 1]) * dims[n - 1] * sumR[n]);
+    ymax = std::max(ymax, size_t(l[n - 1]) * dims[n - 1] * l[n]);
+    mmax = std::max(mmax, size_t(l[n]) * sumR[n]);
+  }
+  DBuf Xa, Xb, Yb, Mb, Stk;
+  TTR_TRY(dalloc(Xa, xmax, s));
+  TTR_TRY(dalloc(Xb, xmax, s));
+  TTR_TRY(dalloc(Yb, ymax, s));
+  TTR_TRY(dalloc(Mb, mmax, s));
+  TTR_TRY(dalloc(Stk, size_t(sumR[d - 1]) * dims[d - 1], s));
+
+  out.d = d;
+  out.dims = dims;
+  out.ranks = l;
+  out.bufs.clear();
+  out.bufs.resize(d);
+  for (int n = 1; n <= d; ++n)
+    TTR_TRY(dalloc(out.bufs[n - 1], size_t(l[n - 1]) * dims[n - 1] * l[n], s));
+
+  std::vector<GemmDesc> gd(S);
   // ---------------- phase 2: Alg. 7 lines 6-16
   TTR_TRY(wait_core(c, T, 0));
   double* Xcur = Xa.p;
@@ -487,7 +509,7 @@ int truncate(Ctx& c, tt_tensor& X, double tol, int64_t rmax, std::vector<int64_t
     TTR_TRY(dalloc(newn, size_t(k) * mrow, s));
     if (fast) {
       TTR_TRY(dalloc(Bk, size_t(r0) * k, s));
-      TTR_TRY(scale_by_inv_sigma(c, AV.p, r0, k, sig.p, Bk.p, 2, s));
+      TTR_TRY(scale_by_inv_sigma(c, AV.p, r0, k, sig.p, Bk.p, 4, double(r0) * 0x1p-52, s));
       TTR_TRY(gemm1(c, true, false, int(k), int(mrow), int(r0), 1.0, Bk.p, int(r0),
                     X.bufs[n - 1].p, int(r0), 0.0, newn.p, int(k), s));
     } else if (mrow >= r0) {
@@ -670,6 +692,254 @@ int round_sum_impl(tt_ctx* c, int S, const tt_view* terms, const tt_round_opts* 
   return TT_OK;
 }
 
+// ------------------------------------------------------------------ Alg. 6
+// Two-Sided-Randomization (generalized Nystrom) of the sum
+// sum_j Y^(j) (readings R18-R21).  Left sketch L (ranks l,
+// cores 1..d-1), right sketch R (ranks rho >= l, cores 2..d).  Per bond n:
+//   W^L_n = [Psi_n V(Y^(j)_{1:n})]_j   (l_n x sumR_n; PartialContractionsLR, R18)
+//   W^R_n = [H(Y^(j)_{n+1:N}) Omega_n]_j stacked  (sumR_n x rho_n; Alg. 3)
+//   P_n = W^L_n W^R_n = U Sigma V^T                (line 8; all-reduced over GPUs)
+//   R_n = Sigma^{-1/2} U^T W^L_n, L_n = W^R_n V Sigma^{-1/2}   (lines 9-10)
+//   X_n = sum_j Y^(j)_n x1 R^(j)_{n-1} x3 L^(j)_n  (lines 12-16, R19)
+// The SVD of the l x rho matrix P_n: R-only QR of P_n^T, V-free Jacobi of R^T
+// (U Sigma), then V Sigma^{-1/2} = P_n^T (U Sigma) Sigma^{-5/2} and
+// Sigma^{-1/2} U^T = (U Sigma Sigma^{-3/2})^T, pseudo-inverse cutoff
+// sigma_i > max(l, rho) eps sigma_1 (R20).  Every product is a DMMA GEMM; the
+// left contraction and the assembly reuse Alg. 7's carry / projection shapes.
+int two_sided_impl(tt_ctx* c, int S, const tt_view* terms, int64_t ell, int64_t rho,
+                   uint64_t seed, tt_tensor** outp) {
+  std::vector<int64_t> dims;
+  TTR_TRY(validate(terms, S, dims));
+  if (ell < 1) {
+    set_error("two-sided rounding needs ell >= 1");
+    return TT_ERR_ARG;
+  }
+  if (rho <= 0) rho = (3 * ell + 1) / 2;   // ceil(1.5 l)
+  if (rho < ell) {
+    set_error("two-sided rounding needs rho >= ell (P:763)");
+    return TT_ERR_ARG;
+  }
+  const int d = int(dims.size());
+  TTR_CUDA(cudaSetDevice(c->device));
+  Ctx& C = *c;
+  cudaStream_t s = C.stream;
+  PhaseTimer tm(C);
+  tm.begin(6);
+  Terms T;
+  TTR_TRY(stage_terms(C, terms, S, T));
+  std::vector<int64_t> gsumR(d + 1, 0);
+  for (int n = 0; n <= d; ++n)
+    for (int j = 0; j < S; ++j) gsumR[n] += T.R[j][n];
+  TTR_TRY(allreduce_sum_i64(C, gsumR.data(), gsumR.size()));
+  const std::vector<int64_t> l = rank_caps(dims, gsumR, ell);
+  const std::vector<int64_t> r = rank_caps(dims, gsumR, rho);
+  TTR_CUDA(cudaMemsetAsync(C.flags.p, 0, sizeof(int) * C.nflags, s));
+  // local summed ranks and per-summand offsets
+  std::vector<int64_t> sumR(d + 1, 0);
+  std::vector<std::vector<int64_t>> off(d + 1, std::vector<int64_t>(S + 1, 0));
+  for (int n = 0; n <= d; ++n)
+    for (int j = 0; j < S; ++j) {
+      off[n][j + 1] = off[n][j] + T.R[j][n];
+      sumR[n] = off[n][j + 1];
+    }
+  tt_sketch skL, skR;
+  tm.begin(0);
+  TTR_TRY(make_sketch(C, dims, l, seed, 0x10001u, skL, 1, d - 1));   // R21
+  TTR_TRY(make_sketch(C, dims, r, seed, 0x10002u, skR, 2, d));
+  tm.end(0);
+  // line 5: W^R (Alg. 3 with the right sketch)
+  std::vector<size_t> woff;
+  DBuf WR;
+  tm.begin(1);
+  TTR_TRY(partial_contractions_rl(C, T, dims, r, skR, off, sumR, WR, woff));
+  tm.end(1);
+
+  size_t xmax = 1, lsr = 1, lr = 1, lmax = 1;
+  for (int n = 1; n <= d; ++n)
+    xmax = std::max(xmax, size_t(n == 1 ? 1 : l[n - 1]) * dims[n - 1] * sumR[n == d ? d - 1 : n]);
+  for (int n = 1; n < d; ++n) {
+    lsr = std::max(lsr, size_t(l[n]) * sumR[n]);
+    lr = std::max(lr, size_t(l[n]) * r[n]);
+    lmax = std::max<size_t>(lmax, size_t(l[n]));
+  }
+  DBuf Xa, WLa, WLb, Ra, Rb, Lf, Pb, Rq, Rt, AV, sig, B3, B5, Tm, Stk, sig0;
+  TTR_TRY(dalloc(Xa, xmax, s));
+  TTR_TRY(dalloc(WLa, lsr, s));
+  TTR_TRY(dalloc(WLb, lsr, s));
+  TTR_TRY(dalloc(Ra, lsr, s));
+  TTR_TRY(dalloc(Rb, lsr, s));
+  TTR_TRY(dalloc(Lf, lsr, s));
+  TTR_TRY(dalloc(Pb, lr, s));
+  TTR_TRY(dalloc(Rq, lmax * lmax, s));
+  TTR_TRY(dalloc(Rt, lmax * lmax, s));
+  TTR_TRY(dalloc(AV, lr, s));
+  TTR_TRY(dalloc(sig, lmax, s));
+  TTR_TRY(dalloc(B3, lr, s));
+  TTR_TRY(dalloc(B5, lmax * lmax, s));
+  TTR_TRY(dalloc(Tm, lr, s));
+  TTR_TRY(dalloc(Stk, size_t(sumR[d - 1]) * dims[d - 1], s));
+  TTR_TRY(dalloc(sig0, size_t(d), s));
+  TTR_TRY(fill_zero(C, sig0.p, d, s));
+
+  std::unique_ptr<tt_tensor> out(new tt_tensor);
+  out->stream = s;
+  out->d = d;
+  out->dims = dims;
+  out->ranks = l;
+  out->bufs.resize(d);
+  for (int n = 1; n <= d; ++n)
+    TTR_TRY(dalloc(out->bufs[n - 1], size_t(l[n - 1]) * dims[n - 1] * l[n], s));
+
+  std::vector<GemmDesc> gd(S);
+  // [A^(j) H(Y^(j)_n)]_j for an lrows x sumR_{n-1} block row A (ld lrows), written
+  // side by side along the right rank: dst is lrows x I_n x sumR_n (n 1-based)
+  auto carry = [&](const double* A, int64_t lrows, int n, double* dst) -> int {
+    const int64_t In = dims[n - 1];
+    for (int j = 0; j < S; ++j)
+      gd[j] = GemmDesc{A + lrows * off[n - 1][j], T.core[j][n - 1],
+                       dst + lrows * In * off[n][j], int(lrows), int(In * T.R[j][n]),
+                       int(T.R[j][n - 1]), int(lrows), int(T.R[j][n - 1]), int(lrows)};
+    return gemm(C, false, false, gd.data(), S, 1.0, 0.0, s);
+  };
+  const double rel_thr_base = 0x1p-52;
+  double* WLcur = WLa.p;
+  double* WLnext = WLb.p;
+  double* Rprev = Ra.p;
+  double* Rcur = Rb.p;
+  // X_1 = [Y^(1)_1 ... Y^(s)_1] (I_1 x sumR_1), then line 4 at n = 1: W^L_1 = V(L_1)^T X_1
+  TTR_TRY(wait_core(C, T, 0));
+  for (int j = 0; j < S; ++j)
+    TTR_CUDA(cudaMemcpyAsync(Xa.p + dims[0] * off[1][j], T.core[j][0],
+                             sizeof(double) * dims[0] * T.R[j][1], cudaMemcpyDeviceToDevice, s));
+  tm.begin(2);
+  TTR_TRY(gemm1(C, true, false, int(l[1]), int(sumR[1]), int(dims[0]), 1.0, skL.cores[0].p,
+                int(dims[0]), Xa.p, int(dims[0]), 0.0, WLcur, int(l[1]), s));
+  tm.end(2);
+  for (int n = 1; n <= d - 1; ++n) {
+    const int64_t ln = l[n], rn = r[n], Sn = sumR[n];
+    const double* WRn = WR.p + woff[n];   // sumR_n x rho_n (ld sumR_n)
+    // ---- lines 7-10 for bond n
+    tm.begin(5);
+    TTR_TRY(gemm1(C, false, false, int(ln), int(rn), int(Sn), 1.0, WLcur, int(ln), WRn, int(Sn),
+                  0.0, Pb.p, int(ln), s));   // P_n = W^L_n W^R_n
+    tm.end(5);
+    tm.begin(4);
+    TTR_TRY(allreduce_sum(C, Pb.p, size_t(ln) * rn));
+    tm.end(4);
+    tm.begin(3);
+    const double rel_thr = double(std::max(ln, rn)) * rel_thr_base;
+    if (svd_nov_fits(ln, ln)) {
+      TTR_TRY(qr(C, rn, ln, Pb.p, ln, true, nullptr, Rq.p, s));   // P^T = Q R
+      TTR_TRY(transpose(C, Rq.p, ln, ln, ln, Rt.p, ln, s));
+      TTR_TRY(svd_nov(C, ln, ln, Rt.p, ln, AV.p, sig.p, s));       // R^T = U Sigma W^T
+      tm.end(3);
+      tm.begin(5);
+      // R_n = Sigma^{-1/2} U^T W^L_n = (U Sigma . Sigma^{-3/2})^T W^L_n
+      TTR_TRY(scale_by_inv_sigma(C, AV.p, ln, ln, sig.p, B3.p, 3, rel_thr, s));
+      TTR_TRY(gemm1(C, true, false, int(ln), int(Sn), int(ln), 1.0, B3.p, int(ln), WLcur,
+                    int(ln), 0.0, Rcur, int(ln), s));
+      // L_n = W^R_n V Sigma^{-1/2} = W^R_n P^T (U Sigma . Sigma^{-5/2})
+      TTR_TRY(scale_by_inv_sigma(C, AV.p, ln, ln, sig.p, B5.p, 5, rel_thr, s));
+      TTR_TRY(gemm1(C, true, false, int(rn), int(ln), int(ln), 1.0, Pb.p, int(ln), B5.p,
+                    int(ln), 0.0, Tm.p, int(rn), s));
+    } else {
+      // general size: Jacobi of P^T (rho x l) accumulating its rotations:
+      // P^T W = (V Sigma), W = U
+      TTR_TRY(transpose(C, Pb.p, ln, rn, ln, Tm.p, rn, s));
+      DBuf Wj;
+      TTR_TRY(dalloc(Wj, size_t(ln) * ln, s));
+      TTR_TRY(svd_jacobi(C, rn, ln, Tm.p, rn, AV.p, Wj.p, sig.p, s));
+      tm.end(3);
+      tm.begin(5);
+      TTR_TRY(scale_by_inv_sigma(C, Wj.p, ln, ln, sig.p, B3.p, 1, rel_thr, s));
+      TTR_TRY(gemm1(C, true, false, int(ln), int(Sn), int(ln), 1.0, B3.p, int(ln), WLcur,
+                    int(ln), 0.0, Rcur, int(ln), s));
+      TTR_TRY(scale_by_inv_sigma(C, AV.p, rn, ln, sig.p, Tm.p, 3, rel_thr, s));
+    }
+    TTR_TRY(gemm1(C, false, false, int(Sn), int(ln), int(rn), 1.0, WRn, int(Sn), Tm.p, int(rn),
+                  0.0, Lf.p, int(Sn), s));
+    TTR_CUDA(cudaMemcpyAsync(sig0.p + n, sig.p, sizeof(double), cudaMemcpyDeviceToDevice, s));
+    tm.end(5);
+    // ---- lines 12-15: X_n = sum_j Y^(j)_n x1 R^(j)_{n-1} x3 L^(j)_n
+    tm.begin(2);
+    const int64_t In = dims[n - 1];
+    if (n == 1) {
+      // X_1 = [Y^(j)_1]_j L_1   (Xa still holds the concatenated first cores)
+      TTR_TRY(gemm1(C, false, false, int(In), int(ln), int(Sn), 1.0, Xa.p, int(In), Lf.p,
+                    int(Sn), 0.0, out->bufs[0].p, int(In), s));
+    } else {
+      TTR_TRY(carry(Rprev, l[n - 1], n, Xa.p));   // [R^(j)_{n-1} H(Y^(j)_n)]_j
+      const int64_t m = l[n - 1] * In;
+      TTR_TRY(gemm1(C, false, false, int(m), int(ln), int(Sn), 1.0, Xa.p, int(m), Lf.p, int(Sn),
+                    0.0, out->bufs[n - 1].p, int(m), s));
+    }
+    tm.end(2);
+    tm.begin(4);
+    TTR_TRY(allreduce_sum(C, out->bufs[n - 1].p, size_t(l[n - 1]) * In * ln));
+    tm.end(4);
+    // ---- line 4 at n + 1: W^L_{n+1} = V(L_{n+1})^T V([W^L(j)_n H(Y^(j)_{n+1})]_j)
+    if (n + 1 <= d - 1) {
+      tm.begin(2);
+      TTR_TRY(wait_core(C, T, n));
+      TTR_TRY(carry(WLcur, ln, n + 1, Xa.p));
+      const int64_t m1 = ln * dims[n];
+      TTR_TRY(gemm1(C, true, false, int(l[n + 1]), int(sumR[n + 1]), int(m1), 1.0,
+                    skL.cores[n].p, int(m1), Xa.p, int(m1), 0.0, WLnext, int(l[n + 1]), s));
+      tm.end(2);
+      std::swap(WLcur, WLnext);
+    }
+    std::swap(Rprev, Rcur);
+  }
+  // ---- line 16: X_N = sum_j R^(j)_{N-1} H(Y^(j)_N) = [R^(j)_{N-1}]_j [H(Y^(j)_N); ...]
+  {
+    tm.begin(2);
+    const int64_t Id = dims[d - 1];
+    for (int j = 0; j < S; ++j)
+      TTR_CUDA(cudaMemcpy2DAsync(Stk.p + off[d - 1][j], sizeof(double) * sumR[d - 1],
+                                 T.core[j][d - 1], sizeof(double) * T.R[j][d - 1],
+                                 sizeof(double) * T.R[j][d - 1], Id, cudaMemcpyDeviceToDevice,
+                                 s));
+    TTR_TRY(gemm1(C, false, false, int(l[d - 1]), int(Id), int(sumR[d - 1]), 1.0, Rprev,
+                  int(l[d - 1]), Stk.p, int(sumR[d - 1]), 0.0, out->bufs[d - 1].p,
+                  int(l[d - 1]), s));
+    tm.end(2);
+    tm.begin(4);
+    TTR_TRY(allreduce_sum(C, out->bufs[d - 1].p, size_t(l[d - 1]) * Id));
+    tm.end(4);
+  }
+  tm.end(6);
+  std::vector<double> s0(d, 1.0);
+  TTR_CUDA(cudaMemcpyAsync(s0.data(), sig0.p, sizeof(double) * d, cudaMemcpyDeviceToHost, s));
+  TTR_CUDA(cudaStreamSynchronize(s));
+  tm.finish();
+  int fl[4];
+  TTR_TRY(read_flags(C, fl, 4));
+  if (fl[3] & 1) {
+    set_error("QR breakdown in the two-sided bond factorisation");
+    return TT_ERR_NUMERIC;
+  }
+  bool capped = false, zero = false;
+  for (int n = 1; n < d; ++n) {
+    capped |= l[n] < ell;
+    if (!std::isfinite(s0[n])) {
+      set_error("non-finite singular value at bond %d of the two-sided rounding", n);
+      return TT_ERR_NUMERIC;
+    }
+    zero |= s0[n] == 0.0;
+  }
+  out->ptrs.resize(d);
+  for (int n = 0; n < d; ++n) out->ptrs[n] = out->bufs[n].p;
+  out->flags = (capped ? TT_FLAG_RANK_CAPPED : 0) | (fl[1] ? TT_FLAG_QR_FALLBACK : 0);
+  if (zero) {   // sigma_1 = 0 at a bond: the sum is zero (R20, R16)
+    TTR_TRY(make_zero(C, dims, *out));
+    out->flags = TT_FLAG_ZERO | (capped ? TT_FLAG_RANK_CAPPED : 0);
+    TTR_CUDA(cudaStreamSynchronize(s));
+  }
+  out->passes = 1;
+  *outp = out.release();
+  return TT_OK;
+}
+
 // ------------------------------------------------------------------ Alg. 1 + 2
 // Deterministic TT-rounding of the assembled sum (NEXT-1; the
 // baseline the paper compares with), on the same kernels.
@@ -821,7 +1091,7 @@ int deterministic_impl(tt_ctx* c, int S, const tt_view* terms, const tt_round_op
     TTR_TRY(dalloc(B, size_t(k) * r1, s));
     if (!wide) {
       TTR_TRY(dalloc(Uk, size_t(r1) * k, s));
-      TTR_TRY(scale_by_inv_sigma(*c, AV.p, r1, k, sig.p, Uk.p, 1, s));       // U_k
+      TTR_TRY(scale_by_inv_sigma(*c, AV.p, r1, k, sig.p, Uk.p, 2, double(r1) * 0x1p-52, s));       // U_k
       TTR_TRY(gemm1(*c, false, false, int(m), int(k), int(r1), 1.0, Q.p, int(m), Uk.p,
                     int(r1), 0.0, newn.p, int(m), s));                        // line 8: Q U_k
       TTR_TRY(gemm1(*c, true, false, int(k), int(r1), int(r1), 1.0, Uk.p, int(r1), R.p,
@@ -1071,6 +1341,15 @@ int tt_round_sum(tt_ctx_t c, int32_t S_local, const tt_view* terms, const tt_rou
     return TT_ERR_ARG;
   }
   return guarded([&] { return round_sum_impl(c, S_local, terms, opts, sketch, out); });
+}
+
+int tt_round_sum_two_sided(tt_ctx_t c, int32_t S_local, const tt_view* terms, int64_t ell,
+                           int64_t rho, uint64_t seed, tt_tensor_t* out) {
+  if (!c || !out) {
+    set_error("null ctx/out");
+    return TT_ERR_ARG;
+  }
+  return guarded([&] { return two_sided_impl(c, S_local, terms, ell, rho, seed, out); });
 }
 
 int tt_round_deterministic(tt_ctx_t c, int32_t S, const tt_view* terms, const tt_round_opts* opts,

@@ -165,9 +165,10 @@ int svd_jacobi(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, doubl
 int svd_nov(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, double* AV,
             double* sigma, cudaStream_t s);
 bool svd_nov_fits(int64_t m, int64_t n);
-// B(:, c) = AV(:, c) / sigma_c^pw, c < k, pw in {1, 2} (0 for negligible sigma_c)
+// B(:, c) = AV(:, c) / sigma_c^(halfpow/2), c < k; 0 where sigma_c <= rel_thr sigma_0
+// (negligible / pseudo-inverse cutoff)
 int scale_by_inv_sigma(Ctx& c, const double* AV, int64_t m, int64_t k, const double* sigma,
-                       double* B, int pw, cudaStream_t s);
+                       double* B, int halfpow, double rel_thr, cudaStream_t s);
 // k = eps-rank of sigma (n values, descending) given absolute eps and cap rmax
 // (0 = none), written to dst (device int).
 int eps_rank_dev(Ctx& c, const double* sigma, int n, const double* eps_dev, double eps_host,

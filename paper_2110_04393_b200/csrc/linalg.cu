@@ -1296,12 +1296,14 @@ __global__ void __launch_bounds__(kJacThreads)
 // B^T H(X_n) = V_k^T Q^T (pw = 2, see svd_nov) or B = U_k (pw = 1).
 __global__ void scale_by_inv_sigma_kernel(const double* __restrict__ AV, int m, int k,
                                           const double* __restrict__ sigma,
-                                          double* __restrict__ B, int pw) {
+                                          double* __restrict__ B, int halfpow, double rel_thr) {
   const double s0 = sigma[0];
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < m * k; e += gridDim.x * blockDim.x) {
     const int c = e / m;
     const double sc = sigma[c];
-    B[e] = (sc > s0 * double(m) * 0x1p-52) ? AV[e] / (pw == 2 ? sc * sc : sc) : 0.0;
+    double p = (halfpow & 1) ? sqrt(sc) : 1.0;   // sigma^(halfpow/2)
+    for (int h = 0; h < (halfpow >> 1); ++h) p *= sc;
+    B[e] = (sc > s0 * rel_thr) ? AV[e] / p : 0.0;
   }
 }
 
@@ -1391,9 +1393,10 @@ int svd_jacobi(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, doubl
 }
 
 int scale_by_inv_sigma(Ctx& c, const double* AV, int64_t m, int64_t k, const double* sigma,
-                       double* B, int pw, cudaStream_t s) {
+                       double* B, int halfpow, double rel_thr, cudaStream_t s) {
   const int blocks = int(std::min<int64_t>((m * k + 255) / 256, c.sm_count * 4));
-  scale_by_inv_sigma_kernel<<<std::max(1, blocks), 256, 0, s>>>(AV, int(m), int(k), sigma, B, pw);
+  scale_by_inv_sigma_kernel<<<std::max(1, blocks), 256, 0, s>>>(AV, int(m), int(k), sigma, B,
+                                                               halfpow, rel_thr);
   return launched();
 }
 

@@ -40,3 +40,22 @@ def test_caps_match_oracle_rule():
     import oracle
     dims = [4, 4, 4, 4]
     assert cost.caps(dims, [1, 6, 6, 6, 1], 6) == [1] + oracle.rank_caps(dims, [1, 6, 6, 6, 1], 6) + [1]
+
+
+@pytest.mark.parametrize("rho_factor", [1.0, 1.5])
+def test_two_sided_count_matches_paper(rho_factor):
+    """Alg. 6 on one TT: Table 1's (6β + 6β²)(N-2)IR³ for ρ = ℓ and
+    P:944's I(N-2)(7R²ℓ + 8.5Rℓ²) for ρ = 1.5ℓ, to leading order."""
+    N, I, R, ell = 60, 300, 80, 40
+    rho = int(rho_factor * ell)
+    dims = [I] * N
+    tr = [[1] + [R] * (N - 1) + [1]]
+    sumR = [1] + [R] * (N - 1) + [1]
+    f = cost.two_sided_flops(dims, tr, cost.caps(dims, sumR, ell), cost.caps(dims, sumR, rho))
+    if rho_factor == 1.0:
+        beta = ell / R
+        lead = cost.table1_simplified(beta)["two_sided"] * (N - 2) * I * R ** 3
+    else:
+        lead = I * (N - 2) * (7.0 * R * R * ell + 8.5 * R * ell * ell)
+    assert f["total"] / lead == pytest.approx(1.0, abs=0.03)
+    assert cost.paper_two_sided(N, I, R, ell, rho) == pytest.approx(lead, rel=1e-12)

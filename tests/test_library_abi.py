@@ -28,6 +28,7 @@ def lib():
 def test_header_declares_the_boundary_calls():
     f = declared_functions()
     for name in ["tt_sketch_create", "tt_round_sum", "tt_round_deterministic", "tt_inner",
+                 "tt_round_sum_two_sided",
                  "tt_ctx_create", "tt_tensor_info", "tt_last_error"]:
         assert name in f
     assert len(f) >= 20
@@ -55,6 +56,8 @@ def test_argument_errors_without_gpu(lib):
     import paper_2110_04393_b200 as P
     # null ctx / out must fail cleanly with a message, not crash
     rc = lib.tt_round_sum(None, 1, None, None, None, None)
+    assert rc == -1 and b"null" in lib.tt_last_error()
+    rc = lib.tt_round_sum_two_sided(None, 1, None, 4, 0, 1, None)
     assert rc == -1 and b"null" in lib.tt_last_error()
     rc = lib.tt_ctx_create(0, None, None, 2, 1, None)
     assert rc == -1
