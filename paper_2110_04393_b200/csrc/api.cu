@@ -702,9 +702,9 @@ int round_sum_impl(tt_ctx* c, int S, const tt_view* terms, const tt_round_opts* 
 //   R_n = Sigma^{-1/2} U^T W^L_n, L_n = W^R_n V Sigma^{-1/2}   (lines 9-10)
 //   X_n = sum_j Y^(j)_n x1 R^(j)_{n-1} x3 L^(j)_n  (lines 12-16, R19)
 // The SVD of the l x rho matrix P_n: R-only QR of P_n^T, V-free Jacobi of R^T
-// (U Sigma), then V Sigma^{-1/2} = P_n^T (U Sigma) Sigma^{-5/2} and
-// Sigma^{-1/2} U^T = (U Sigma Sigma^{-3/2})^T, pseudo-inverse cutoff
-// sigma_i > max(l, rho) eps sigma_1 (R20).  Every product is a DMMA GEMM; the
+// (U Sigma), Sigma^{-1/2} U^T = (U Sigma Sigma^{-3/2})^T, and V = the Q factor
+// of P_n^T U Sigma^{-1} (columns in descending-sigma order), pseudo-inverse
+// cutoff sigma_i > max(l, rho) eps sigma_1 (R20).  Every product is a DMMA GEMM; the
 // left contraction and the assembly reuse Alg. 7's carry / projection shapes.
 int two_sided_impl(tt_ctx* c, int S, const tt_view* terms, int64_t ell, int64_t rho,
                    uint64_t seed, tt_tensor** outp) {
@@ -762,7 +762,7 @@ int two_sided_impl(tt_ctx* c, int S, const tt_view* terms, int64_t ell, int64_t 
     lr = std::max(lr, size_t(l[n]) * r[n]);
     lmax = std::max<size_t>(lmax, size_t(l[n]));
   }
-  DBuf Xa, WLa, WLb, Ra, Rb, Lf, Pb, Rq, Rt, AV, sig, B3, B5, Tm, Stk, sig0;
+  DBuf Xa, WLa, WLb, Ra, Rb, Lf, Pb, Rq, Rt, AV, sig, B3, B5, Tm, Vq, Stk, sig0;
   TTR_TRY(dalloc(Xa, xmax, s));
   TTR_TRY(dalloc(WLa, lsr, s));
   TTR_TRY(dalloc(WLb, lsr, s));
@@ -777,6 +777,7 @@ int two_sided_impl(tt_ctx* c, int S, const tt_view* terms, int64_t ell, int64_t 
   TTR_TRY(dalloc(B3, lr, s));
   TTR_TRY(dalloc(B5, lmax * lmax, s));
   TTR_TRY(dalloc(Tm, lr, s));
+  TTR_TRY(dalloc(Vq, lr, s));
   TTR_TRY(dalloc(Stk, size_t(sumR[d - 1]) * dims[d - 1], s));
   TTR_TRY(dalloc(sig0, size_t(d), s));
   TTR_TRY(fill_zero(C, sig0.p, d, s));
@@ -838,10 +839,17 @@ int two_sided_impl(tt_ctx* c, int S, const tt_view* terms, int64_t ell, int64_t 
       TTR_TRY(scale_by_inv_sigma(C, AV.p, ln, ln, sig.p, B3.p, 3, rel_thr, s));
       TTR_TRY(gemm1(C, true, false, int(ln), int(Sn), int(ln), 1.0, B3.p, int(ln), WLcur,
                     int(ln), 0.0, Rcur, int(ln), s));
-      // L_n = W^R_n V Sigma^{-1/2} = W^R_n P^T (U Sigma . Sigma^{-5/2})
-      TTR_TRY(scale_by_inv_sigma(C, AV.p, ln, ln, sig.p, B5.p, 5, rel_thr, s));
+      // L_n = W^R_n V Sigma^{-1/2}.  V = P^T U Sigma^{-1} alone loses accuracy in
+      // the columns of small sigma (errors ~ u sigma_1 / sigma_i, all along the
+      // leading directions); those errors are removed by orthogonalising the
+      // columns in descending-sigma order (a QR, signs kept), R20.
+      TTR_TRY(scale_by_inv_sigma(C, AV.p, ln, ln, sig.p, B5.p, 4, rel_thr, s));
       TTR_TRY(gemm1(C, true, false, int(rn), int(ln), int(ln), 1.0, Pb.p, int(ln), B5.p,
                     int(ln), 0.0, Tm.p, int(rn), s));
+      TTR_TRY(unit_cut_columns(C, Tm.p, rn, ln, sig.p, rel_thr, s));
+      TTR_TRY(qr_near_orthonormal(C, rn, ln, Tm.p, rn, Vq.p, s));
+      TTR_TRY(align_column_signs(C, Vq.p, Tm.p, rn, ln, s));
+      TTR_TRY(scale_by_inv_sigma(C, Vq.p, rn, ln, sig.p, Tm.p, 1, rel_thr, s));
     } else {
       // general size: Jacobi of P^T (rho x l) accumulating its rotations:
       // P^T W = (V Sigma), W = U
@@ -918,10 +926,12 @@ int two_sided_impl(tt_ctx* c, int S, const tt_view* terms, int64_t ell, int64_t 
     set_error("QR breakdown in the two-sided bond factorisation");
     return TT_ERR_NUMERIC;
   }
-  bool capped = false, zero = false;
+  // zero sum: a bond matrix P_n = 0 (its Gram has zero trace, status word 2) or
+  // sigma_1 = 0 (R20, R16)
+  bool capped = false, zero = (fl[2] & 1) != 0;
   for (int n = 1; n < d; ++n) {
     capped |= l[n] < ell;
-    if (!std::isfinite(s0[n])) {
+    if (!zero && !std::isfinite(s0[n])) {
       set_error("non-finite singular value at bond %d of the two-sided rounding", n);
       return TT_ERR_NUMERIC;
     }

@@ -169,6 +169,16 @@ bool svd_nov_fits(int64_t m, int64_t n);
 // (negligible / pseudo-inverse cutoff)
 int scale_by_inv_sigma(Ctx& c, const double* AV, int64_t m, int64_t k, const double* sigma,
                        double* B, int halfpow, double rel_thr, cudaStream_t s);
+// Q of an m x n matrix whose columns are already close to orthonormal: one
+// CholeskyQR pass (n <= 160; else qr())
+int qr_near_orthonormal(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, double* Q,
+                        cudaStream_t s);
+// columns c of the m x n matrix A with sigma_c <= rel_thr sigma_0 set to e_c
+int unit_cut_columns(Ctx& c, double* A, int64_t m, int64_t n, const double* sigma,
+                     double rel_thr, cudaStream_t s);
+// Q(:, c) negated where Q(:, c) . ref(:, c) < 0 (m x n, ld m)
+int align_column_signs(Ctx& c, double* Q, const double* ref, int64_t m, int64_t n,
+                       cudaStream_t s);
 // k = eps-rank of sigma (n values, descending) given absolute eps and cap rmax
 // (0 = none), written to dst (device int).
 int eps_rank_dev(Ctx& c, const double* sigma, int n, const double* eps_dev, double eps_host,
@@ -181,7 +191,5 @@ int transpose(Ctx& c, const double* src, int64_t rows, int64_t cols, int64_t lds
 int fill_zero(Ctx& c, double* p, int64_t n, cudaStream_t s);
 // diagonal of the n x n matrix p (ld n) set to 1 (other entries untouched)
 int set_identity(Ctx& c, double* p, int64_t n, cudaStream_t s);
-// dst[i] = (flag && *flag) ? 0 : src? (helper for degenerate cases)
-int max_abs_is_zero(Ctx& c, const double* x, int64_t n, int* flag_dst, cudaStream_t s);
 
 }  // namespace ttr

@@ -1307,6 +1307,39 @@ __global__ void scale_by_inv_sigma_kernel(const double* __restrict__ AV, int m, 
   }
 }
 
+// columns c with sigma_c <= rel_thr sigma_0 (cut by the pseudo-inverse) become e_c,
+// so a QR of the matrix stays full rank and finite (two-sided rounding, R20)
+__global__ void unit_cut_columns_kernel(double* __restrict__ A, int m, int n,
+                                        const double* __restrict__ sigma, double rel_thr) {
+  const double s0 = sigma[0];
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < m * n; e += gridDim.x * blockDim.x) {
+    const int c = e / m, i = e - c * m;
+    if (!(sigma[c] > s0 * rel_thr)) A[e] = (i == c) ? 1.0 : 0.0;
+  }
+}
+
+// Q(:, c) *= sign(Q(:, c) . ref(:, c)): a QR's column signs follow its reference
+// (the Householder fallback's R may have negative diagonal entries)
+__global__ void align_column_signs_kernel(double* __restrict__ Q, const double* __restrict__ ref,
+                                          int m) {
+  __shared__ double red[32];
+  const int c = blockIdx.x;
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < m; i += blockDim.x)
+    acc += Q[int64_t(c) * m + i] * ref[int64_t(c) * m + i];
+  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double v = (threadIdx.x < blockDim.x / 32) ? red[threadIdx.x] : 0.0;
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (threadIdx.x == 0) red[0] = v;
+  }
+  __syncthreads();
+  if (red[0] < 0.0)
+    for (int i = threadIdx.x; i < m; i += blockDim.x) Q[int64_t(c) * m + i] = -Q[int64_t(c) * m + i];
+}
+
 __global__ void eps_rank_kernel(const double* __restrict__ sigma, int n, const double* eps_dev,
                                 double eps_host, int rmax, int* dst) {
   if (threadIdx.x != 0) return;
@@ -1397,6 +1430,36 @@ int scale_by_inv_sigma(Ctx& c, const double* AV, int64_t m, int64_t k, const dou
   const int blocks = int(std::min<int64_t>((m * k + 255) / 256, c.sm_count * 4));
   scale_by_inv_sigma_kernel<<<std::max(1, blocks), 256, 0, s>>>(AV, int(m), int(k), sigma, B,
                                                                halfpow, rel_thr);
+  return launched();
+}
+
+// One CholeskyQR pass, Q only, for inputs whose columns are already close to
+// orthonormal (kappa - 1 small): Q^T Q = I + O(kappa^2 u).  The two-sided
+// rounding's V refinement; n <= 160 (blocked Cholesky), else the routed qr().
+int qr_near_orthonormal(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, double* Q,
+                        cudaStream_t s) {
+  if (n > 160 || m < n) return qr(c, m, n, A, lda, false, Q, nullptr, s);
+  const int ni = int(n), mi = int(m);
+  DBuf Gm, Rinv;
+  TTR_TRY(dalloc(Gm, size_t(n) * n, s));
+  TTR_TRY(dalloc(Rinv, size_t(n) * n, s));
+  TTR_TRY(gemm1(c, true, false, ni, ni, mi, 1.0, A, int(lda), A, int(lda), 0.0, Gm.p, ni, s,
+                nullptr, 0, kGemmLower));
+  TTR_TRY(launch_chol(c, Gm.p, ni, m, CH_RCLAMP, Rinv.p, nullptr, nullptr, nullptr, 0, s));
+  return gemm1(c, false, false, mi, ni, ni, 1.0, A, int(lda), Rinv.p, ni, 0.0, Q, mi, s, nullptr,
+               0, kGemmTriB);
+}
+
+int unit_cut_columns(Ctx& c, double* A, int64_t m, int64_t n, const double* sigma,
+                     double rel_thr, cudaStream_t s) {
+  const int blocks = int(std::min<int64_t>((m * n + 255) / 256, c.sm_count * 4));
+  unit_cut_columns_kernel<<<std::max(1, blocks), 256, 0, s>>>(A, int(m), int(n), sigma, rel_thr);
+  return launched();
+}
+
+int align_column_signs(Ctx& c, double* Q, const double* ref, int64_t m, int64_t n,
+                       cudaStream_t s) {
+  align_column_signs_kernel<<<int(n), 256, 0, s>>>(Q, ref, int(m));
   return launched();
 }
 
