@@ -53,6 +53,47 @@ def sharded_alg7(local_terms, G, allreduce):
     return X
 
 
+def sharded_alg6(local_terms, L, R, allreduce):
+    """Alg. 6 on the sum (R19) with the summands split over ranks, as
+    tt_round_sum_two_sided does: W^L / W^R stay local, P_n = Σ_j W^L_j W^R_j is
+    all-reduced, its SVD is replicated, and every output core X_n = Σ_j (…) is a
+    sum over summands (one all-reduce each)."""
+    N = len(local_terms[0])
+    Lc = [g if g is not None else np.zeros((1, 1, 1)) for g in L]
+    Rc = [g if g is not None else np.zeros((1, 1, 1)) for g in R]
+    WL = [oracle.partial_contractions_lr(Lc, t) for t in local_terms]
+    WR = [oracle.partial_contractions_rl(t, Rc) for t in local_terms]
+    Lb, Rb = {}, {}
+    for n in range(1, N):
+        P = allreduce(sum(WL[j][n] @ WR[j][n] for j in range(len(local_terms))))
+        U, s, Vt = np.linalg.svd(P, full_matrices=False)
+        keep = s > oracle.pinv_rtol(P.shape) * s[0]
+        sih = np.where(keep, 1.0 / np.sqrt(np.where(keep, s, 1.0)), 0.0)
+        Lb[n] = [(WR[j][n] @ Vt.T) * sih[None, :] for j in range(len(local_terms))]
+        Rb[n] = [sih[:, None] * (U.T @ WL[j][n]) for j in range(len(local_terms))]
+    X = [None] * N
+    I1 = local_terms[0][0].shape[1]
+    X[0] = oracle.fold_V(allreduce(sum(oracle.V(t[0]) @ Lb[1][j]
+                                       for j, t in enumerate(local_terms))), I1)
+    for n in range(2, N):
+        I = local_terms[0][n - 1].shape[1]
+        X[n - 1] = allreduce(sum(
+            oracle.fold_H(Rb[n - 1][j] @ oracle.H(oracle.fold_V(oracle.V(t[n - 1]) @ Lb[n][j], I)), I)
+            for j, t in enumerate(local_terms)))
+    IN = local_terms[0][N - 1].shape[1]
+    X[N - 1] = oracle.fold_H(allreduce(sum(Rb[N - 1][j] @ oracle.H(t[N - 1])
+                                           for j, t in enumerate(local_terms))), IN)
+    return X
+
+
+def _sketches_2s(terms, ell):
+    dims = oracle.dims_of(terms[0])
+    sumR = [1] + [sum(t[n].shape[2] for t in terms) for n in range(len(dims) - 1)] + [1]
+    lc, rc = oracle.two_sided_ranks(dims, sumR, ell)
+    return (oracle.gaussian_sketch_left(dims, lc, 2),
+            oracle.gaussian_sketch(dims, rc, 2, tag=oracle.TAG_2S_R))
+
+
 def _worker(rank, world, port, out_q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -70,7 +111,9 @@ def _worker(rank, world, port, out_q):
             return t.numpy()
 
         X = sharded_alg7(terms[lo:hi], G, allreduce)
-        out_q.put((rank, [c.copy() for c in X]))
+        L, R = _sketches_2s(terms, 7)
+        X2 = sharded_alg6(terms[lo:hi], L, R, allreduce)
+        out_q.put((rank, ([c.copy() for c in X], [c.copy() for c in X2])))
     finally:
         dist.destroy_process_group()
 
@@ -84,7 +127,7 @@ def test_shard_bounds_cover_contiguously():
             assert max(h - l for l, h in b) - min(h - l for l, h in b) <= 1
 
 
-def test_sharded_sweep_world2_matches_unsharded_oracle():
+def test_sharded_alg7_and_alg6_world2_match_unsharded_oracle():
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
@@ -102,8 +145,15 @@ def test_sharded_sweep_world2_matches_unsharded_oracle():
     G = oracle.gaussian_sketch(dims, oracle.rank_caps(dims, sumR, 9), seed=1)
     ref = oracle.round_sum_rand_orth(terms, G)
     for r in (0, 1):
-        assert oracle.rel_diff(res[r], ref) <= 1e-12
+        assert oracle.rel_diff(res[r][0], ref) <= 1e-12
     # replicated QR on identical all-reduced inputs: ranks agree bit for bit
-    for a, b in zip(res[0], res[1]):
+    for a, b in zip(res[0][0], res[1][0]):
         assert np.array_equal(a, b)
-    assert oracle.left_orth_residual(res[0]) < 1e-12
+    assert oracle.left_orth_residual(res[0][0]) < 1e-12
+    # Alg. 6 (NEXT-3): sharded == unsharded oracle, identical on both ranks
+    L, R = _sketches_2s(terms, 7)
+    ref2 = oracle.round_sum_two_sided(terms, L, R)
+    for r in (0, 1):
+        assert oracle.rel_diff(res[r][1], ref2) <= 1e-12
+    for a, b in zip(res[0][1], res[1][1]):
+        assert np.array_equal(a, b)
