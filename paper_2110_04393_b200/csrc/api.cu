@@ -755,20 +755,19 @@ int two_sided_impl(tt_ctx* c, int S, const tt_view* terms, int64_t ell, int64_t 
   tm.end(1);
 
   size_t xmax = 1, lsr = 1, lr = 1, lmax = 1;
-  for (int n = 1; n <= d; ++n)
-    xmax = std::max(xmax, size_t(n == 1 ? 1 : l[n - 1]) * dims[n - 1] * sumR[n == d ? d - 1 : n]);
+  for (int n = 2; n < d; ++n)
+    xmax = std::max(xmax, size_t(l[n - 1]) * dims[n - 1] * sumR[n]);
   for (int n = 1; n < d; ++n) {
     lsr = std::max(lsr, size_t(l[n]) * sumR[n]);
     lr = std::max(lr, size_t(l[n]) * r[n]);
     lmax = std::max<size_t>(lmax, size_t(l[n]));
   }
-  DBuf Xa, WLa, WLb, Ra, Rb, Lf, Pb, Rq, Rt, AV, sig, B3, B5, Tm, Vq, Stk, sig0;
+  DBuf Xa, X1c, WLb[2], Rb[3], Lb[2], Pb, Rq, Rt, AV, sig, B3, B5, Tm, Vq, Stk, sig0;
   TTR_TRY(dalloc(Xa, xmax, s));
-  TTR_TRY(dalloc(WLa, lsr, s));
-  TTR_TRY(dalloc(WLb, lsr, s));
-  TTR_TRY(dalloc(Ra, lsr, s));
-  TTR_TRY(dalloc(Rb, lsr, s));
-  TTR_TRY(dalloc(Lf, lsr, s));
+  TTR_TRY(dalloc(X1c, size_t(dims[0]) * sumR[1], s));
+  for (auto& b : WLb) TTR_TRY(dalloc(b, lsr, s));
+  for (auto& b : Rb) TTR_TRY(dalloc(b, lsr, s));
+  for (auto& b : Lb) TTR_TRY(dalloc(b, lsr, s));
   TTR_TRY(dalloc(Pb, lr, s));
   TTR_TRY(dalloc(Rq, lmax * lmax, s));
   TTR_TRY(dalloc(Rt, lmax * lmax, s));
@@ -791,6 +790,45 @@ int two_sided_impl(tt_ctx* c, int S, const tt_view* terms, int64_t ell, int64_t 
   for (int n = 1; n <= d; ++n)
     TTR_TRY(dalloc(out->bufs[n - 1], size_t(l[n - 1]) * dims[n - 1] * l[n], s));
 
+  // The bond factorisations (lines 7-10; latency-bound QR + Jacobi) are
+  // independent of one another once W^L_n and W^R_n exist: on one GPU they run on
+  // a side stream with its own GEMM workspace, overlapped with the left
+  // contraction and the assembly on the main stream.  With NCCL in the loop
+  // (world > 1) everything stays on the main stream (the collectives of one
+  // communicator must not be issued from two streams).
+  const bool overlap = C.world == 1 && d > 2;
+  Ctx side;
+  struct SideGuard {
+    Ctx& x;
+    std::vector<cudaEvent_t> ev;
+    ~SideGuard() {
+      if (x.stream) cudaStreamSynchronize(x.stream);
+      x.gemm_ws.release();
+      x.flags.p = nullptr;   // borrowed from the main context
+      if (x.stream) cudaStreamDestroy(x.stream);
+      x.stream = nullptr;
+      for (auto e : ev) cudaEventDestroy(e);
+    }
+  } guard{side, {}};
+  if (overlap) {
+    side.device = C.device;
+    side.sm_count = C.sm_count;
+    side.copy_stream = C.copy_stream;
+    side.flags.p = C.flags.p;
+    side.flags.s = nullptr;
+    side.nflags = C.nflags;
+    TTR_CUDA(cudaStreamCreateWithFlags(&side.stream, cudaStreamNonBlocking));
+  }
+  Ctx& B = overlap ? side : C;
+  cudaStream_t ss = overlap ? side.stream : s;
+  std::vector<cudaEvent_t> eWL(d + 1), eF(d + 1);
+  for (int n = 0; n <= d; ++n) {
+    TTR_CUDA(cudaEventCreateWithFlags(&eWL[n], cudaEventDisableTiming));
+    guard.ev.push_back(eWL[n]);
+    TTR_CUDA(cudaEventCreateWithFlags(&eF[n], cudaEventDisableTiming));
+    guard.ev.push_back(eF[n]);
+  }
+
   std::vector<GemmDesc> gd(S);
   // [A^(j) H(Y^(j)_n)]_j for an lrows x sumR_{n-1} block row A (ld lrows), written
   // side by side along the right rank: dst is lrows x I_n x sumR_n (n 1-based)
@@ -802,102 +840,123 @@ int two_sided_impl(tt_ctx* c, int S, const tt_view* terms, int64_t ell, int64_t 
                        int(T.R[j][n - 1]), int(lrows), int(T.R[j][n - 1]), int(lrows)};
     return gemm(C, false, false, gd.data(), S, 1.0, 0.0, s);
   };
-  const double rel_thr_base = 0x1p-52;
-  double* WLcur = WLa.p;
-  double* WLnext = WLb.p;
-  double* Rprev = Ra.p;
-  double* Rcur = Rb.p;
-  // X_1 = [Y^(1)_1 ... Y^(s)_1] (I_1 x sumR_1), then line 4 at n = 1: W^L_1 = V(L_1)^T X_1
-  TTR_TRY(wait_core(C, T, 0));
-  for (int j = 0; j < S; ++j)
-    TTR_CUDA(cudaMemcpyAsync(Xa.p + dims[0] * off[1][j], T.core[j][0],
-                             sizeof(double) * dims[0] * T.R[j][1], cudaMemcpyDeviceToDevice, s));
-  tm.begin(2);
-  TTR_TRY(gemm1(C, true, false, int(l[1]), int(sumR[1]), int(dims[0]), 1.0, skL.cores[0].p,
-                int(dims[0]), Xa.p, int(dims[0]), 0.0, WLcur, int(l[1]), s));
-  tm.end(2);
-  for (int n = 1; n <= d - 1; ++n) {
+  // ---- lines 7-10 for bond n, on context X / stream st
+  auto bond = [&](int n, Ctx& X, cudaStream_t st) -> int {
     const int64_t ln = l[n], rn = r[n], Sn = sumR[n];
+    const double* WLn = WLb[n % 2].p;
     const double* WRn = WR.p + woff[n];   // sumR_n x rho_n (ld sumR_n)
-    // ---- lines 7-10 for bond n
-    tm.begin(5);
-    TTR_TRY(gemm1(C, false, false, int(ln), int(rn), int(Sn), 1.0, WLcur, int(ln), WRn, int(Sn),
-                  0.0, Pb.p, int(ln), s));   // P_n = W^L_n W^R_n
-    tm.end(5);
-    tm.begin(4);
-    TTR_TRY(allreduce_sum(C, Pb.p, size_t(ln) * rn));
-    tm.end(4);
-    tm.begin(3);
-    const double rel_thr = double(std::max(ln, rn)) * rel_thr_base;
+    double* Rout = Rb[n % 3].p;
+    double* Lout = Lb[n % 2].p;
+    if (!overlap) tm.begin(5);
+    TTR_TRY(gemm1(X, false, false, int(ln), int(rn), int(Sn), 1.0, WLn, int(ln), WRn, int(Sn),
+                  0.0, Pb.p, int(ln), st));   // P_n = W^L_n W^R_n
+    if (!overlap) {
+      tm.end(5);
+      tm.begin(4);
+      TTR_TRY(allreduce_sum(C, Pb.p, size_t(ln) * rn));
+      tm.end(4);
+      tm.begin(3);
+    }
+    const double rel_thr = double(std::max(ln, rn)) * 0x1p-52;
     if (svd_nov_fits(ln, ln)) {
-      TTR_TRY(qr(C, rn, ln, Pb.p, ln, true, nullptr, Rq.p, s));   // P^T = Q R
-      TTR_TRY(transpose(C, Rq.p, ln, ln, ln, Rt.p, ln, s));
-      TTR_TRY(svd_nov(C, ln, ln, Rt.p, ln, AV.p, sig.p, s));       // R^T = U Sigma W^T
-      tm.end(3);
-      tm.begin(5);
+      TTR_TRY(qr(X, rn, ln, Pb.p, ln, true, nullptr, Rq.p, st));   // P^T = Q R
+      TTR_TRY(transpose(X, Rq.p, ln, ln, ln, Rt.p, ln, st));
+      TTR_TRY(svd_nov(X, ln, ln, Rt.p, ln, AV.p, sig.p, st));       // R^T = U Sigma W^T
+      if (!overlap) {
+        tm.end(3);
+        tm.begin(5);
+      }
       // R_n = Sigma^{-1/2} U^T W^L_n = (U Sigma . Sigma^{-3/2})^T W^L_n
-      TTR_TRY(scale_by_inv_sigma(C, AV.p, ln, ln, sig.p, B3.p, 3, rel_thr, s));
-      TTR_TRY(gemm1(C, true, false, int(ln), int(Sn), int(ln), 1.0, B3.p, int(ln), WLcur,
-                    int(ln), 0.0, Rcur, int(ln), s));
+      TTR_TRY(scale_by_inv_sigma(X, AV.p, ln, ln, sig.p, B3.p, 3, rel_thr, st));
+      TTR_TRY(gemm1(X, true, false, int(ln), int(Sn), int(ln), 1.0, B3.p, int(ln), WLn,
+                    int(ln), 0.0, Rout, int(ln), st));
       // L_n = W^R_n V Sigma^{-1/2}.  V = P^T U Sigma^{-1} alone loses accuracy in
       // the columns of small sigma (errors ~ u sigma_1 / sigma_i, all along the
       // leading directions); those errors are removed by orthogonalising the
       // columns in descending-sigma order (a QR, signs kept), R20.
-      TTR_TRY(scale_by_inv_sigma(C, AV.p, ln, ln, sig.p, B5.p, 4, rel_thr, s));
-      TTR_TRY(gemm1(C, true, false, int(rn), int(ln), int(ln), 1.0, Pb.p, int(ln), B5.p,
-                    int(ln), 0.0, Tm.p, int(rn), s));
-      TTR_TRY(unit_cut_columns(C, Tm.p, rn, ln, sig.p, rel_thr, s));
-      TTR_TRY(qr_near_orthonormal(C, rn, ln, Tm.p, rn, Vq.p, s));
-      TTR_TRY(align_column_signs(C, Vq.p, Tm.p, rn, ln, s));
-      TTR_TRY(scale_by_inv_sigma(C, Vq.p, rn, ln, sig.p, Tm.p, 1, rel_thr, s));
+      TTR_TRY(scale_by_inv_sigma(X, AV.p, ln, ln, sig.p, B5.p, 4, rel_thr, st));
+      TTR_TRY(gemm1(X, true, false, int(rn), int(ln), int(ln), 1.0, Pb.p, int(ln), B5.p,
+                    int(ln), 0.0, Tm.p, int(rn), st));
+      TTR_TRY(unit_cut_columns(X, Tm.p, rn, ln, sig.p, rel_thr, st));
+      TTR_TRY(qr_near_orthonormal(X, rn, ln, Tm.p, rn, Vq.p, st));
+      TTR_TRY(align_column_signs(X, Vq.p, Tm.p, rn, ln, st));
+      TTR_TRY(scale_by_inv_sigma(X, Vq.p, rn, ln, sig.p, Tm.p, 1, rel_thr, st));
     } else {
       // general size: Jacobi of P^T (rho x l) accumulating its rotations:
       // P^T W = (V Sigma), W = U
-      TTR_TRY(transpose(C, Pb.p, ln, rn, ln, Tm.p, rn, s));
+      TTR_TRY(transpose(X, Pb.p, ln, rn, ln, Tm.p, rn, st));
       DBuf Wj;
-      TTR_TRY(dalloc(Wj, size_t(ln) * ln, s));
-      TTR_TRY(svd_jacobi(C, rn, ln, Tm.p, rn, AV.p, Wj.p, sig.p, s));
-      tm.end(3);
-      tm.begin(5);
-      TTR_TRY(scale_by_inv_sigma(C, Wj.p, ln, ln, sig.p, B3.p, 1, rel_thr, s));
-      TTR_TRY(gemm1(C, true, false, int(ln), int(Sn), int(ln), 1.0, B3.p, int(ln), WLcur,
-                    int(ln), 0.0, Rcur, int(ln), s));
-      TTR_TRY(scale_by_inv_sigma(C, AV.p, rn, ln, sig.p, Tm.p, 3, rel_thr, s));
+      TTR_TRY(dalloc(Wj, size_t(ln) * ln, st));
+      TTR_TRY(svd_jacobi(X, rn, ln, Tm.p, rn, AV.p, Wj.p, sig.p, st));
+      if (!overlap) {
+        tm.end(3);
+        tm.begin(5);
+      }
+      TTR_TRY(scale_by_inv_sigma(X, Wj.p, ln, ln, sig.p, B3.p, 1, rel_thr, st));
+      TTR_TRY(gemm1(X, true, false, int(ln), int(Sn), int(ln), 1.0, B3.p, int(ln), WLn,
+                    int(ln), 0.0, Rout, int(ln), st));
+      TTR_TRY(scale_by_inv_sigma(X, AV.p, rn, ln, sig.p, Tm.p, 3, rel_thr, st));
     }
-    TTR_TRY(gemm1(C, false, false, int(Sn), int(ln), int(rn), 1.0, WRn, int(Sn), Tm.p, int(rn),
-                  0.0, Lf.p, int(Sn), s));
-    TTR_CUDA(cudaMemcpyAsync(sig0.p + n, sig.p, sizeof(double), cudaMemcpyDeviceToDevice, s));
-    tm.end(5);
-    // ---- lines 12-15: X_n = sum_j Y^(j)_n x1 R^(j)_{n-1} x3 L^(j)_n
+    TTR_TRY(gemm1(X, false, false, int(Sn), int(ln), int(rn), 1.0, WRn, int(Sn), Tm.p, int(rn),
+                  0.0, Lout, int(Sn), st));
+    TTR_CUDA(cudaMemcpyAsync(sig0.p + n, sig.p, sizeof(double), cudaMemcpyDeviceToDevice, st));
+    if (!overlap) tm.end(5);
+    return TT_OK;
+  };
+  // ---- lines 12-15: X_n = sum_j Y^(j)_n x1 R^(j)_{n-1} x3 L^(j)_n (main stream)
+  auto assemble = [&](int n) -> int {
+    const int64_t In = dims[n - 1], ln = l[n], Sn = sumR[n];
     tm.begin(2);
-    const int64_t In = dims[n - 1];
     if (n == 1) {
-      // X_1 = [Y^(j)_1]_j L_1   (Xa still holds the concatenated first cores)
-      TTR_TRY(gemm1(C, false, false, int(In), int(ln), int(Sn), 1.0, Xa.p, int(In), Lf.p,
-                    int(Sn), 0.0, out->bufs[0].p, int(In), s));
+      TTR_TRY(gemm1(C, false, false, int(In), int(ln), int(Sn), 1.0, X1c.p, int(In),
+                    Lb[1].p, int(Sn), 0.0, out->bufs[0].p, int(In), s));
     } else {
-      TTR_TRY(carry(Rprev, l[n - 1], n, Xa.p));   // [R^(j)_{n-1} H(Y^(j)_n)]_j
+      TTR_TRY(carry(Rb[(n - 1) % 3].p, l[n - 1], n, Xa.p));   // [R^(j)_{n-1} H(Y^(j)_n)]_j
       const int64_t m = l[n - 1] * In;
-      TTR_TRY(gemm1(C, false, false, int(m), int(ln), int(Sn), 1.0, Xa.p, int(m), Lf.p, int(Sn),
-                    0.0, out->bufs[n - 1].p, int(m), s));
+      TTR_TRY(gemm1(C, false, false, int(m), int(ln), int(Sn), 1.0, Xa.p, int(m),
+                    Lb[n % 2].p, int(Sn), 0.0, out->bufs[n - 1].p, int(m), s));
     }
     tm.end(2);
     tm.begin(4);
     TTR_TRY(allreduce_sum(C, out->bufs[n - 1].p, size_t(l[n - 1]) * In * ln));
     tm.end(4);
-    // ---- line 4 at n + 1: W^L_{n+1} = V(L_{n+1})^T V([W^L(j)_n H(Y^(j)_{n+1})]_j)
+    return TT_OK;
+  };
+
+  // X_1 = [Y^(1)_1 ... Y^(s)_1] (I_1 x sumR_1); line 4 at n = 1: W^L_1 = V(L_1)^T X_1
+  TTR_TRY(wait_core(C, T, 0));
+  for (int j = 0; j < S; ++j)
+    TTR_CUDA(cudaMemcpyAsync(X1c.p + dims[0] * off[1][j], T.core[j][0],
+                             sizeof(double) * dims[0] * T.R[j][1], cudaMemcpyDeviceToDevice, s));
+  tm.begin(2);
+  TTR_TRY(gemm1(C, true, false, int(l[1]), int(sumR[1]), int(dims[0]), 1.0, skL.cores[0].p,
+                int(dims[0]), X1c.p, int(dims[0]), 0.0, WLb[1].p, int(l[1]), s));
+  tm.end(2);
+  TTR_CUDA(cudaEventRecord(eWL[1], s));
+  for (int n = 1; n <= d - 1; ++n) {
+    // side: bond n once W^L_n exists
+    TTR_CUDA(cudaStreamWaitEvent(ss, eWL[n], 0));
+    TTR_TRY(bond(n, B, ss));
+    TTR_CUDA(cudaEventRecord(eF[n], ss));
+    // main: X_{n-1} (needs bond n-1), then W^L_{n+1} into the slot of W^L_{n-1}
+    if (n >= 2) {
+      TTR_CUDA(cudaStreamWaitEvent(s, eF[n - 1], 0));
+      TTR_TRY(assemble(n - 1));
+    }
     if (n + 1 <= d - 1) {
       tm.begin(2);
       TTR_TRY(wait_core(C, T, n));
-      TTR_TRY(carry(WLcur, ln, n + 1, Xa.p));
-      const int64_t m1 = ln * dims[n];
+      TTR_TRY(carry(WLb[n % 2].p, l[n], n + 1, Xa.p));
+      const int64_t m1 = l[n] * dims[n];
       TTR_TRY(gemm1(C, true, false, int(l[n + 1]), int(sumR[n + 1]), int(m1), 1.0,
-                    skL.cores[n].p, int(m1), Xa.p, int(m1), 0.0, WLnext, int(l[n + 1]), s));
+                    skL.cores[n].p, int(m1), Xa.p, int(m1), 0.0, WLb[(n + 1) % 2].p,
+                    int(l[n + 1]), s));
       tm.end(2);
-      std::swap(WLcur, WLnext);
+      TTR_CUDA(cudaEventRecord(eWL[n + 1], s));
     }
-    std::swap(Rprev, Rcur);
   }
+  TTR_CUDA(cudaStreamWaitEvent(s, eF[d - 1], 0));
+  TTR_TRY(assemble(d - 1));
   // ---- line 16: X_N = sum_j R^(j)_{N-1} H(Y^(j)_N) = [R^(j)_{N-1}]_j [H(Y^(j)_N); ...]
   {
     tm.begin(2);
@@ -907,9 +966,9 @@ int two_sided_impl(tt_ctx* c, int S, const tt_view* terms, int64_t ell, int64_t 
                                  T.core[j][d - 1], sizeof(double) * T.R[j][d - 1],
                                  sizeof(double) * T.R[j][d - 1], Id, cudaMemcpyDeviceToDevice,
                                  s));
-    TTR_TRY(gemm1(C, false, false, int(l[d - 1]), int(Id), int(sumR[d - 1]), 1.0, Rprev,
-                  int(l[d - 1]), Stk.p, int(sumR[d - 1]), 0.0, out->bufs[d - 1].p,
-                  int(l[d - 1]), s));
+    TTR_TRY(gemm1(C, false, false, int(l[d - 1]), int(Id), int(sumR[d - 1]), 1.0,
+                  Rb[(d - 1) % 3].p, int(l[d - 1]), Stk.p, int(sumR[d - 1]), 0.0,
+                  out->bufs[d - 1].p, int(l[d - 1]), s));
     tm.end(2);
     tm.begin(4);
     TTR_TRY(allreduce_sum(C, out->bufs[d - 1].p, size_t(l[d - 1]) * Id));
