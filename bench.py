@@ -199,7 +199,7 @@ def main():
     ap.add_argument("--batch", type=int, default=1,
                     help="B independent roundings per step (distinct sketch seeds), spread "
                          "over --streams contexts (SURVEY 8d batched throughput of C1/C2)")
-    ap.add_argument("--streams", type=int, default=8)
+    ap.add_argument("--streams", type=int, default=1)
     ap.add_argument("--algo", default="rand_orth", choices=["rand_orth", "two_sided"],
                     help="rand_orth: tt_round_sum (Alg. 7 + truncation, the headline); "
                          "two_sided: tt_round_sum_two_sided (Alg. 6)")

@@ -179,6 +179,9 @@ int tt_tensor_info(tt_tensor_t t, int32_t* d, const int64_t** dims,
 int tt_tensor_copy_core(tt_tensor_t t, int32_t n, double* dst);
 /* Number of rounding passes the adaptive loop made (1 if not adaptive). */
 int tt_tensor_passes(tt_tensor_t t, int32_t* passes);
+/* Frees a result: stream-ordered on the creating context's stream (no host
+ * synchronisation) while that context lives, else after a device-wide sync.
+ * Work reading the cores on OTHER streams must be complete before the call. */
 int tt_tensor_destroy(tt_tensor_t t);
 
 /* ---- diagnostics --------------------------------------------------------- */

@@ -16,6 +16,10 @@ namespace ttr {
 std::atomic<uint64_t> g_launches{0};
 
 static thread_local std::string t_err;
+std::mutex& init_mutex() {
+  static std::mutex m;
+  return m;
+}
 
 void set_error(const char* fmt, ...) {
   char buf[1024];
@@ -68,6 +72,8 @@ using namespace ttr;
 struct tt_ctx : Ctx {};
 
 struct tt_sketch {
+  std::shared_ptr<std::atomic<bool>> alive;   // of the creating context
+  cudaStream_t stream = nullptr;
   int d = 0;
   std::vector<int64_t> dims, ranks;
   uint64_t seed = 0;
@@ -83,6 +89,7 @@ struct tt_tensor {
   uint32_t flags = 0;
   int passes = 1;
   cudaStream_t stream = nullptr;
+  std::shared_ptr<std::atomic<bool>> alive;   // of the creating context
 };
 
 namespace {
@@ -609,6 +616,7 @@ int round_sum_impl(tt_ctx* c, int S, const tt_view* terms, const tt_round_opts* 
 
   std::unique_ptr<tt_tensor> out(new tt_tensor);
   out->stream = c->stream;
+  out->alive = c->alive;
   int64_t cur = ell;
   int passes = 0;
   for (;;) {
@@ -628,6 +636,7 @@ int round_sum_impl(tt_ctx* c, int S, const tt_view* terms, const tt_round_opts* 
     }
     tt_tensor X;
     X.stream = c->stream;
+    X.alive = c->alive;
     TTR_TRY(alg7(*c, T, dims, l, *sk, X, tm));
     ++passes;
     bool capped = false;
@@ -783,6 +792,7 @@ int two_sided_impl(tt_ctx* c, int S, const tt_view* terms, int64_t ell, int64_t 
 
   std::unique_ptr<tt_tensor> out(new tt_tensor);
   out->stream = s;
+  out->alive = C.alive;
   out->d = d;
   out->dims = dims;
   out->ranks = l;
@@ -1053,6 +1063,7 @@ int deterministic_impl(tt_ctx* c, int S, const tt_view* terms, const tt_round_op
     for (int j = 0; j < S; ++j) r[n] += T.R[j][n];
   std::unique_ptr<tt_tensor> X(new tt_tensor);
   X->stream = s;
+  X->alive = c->alive;
   X->d = d;
   X->dims = dims;
   X->ranks = r;
@@ -1325,6 +1336,7 @@ int tt_ctx_destroy(tt_ctx_t c) {
   if (!c) return TT_OK;
   return guarded([&]() -> int {
     cudaSetDevice(c->device);
+    c->alive->store(false);
     cudaStreamSynchronize(c->stream);
     nccl_comm_destroy(*c);
     c->gemm_ws.release();
@@ -1380,6 +1392,8 @@ int tt_sketch_create(tt_ctx_t c, int32_t d, const int64_t* dims, const int64_t* 
     std::unique_ptr<tt_sketch> sk(new tt_sketch);
     std::vector<int64_t> dv(dims, dims + d), rv(ranks, ranks + d + 1);
     TTR_TRY(make_sketch(*c, dv, rv, seed, tag, *sk));
+    sk->alive = c->alive;
+    sk->stream = c->stream;
     TTR_CUDA(cudaStreamSynchronize(c->stream));
     *out = sk.release();
     return TT_OK;
@@ -1397,9 +1411,11 @@ int tt_sketch_core(tt_sketch_t sk, int32_t n, const double** core) {
 
 int tt_sketch_destroy(tt_sketch_t sk) {
   if (!sk) return TT_OK;
-  cudaDeviceSynchronize();
-  for (auto& b : sk->cores) b.s = nullptr;   // the creating stream may be gone
-  delete sk;
+  if (!(sk->alive && sk->alive->load())) {   // the creating stream is gone
+    cudaDeviceSynchronize();
+    for (auto& b : sk->cores) b.s = nullptr;
+  }
+  delete sk;   // else stream-ordered frees on the creating context's stream
   return TT_OK;
 }
 
@@ -1472,9 +1488,11 @@ int tt_tensor_passes(tt_tensor_t t, int32_t* passes) {
 
 int tt_tensor_destroy(tt_tensor_t t) {
   if (!t) return TT_OK;
-  cudaDeviceSynchronize();
-  for (auto& b : t->bufs) b.s = nullptr;     // the creating stream may be gone
-  delete t;
+  if (!(t->alive && t->alive->load())) {     // the creating stream is gone
+    cudaDeviceSynchronize();
+    for (auto& b : t->bufs) b.s = nullptr;
+  }
+  delete t;   // else stream-ordered frees on the creating context's stream (no host sync)
   return TT_OK;
 }
 

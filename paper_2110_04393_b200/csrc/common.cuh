@@ -6,12 +6,18 @@
 
 #include <atomic>
 #include <cstdio>
+#include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
 #include "../../include/ttround.h"
 
 namespace ttr {
+
+// guards the one-time kernel attribute setup (calls may come from several host
+// threads, one context each)
+std::mutex& init_mutex();
 
 // ---------------------------------------------------------------- errors
 void set_error(const char* fmt, ...);
@@ -109,6 +115,9 @@ struct Ctx {
   // device status words, see linalg.cu (route flags 0/4/5, sticky 1-3, counters 8-13)
   IBuf flags;
   int nflags = 0;
+  // false once the context (and its stream) is destroyed: results and sketches
+  // created on it then free their memory after a device-wide synchronisation
+  std::shared_ptr<std::atomic<bool>> alive = std::make_shared<std::atomic<bool>>(true);
 };
 
 int allreduce_sum(Ctx& c, double* buf, size_t n);   // in place, fp64 sum on c.stream

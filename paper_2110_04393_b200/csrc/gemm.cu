@@ -320,9 +320,11 @@ template <class S, bool TA, bool TB>
 int launch_cfg(Ctx& c, GemmParams& P, int maxM, int maxN, int maxK, cudaStream_t s) {
   using C = Cfg<S::bm, S::bn, S::bk, S::wm, S::wn, S::st, TA, TB>;
   auto kern = dgemm_kernel<S::bm, S::bn, S::bk, S::wm, S::wn, S::st, TA, TB>;
-  static bool attr_set[64] = {false};
+  static std::atomic<bool> attr_set[64];
   static int resident[64] = {0};   // CTAs of this configuration per SM
   int dev = c.device;
+  std::unique_lock<std::mutex> init_lock(init_mutex(), std::defer_lock);
+  if (!attr_set[dev & 63]) init_lock.lock();   // first calls may come from several threads
   if (!attr_set[dev & 63]) {
     TTR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   int(C::SMEM)));

@@ -939,7 +939,9 @@ static int tsqr_r(Ctx& c, int64_t m, int n, const double* A, int64_t lda, bool t
   DBuf W0, W1;
   TTR_TRY(dalloc(W0, size_t(P * tri), s));
   TTR_TRY(dalloc(W1, size_t((P + 1) / 2 * tri), s));
-  static bool attr = false;
+  static std::atomic<bool> attr{false};
+  std::unique_lock<std::mutex> init_lock(init_mutex(), std::defer_lock);
+  if (!attr) init_lock.lock();
   if (!attr) {
     TTR_CUDA(cudaFuncSetAttribute(tsqr_leaf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   kSmemLimitDoubles * 8));
@@ -971,7 +973,9 @@ bool tsqr_fits(int n) { return n >= 1 && 2 * (int64_t(n) * (n + 1) / 2) <= kSmem
 // Launch one Cholesky(+inverse) of the n x n Gram Gm (see chol_blk_kernel).
 static int launch_chol(Ctx& c, const double* Gm, int n, int64_t m, int mode, double* Rinv,
                        double* Rk, double* gw, const int* gate, int gv, cudaStream_t s) {
-  static bool attr_done = false;
+  static std::atomic<bool> attr_done{false};
+  std::unique_lock<std::mutex> init_lock(init_mutex(), std::defer_lock);
+  if (!attr_done) init_lock.lock();
   if (!attr_done) {
     TTR_CUDA(cudaFuncSetAttribute(chol_inv_kernel<32>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1402,7 +1406,9 @@ int svd_jacobi(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, doubl
               (long long)n);
     return TT_ERR_ARG;
   }
-  static bool attr = false;
+  static std::atomic<bool> attr{false};
+  std::unique_lock<std::mutex> init_lock(init_mutex(), std::defer_lock);
+  if (!attr) init_lock.lock();
   if (!attr) {
     TTR_CUDA(cudaFuncSetAttribute(jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   kSmemLimitDoubles * 8));

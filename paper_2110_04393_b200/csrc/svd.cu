@@ -165,8 +165,10 @@ __global__ void __launch_bounds__(32 * RPT) __maxnreg__(RPT >= 18 ? 96 : 128)
 template <int RPT>
 int launch_rr(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, double* AV,
               double* sigma, cudaStream_t s) {
-  static bool attr[64] = {false};
+  static std::atomic<bool> attr[64];
   const size_t shm = size_t(n) * 8 * RPT * sizeof(double);
+  std::unique_lock<std::mutex> init_lock(init_mutex(), std::defer_lock);
+  if (!attr[c.device & 63]) init_lock.lock();
   if (!attr[c.device & 63]) {
     TTR_CUDA(cudaFuncSetAttribute(jacobi_rr_kernel<RPT>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 222 * 1024));
@@ -519,8 +521,10 @@ bool svd_cluster_fits(int64_t m, int64_t n) {
 
 int svd_nov_cluster(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, double* AV,
                     double* sigma, cudaStream_t s) {
-  static bool attr[64] = {false};
+  static std::atomic<bool> attr[64];
   const size_t shm = sizeof(JcShared);
+  std::unique_lock<std::mutex> init_lock(init_mutex(), std::defer_lock);
+  if (!attr[c.device & 63]) init_lock.lock();
   if (!attr[c.device & 63]) {
     TTR_CUDA(cudaFuncSetAttribute(jacobi_cluster_kernel,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, int(shm)));

@@ -11,4 +11,7 @@ timeout 900 ncu --set full --clock-control none --import-source on --kernel-name
 for w in tiny single sum10 gmres; do timeout 300 python bench.py --workload $w --steps 5 --warmup 3 --no-cpu > gpurun_out/bench_$w.log 2>&1; done
 timeout 300 python bench.py --workload tiny --batch 256 --steps 3 --warmup 3 > gpurun_out/bench_tiny_batch.log 2>&1
 timeout 300 python bench.py --workload single --batch 64 --steps 3 --warmup 3 > gpurun_out/bench_single_batch.log 2>&1
+timeout 600 python bench.py --algo two_sided --no-cpu > gpurun_out/bench_large_two_sided.log 2>&1; echo "bench 2s rc=$?"
+timeout 600 python bench.py --algo two_sided --steps 2 --warmup 3 --no-cpu --no-e2e > gpurun_out/bench_plain_2s.log 2>&1 && \
+timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none -c 100000 --csv --log-file gpurun_out/launches_bench_2s.csv python bench.py --algo two_sided --steps 2 --warmup 3 --no-cpu --no-e2e > gpurun_out/ncu_bench_2s.log 2>&1; echo "ncu 2s launches rc=$?"
 timeout 120 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
