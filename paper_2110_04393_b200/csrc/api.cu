@@ -789,6 +789,11 @@ int two_sided_impl(tt_ctx* c, int S, const tt_view* terms, int64_t ell, int64_t 
   TTR_TRY(dalloc(Stk, size_t(sumR[d - 1]) * dims[d - 1], s));
   TTR_TRY(dalloc(sig0, size_t(d), s));
   TTR_TRY(fill_zero(C, sig0.p, d, s));
+  DBuf pssq, ppart;
+  IBuf pexp;
+  TTR_TRY(dalloc(pssq, 1, s));
+  TTR_TRY(dalloc(ppart, 256, s));
+  TTR_TRY(ialloc(pexp, size_t(d), s));
 
   std::unique_ptr<tt_tensor> out(new tt_tensor);
   out->stream = s;
@@ -827,7 +832,11 @@ int two_sided_impl(tt_ctx* c, int S, const tt_view* terms, int64_t ell, int64_t 
     side.flags.p = C.flags.p;
     side.flags.s = nullptr;
     side.nflags = C.nflags;
-    TTR_CUDA(cudaStreamCreateWithFlags(&side.stream, cudaStreamNonBlocking));
+    // highest priority: the latency-bound chain's CTAs (one-CTA Cholesky, 8-CTA
+    // Jacobi cluster) take SMs as the main stream's GEMM CTAs retire
+    int lo_pri = 0, hi_pri = 0;
+    TTR_CUDA(cudaDeviceGetStreamPriorityRange(&lo_pri, &hi_pri));
+    TTR_CUDA(cudaStreamCreateWithPriority(&side.stream, cudaStreamNonBlocking, hi_pri));
   }
   Ctx& B = overlap ? side : C;
   cudaStream_t ss = overlap ? side.stream : s;
@@ -867,6 +876,10 @@ int two_sided_impl(tt_ctx* c, int S, const tt_view* terms, int64_t ell, int64_t 
       tm.end(4);
       tm.begin(3);
     }
+    // P_n <- 2^{-e} P_n with ||P_n|| in [1, 4): the sketch contractions give
+    // P_n ~ a^n b^{N-n} (C5: ~1e-80), and the Jacobi's squared column norms /
+    // d^2 + e^2 would underflow; 2^{-e} is folded back into R_n below (exact)
+    TTR_TRY(normalize_pow2(X, Pb.p, ln * rn, pssq.p, ppart.p, pexp.p + n, st));
     const double rel_thr = double(std::max(ln, rn)) * 0x1p-52;
     if (svd_nov_fits(ln, ln)) {
       TTR_TRY(qr(X, rn, ln, Pb.p, ln, true, nullptr, Rq.p, st));   // P^T = Q R
@@ -909,6 +922,8 @@ int two_sided_impl(tt_ctx* c, int S, const tt_view* terms, int64_t ell, int64_t 
     }
     TTR_TRY(gemm1(X, false, false, int(Sn), int(ln), int(rn), 1.0, WRn, int(Sn), Tm.p, int(rn),
                   0.0, Lout, int(Sn), st));
+    // L_n R_n = W^R (2^{-e} P_n)^+ W^L 2^{-e}
+    TTR_TRY(scale_pow2_dev(X, Rout, ln * Sn, pexp.p + n, -1, st));
     TTR_CUDA(cudaMemcpyAsync(sig0.p + n, sig.p, sizeof(double), cudaMemcpyDeviceToDevice, st));
     if (!overlap) tm.end(5);
     return TT_OK;
@@ -984,10 +999,46 @@ int two_sided_impl(tt_ctx* c, int S, const tt_view* terms, int64_t ell, int64_t 
     TTR_TRY(allreduce_sum(C, out->bufs[d - 1].p, size_t(l[d - 1]) * Id));
     tm.end(4);
   }
+  // Output gauge: the split S^{-1/2} | S^{-1/2} of line 9-10 puts the sketch
+  // contractions' geometric scale (~ b^{-N/2} .. b^{N/2} over the bonds) into
+  // the cores; at d = 50 the partial contractions of the result then overflow.
+  // Cores are rebalanced by powers of two (exact; the tensor is unchanged, R20).
+  DBuf ssq, part;
+  TTR_TRY(dalloc(ssq, size_t(d), s));
+  TTR_TRY(dalloc(part, 256, s));
+  for (int n = 0; n < d; ++n)
+    TTR_TRY(sumsq_det(C, out->bufs[n].p, size_t(l[n]) * dims[n] * l[n + 1], ssq.p + n, part.p, s));
+  std::vector<double> h_ssq(d, 0.0);
+  TTR_CUDA(cudaMemcpyAsync(h_ssq.data(), ssq.p, sizeof(double) * d, cudaMemcpyDeviceToHost, s));
   tm.end(6);
   std::vector<double> s0(d, 1.0);
   TTR_CUDA(cudaMemcpyAsync(s0.data(), sig0.p, sizeof(double) * d, cudaMemcpyDeviceToHost, s));
   TTR_CUDA(cudaStreamSynchronize(s));
+  {
+    // e_n = exponent of ||X_n||; shift every core to the mean exponent, the
+    // rounding residue goes to core N so the shifts sum to zero
+    std::vector<int> e(d, 0), sh(d, 0);
+    bool ok = true;
+    long tot = 0;
+    for (int n = 0; n < d; ++n) {
+      if (!(h_ssq[n] > 0.0) || !std::isfinite(h_ssq[n])) ok = false;
+      else e[n] = std::ilogb(h_ssq[n]) / 2;
+      tot += e[n];
+    }
+    if (ok) {
+      const long t = std::lround(double(tot) / d);
+      long sum = 0;
+      for (int n = 0; n < d; ++n) {
+        sh[n] = int(t - e[n]);
+        sum += sh[n];
+      }
+      sh[d - 1] -= int(sum);
+      for (int n = 0; n < d; ++n)
+        if (sh[n] != 0)
+          TTR_TRY(scale_pow2(C, out->bufs[n].p, size_t(l[n]) * dims[n] * l[n + 1], sh[n], s));
+      TTR_CUDA(cudaStreamSynchronize(s));
+    }
+  }
   tm.finish();
   int fl[4];
   TTR_TRY(read_flags(C, fl, 4));

@@ -192,6 +192,16 @@ int align_column_signs(Ctx& c, double* Q, const double* ref, int64_t m, int64_t 
 // (0 = none), written to dst (device int).
 int eps_rank_dev(Ctx& c, const double* sigma, int n, const double* eps_dev, double eps_host,
                  int rmax, int* dst, cudaStream_t s);
+// *out = sum x_i^2 in a fixed order (partial: 256 doubles of scratch)
+int sumsq_det(Ctx& c, const double* x, int64_t n, double* out, double* partial,
+              cudaStream_t s);
+// x <- 2^shift x (exact)
+int scale_pow2(Ctx& c, double* x, int64_t n, int shift, cudaStream_t s);
+// x <- 2^{-e} x, e = floor(log2 ||x||_F) computed and stored (*e_out) on the device
+int normalize_pow2(Ctx& c, double* x, int64_t n, double* ssq, double* partial, int* e_out,
+                   cudaStream_t s);
+// x <- 2^{sign * *e} x (device exponent)
+int scale_pow2_dev(Ctx& c, double* x, int64_t n, const int* e, int sign, cudaStream_t s);
 // out = ||x||_F (device scalar)
 int fro_norm(Ctx& c, const double* x, int64_t n, double* out, cudaStream_t s);
 // dst (cols x rows, ld ldd) = src^T (src rows x cols, ld lds)

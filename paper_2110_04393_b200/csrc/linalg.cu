@@ -1344,6 +1344,62 @@ __global__ void align_column_signs_kernel(double* __restrict__ Q, const double* 
     for (int i = threadIdx.x; i < m; i += blockDim.x) Q[int64_t(c) * m + i] = -Q[int64_t(c) * m + i];
 }
 
+// deterministic sum of squares: fixed grid, per-block partials in block order
+constexpr int kSsqBlocks = 256;
+__global__ void sumsq_partial_kernel(const double* __restrict__ x, int64_t n,
+                                     double* __restrict__ partial) {
+  __shared__ double red[32];
+  double acc = 0.0;
+  for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < n;
+       e += int64_t(gridDim.x) * blockDim.x)
+    acc = fma(x[e], x[e], acc);
+  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < int(blockDim.x >> 5); ++w) t += red[w];
+    partial[blockIdx.x] = t;
+  }
+}
+
+__global__ void sumsq_final_kernel(const double* __restrict__ partial, int np,
+                                   double* __restrict__ out) {
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int i = 0; i < np; ++i) t += partial[i];
+    *out = t;
+  }
+}
+
+__global__ void scale_pow2_kernel(double* __restrict__ x, int64_t n, int shift) {
+  for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < n;
+       e += int64_t(gridDim.x) * blockDim.x)
+    x[e] = ldexp(x[e], shift);
+}
+
+// x <- 2^{-e} x with e = floor(log2 ||x||) from *ssq = ||x||^2 (every thread
+// derives e itself; thread 0 stores it): brings ||x|| into [1, 4) exactly
+__global__ void normalize_pow2_kernel(double* __restrict__ x, int64_t n,
+                                      const double* __restrict__ ssq, int* __restrict__ e_out) {
+  const double q = *ssq;
+  const int e = (q > 0.0 && q <= 1.7976931348623157e308) ? ilogb(q) / 2 : 0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *e_out = e;
+  if (e == 0) return;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x)
+    x[i] = ldexp(x[i], -e);
+}
+
+__global__ void scale_pow2_dev_kernel(double* __restrict__ x, int64_t n, const int* __restrict__ e,
+                                      int sign) {
+  const int sh = sign * *e;
+  if (sh == 0) return;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x)
+    x[i] = ldexp(x[i], sh);
+}
+
 __global__ void eps_rank_kernel(const double* __restrict__ sigma, int n, const double* eps_dev,
                                 double eps_host, int rmax, int* dst) {
   if (threadIdx.x != 0) return;
@@ -1466,6 +1522,34 @@ int unit_cut_columns(Ctx& c, double* A, int64_t m, int64_t n, const double* sigm
 int align_column_signs(Ctx& c, double* Q, const double* ref, int64_t m, int64_t n,
                        cudaStream_t s) {
   align_column_signs_kernel<<<int(n), 256, 0, s>>>(Q, ref, int(m));
+  return launched();
+}
+
+int sumsq_det(Ctx& c, const double* x, int64_t n, double* out, double* partial,
+              cudaStream_t s) {
+  sumsq_partial_kernel<<<kSsqBlocks, 256, 0, s>>>(x, n, partial);
+  TTR_TRY(launched());
+  sumsq_final_kernel<<<1, 32, 0, s>>>(partial, kSsqBlocks, out);
+  return launched();
+}
+
+int scale_pow2(Ctx& c, double* x, int64_t n, int shift, cudaStream_t s) {
+  const int blocks = int(std::min<int64_t>((n + 255) / 256, c.sm_count * 8));
+  scale_pow2_kernel<<<std::max(1, blocks), 256, 0, s>>>(x, n, shift);
+  return launched();
+}
+
+int normalize_pow2(Ctx& c, double* x, int64_t n, double* ssq, double* partial, int* e_out,
+                   cudaStream_t s) {
+  TTR_TRY(sumsq_det(c, x, n, ssq, partial, s));
+  const int blocks = int(std::min<int64_t>((n + 255) / 256, c.sm_count * 8));
+  normalize_pow2_kernel<<<std::max(1, blocks), 256, 0, s>>>(x, n, ssq, e_out);
+  return launched();
+}
+
+int scale_pow2_dev(Ctx& c, double* x, int64_t n, const int* e, int sign, cudaStream_t s) {
+  const int blocks = int(std::min<int64_t>((n + 255) / 256, c.sm_count * 8));
+  scale_pow2_dev_kernel<<<std::max(1, blocks), 256, 0, s>>>(x, n, e, sign);
   return launched();
 }
 
