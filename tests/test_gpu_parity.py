@@ -304,3 +304,36 @@ def test_tolerance_bound_holds(ctx):
     check(res, ref)
     S = oracle.tt_add([ttsynth.to_numpy(t) for t in terms])
     assert oracle.rel_diff(res.numpy(), S) <= tol * (1 + 1e-10)
+
+
+def test_concurrent_contexts_on_host_threads_match_sequential():
+    """Several contexts (one stream each) driven from host threads, as bench.py
+    --batch does: results free stream-ordered and the one-time kernel setup is
+    thread-safe, so concurrent roundings give the bits of sequential ones."""
+    import concurrent.futures as cf
+    import paper_2110_04393_b200 as P
+    w = ttsynth.config3_sum10(d=6, I=24, S=4)
+    t = gpu_terms(w.terms)
+    torch.cuda.synchronize()
+    seq = [P.Context(0).tt_round_sum(t, mode="rank", rank=12, oversample=4, seed=s).numpy()
+           for s in range(1, 9)]
+    ctxs = [P.Context(0) for _ in range(4)]
+
+    def lane(k):
+        out = {}
+        for s in range(1 + k, 9, 4):
+            r = ctxs[k].tt_round_sum(t, mode="rank", rank=12, oversample=4, seed=s)
+            out[s] = r.numpy()
+            del r
+        a = ctxs[k].tt_round_sum_two_sided(t, 10, seed=k + 1).numpy()
+        return out, a
+
+    with cf.ThreadPoolExecutor(4) as ex:
+        res = list(ex.map(lane, range(4)))
+    for k, (out, a) in enumerate(res):
+        for s, X in out.items():
+            for x, y in zip(X, seq[s - 1]):
+                assert np.array_equal(x, y)
+        b = P.Context(0).tt_round_sum_two_sided(t, 10, seed=k + 1).numpy()
+        for x, y in zip(a, b):
+            assert np.array_equal(x, y)
