@@ -117,6 +117,8 @@ def two_sided_ell(wl):
 def flops_of(wl, ranks_out, algo="rand_orth"):
     from paper_2110_04393_b200 import cost
     dims = wl.dims
+    if algo == "deterministic":
+        return {"total": None, "phase1": None}, None
     tr = [[int(t[0].shape[0])] + [int(c.shape[2]) for c in t] for t in wl.terms]
     sumR = [sum(r[n] for r in tr) for n in range(len(dims) + 1)]
     if algo == "two_sided":
@@ -200,9 +202,12 @@ def main():
                     help="B independent roundings per step (distinct sketch seeds), spread "
                          "over --streams contexts (SURVEY 8d batched throughput of C1/C2)")
     ap.add_argument("--streams", type=int, default=1)
-    ap.add_argument("--algo", default="rand_orth", choices=["rand_orth", "two_sided"],
+    ap.add_argument("--algo", default="rand_orth",
+                    choices=["rand_orth", "two_sided", "deterministic"],
                     help="rand_orth: tt_round_sum (Alg. 7 + truncation, the headline); "
-                         "two_sided: tt_round_sum_two_sided (Alg. 6)")
+                         "two_sided: tt_round_sum_two_sided (Alg. 6); deterministic: "
+                         "tt_round_deterministic (Alg. 1 + 2 on the assembled sum, the "
+                         "paper's baseline; one GPU, no flop accounting)")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -246,8 +251,13 @@ def main():
         kw = dict(mode="rank", rank=wl.rank, oversample=wl.ell - wl.rank)
 
     two_sided = args.algo == "two_sided"
+    determ = args.algo == "deterministic"
+    if determ and world > 1:
+        raise SystemExit("--algo deterministic runs on one GPU")
 
     def call(terms):
+        if determ:
+            return ctx.tt_round_deterministic(terms, tol=wl.tol, rank=0 if wl.tol > 0 else wl.rank)
         if two_sided:
             return ctx.tt_round_sum_two_sided(terms, ell=two_sided_ell(wl), rho=0, seed=1)
         return ctx.tt_round_sum(terms, seed=1, **kw)
@@ -295,18 +305,18 @@ def main():
     fl, l = flops_of(wl, ranks_out, args.algo)
     peak, peak_src = fp64_peak()
     value = 1000.0 / ms                       # roundings/s (one rounding per step, all ranks)
-    tflops = fl["total"] / (ms * 1e-3) / 1e12
+    tflops = fl["total"] / (ms * 1e-3) / 1e12 if fl["total"] else None
     # dominant kernel family: the phase-1 DMMA contractions (Alg. 3), timed live
     p1_ms = phase[1]
-    p1_flops_local = fl["phase1"] * (hi - lo) / S
-    p1_achieved = p1_flops_local / (p1_ms * 1e-3) / 1e12 if p1_ms > 0 else None
+    p1_flops_local = fl["phase1"] * (hi - lo) / S if fl["phase1"] else None
+    p1_achieved = p1_flops_local / (p1_ms * 1e-3) / 1e12 if (p1_ms > 0 and p1_flops_local) else None
 
     e2e = None
     if not args.no_e2e:
         e2e = e2e_run(args, call, local_terms, dev, world, dist if world > 1 else None)
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
+    if rank == 0 and world == 1 and not args.no_cpu and not determ:
         rate, desc, cores, gfs = cpu_oracle_sample(args.workload, algo=args.algo)
         cpu = {"value": rate, "unit": "roundings/s", "cores": cores, "kind": "oracle",
                "sample": desc}
@@ -329,10 +339,11 @@ def main():
                        "rank": wl.rank, "tol": wl.tol, "parallelism": f"summands/{world}",
                        "algo": ("two_sided (Alg. 6): l = %d, rho = %d" % (
                            two_sided_ell(wl), (3 * two_sided_ell(wl) + 1) // 2))
-                       if two_sided else "rand_orth (Alg. 7 + truncation)",
+                       if two_sided else ("deterministic (Alg. 1 + 2 on the assembled sum)"
+                                          if determ else "rand_orth (Alg. 7 + truncation)"),
                        "l2": "inputs (12.9 GB) larger than L2 (126 MB); no flush"},
             "tflops": tflops, "fp64_peak_tflops": peak, "fp64_peak_source": peak_src,
-            "frac_of_fp64_peak": tflops / peak,
+            "frac_of_fp64_peak": tflops / peak if tflops else None,
             "flops_per_rounding": fl,
             "phase_ms": ({"sketches": phase[0], "right_contractions": phase[1],
                           "left_contraction_and_assembly": phase[2], "bond_qr_svd": phase[3],
