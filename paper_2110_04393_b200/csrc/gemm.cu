@@ -412,6 +412,10 @@ int dispatch(Ctx& c, GemmParams& P, int maxM, int maxN, int maxK, cudaStream_t s
     const double wv = waste(x.bm, x.bn) * (1.0 - 1e-3 * (x.bm * x.bn) / 6144.0);
     if (wv < bw) { bw = wv; best = x.id; }
   }
+  // short K (phase-1 Z: K = R = 64, four k-tiles): each CTA is mostly load
+  // prologue and store epilogue, hidden only by other resident CTAs -- the
+  // 64 x 48 tile (80 registers, 57 KB) fits 3 per SM against 2 for 128 x 48
+  if (best == 0 && maxK <= 64 && maxM % 64 == 0) best = 3;
   switch (best) {
     case 0: return launch_cfg<TallS, TA, TB>(c, P, maxM, maxN, maxK, s);
     case 1: return launch_cfg<WideS, TA, TB>(c, P, maxM, maxN, maxK, s);
