@@ -393,6 +393,7 @@ using SqS = Shape<64, 64, 16, 2, 2, 4>;      // general / split-K
 using RowS = Shape<64, 48, 16, 4, 2, 4>;     // M = R = 64, N = l = 144 (phase-1 W, split-K)
 using GramS = Shape<48, 48, 16, 2, 2, 4>;    // l x l Grams (split-K)
 using SmallS = Shape<32, 32, 16, 2, 2, 3>;   // tiny problems
+using WideK = Shape<48, 64, 16, 2, 2, 4>;    // short-K wide (carry: K = R = 64), more CTAs/SM
 
 template <bool TA, bool TB>
 int dispatch(Ctx& c, GemmParams& P, int maxM, int maxN, int maxK, cudaStream_t s) {
@@ -416,12 +417,14 @@ int dispatch(Ctx& c, GemmParams& P, int maxM, int maxN, int maxK, cudaStream_t s
   // prologue and store epilogue, hidden only by other resident CTAs -- the
   // 64 x 48 tile (80 registers, 57 KB) fits 3 per SM against 2 for 128 x 48
   if (best == 0 && maxK <= 64 && maxM % 64 == 0) best = 3;
+  if (best == 1 && maxK <= 64 && maxN % 64 == 0) best = 6;   // the same for wide ones
   switch (best) {
     case 0: return launch_cfg<TallS, TA, TB>(c, P, maxM, maxN, maxK, s);
     case 1: return launch_cfg<WideS, TA, TB>(c, P, maxM, maxN, maxK, s);
     case 2: return launch_cfg<SqS, TA, TB>(c, P, maxM, maxN, maxK, s);
     case 3: return launch_cfg<RowS, TA, TB>(c, P, maxM, maxN, maxK, s);
     case 4: return launch_cfg<GramS, TA, TB>(c, P, maxM, maxN, maxK, s);
+    case 6: return launch_cfg<WideK, TA, TB>(c, P, maxM, maxN, maxK, s);
     default: return launch_cfg<SmallS, TA, TB>(c, P, maxM, maxN, maxK, s);
   }
 }
