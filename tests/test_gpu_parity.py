@@ -337,3 +337,23 @@ def test_concurrent_contexts_on_host_threads_match_sequential():
         b = P.Context(0).tt_round_sum_two_sided(t, 10, seed=k + 1).numpy()
         for x, y in zip(a, b):
             assert np.array_equal(x, y)
+
+
+# ------------------------------------------------------------------ ε threshold (closed form)
+@pytest.mark.parametrize("N,eps0,k", [(3, 1.2e-3, 4), (3, 1.6e-3, 3), (5, 1.8e-3, 4),
+                                      (5, 2.2e-3, 3)])
+def test_eps_threshold_closed_form_spectra(ctx, N, eps0, k):
+    """Both GPU paths keep the ranks fixed by ε = ‖X‖ε0/√(N-1) on a
+    TT whose bond spectra are 10^-a exactly (tests/test_oracle_tt.py pins)."""
+    from test_oracle_tt import SPECTRUM, _known_spectrum_tt
+    rng = np.random.default_rng(101 + N)
+    Y = _known_spectrum_tt(rng, [7] * N, SPECTRUM, left_orth=False, gauge="general")
+    terms = [[torch.from_numpy(np.ascontiguousarray(c)) for c in Y]]
+    exact = math.sqrt(sum(x * x for x in SPECTRUM[k:]))
+    # randomized: sketch rank 6 >= true rank, so Alg. 7 is exact and only truncation cuts
+    res = ctx.tt_round_sum(gpu_terms(terms), mode="tol", tol=eps0, oversample=6, seed=3)
+    assert res.ranks == [1] + [k] * (N - 1) + [1]
+    assert abs(oracle.diff_norm(res.numpy(), Y) - exact) < 1e-12
+    det = ctx.tt_round_deterministic(gpu_terms(terms), tol=eps0)
+    assert det.ranks == [1] + [k] * (N - 1) + [1]
+    assert abs(oracle.diff_norm(det.numpy(), Y) - exact) < 1e-12

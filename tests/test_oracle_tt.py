@@ -319,3 +319,71 @@ def test_hilbert_type_tensor_rounding():
         assert np.linalg.norm(oracle.full(Xd) - F) <= eps0 * np.linalg.norm(F)
         r = oracle.round_sum([Y], ell=6, seed=1, tol=eps0, adaptive=True)
         assert np.linalg.norm(oracle.full(r.X) - F) <= 2 * eps0 * np.linalg.norm(F)
+
+
+# ---------------------------------------------------------------- ε threshold of Alg. 2
+def _known_spectrum_tt(rng, dims, s, left_orth, gauge="orthogonal"):
+    """TT whose every bond has singular values exactly ``s`` (closed form).
+
+    Core 1: V(X_1) = U (orthonormal columns); middle cores X_n(a,i,b) = δ_ab·δ_{i,0}
+    (an isometry in the V unfolding); last core H(X_N) = diag(s)·Vt with orthonormal
+    rows.  The tensor is Σ_a s_a u_a ⊗ e_0 ⊗ … ⊗ e_0 ⊗ v_a, so the unfolding at
+    every bond has singular values s.  Random gauges G_n between cores (orthogonal,
+    which keeps X left-orthogonal, or general invertible) do not change the tensor."""
+    N, r = len(dims), len(s)
+    U, _ = np.linalg.qr(rng.standard_normal((dims[0], r)))
+    Vt = np.linalg.qr(rng.standard_normal((dims[-1], r)))[0].T
+    X = [U.reshape(1, dims[0], r)]
+    for n in range(1, N - 1):
+        c = np.zeros((r, dims[n], r))
+        c[:, 0, :] = np.eye(r)
+        X.append(c)
+    X.append((np.asarray(s)[:, None] * Vt).reshape(r, dims[-1], 1))
+    for n in range(N - 1):   # gauge on bond n+1: X_n ×₃ G, G⁻¹ ×₁ X_{n+1}
+        if gauge == "orthogonal":
+            G = np.linalg.qr(rng.standard_normal((r, r)))[0]
+        else:
+            G = rng.standard_normal((r, r)) + 3 * np.eye(r)
+        X[n] = np.einsum("aib,bc->aic", X[n], G)
+        X[n + 1] = np.einsum("ab,bic->aic", np.linalg.inv(G), X[n + 1])
+    if left_orth:
+        assert oracle.left_orth_residual(X) < 1e-12
+    return X
+
+
+# s = 10^-a, a = 0..5: ‖X‖ = 1.00504; the tail after keeping k is t_k ≈ 1.005·10^-k.
+# Per-bond threshold ε = ‖X‖ε0/√(N-1) (P:463 "ε = ‖Y‖ε0/√(N-1)", Alg. 2 line 3 P:473;
+# applied bond by bond at line 7 P:477).  Hand-computed kept ranks (all bonds equal,
+# since truncating bond n leaves the spectrum s[:k] at every other bond):
+#   N=3, ε0=1.2e-3: ε=8.53e-4 -> t_3=1.005e-3 > ε, keep 4   (no √: 1.21e-3 -> 3)
+#   N=3, ε0=1.6e-3: ε=1.14e-3 -> keep 3                    (1/(N-1): 8.0e-4 -> 4; 1/√N: 9.3e-4 -> 4)
+#   N=5, ε0=1.8e-3: ε=9.05e-4 -> keep 4                    (no √: 1.81e-3 -> 3)
+#   N=5, ε0=2.2e-3: ε=1.11e-3 -> keep 3                    (1/(N-1): 5.5e-4 -> 4)
+EPS_CASES = [(3, 1.2e-3, 4), (3, 1.6e-3, 3), (5, 1.8e-3, 4), (5, 2.2e-3, 3)]
+SPECTRUM = [10.0 ** -a for a in range(6)]
+
+
+@pytest.mark.parametrize("N,eps0,k", EPS_CASES)
+def test_eps_threshold_sqrt_n_minus_1_tt_round(N, eps0, k):
+    """Alg. 2 on a TT with closed-form bond spectra: the kept ranks
+    straddle ε0‖Y‖/√(N-1), so a dropped or changed √(N-1) changes them."""
+    rng = np.random.default_rng(7 + N)
+    Y = _known_spectrum_tt(rng, [7] * N, SPECTRUM, left_orth=False, gauge="general")
+    X = oracle.tt_round(Y, eps0)
+    assert oracle.ranks_of(X) == [1] + [k] * (N - 1) + [1]
+    # the dropped mass is exactly the discarded singular values, bond by bond
+    err = oracle.diff_norm(X, Y)
+    assert abs(err - math.sqrt(sum(x * x for x in SPECTRUM[k:]))) < 1e-12
+
+
+@pytest.mark.parametrize("N,eps0,k", EPS_CASES)
+def test_eps_threshold_sqrt_n_minus_1_truncation(N, eps0, k):
+    """The mirrored truncation of a left-orthogonal TT (P:667-670 via Alg. 2
+    lines 3-10) uses the same per-bond ε = ‖X‖ε0/√(N-1)."""
+    rng = np.random.default_rng(11 + N)
+    X = _known_spectrum_tt(rng, [7] * N, SPECTRUM, left_orth=True)
+    T, ks = oracle.truncate_left_orthogonal(X, eps0)
+    assert ks == [k] * (N - 1)
+    assert oracle.ranks_of(T) == [1] + [k] * (N - 1) + [1]
+    err = oracle.diff_norm(T, X)
+    assert abs(err - math.sqrt(sum(x * x for x in SPECTRUM[k:]))) < 1e-12
