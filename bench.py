@@ -102,6 +102,29 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
+CONFIG_SHAPES = {   # (S, d, I, sketch rank, rank, tol) of each workload (ttsynth recipes)
+    "large": (32, 50, 256, 144, 128, 0.0), "sum10": (10, 20, 100, 70, 60, 0.0),
+    "gmres": (20, 12, 128, 80, 0, 1e-8), "single": (1, 16, 64, 35, 25, 0.0),
+    "tiny": (2, 4, 4, 6, 4, 0.0),
+}
+
+
+def bench_config(name, algo, world):
+    """The `config` object of the JSON line; identical for both arms."""
+    S, d, I, ell, r, tol = CONFIG_SHAPES[name]
+    l2 = "L2 (126 MB) flushed by the inputs themselves: inputs %s than L2" % (
+        "larger" if name in ("large", "sum10", "gmres") else "smaller (cache-resident; no flush)")
+    if algo == "two_sided":
+        a = "two_sided (Alg. 6): l = %d, rho = %d" % (r or ell, (3 * (r or ell) + 1) // 2)
+    elif algo == "deterministic":
+        a = "deterministic (Alg. 1 + 2 on the assembled sum)"
+    else:
+        a = "rand_orth (Alg. 7 + truncation)"
+    return {"workload": name, "desc": WORKLOADS[name]["desc"], "summands": S, "d": d, "I": I,
+            "sketch_rank": ell, "rank": r, "tol": tol, "parallelism": f"summands/{world}",
+            "algo": a, "l2": l2}
+
+
 def make_workload(name, device, seed_offset=0):
     import ttsynth
     w = WORKLOADS[name]
@@ -130,62 +153,110 @@ def flops_of(wl, ranks_out, algo="rand_orth"):
     return cost.rounding_flops(dims, tr, l, kept), l
 
 
-def cpu_oracle_sample(name, budget_s=20.0, algo="rand_orth"):
-    """Time the oracle (as it stands) on a bounded sample of the workload: the same
-    S, I, ranks, sketch rank at reduced order d, scaled to the full config by the
-    exact flop ratio.  Returns (roundings/s for the full config, description, cores)."""
-    import numpy as np
-    import oracle
-    import ttsynth
-    from paper_2110_04393_b200 import cost
-    full = make_workload(name, "cpu") if name in ("tiny", "single") else None
-    w = WORKLOADS[name]
-    fn = getattr(ttsynth, w["cfg"])
-    d_full = {"large": 50, "sum10": 20, "gmres": 12, "single": 16, "tiny": 4}[name]
-    d_s = min(d_full, 4 if name == "large" else d_full)
-    sample = fn(device="cpu", d=d_s) if d_s != d_full else (full or fn(device="cpu"))
-    terms = [ttsynth.to_numpy(t) for t in sample.terms]
-    t0 = time.perf_counter()
-    reps = 0
-    while True:
-        if algo == "two_sided":
-            X2, lc, _ = oracle.round_sum_2s(terms, ell=two_sided_ell(sample), seed=1)
-            ranks_s = lc
-        else:
-            r = oracle.round_sum(terms, ell=sample.ell, seed=1, rank=sample.rank, tol=sample.tol,
-                                 adaptive=sample.adaptive)
-            ranks_s = list(r.ranks)
-        reps += 1
-        if time.perf_counter() - t0 > budget_s or reps >= 50:
-            break
-    dt = (time.perf_counter() - t0) / reps
-    fs, _ = flops_of(sample, [1] + ranks_s + [1], algo)
-    # flops of the full config (ranks after truncation taken as the target rank)
-    fw = sample if d_s == d_full else None
-    if fw is None:
-        dims = [sample.dims[0]] * d_full
-        tr = [[1] + [int(sample.terms[0][1].shape[0])] * (d_full - 1) + [1]] * len(sample.terms)
-        sumR = [sum(x[n] for x in tr) for n in range(d_full + 1)]
-        if algo == "two_sided":
-            e2 = two_sided_ell(sample)
-            ff = cost.two_sided_flops(dims, tr, cost.caps(dims, sumR, e2),
-                                      cost.caps(dims, sumR, (3 * e2 + 1) // 2))["total"]
-        else:
-            l = cost.caps(dims, sumR, sample.ell)
-            kept = [1] + [min(sample.rank, x) for x in l[1:-1]] + [1]
-            ff = cost.rounding_flops(dims, tr, l, kept)["total"]
-    else:
-        ff = fs["total"]
-    rate = 1.0 / (dt * ff / fs["total"])
+def _cores_used():
     try:
         from threadpoolctl import threadpool_info
-        cores = max([x.get("num_threads", 1) for x in threadpool_info()] + [1])
+        return max([x.get("num_threads", 1) for x in threadpool_info()] + [1])
     except Exception:
-        cores = os.cpu_count()
-    desc = (f"oracle{' Alg. 6' if algo == 'two_sided' else ''} (NumPy fp64, BLAS/LAPACK steps) on {w['desc']} at d={d_s} "
-            f"({reps} run(s), {dt:.2f} s each, {fs['total'] / dt / 1e9:.2f} GFLOP/s), "
-            f"scaled to d={d_full} by the exact flop ratio")
-    return rate, desc, cores, fs["total"] / dt
+        return os.cpu_count()
+
+
+def _oracle_round(terms, wl, algo):
+    import oracle
+    if algo == "two_sided":
+        _, lc, _ = oracle.round_sum_2s(terms, ell=two_sided_ell(wl), seed=1)
+        return lc
+    r = oracle.round_sum(terms, ell=wl.ell, seed=1, rank=wl.rank, tol=wl.tol,
+                         adaptive=wl.adaptive)
+    return list(r.ranks)
+
+
+def large_bond_sample(seed=5):
+    """Full-shape sample of config 5 for the oracle: the S = 32 summands cut to a
+    3-mode chain whose left boundary carries the interior sketch rank
+    (cores 144x256x64, 64x256x64, 64x256x1), so Alg. 3, the Alg. 7 sweep and the
+    truncation each run at exactly config 5's per-bond shapes: one interior bond
+    (m = 144*256 rows, sum R = 2048) plus the last bond.  Returns (terms, flops
+    of the sample, flops of the full rounding)."""
+    import numpy as np
+    from paper_2110_04393_b200 import cost
+    S, I, R, ell, r = 32, 256, 64, 144, 128
+    rng = np.random.default_rng(seed)
+    sd = 1.0 / math.sqrt(R * I)
+    terms = [[rng.standard_normal((ell, I, R)) * sd, rng.standard_normal((R, I, R)) * sd,
+              rng.standard_normal((R, I, 1)) * sd] for _ in range(S)]
+    f_s = cost.rounding_flops([I] * 3, [[ell, R, R, 1]] * S, [ell, ell, ell, 1],
+                              kept=[ell, r, r, 1])["total"]
+    d = 50
+    tr = [[1] + [R] * (d - 1) + [1]] * S
+    l = cost.caps([I] * d, [sum(x[n] for x in tr) for n in range(d + 1)], ell)
+    f_f = cost.rounding_flops([I] * d, tr, l, [1] + [r] * (d - 1) + [1])["total"]
+    return terms, f_s, f_f
+
+
+def cpu_oracle_sample(name, algo="rand_orth", reps=1):
+    """The oracle (as it stands) on a bounded sample of the workload, timed on the
+    host cores.  Config 5: the full-shape bond sample of large_bond_sample(),
+    scaled to one rounding by the exact flop ratio; the smaller configs: complete
+    roundings of the full config.  Returns (roundings/s, description, cores,
+    seconds per sample)."""
+    import oracle
+    import ttsynth
+    w = WORKLOADS[name]
+    if name == "large" and algo != "two_sided":
+        terms, f_s, f_f = large_bond_sample()
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            oracle.round_sum(terms, ell=144, seed=1, rank=128)
+        dt = (time.perf_counter() - t0) / reps
+        rate = 1.0 / (dt * f_f / f_s)
+        desc = (f"oracle (NumPy fp64, BLAS/LAPACK steps) on a full-shape sample of {w['desc']}: "
+                f"S=32 summands as a 3-mode chain 144x256x64 | 64x256x64 | 64x256x1 (one interior "
+                f"bond + the last bond at exactly config 5's shapes; {f_s / 1e9:.1f} GFLOP), "
+                f"{dt:.2f} s per sample ({f_s / dt / 1e9:.1f} GFLOP/s), scaled to one d=50 "
+                f"rounding by the exact flop ratio {f_f / f_s:.2f}")
+        return rate, desc, _cores_used(), dt
+    if name == "large":   # Alg. 6: the same chain trick does not apply; reduced order d = 4
+        wl = getattr(ttsynth, w["cfg"])(device="cpu", d=4)
+    else:
+        wl = getattr(ttsynth, w["cfg"])(device="cpu")
+    terms = [ttsynth.to_numpy(t) for t in wl.terms]
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        ranks_s = _oracle_round(terms, wl, algo)
+    dt = (time.perf_counter() - t0) / reps
+    rate = 1.0 / dt
+    desc = (f"oracle{' Alg. 6' if algo == 'two_sided' else ''} (NumPy fp64, BLAS/LAPACK steps): "
+            f"complete rounding(s) of {w['desc']}, {dt:.2f} s each")
+    if name == "large":
+        fs, _ = flops_of(wl, [1] + ranks_s + [1], algo)
+        full = make_workload_shapes_flops(algo)
+        rate = 1.0 / (dt * full / fs["total"])
+        desc += f" at d=4, scaled to d=50 by the exact flop ratio {full / fs['total']:.2f}"
+    return rate, desc, _cores_used(), dt
+
+
+def make_workload_shapes_flops(algo):
+    from paper_2110_04393_b200 import cost
+    d, S, I, R, ell = 50, 32, 256, 64, 128
+    tr = [[1] + [R] * (d - 1) + [1]] * S
+    sumR = [sum(x[n] for x in tr) for n in range(d + 1)]
+    return cost.two_sided_flops([I] * d, tr, cost.caps([I] * d, sumR, ell),
+                                cost.caps([I] * d, sumR, (3 * ell + 1) // 2))["total"]
+
+
+def cpu_oracle_full(wl, algo="rand_orth"):
+    """One complete rounding of the benchmarked workload (the same input bits the
+    GPU rounded, copied to the host) by the oracle as it stands: a measurement of
+    the full config, no scaling.  Returns (roundings/s, description, cores, s)."""
+    import ttsynth
+    terms = [ttsynth.to_numpy(t) for t in wl.terms]
+    t0 = time.perf_counter()
+    _oracle_round(terms, wl, algo)
+    dt = time.perf_counter() - t0
+    del terms
+    return 1.0 / dt, ("oracle (NumPy fp64, BLAS/LAPACK steps): one complete rounding of the "
+                      f"benchmarked inputs (full config, no scaling), {dt:.1f} s"), _cores_used(), dt
 
 
 def main():
@@ -197,6 +268,9 @@ def main():
     ap.add_argument("--workload", default="large", choices=list(WORKLOADS))
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-sample", action="store_true",
+                    help="cpu_baseline from the bounded full-shape sample instead of one "
+                         "complete oracle rounding of the benchmarked inputs")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--batch", type=int, default=1,
                     help="B independent roundings per step (distinct sketch seeds), spread "
@@ -210,9 +284,22 @@ def main():
                          "paper's baseline; one GPU, no flop accounting)")
     args = ap.parse_args()
 
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # `python bench.py --gpus N` without a launcher: re-run this command under
+        # torchrun with one process per GPU (the driver's own launch form)
+        import socket
+        with socket.socket() as so:
+            so.bind(("127.0.0.1", 0))
+            port = so.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+               "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+        raise SystemExit(subprocess.call(cmd))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}: launch one process per GPU")
 
     if args.impl == "reference":
         return reference_arm(args, world, rank)
@@ -317,7 +404,10 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu and not determ:
-        rate, desc, cores, gfs = cpu_oracle_sample(args.workload, algo=args.algo)
+        if args.cpu_sample:
+            rate, desc, cores, _ = cpu_oracle_sample(args.workload, algo=args.algo)
+        else:
+            rate, desc, cores, _ = cpu_oracle_full(wl, algo=args.algo)
         cpu = {"value": rate, "unit": "roundings/s", "cores": cores, "kind": "oracle",
                "sample": desc}
 
@@ -334,14 +424,7 @@ def main():
             "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic (ttsynth, seeded; DESIGN.md input recipe)",
-            "config": {"workload": args.workload, "desc": WORKLOADS[args.workload]["desc"],
-                       "summands": S, "d": wl.d, "I": wl.dims[0], "sketch_rank": wl.ell,
-                       "rank": wl.rank, "tol": wl.tol, "parallelism": f"summands/{world}",
-                       "algo": ("two_sided (Alg. 6): l = %d, rho = %d" % (
-                           two_sided_ell(wl), (3 * two_sided_ell(wl) + 1) // 2))
-                       if two_sided else ("deterministic (Alg. 1 + 2 on the assembled sum)"
-                                          if determ else "rand_orth (Alg. 7 + truncation)"),
-                       "l2": "inputs (12.9 GB) larger than L2 (126 MB); no flush"},
+            "config": bench_config(args.workload, args.algo, world),
             "tflops": tflops, "fp64_peak_tflops": peak, "fp64_peak_source": peak_src,
             "frac_of_fp64_peak": tflops / peak if tflops else None,
             "flops_per_rounding": fl,
@@ -487,25 +570,28 @@ def e2e_run(args, call, local_terms, dev, world, dist):
 
 
 def reference_arm(args, world, rank):
-    """--impl reference: the oracle (as it stands) on the host cores, rank 0 only."""
+    """--impl reference: the oracle (as it stands) on the host cores, rank 0 only
+    (other ranks exit without work).  Each step is one bounded sample of the
+    workload (cpu_oracle_sample: for config 5 the full-shape bond sample, for the
+    smaller configs one complete rounding); ms_per_step is the observed time of
+    one such sample, value = roundings/s after the stated scaling."""
     if rank != 0:
         return
-    steps = []
     desc = cores = None
     for _ in range(args.warmup):
-        cpu_oracle_sample(args.workload, budget_s=2.0, algo=args.algo)
+        cpu_oracle_sample(args.workload, algo=args.algo)
+    dts, rates = [], []
     for _ in range(args.steps):
-        rate, desc, cores, _ = cpu_oracle_sample(args.workload, budget_s=10.0, algo=args.algo)
-        steps.append(1.0 / rate)
-    ms = 1000.0 * statistics.mean(steps)
-    value = 1000.0 / ms
+        rate, desc, cores, dt = cpu_oracle_sample(args.workload, algo=args.algo)
+        dts.append(dt)
+        rates.append(rate)
+    ms = 1000.0 * statistics.mean(dts)
+    value = statistics.mean(rates)
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": "roundings/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": {"workload": args.workload,
-                                        "desc": WORKLOADS[args.workload]["desc"],
-                                        "algo": args.algo},
+        "data": "synthetic", "config": bench_config(args.workload, args.algo, world),
         "cpu_baseline": {"value": value, "unit": "roundings/s", "cores": cores,
                          "kind": "oracle", "sample": desc},
         "e2e": {"value": value, "unit": "roundings/s", "h2d_bytes_per_step": 0,
