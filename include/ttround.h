@@ -52,7 +52,7 @@ extern "C" {
 
 /* ---- return codes ------------------------------------------------------- */
 #define TT_OK             0
-#define TT_ERR_ARG       -1   /* null pointer, d < 2, S < 1, bad mode/option       */
+#define TT_ERR_ARG       -1   /* null pointer, d < 2, S < 1 (world 1), bad mode/option */
 #define TT_ERR_SHAPE     -2   /* dims differ across summands; bond ranks mismatch   */
 #define TT_ERR_RANK      -3   /* a rank < 1, or R_0 != 1 or R_d != 1                */
 #define TT_ERR_NONFINITE -4   /* (reserved) non-finite input detected               */
@@ -112,6 +112,25 @@ int tt_ctx_create(int device, void* cuda_stream, const uint8_t* nccl_id,
                   int rank, int world, tt_ctx_t* out);
 int tt_ctx_destroy(tt_ctx_t ctx);
 
+/* Loopback communicator: `world` ranks as contexts of ONE process on one
+ * device, each driven by its own host thread (calls release no lock, so the
+ * ranks run concurrently).  It runs the sharded code path of tt_round_sum /
+ * tt_round_sum_two_sided (per-rank summand shards, one exchange of
+ * Y_n per sweep step; the last core) where only one GPU exists:
+ * a rank's allreduce copies its partial into its own device slot, synchronises
+ * its stream, meets the other ranks at a host barrier, sums all slots in rank
+ * order 0..world-1 (so every rank holds identical bits) and meets them at a
+ * second barrier.  No kernel waits on another rank.  A barrier that waits more
+ * than 300 s returns TT_ERR_NCCL.  Correctness/test path, not a performance
+ * path (the NCCL communicator of tt_ctx_create is).  1 <= world <= 16.  The
+ * group must outlive every context created on it. */
+typedef struct tt_loopback* tt_loopback_t;
+int tt_loopback_create(int world, tt_loopback_t* out);
+int tt_loopback_destroy(tt_loopback_t group);
+/* Context of rank `rank` of a loopback group (device/stream as tt_ctx_create). */
+int tt_ctx_create_loopback(int device, void* cuda_stream, tt_loopback_t group, int rank,
+                           tt_ctx_t* out);
+
 /* ---- sketch (Def. 3.1) --------------------------------------- */
 /* Random Gaussian TT with ranks (1, l_1..l_{d-1}, 1): cores n = 2..d filled
  * in place with N(0, 1/(l_{n-1} I_n l_n)) entries from Philox4x32-10 keyed by
@@ -126,7 +145,11 @@ int tt_sketch_core(tt_sketch_t sk, int32_t n, const double** core);
 int tt_sketch_destroy(tt_sketch_t sk);
 
 /* ---- the hot path: Alg. 7 + truncation ----------- */
-/* Round Y = sum_j Y^(j) of S_local summands (this process's shard).
+/* Round Y = sum_j Y^(j) of S_local summands (this process's shard; with
+ * world > 1 a rank may hold none, S_local = 0 and terms = NULL, and then adds
+ * zeros to every exchange; every rank must pass the same opts and sketch-ness;
+ * the shapes and options are agreed across ranks before the first collective,
+ * so a bad argument on one rank makes every rank return an error, never hang).
  *  1. caps l_n = min(l, l_{n-1} I_n, prod_{k>n} I_k, sum_j R^(j)_n)    (R7)
  *  2. sketch R (Def. 3.1) — from opts->seed, or `sketch` if non-NULL (it must
  *     have exactly the capped ranks, else TT_ERR_SHAPE)

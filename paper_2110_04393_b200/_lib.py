@@ -51,6 +51,9 @@ def load_library(path: str = LIB_PATH):
         "tt_get_nccl_unique_id": (C.c_int, [P]),
         "tt_ctx_create": (C.c_int, [C.c_int, P, P, C.c_int, C.c_int, C.POINTER(P)]),
         "tt_ctx_destroy": (C.c_int, [P]),
+        "tt_loopback_create": (C.c_int, [C.c_int, C.POINTER(P)]),
+        "tt_loopback_destroy": (C.c_int, [P]),
+        "tt_ctx_create_loopback": (C.c_int, [C.c_int, P, P, C.c_int, C.POINTER(P)]),
         "tt_ctx_set_timing": (C.c_int, [P, C.c_int]),
         "tt_ctx_last_timing": (C.c_int, [P, C.POINTER(dbl), C.c_int]),
         "tt_ctx_flags": (C.c_int, [P, C.POINTER(C.c_int), C.c_int]),
@@ -215,6 +218,18 @@ class Sketch:
                                device=self.device)
 
 
+class LoopbackGroup:
+    """tt_loopback_t: `world` ranks as contexts of this process on one device
+    (drive each from its own thread); see include/ttround.h."""
+
+    def __init__(self, world: int):
+        L = load_library()
+        h = C.c_void_p()
+        _check(L.tt_loopback_create(int(world), C.byref(h)))
+        self._h = _Handle(h.value, L.tt_loopback_destroy)
+        self.world = int(world)
+
+
 class Context:
     """tt_ctx_t: one CUDA device + stream (+ NCCL communicator when world > 1).
 
@@ -222,7 +237,8 @@ class Context:
     ordered with the torch kernels that produce the inputs."""
 
     def __init__(self, device: int = 0, stream: Optional[torch.cuda.Stream] = None,
-                 nccl_id: Optional[bytes] = None, rank: int = 0, world: int = 1):
+                 nccl_id: Optional[bytes] = None, rank: int = 0, world: int = 1,
+                 loopback: Optional[LoopbackGroup] = None):
         L = load_library()
         self.device = torch.device("cuda", device)
         if stream is None:
@@ -235,7 +251,12 @@ class Context:
         sp = C.c_void_p(stream.cuda_stream or 0x1)
         idbuf = (C.c_uint8 * 128)(*nccl_id) if nccl_id is not None else None
         h = C.c_void_p()
-        _check(L.tt_ctx_create(device, sp, idbuf, rank, world, C.byref(h)))
+        if loopback is not None:
+            _check(L.tt_ctx_create_loopback(device, sp, loopback._h.ptr, rank, C.byref(h)))
+            world = loopback.world
+            self._group = loopback          # the group outlives the context
+        else:
+            _check(L.tt_ctx_create(device, sp, idbuf, rank, world, C.byref(h)))
         self._h = _Handle(h.value, L.tt_ctx_destroy)
         self.rank, self.world = rank, world
 
@@ -279,7 +300,7 @@ class Context:
         """Round sum_j terms[j] (Alg. 7 + truncation); see include/ttround.h."""
         L = load_library()
         views = [_View(t) for t in terms]
-        arr = (tt_view * len(views))(*[v.view for v in views])
+        arr = (tt_view * len(views))(*[v.view for v in views]) if views else None
         opts = tt_round_opts(_MODES[mode], int(adaptive), int(rank), int(oversample),
                              float(tol), C.c_uint64(seed).value, int(max_rank))
         h = C.c_void_p()
@@ -308,7 +329,7 @@ class Context:
         ceil(1.5 ell).  See include/ttround.h."""
         L = load_library()
         views = [_View(t) for t in terms]
-        arr = (tt_view * len(views))(*[v.view for v in views])
+        arr = (tt_view * len(views))(*[v.view for v in views]) if views else None
         h = C.c_void_p()
         _check(L.tt_round_sum_two_sided(self.handle, len(views), arr, int(ell), int(rho),
                                         C.c_uint64(seed).value, C.byref(h)))

@@ -194,6 +194,72 @@ int validate(const tt_view* v, int S, std::vector<int64_t>& dims) {
   return TT_OK;
 }
 
+// Validation agreed across ranks BEFORE any collective of the call: each rank
+// checks its own summands (S_local = 0 is allowed when world > 1: the rank then
+// contributes zeros to every exchange), then the failure flag, d, the mode sizes
+// and the call's options (`extra`) are combined with MAX/MIN allreduces, so either
+// every rank proceeds with the same shapes or every rank returns an error -- a
+// shape error on one rank can never leave the others waiting in a collective.
+int validate_sharded(Ctx& c, const tt_view* v, int S, int local_rc,
+                     const std::vector<int64_t>& extra, std::vector<int64_t>& dims) {
+  int rc = local_rc;
+  if (rc == TT_OK) {
+    if (S < 0 || (S > 0 && !v)) {
+      set_error("need S_local >= 0 summands (and a terms array when S_local > 0)");
+      rc = TT_ERR_ARG;
+    } else if (S == 0 && c.world == 1) {
+      set_error("need S >= 1 summands");
+      rc = TT_ERR_ARG;
+    } else if (S > 0) {
+      rc = validate(v, S, dims);
+    }
+  }
+  if (c.world == 1) return rc;
+  const bool have = rc == TT_OK && S > 0;
+  const int64_t big = INT64_MAX;
+  const size_t ne = extra.size();
+  std::vector<int64_t> mx = {rc != TT_OK ? 1 : 0, have ? int64_t(dims.size()) : 0};
+  std::vector<int64_t> mn = {have ? int64_t(dims.size()) : big};
+  for (size_t i = 0; i < ne; ++i) {
+    mx.push_back(extra[i]);
+    mn.push_back(extra[i]);
+  }
+  TTR_TRY(allreduce_i64(c, mx.data(), mx.size(), kOpMax));
+  TTR_TRY(allreduce_i64(c, mn.data(), mn.size(), kOpMin));
+  if (rc != TT_OK) return rc;   // this rank's own message is kept
+  if (mx[0]) {
+    set_error("another rank rejected its summands or options");
+    return TT_ERR_ARG;
+  }
+  if (mx[1] < 2) {
+    set_error("no rank holds a summand");
+    return TT_ERR_ARG;
+  }
+  if (mn[0] != mx[1]) {
+    set_error("ranks disagree on the number of modes");
+    return TT_ERR_SHAPE;
+  }
+  for (size_t i = 0; i < ne; ++i)
+    if (mx[2 + i] != mn[1 + i]) {
+      set_error("ranks disagree on the options of the call");
+      return TT_ERR_ARG;
+    }
+  const int d = int(mx[1]);
+  std::vector<int64_t> hi(d), lo(d);
+  for (int n = 0; n < d; ++n) {
+    hi[n] = have ? dims[n] : 0;
+    lo[n] = have ? dims[n] : big;
+  }
+  TTR_TRY(allreduce_i64(c, hi.data(), size_t(d), kOpMax));
+  TTR_TRY(allreduce_i64(c, lo.data(), size_t(d), kOpMin));
+  if (hi != lo) {
+    set_error("ranks disagree on the mode sizes");
+    return TT_ERR_SHAPE;
+  }
+  dims = hi;
+  return TT_OK;
+}
+
 // R7: l_n = min(l, l_{n-1} I_n, prod_{k>n} I_k, sum_j R_n), n = 1..d-1; l_0 = l_d = 1
 std::vector<int64_t> rank_caps(const std::vector<int64_t>& dims, const std::vector<int64_t>& sumR,
                                int64_t ell) {
@@ -218,15 +284,20 @@ struct Terms {
   std::vector<std::vector<int64_t>> R;             // [j][n], n = 0..d
   std::vector<DBuf> staged;
   std::vector<cudaEvent_t> ready;                  // per core n (host staging), or empty
+  cudaStream_t free_stream = nullptr;              // the compute stream the staged buffers free on
   ~Terms() {
+    // the staged buffers are freed (stream-ordered) on the compute stream: make it
+    // wait for every H2D copy first, so that an early error return can never hand
+    // memory a DMA is still writing back to the pool
+    if (free_stream)
+      for (auto e : ready) cudaStreamWaitEvent(free_stream, e, 0);
     for (auto e : ready) cudaEventDestroy(e);
   }
 };
 
-int stage_terms(Ctx& c, const tt_view* v, int S, Terms& T) {
+int stage_terms(Ctx& c, const tt_view* v, int S, int d, Terms& T) {
   T.S = S;
-  T.d = v[0].d;
-  const int d = T.d;
+  T.d = d;
   T.core.assign(S, std::vector<const double*>(d, nullptr));
   T.R.assign(S, std::vector<int64_t>(d + 1));
   bool any_host = false;
@@ -242,6 +313,7 @@ int stage_terms(Ctx& c, const tt_view* v, int S, Terms& T) {
   // left), one event per core so the sweep overlaps the transfer
   T.ready.resize(d);
   for (auto& e : T.ready) TTR_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  T.free_stream = c.stream;
   cudaEvent_t start;
   TTR_CUDA(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
   TTR_CUDA(cudaEventRecord(start, c.stream));
@@ -565,47 +637,54 @@ constexpr int kPMin = 5;   // adaptive saturation margin (R8)
 int round_sum_impl(tt_ctx* c, int S, const tt_view* terms, const tt_round_opts* o,
                    tt_sketch* user_sk, tt_tensor** outp) {
   std::vector<int64_t> dims;
-  TTR_TRY(validate(terms, S, dims));
-  if (!o) {
-    set_error("opts is null");
-    return TT_ERR_ARG;
-  }
-  const int d = int(dims.size());
-  int64_t ell;
+  int64_t ell = 0;
   double tol = 0.0;
   int64_t rank = 0;
   bool adaptive = false;
-  switch (o->mode) {
-    case TT_SKETCH_ONLY: ell = o->oversample; break;
-    case TT_RANK:
-      if (o->rank < 1 || o->oversample < 0) {
-        set_error("TT_RANK needs rank >= 1 and oversample >= 0");
-        return TT_ERR_ARG;
-      }
-      ell = o->rank + o->oversample;
-      rank = o->rank;
-      break;
-    case TT_TOL:
-      if (!(o->tol > 0.0)) {
-        set_error("TT_TOL needs tol > 0");
-        return TT_ERR_ARG;
-      }
-      ell = o->oversample;
-      tol = o->tol;
-      rank = std::max<int64_t>(0, o->rank);
-      adaptive = o->adaptive != 0 && user_sk == nullptr;
-      break;
-    default: set_error("unknown mode %d", o->mode); return TT_ERR_ARG;
+  int orc = TT_OK;
+  std::vector<int64_t> extra;
+  if (!o) {
+    set_error("opts is null");
+    orc = TT_ERR_ARG;
+  } else {
+    switch (o->mode) {
+      case TT_SKETCH_ONLY: ell = o->oversample; break;
+      case TT_RANK:
+        if (o->rank < 1 || o->oversample < 0) {
+          set_error("TT_RANK needs rank >= 1 and oversample >= 0");
+          orc = TT_ERR_ARG;
+        }
+        ell = o->rank + o->oversample;
+        rank = o->rank;
+        break;
+      case TT_TOL:
+        if (!(o->tol > 0.0)) {
+          set_error("TT_TOL needs tol > 0");
+          orc = TT_ERR_ARG;
+        }
+        ell = o->oversample;
+        tol = o->tol;
+        rank = std::max<int64_t>(0, o->rank);
+        adaptive = o->adaptive != 0 && user_sk == nullptr;
+        break;
+      default: set_error("unknown mode %d", o->mode); orc = TT_ERR_ARG;
+    }
+    if (orc == TT_OK && ell < 1) {
+      set_error("sketch rank must be >= 1");
+      orc = TT_ERR_ARG;
+    }
+    int64_t tbits;
+    memcpy(&tbits, &o->tol, sizeof tbits);
+    extra = {o->mode, o->adaptive, o->rank, o->oversample, tbits, int64_t(o->seed & 0x7fffffffffffffffull),
+             int64_t(o->seed >> 63), o->max_rank, user_sk != nullptr};
   }
-  if (ell < 1) {
-    set_error("sketch rank must be >= 1");
-    return TT_ERR_ARG;
-  }
+  TTR_TRY(validate_sharded(*c, terms, S, orc, extra, dims));
+  const int d = int(dims.size());
   TTR_CUDA(cudaSetDevice(c->device));
   PhaseTimer tm(*c);
   tm.begin(6);
   Terms T;
-  TTR_TRY(stage_terms(*c, terms, S, T));
+  TTR_TRY(stage_terms(*c, terms, S, d, T));
   // global summed ranks (all shards)
   std::vector<int64_t> sumR(d + 1, 0);
   for (int n = 0; n <= d; ++n)
@@ -718,16 +797,19 @@ int round_sum_impl(tt_ctx* c, int S, const tt_view* terms, const tt_round_opts* 
 int two_sided_impl(tt_ctx* c, int S, const tt_view* terms, int64_t ell, int64_t rho,
                    uint64_t seed, tt_tensor** outp) {
   std::vector<int64_t> dims;
-  TTR_TRY(validate(terms, S, dims));
+  int orc = TT_OK;
   if (ell < 1) {
     set_error("two-sided rounding needs ell >= 1");
-    return TT_ERR_ARG;
+    orc = TT_ERR_ARG;
   }
   if (rho <= 0) rho = (3 * ell + 1) / 2;   // ceil(1.5 l)
-  if (rho < ell) {
+  if (orc == TT_OK && rho < ell) {
     set_error("two-sided rounding needs rho >= ell (P:763)");
-    return TT_ERR_ARG;
+    orc = TT_ERR_ARG;
   }
+  TTR_TRY(validate_sharded(*c, terms, S, orc,
+                           {ell, rho, int64_t(seed & 0x7fffffffffffffffull), int64_t(seed >> 63)},
+                           dims));
   const int d = int(dims.size());
   TTR_CUDA(cudaSetDevice(c->device));
   Ctx& C = *c;
@@ -735,7 +817,7 @@ int two_sided_impl(tt_ctx* c, int S, const tt_view* terms, int64_t ell, int64_t 
   PhaseTimer tm(C);
   tm.begin(6);
   Terms T;
-  TTR_TRY(stage_terms(C, terms, S, T));
+  TTR_TRY(stage_terms(C, terms, S, d, T));
   std::vector<int64_t> gsumR(d + 1, 0);
   for (int n = 0; n <= d; ++n)
     for (int j = 0; j < S; ++j) gsumR[n] += T.R[j][n];
@@ -1091,6 +1173,10 @@ int two_sided_impl(tt_ctx* c, int S, const tt_view* terms, int64_t ell, int64_t 
 int deterministic_impl(tt_ctx* c, int S, const tt_view* terms, const tt_round_opts* o,
                        tt_tensor** outp) {
   std::vector<int64_t> dims;
+  if (c->world > 1) {   // before any check, identically on every rank (no collective)
+    set_error("tt_round_deterministic runs on one GPU (world size %d)", c->world);
+    return TT_ERR_ARG;
+  }
   TTR_TRY(validate(terms, S, dims));
   if (!o || o->tol < 0.0 || o->rank < 0) {
     set_error("tt_round_deterministic: need opts with tol >= 0 and rank >= 0");
@@ -1106,7 +1192,7 @@ int deterministic_impl(tt_ctx* c, int S, const tt_view* terms, const tt_round_op
   PhaseTimer tm(*c);
   tm.begin(6);
   Terms T;
-  TTR_TRY(stage_terms(*c, terms, S, T));
+  TTR_TRY(stage_terms(*c, terms, S, d, T));
   for (int n = 0; n < d; ++n) TTR_TRY(wait_core(*c, T, n));
   std::vector<int64_t> r(d + 1, 0);
   r[0] = r[d] = 1;
@@ -1285,8 +1371,8 @@ int inner_impl(tt_ctx* c, const tt_view* x, const tt_view* y, double* out) {
   }
   TTR_CUDA(cudaSetDevice(c->device));
   Terms TX, TY;
-  TTR_TRY(stage_terms(*c, x, 1, TX));
-  TTR_TRY(stage_terms(*c, y, 1, TY));
+  TTR_TRY(stage_terms(*c, x, 1, x->d, TX));
+  TTR_TRY(stage_terms(*c, y, 1, y->d, TY));
   cudaStream_t s = c->stream;
   const int d = int(dx.size());
   const auto& Rx = TX.R[0];
@@ -1338,8 +1424,13 @@ int tt_get_nccl_unique_id(uint8_t id[128]) {
   return guarded([&] { return nccl_unique_id(id); });
 }
 
-int tt_ctx_create(int device, void* cuda_stream, const uint8_t* nccl_id, int rank, int world,
-                  tt_ctx_t* out) {
+struct tt_loopback {
+  ttr::LoopGroup* g = nullptr;
+  int world = 1;
+};
+
+static int ctx_create(int device, void* cuda_stream, const uint8_t* nccl_id, tt_loopback* loop,
+                      int rank, int world, tt_ctx_t* out) {
   if (!out) {
     set_error("out is null");
     return TT_ERR_ARG;
@@ -1370,7 +1461,9 @@ int tt_ctx_create(int device, void* cuda_stream, const uint8_t* nccl_id, int ran
     TTR_CUDA(cudaMemsetAsync(c->flags.p, 0, sizeof(int) * c->nflags, c->stream));
     c->rank = rank;
     c->world = world;
-    if (world > 1) {
+    if (loop) {
+      c->loop = loop->g;
+    } else if (world > 1) {
       if (!nccl_id) {
         set_error("world > 1 needs an NCCL unique id");
         return TT_ERR_ARG;
@@ -1381,6 +1474,41 @@ int tt_ctx_create(int device, void* cuda_stream, const uint8_t* nccl_id, int ran
     *out = c.release();
     return TT_OK;
   });
+}
+
+int tt_ctx_create(int device, void* cuda_stream, const uint8_t* nccl_id, int rank, int world,
+                  tt_ctx_t* out) {
+  return ctx_create(device, cuda_stream, nccl_id, nullptr, rank, world, out);
+}
+
+int tt_loopback_create(int world, tt_loopback_t* out) {
+  if (!out || world < 1 || world > 16) {
+    set_error("tt_loopback_create: need 1 <= world <= 16 and out");
+    return TT_ERR_ARG;
+  }
+  return guarded([&]() -> int {
+    std::unique_ptr<tt_loopback> l(new tt_loopback);
+    l->g = loop_create(world);
+    l->world = world;
+    *out = l.release();
+    return TT_OK;
+  });
+}
+
+int tt_loopback_destroy(tt_loopback_t l) {
+  if (!l) return TT_OK;
+  loop_destroy(l->g);
+  delete l;
+  return TT_OK;
+}
+
+int tt_ctx_create_loopback(int device, void* cuda_stream, tt_loopback_t group, int rank,
+                           tt_ctx_t* out) {
+  if (!group) {
+    set_error("tt_ctx_create_loopback: null group");
+    return TT_ERR_ARG;
+  }
+  return ctx_create(device, cuda_stream, nullptr, group, rank, group->world, out);
 }
 
 int tt_ctx_destroy(tt_ctx_t c) {

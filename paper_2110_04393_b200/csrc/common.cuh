@@ -97,6 +97,7 @@ int ialloc(IBuf& b, size_t n, cudaStream_t s);
 
 // ---------------------------------------------------------------- context
 struct NcclApi;
+struct LoopGroup;   // in-process loopback communicator (comm.cu)
 
 struct Ctx {
   int device = 0;
@@ -105,6 +106,7 @@ struct Ctx {
   bool own_stream = false;
   int rank = 0, world = 1;
   void* comm = nullptr;                 // ncclComm_t
+  LoopGroup* loop = nullptr;            // loopback communicator (borrowed), else NCCL
   bool timing = false;
   double last_ms[8] = {0};
   int sm_count = 148;
@@ -121,7 +123,11 @@ struct Ctx {
 };
 
 int allreduce_sum(Ctx& c, double* buf, size_t n);   // in place, fp64 sum on c.stream
+constexpr int kOpSum = 0, kOpMax = 1, kOpMin = 2;
+int allreduce_i64(Ctx& c, int64_t* hostbuf, size_t n, int op);   // host words, blocking
 int allreduce_sum_i64(Ctx& c, int64_t* hostbuf, size_t n);
+LoopGroup* loop_create(int world);
+void loop_destroy(LoopGroup* g);
 
 // ---------------------------------------------------------------- GEMM
 // C = alpha * op(A) * op(B) + beta * C, column-major, per batch entry.

@@ -442,9 +442,15 @@ int gemm(Ctx& c, bool ta, bool tb, const GemmDesc* d, int nbatch, double alpha, 
       const GemmDesc& x = d[done + i];
       if (x.M <= 0 || x.N <= 0) continue;
       if (x.K <= 0) {
-        // C = beta*C: not needed by the library (K >= 1 always); refuse loudly
-        set_error("gemm with K = 0");
-        return TT_ERR_ARG;
+        // empty contraction (a rank holding no summands in the sharded path):
+        // C = beta*C, only beta = 0 is used (C = 0)
+        if (beta != 0.0 || gate) {
+          set_error("gemm with K = 0 needs beta = 0 and no gate");
+          return TT_ERR_ARG;
+        }
+        TTR_CUDA(cudaMemset2DAsync(x.C, size_t(x.ldc) * sizeof(double), 0,
+                                   size_t(x.M) * sizeof(double), size_t(x.N), s));
+        continue;
       }
       P.d[live++] = x;
       maxM = std::max(maxM, x.M);

@@ -24,7 +24,8 @@ def colmajor(rows, cols, gen, device="cuda"):
 @pytest.mark.parametrize("tb", [False, True])
 @pytest.mark.parametrize("mnk", [(1, 1, 1), (7, 5, 3), (129, 47, 33), (64, 144, 64),
                                  (300, 35, 1000), (144, 144, 20000), (16384, 144, 64),
-                                 (144, 2048, 4096), (35, 1, 2240)])
+                                 (144, 2048, 4096), (35, 1, 2240), (144, 2048, 64),
+                                 (100, 640, 33), (48, 64, 64), (97, 131, 17)])
 def test_dgemm_matches_fp64_reference(ctx, ta, tb, mnk):
     m, n, k = mnk
     g = torch.Generator().manual_seed(m * 7 + n * 3 + k)

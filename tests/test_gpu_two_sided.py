@@ -137,21 +137,19 @@ def test_errors_are_reported(ctx):
 
 
 def test_config5_full_size_in_bench_launch_configuration():
-    """Config 5 at full size (d=50) in bench.py's launch configuration (library on
-    torch's current stream, l = 128, rho = 192).  The oracle needs ~8 CPU-minutes
-    here, so the full-size check is by properties: ranks, finiteness, and the
-    distance to the Alg. 7 result of the same call sequence — both approximate
-    the sum to its 1e-6 noise level (3.1e-6 apart at d = 5 in the oracle) —
-    measured with the library's own tt_inner (Gram identity, adequate at 1e-6)."""
+    """Config 5 at full size (S=32, d=50, I=256, summand rank 64; l = 128,
+    rho = 192) in bench.py's launch configuration (library on torch's current
+    stream), against the oracle's Alg. 6 on the host (round_sum_2s, minutes) in
+    TT arithmetic at the 1e-10 bar -- the depth at which the bond scaling and the
+    output gauge rebalancing matter (DESIGN.md §6 "Two-sided design")."""
     import paper_2110_04393_b200 as P
     w = ttsynth.config5_large()
     c = P.Context(0, stream=torch.cuda.current_stream())
-    t = gpu_terms(w.terms)
-    a = c.tt_round_sum_two_sided(t, w.rank, seed=1)
-    b = c.tt_round_sum(t, mode="rank", rank=w.rank, oversample=w.ell - w.rank, seed=1)
-    assert a.ranks == [1] + [w.rank] * (w.d - 1) + [1]
-    ca, cb = a.cores, b.cores
-    assert all(bool(torch.isfinite(x).all()) for x in ca)
-    aa, bb, ab = c.tt_inner(ca, ca), c.tt_inner(cb, cb), c.tt_inner(ca, cb)
-    d2 = max(aa - 2 * ab + bb, 0.0)
-    assert math.sqrt(d2 / bb) < 1e-4, math.sqrt(d2 / bb)
+    res = c.tt_round_sum_two_sided(gpu_terms(w.terms), w.rank, seed=1)
+    X = res.numpy()
+    assert res.ranks == [1] + [w.rank] * (w.d - 1) + [1]
+    del res
+    ref, _, _ = oracle.round_sum_2s([ttsynth.to_numpy(t) for t in w.terms], w.rank, 0, 1)
+    assert oracle.ranks_of(ref) == [1] + [w.rank] * (w.d - 1) + [1]
+    r = oracle.rel_diff(X, ref)
+    assert r <= TOL, r
