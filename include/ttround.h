@@ -243,6 +243,13 @@ int tt_qr(tt_ctx_t ctx, int64_t m, int64_t n, const double* A, int64_t lda,
 int tt_svd_jacobi(tt_ctx_t ctx, int64_t m, int64_t n, const double* A, int64_t lda,
                   double* AV, double* V, double* sigma);
 
+/* The truncation's SVD (DESIGN.md §6 "Truncation design"): one-sided Jacobi of
+ * the column-major m x n (n <= m <= 160) device matrix A WITHOUT forming V:
+ * AV = U Sigma (m x n, ld m, columns sorted by descending sigma) and sigma (n).
+ * Used on R^T of the truncation's R-only QR (P:667-670 via Alg. 2 line 7). */
+int tt_svd_nov(tt_ctx_t ctx, int64_t m, int64_t n, const double* A, int64_t lda,
+               double* AV, double* sigma);
+
 #ifdef __cplusplus
 }
 #endif

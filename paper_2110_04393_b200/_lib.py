@@ -78,6 +78,7 @@ def load_library(path: str = LIB_PATH):
                                i64]),
         "tt_qr": (C.c_int, [P, i64, i64, P, i64, P, P, C.POINTER(C.c_int)]),
         "tt_svd_jacobi": (C.c_int, [P, i64, i64, P, i64, P, P, P]),
+        "tt_svd_nov": (C.c_int, [P, i64, i64, P, i64, P, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -375,3 +376,14 @@ class Context:
         _check(L.tt_svd_jacobi(self.handle, m, n, A.data_ptr(), A.stride(1), AV.data_ptr(),
                                V.data_ptr(), s.data_ptr()))
         return AV, V, s
+
+    def tt_svd_nov(self, A: torch.Tensor):
+        """V-free one-sided Jacobi (the truncation's SVD): (U Sigma, sigma)."""
+        L = load_library()
+        m, n = A.shape
+        assert A.stride(0) == 1
+        AV = torch.empty((n, m), dtype=torch.float64, device=A.device).t()
+        s = torch.empty((n,), dtype=torch.float64, device=A.device)
+        _check(L.tt_svd_nov(self.handle, m, n, A.data_ptr(), A.stride(1), AV.data_ptr(),
+                            s.data_ptr()))
+        return AV, s

@@ -61,6 +61,34 @@ int ialloc(IBuf& b, size_t n, cudaStream_t s) {
   return TT_OK;
 }
 
+int side_ctx(Ctx& c, Ctx** out) {
+  if (!c.side) {
+    std::unique_ptr<Ctx> x(new Ctx);
+    x->device = c.device;
+    x->sm_count = c.sm_count;
+    x->copy_stream = c.copy_stream;
+    x->flags.p = c.flags.p;   // borrowed (destroy_side clears it)
+    x->flags.s = nullptr;
+    x->nflags = c.nflags;
+    TTR_CUDA(cudaStreamCreateWithFlags(&x->stream, cudaStreamNonBlocking));
+    c.side = std::move(x);
+  }
+  *out = c.side.get();
+  return TT_OK;
+}
+
+void destroy_side(Ctx& c) {
+  if (!c.side) return;
+  Ctx& x = *c.side;
+  cudaStreamSynchronize(x.stream);
+  x.gemm_ws.release();
+  x.scratch.release();
+  x.flags.p = nullptr;
+  cudaStreamSynchronize(x.stream);
+  cudaStreamDestroy(x.stream);
+  c.side.reset();
+}
+
 int nccl_unique_id(uint8_t id[128]);
 int nccl_comm_create(Ctx& c, const uint8_t* id, int rank, int world);
 int nccl_comm_destroy(Ctx& c);
@@ -539,6 +567,41 @@ int truncate(Ctx& c, tt_tensor& X, double tol, int64_t rmax, std::vector<int64_t
   ks.assign(d + 1, 1);
   IBuf kdev;
   TTR_TRY(ialloc(kdev, 1, s));
+  // The final core H(X_n) <- V_k^T Q^T of bond n is off the critical path (bond
+  // n-1 only needs V(X_{n-1}) U_k S_k): it runs on the side stream, overlapped
+  // with the next bond's QR and SVD.  Buffers the side stream still reads are
+  // kept until the join at the end (`keep`) or freed on the side stream itself.
+  Ctx* side = nullptr;
+  TTR_TRY(side_ctx(c, &side));
+  std::vector<DBuf> keep;
+  std::vector<cudaEvent_t> evs;
+  struct EvGuard {
+    std::vector<cudaEvent_t>& e;
+    ~EvGuard() { for (auto x : e) cudaEventDestroy(x); }
+  } evg{evs};
+  // join (also on an error return, before `keep` is released): the main stream
+  // waits for everything the side stream was given
+  struct Join {
+    cudaStream_t main, side;
+    ~Join() {
+      cudaEvent_t e;
+      if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) {
+        cudaStreamSynchronize(side);
+        return;
+      }
+      cudaEventRecord(e, side);
+      cudaStreamWaitEvent(main, e, 0);
+      cudaEventDestroy(e);
+    }
+  } join{s, side->stream};
+  auto fork = [&]() -> int {   // side stream waits for everything enqueued on s so far
+    cudaEvent_t e;
+    TTR_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    evs.push_back(e);
+    TTR_CUDA(cudaEventRecord(e, s));
+    TTR_CUDA(cudaStreamWaitEvent(side->stream, e, 0));
+    return TT_OK;
+  };
   for (int n = d; n >= 2; --n) {
     const int64_t In = X.dims[n - 1];
     const int64_t r0 = r[n - 1];
@@ -588,9 +651,15 @@ int truncate(Ctx& c, tt_tensor& X, double tol, int64_t rmax, std::vector<int64_t
     TTR_TRY(dalloc(newn, size_t(k) * mrow, s));
     if (fast) {
       TTR_TRY(dalloc(Bk, size_t(r0) * k, s));
-      TTR_TRY(scale_by_inv_sigma(c, AV.p, r0, k, sig.p, Bk.p, 4, double(r0) * 0x1p-52, s));
-      TTR_TRY(gemm1(c, true, false, int(k), int(mrow), int(r0), 1.0, Bk.p, int(r0),
-                    X.bufs[n - 1].p, int(r0), 0.0, newn.p, int(k), s));
+      TTR_TRY(fork());
+      const cudaStream_t ss = side->stream;
+      TTR_TRY(scale_by_inv_sigma(*side, AV.p, r0, k, sig.p, Bk.p, 4, double(r0) * 0x1p-52, ss));
+      TTR_TRY(gemm1(*side, true, false, int(k), int(mrow), int(r0), 1.0, Bk.p, int(r0),
+                    X.bufs[n - 1].p, int(r0), 0.0, newn.p, int(k), ss));
+      Bk.s = ss;                     // read by the side stream only
+      X.bufs[n - 1].s = ss;          // the old core: read last by the GEMM above
+      keep.push_back(std::move(AV));   // also read by V(X_{n-1}) U_k S_k below (main)
+      keep.push_back(std::move(sig));
     } else if (mrow >= r0) {
       TTR_TRY(gemm1(c, true, true, int(k), int(mrow), int(r0), 1.0, V.p, int(cols), Q.p,
                     int(mrow), 0.0, newn.p, int(k), s));
@@ -600,7 +669,8 @@ int truncate(Ctx& c, tt_tensor& X, double tol, int64_t rmax, std::vector<int64_t
     // V(X_{n-1}) <- V(X_{n-1}) U_k S_k
     const int64_t mp = r[n - 2] * X.dims[n - 2];
     TTR_TRY(dalloc(newp, size_t(mp) * k, s));
-    TTR_TRY(gemm1(c, false, false, int(mp), int(k), int(r0), 1.0, X.bufs[n - 2].p, int(mp), AV.p,
+    const double* avp = fast ? keep[keep.size() - 2].p : AV.p;
+    TTR_TRY(gemm1(c, false, false, int(mp), int(k), int(r0), 1.0, X.bufs[n - 2].p, int(mp), avp,
                   int(rows_av), 0.0, newp.p, int(mp), s));
     X.bufs[n - 1] = std::move(newn);
     X.bufs[n - 2] = std::move(newp);
@@ -1517,6 +1587,7 @@ int tt_ctx_destroy(tt_ctx_t c) {
     cudaSetDevice(c->device);
     c->alive->store(false);
     cudaStreamSynchronize(c->stream);
+    destroy_side(*c);
     nccl_comm_destroy(*c);
     c->gemm_ws.release();
     c->scratch.release();
@@ -1701,6 +1772,17 @@ int tt_qr(tt_ctx_t c, int64_t m, int64_t n, const double* A, int64_t lda, double
     int fl[16];
     TTR_TRY(read_flags(*c, fl, 16));
     if (fallback) *fallback = (fl[1] || fl[14]) ? 1 : 0;
+    return TT_OK;
+  });
+}
+
+int tt_svd_nov(tt_ctx_t c, int64_t m, int64_t n, const double* A, int64_t lda, double* AV,
+               double* sigma) {
+  if (!c || !A || !AV || !sigma) return TT_ERR_ARG;
+  return guarded([&]() -> int {
+    TTR_CUDA(cudaSetDevice(c->device));
+    TTR_TRY(svd_nov(*c, m, n, A, lda, AV, sigma, c->stream));
+    TTR_CUDA(cudaStreamSynchronize(c->stream));
     return TT_OK;
   });
 }

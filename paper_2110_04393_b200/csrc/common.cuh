@@ -120,7 +120,13 @@ struct Ctx {
   // false once the context (and its stream) is destroyed: results and sketches
   // created on it then free their memory after a device-wide synchronisation
   std::shared_ptr<std::atomic<bool>> alive = std::make_shared<std::atomic<bool>>(true);
+  // lazily created second stream with its own GEMM workspace (side_ctx()),
+  // for work off a sweep's critical path; shares `flags`
+  std::unique_ptr<Ctx> side;
 };
+// The side context of c (created on first use); destroyed with c (destroy_side).
+int side_ctx(Ctx& c, Ctx** out);
+void destroy_side(Ctx& c);
 
 int allreduce_sum(Ctx& c, double* buf, size_t n);   // in place, fp64 sum on c.stream
 constexpr int kOpSum = 0, kOpMax = 1, kOpMin = 2;

@@ -9,6 +9,9 @@
 //
 // On B200 tcgen05.mma has no f64 kind (ptxas rejects .kind::f64), so the
 // warp-level DMMA is the FP64 tensor path; see DESIGN.md §Kernels.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "common.cuh"
 
 namespace ttr {
@@ -280,6 +283,191 @@ __global__ void __launch_bounds__(WM* WN * 32)
   }
 }
 
+// ------------------------------------------------------------------ TMA-fed variant
+// The same tiles, warp layout, k order and epilogue as dgemm_kernel (so the
+// results are bit-identical), but every operand tile is moved global -> shared
+// by the Tensor Memory Accelerator: one elected thread issues a 2-D
+// cp.async.bulk.tensor per operand per stage, completion is tracked by one
+// mbarrier per stage (expect-tx bytes), and no thread computes a global address.
+// The box of a tile is its padded shared-memory footprint (leading dimension
+// LD = tile + 4 doubles, ≡ 4 mod 16: conflict-free fragment loads), i.e. TMA
+// over-fetches 4 rows that the fragments never read; rows/columns past the
+// matrix edge are zero-filled by the TMA unit (the cp.async path's predicate).
+constexpr int kMaxTmaBatch = 32;
+
+struct TmaParams {
+  GemmParams g;
+  alignas(64) CUtensorMap tm[2 * kMaxTmaBatch];   // [2b] = A of entry b, [2b+1] = B
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool TA, bool TB>
+struct TmaCfg {
+  using C = Cfg<BM, BN, BK, WM, WN, STAGES, TA, TB>;
+  static constexpr int AB = ((C::AEL * 8 + 127) / 128) * 128;   // bytes, 128-aligned
+  static constexpr int BB = ((C::BEL * 8 + 127) / 128) * 128;
+  static constexpr int SB = AB + BB;
+  static constexpr size_t SMEM = size_t(STAGES) * SB + 128 + 8 * STAGES;
+  static constexpr uint32_t TX = uint32_t(C::AEL + C::BEL) * 8;   // full boxes, OOB included
+};
+
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool TA, bool TB>
+__global__ void __launch_bounds__(WM* WN * 32)
+    dgemm_tma_kernel(const __grid_constant__ TmaParams T) {
+  using C = Cfg<BM, BN, BK, WM, WN, STAGES, TA, TB>;
+  using X = TmaCfg<BM, BN, BK, WM, WN, STAGES, TA, TB>;
+  extern __shared__ __align__(128) unsigned char tsm[];
+  const GemmParams& P = T.g;
+  if (P.gate && *P.gate != P.gate_val) return;
+  unsigned char* base = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(tsm) + 127) & ~uintptr_t(127));
+  uint64_t* full = reinterpret_cast<uint64_t*>(base + STAGES * X::SB);
+
+  const int tn = blockIdx.x, tm = blockIdx.y;
+  const int b = blockIdx.z % P.nbatch;
+  const int ks = blockIdx.z / P.nbatch;
+  const GemmDesc& D = P.d[b];
+  const int m0 = tm * BM, n0 = tn * BN;
+  if ((P.flags & kGemmLower) && m0 + BM <= n0) return;
+  const bool tile_live = (m0 < D.M) && (n0 < D.N);
+  if (!tile_live && P.kslices == 1) return;
+
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int wm0 = (warp % WM) * C::TM;
+  const int wn0 = (warp / WM) * C::TN;
+  const int kbeg = ks * P.kchunk;
+  const int kend = min(min(D.K, kbeg + P.kchunk), (P.flags & kGemmTriB) ? n0 + BN : D.K);
+  const int KT = (tile_live && kend > kbeg) ? (kend - kbeg + BK - 1) / BK : 0;
+  const CUtensorMap* mapA = &T.tm[2 * b];
+  const CUtensorMap* mapB = &T.tm[2 * b + 1];
+
+  if (tid == 0) {
+#pragma unroll
+    for (int s2 = 0; s2 < STAGES; ++s2) mbar_init(full + s2, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  // stage `slot` <- k-tile kt: A box at (row m0, col k0) [or (k0, m0) when
+  // transposed], B box at (k0, n0) [or (n0, k0)]; coordinates innermost first
+  auto issue = [&](int slot, int kt) {
+    unsigned char* sA = base + slot * X::SB;
+    unsigned char* sB = sA + X::AB;
+    const int k0 = kbeg + kt * BK;
+    mbar_expect_tx(full + slot, X::TX);
+    if (TA) tma_load_2d(sA, mapA, k0, m0, full + slot);
+    else tma_load_2d(sA, mapA, m0, k0, full + slot);
+    if (TB) tma_load_2d(sB, mapB, n0, k0, full + slot);
+    else tma_load_2d(sB, mapB, k0, n0, full + slot);
+  };
+  if (tid == 0) {
+#pragma unroll
+    for (int s2 = 0; s2 < STAGES - 1; ++s2)
+      if (s2 < KT) issue(s2, s2);
+  }
+
+  double acc[C::FM][C::FN][2];
+#pragma unroll
+  for (int i = 0; i < C::FM; ++i)
+#pragma unroll
+    for (int j = 0; j < C::FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  for (int kt = 0; kt < KT; ++kt) {
+    mbar_wait(full + kt % STAGES, uint32_t((kt / STAGES) & 1));
+    __syncthreads();   // every warp is done with the slot refilled below (used at kt - 1)
+    const int nk = kt + STAGES - 1;
+    if (tid == 0 && nk < KT) issue(nk % STAGES, nk);
+    const double* sA = reinterpret_cast<const double*>(base + (kt % STAGES) * X::SB);
+    const double* sB = reinterpret_cast<const double*>(base + (kt % STAGES) * X::SB + X::AB);
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      double af[C::FM], bf[C::FN];
+#pragma unroll
+      for (int i = 0; i < C::FM; ++i) {
+        const int m = wm0 + i * 8 + g;
+        af[i] = TA ? sA[m * C::LDA + kk + t] : sA[(kk + t) * C::LDA + m];
+      }
+#pragma unroll
+      for (int j = 0; j < C::FN; ++j) {
+        const int n = wn0 + j * 8 + g;
+        bf[j] = TB ? sB[(kk + t) * C::LDB + n] : sB[n * C::LDB + kk + t];
+      }
+#pragma unroll
+      for (int i = 0; i < C::FM; ++i)
+#pragma unroll
+        for (int j = 0; j < C::FN; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+  }
+
+  if (P.kslices == 1) {
+    const double alpha = P.alpha, beta = P.beta;
+    double* Cp = D.C;
+    const int64_t ldc = D.ldc;
+#pragma unroll
+    for (int i = 0; i < C::FM; ++i) {
+      const int m = m0 + wm0 + i * 8 + g;
+      if (m >= D.M) continue;
+#pragma unroll
+      for (int j = 0; j < C::FN; ++j) {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int n = n0 + wn0 + j * 8 + 2 * t + e;
+          if (n < D.N) {
+            double* cp = Cp + m + int64_t(n) * ldc;
+            double v = alpha * acc[i][j][e];
+            if (beta != 0.0) v += beta * *cp;
+            *cp = v;
+          }
+        }
+      }
+    }
+  } else {
+    const size_t tile = ((size_t(ks) * P.nbatch + b) * P.tiles_m + tm) * P.tiles_n + tn;
+    double* W = P.ws + tile * (BM * BN);
+#pragma unroll
+    for (int i = 0; i < C::FM; ++i) {
+      const int ml = wm0 + i * 8 + g;
+#pragma unroll
+      for (int j = 0; j < C::FN; ++j) {
+        const int nl = wn0 + j * 8 + 2 * t;
+        W[ml + nl * BM] = acc[i][j][0];
+        W[ml + (nl + 1) * BM] = acc[i][j][1];
+      }
+    }
+  }
+}
+
 // deterministic split-K reduction: slices summed in index order, one output
 // element per thread (grid: tiles x element chunks), slice loads issued ahead
 template <int BM, int BN>
@@ -297,14 +485,25 @@ __global__ void __launch_bounds__(256) splitk_reduce(const __grid_constant__ Gem
   if (m >= D.M || n >= D.N) return;
   const size_t stride = size_t(P.nbatch) * P.tiles_m * P.tiles_n * (BM * BN);
   const double* src = P.ws + ((size_t(b) * P.tiles_m + tm) * P.tiles_n + tn) * (BM * BN) + e;
+  // slices summed in index order (deterministic); loads issued 16 deep so the
+  // few threads of a small reduction keep enough L2 requests in flight
   double s = 0.0;
   int k = 0;
-  for (; k + 4 <= P.kslices; k += 4) {
-    const double v0 = src[k * stride], v1 = src[(k + 1) * stride];
-    const double v2 = src[(k + 2) * stride], v3 = src[(k + 3) * stride];
-    s = (((s + v0) + v1) + v2) + v3;
+  for (; k + 16 <= P.kslices; k += 16) {
+    double v[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) v[q] = __ldcg(src + size_t(k + q) * stride);
+#pragma unroll
+    for (int q = 0; q < 16; ++q) s += v[q];
   }
-  for (; k < P.kslices; ++k) s += src[k * stride];
+  for (; k + 4 <= P.kslices; k += 4) {
+    double v[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) v[q] = __ldcg(src + size_t(k + q) * stride);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) s += v[q];
+  }
+  for (; k < P.kslices; ++k) s += __ldcg(src + size_t(k) * stride);
   double* cp = D.C + m + int64_t(n) * D.ldc;
   double v = P.alpha * s;
   if (P.beta != 0.0) v += P.beta * *cp;
@@ -316,12 +515,54 @@ struct Shape {
   static constexpr int bm = BM, bn = BN, bk = BK, wm = WM, wn = WN, st = STAGES;
 };
 
+// cuTensorMapEncodeTiled from the driver (no link-time dependency on libcuda)
+PFN_cuTensorMapEncodeTiled_v12000 tma_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    else
+      cudaGetLastError();
+  });
+  return fn;
+}
+
+// 2-D map of a column-major rows x cols fp64 matrix (leading dimension ld) with
+// box {box0 (contiguous), box1}; false if TMA cannot address it
+bool encode_map(CUtensorMap* m, const double* ptr, int64_t rows, int64_t cols, int64_t ld,
+                int box0, int box1) {
+  auto enc = tma_encoder();
+  if (!enc || rows < 1 || cols < 1) return false;
+  if ((reinterpret_cast<uintptr_t>(ptr) & 15) || (ld & 1) || ld < rows) return false;
+  cuuint64_t dims[2] = {cuuint64_t(rows), cuuint64_t(cols)};
+  cuuint64_t strides[1] = {cuuint64_t(ld) * 8};
+  cuuint32_t box[2] = {cuuint32_t(box0), cuuint32_t(box1)};
+  cuuint32_t estr[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(ptr), dims, strides, box,
+             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+         CUDA_SUCCESS;
+}
+
+bool tma_disabled() {
+  static const bool off = getenv("TTR_NO_TMA") != nullptr;   // A/B switch (diagnostics)
+  return off;
+}
+
 template <class S, bool TA, bool TB>
 int launch_cfg(Ctx& c, GemmParams& P, int maxM, int maxN, int maxK, cudaStream_t s) {
   using C = Cfg<S::bm, S::bn, S::bk, S::wm, S::wn, S::st, TA, TB>;
+  using X = TmaCfg<S::bm, S::bn, S::bk, S::wm, S::wn, S::st, TA, TB>;
   auto kern = dgemm_kernel<S::bm, S::bn, S::bk, S::wm, S::wn, S::st, TA, TB>;
+  auto tkern = dgemm_tma_kernel<S::bm, S::bn, S::bk, S::wm, S::wn, S::st, TA, TB>;
   static std::atomic<bool> attr_set[64];
-  static int resident[64] = {0};   // CTAs of this configuration per SM
+  static int resident[64] = {0};    // CTAs of this configuration per SM (cp.async kernel)
+  static int tresident[64] = {0};   // ... (TMA kernel)
   int dev = c.device;
   std::unique_lock<std::mutex> init_lock(init_mutex(), std::defer_lock);
   if (!attr_set[dev & 63]) init_lock.lock();   // first calls may come from several threads
@@ -331,14 +572,29 @@ int launch_cfg(Ctx& c, GemmParams& P, int maxM, int maxN, int maxK, cudaStream_t
     int nb = 1;
     TTR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, C::NT, C::SMEM));
     resident[dev & 63] = std::max(1, nb);
+    TTR_CUDA(cudaFuncSetAttribute(tkern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  int(X::SMEM)));
+    nb = 1;
+    TTR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, tkern, C::NT, X::SMEM));
+    tresident[dev & 63] = std::max(1, nb);
     attr_set[dev & 63] = true;
+  }
+  // TMA path when every entry's operands are addressable by a tensor map
+  static thread_local TmaParams TP;
+  bool use_tma = !tma_disabled() && P.nbatch <= kMaxTmaBatch;
+  for (int b = 0; use_tma && b < P.nbatch; ++b) {
+    const GemmDesc& D = P.d[b];
+    use_tma = (TA ? encode_map(&TP.tm[2 * b], D.A, D.K, D.M, D.lda, C::LDA, S::bm)
+                  : encode_map(&TP.tm[2 * b], D.A, D.M, D.K, D.lda, C::LDA, S::bk)) &&
+              (TB ? encode_map(&TP.tm[2 * b + 1], D.B, D.N, D.K, D.ldb, C::LDB, S::bk)
+                  : encode_map(&TP.tm[2 * b + 1], D.B, D.K, D.N, D.ldb, C::LDB, S::bn));
   }
   P.tiles_m = (maxM + S::bm - 1) / S::bm;
   P.tiles_n = (maxN + S::bn - 1) / S::bn;
   // split-K, wave-aware: pick the slice count whose grid fills the resident CTA
   // slots (SMs x CTAs per SM) best -- a grid of 1.13 waves runs at 57% -- with
   // a small penalty per slice for the extra partial traffic and reduction
-  const long slots = long(c.sm_count) * resident[dev & 63];
+  const long slots = long(c.sm_count) * (use_tma ? tresident[dev & 63] : resident[dev & 63]);
   const long tiles = long(P.tiles_m) * P.tiles_n * P.nbatch;
   const int ktiles = (maxK + S::bk - 1) / S::bk;
   int ksl = 1;
@@ -376,7 +632,12 @@ int launch_cfg(Ctx& c, GemmParams& P, int maxM, int maxN, int maxK, cudaStream_t
     set_error("gemm grid too large (%d x %d x %d)", grid.x, grid.y, grid.z);
     return TT_ERR_ARG;
   }
-  kern<<<grid, C::NT, C::SMEM, s>>>(P);
+  if (use_tma) {
+    TP.g = P;
+    tkern<<<grid, C::NT, X::SMEM, s>>>(TP);
+  } else {
+    kern<<<grid, C::NT, C::SMEM, s>>>(P);
+  }
   TTR_TRY(launched());
   if (ksl > 1) {
     splitk_reduce<S::bm, S::bn><<<dim3(P.tiles_n * P.tiles_m * P.nbatch,

@@ -18,6 +18,8 @@
 // rank-deficient bond matrices of config 5.
 #include <cooperative_groups.h>
 #include <math.h>
+#include <stdlib.h>
+#include <string.h>
 
 #include "common.cuh"
 
@@ -205,7 +207,9 @@ int svd_nov(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, double* 
     set_error("svd_nov: unsupported shape m=%lld n=%lld", (long long)m, (long long)n);
     return TT_ERR_ARG;
   }
-  if (svd_cluster_fits(m, n)) return svd_nov_cluster(c, m, n, A, lda, AV, sigma, s);
+  static const char* force = getenv("TTR_JACOBI");   // diagnostics: "cta" = single-CTA kernel
+  const bool cta = force && strcmp(force, "cta") == 0;
+  if (!cta && svd_cluster_fits(m, n)) return svd_nov_cluster(c, m, n, A, lda, AV, sigma, s);
   if (m <= 16) return launch_rr<2>(c, m, n, A, lda, AV, sigma, s);
   if (m <= 32) return launch_rr<4>(c, m, n, A, lda, AV, sigma, s);
   if (m <= 64) return launch_rr<8>(c, m, n, A, lda, AV, sigma, s);
