@@ -554,12 +554,19 @@ bool tma_disabled() {
   return off;
 }
 
+#ifndef TTR_TMA_STAGES
+#define TTR_TMA_STAGES 0   // 0: the shape's own stage count
+#endif
+template <class S>
+constexpr int tma_stages() { return TTR_TMA_STAGES > 0 ? TTR_TMA_STAGES : S::st; }
+
 template <class S, bool TA, bool TB>
 int launch_cfg(Ctx& c, GemmParams& P, int maxM, int maxN, int maxK, cudaStream_t s) {
   using C = Cfg<S::bm, S::bn, S::bk, S::wm, S::wn, S::st, TA, TB>;
-  using X = TmaCfg<S::bm, S::bn, S::bk, S::wm, S::wn, S::st, TA, TB>;
+  constexpr int TS = tma_stages<S>();
+  using X = TmaCfg<S::bm, S::bn, S::bk, S::wm, S::wn, TS, TA, TB>;
   auto kern = dgemm_kernel<S::bm, S::bn, S::bk, S::wm, S::wn, S::st, TA, TB>;
-  auto tkern = dgemm_tma_kernel<S::bm, S::bn, S::bk, S::wm, S::wn, S::st, TA, TB>;
+  auto tkern = dgemm_tma_kernel<S::bm, S::bn, S::bk, S::wm, S::wn, TS, TA, TB>;
   static std::atomic<bool> attr_set[64];
   static int resident[64] = {0};    // CTAs of this configuration per SM (cp.async kernel)
   static int tresident[64] = {0};   // ... (TMA kernel)

@@ -317,7 +317,8 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
   if (gate && *gate != gate_val) return;
   extern __shared__ double S[];
   __shared__ double rdiag[32 * NB];   // 1 / L(i, i)
-  __shared__ double colb[64];         // pivot column broadcast (C1), doubled
+  __shared__ double colb[128];        // pivot column broadcast (C1), doubled, x2 buffers
+  __shared__ double ttmp[256];        // 16 x 16 product L21 X11 of the diagonal-block inverse
   __shared__ double s_tr, s_dmax;
   __shared__ int s_bad, s_zero, s_clamped;
   constexpr int NW = kBlkThreads / 32;
@@ -424,51 +425,116 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
         if (bad) s_bad = 1;
         if (nclamp) s_clamped += nclamp;
       }
+      CHOL_PROF(6);
+      // X_kk = L_kk^{-1} (lower), 2 x 2 blocked: lanes 0-15 invert the 16 x 16
+      // L11, lanes 16-31 L22 (column-wise forward substitution, lane = column,
+      // the column in registers, L rows broadcast from shared memory); then
+      // X21 = -X22 (L21 X11) on DMMA tiles.  X(r, c), r > c, is parked at (c, r)
+      // in the unused upper triangle of the block, the diagonal is rdiag (the
+      // panel below and the inverse phase read it there)
+      __syncwarp();
+      {
+        const int h = lane >> 4, c = lane & 15, o = 16 * h;
+        double x[16];
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+          double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+          for (int t = 0; t < r; ++t) {
+            const double l = (o + r < kb) ? S[(k0 + o + r) + (k0 + o + t) * ld] : 0.0;
+            if (t & 1) s1 = fma(l, x[t], s1);
+            else s0 = fma(l, x[t], s0);
+          }
+          const double rdr = (o + r < kb) ? rdiag[k0 + o + r] : 0.0;
+          x[r] = (r < c || o + r >= kb) ? 0.0 : (r == c ? rdr : -rdr * (s0 + s1));
+        }
+#pragma unroll
+        for (int r = 1; r < 16; ++r)
+          if (r > c && o + r < kb) S[(k0 + o + c) + (k0 + o + r) * ld] = x[r];
+      }
+      __syncwarp();
+      if (kb > 16) {
+        // X11(row, col) / X22(row, col), block-local 0..15, row >= col
+        auto x11 = [&](int row, int col) -> double {
+          return row < col ? 0.0
+                           : (row == col ? rdiag[k0 + row] : S[(k0 + col) + (k0 + row) * ld]);
+        };
+        auto x22 = [&](int row, int col) -> double {
+          if (row < col || 16 + row >= kb) return 0.0;
+          return row == col ? rdiag[k0 + 16 + row] : S[(k0 + 16 + col) + (k0 + 16 + row) * ld];
+        };
+        double tacc[4][2];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {   // T = L21 X11, tile (8 (q >> 1), 8 (q & 1))
+          const int R = 8 * (q >> 1), C = 8 * (q & 1);
+          tacc[q][0] = tacc[q][1] = 0.0;
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+            const int kc = 4 * kk + t4;
+            const double av = (16 + R + g < kb) ? S[(k0 + 16 + R + g) + (k0 + kc) * ld] : 0.0;
+            dmma884(tacc[q][0], tacc[q][1], av, x11(kc, C + g));
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int R = 8 * (q >> 1), C = 8 * (q & 1);
+          ttmp[(R + g) + 16 * (C + 2 * t4)] = tacc[q][0];
+          ttmp[(R + g) + 16 * (C + 2 * t4 + 1)] = tacc[q][1];
+        }
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {   // X21 = -X22 T
+          const int R = 8 * (q >> 1), C = 8 * (q & 1);
+          double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+            const int kc = 4 * kk + t4;
+            dmma884(c0, c1, x22(R + g, kc), ttmp[kc + 16 * (C + g)]);
+          }
+          const int r = R + g, cA = C + 2 * t4;   // X(16 + r, cA) parked at (cA, 16 + r)
+          if (16 + r < kb) {
+            S[(k0 + cA) + (k0 + 16 + r) * ld] = -c0;
+            S[(k0 + cA + 1) + (k0 + 16 + r) * ld] = -c1;
+          }
+        }
+      }
     }
     __syncthreads();
     CHOL_PROF(0);
     if (s_bad) break;
     const int r0 = k0 + kb;   // first row below the block (kb == 32 if r0 < n)
     if (r0 >= n) break;
-    // ---- C2: panel, row r by 4 threads (columns 8q .. 8q+7 of the block)
+    // ---- C2: panel L_ik = A_ik X_kk^T on 8x8 DMMA tiles (K = 32); all tiles
+    // to registers first (a tile reads the whole 32-column row block it overwrites)
     {
-      const int rho = tid >> 2, qt = tid & 3;
-      const int r = r0 + rho;
-      const bool live = r < n;
-      double a[8];
+      const int tb = r0 / 8, nrt = nt8 - tb, ntiles = nrt * 4;
+      double acc[4][2];
 #pragma unroll
-      for (int jj = 0; jj < 8; ++jj) a[jj] = live ? S[r + (k0 + 8 * qt + jj) * ld] : 0.0;
+      for (int q = 0; q < 4; ++q) {
+        acc[q][0] = acc[q][1] = 0.0;
+        const int tt = w + NW * q;
+        if (tt < ntiles) {
+          const int R = 8 * (tb + tt / 4), cb = 8 * (tt % 4);
 #pragma unroll
-      for (int qq = 0; qq < 4; ++qq) {
-        if (qt == qq) {
-#pragma unroll
-          for (int jj = 0; jj < 8; ++jj) {
-            const int c = 8 * qq + jj;
-            a[jj] *= rdiag[k0 + c];
-#pragma unroll
-            for (int j2 = jj + 1; j2 < 8; ++j2)
-              a[j2] = fma(-a[jj], S[(k0 + 8 * qq + j2) + (k0 + c) * ld], a[j2]);
-          }
-        }
-        double xq[8];
-#pragma unroll
-        for (int jj = 0; jj < 8; ++jj)   // every lane reaches this: full mask, no divergence checks
-          xq[jj] = __shfl_sync(0xffffffffu, a[jj], (lane & 28) | qq);
-        if (qt > qq) {
-#pragma unroll
-          for (int j2 = 0; j2 < 8; ++j2) {
-            const int c2 = 8 * qt + j2;
-            double acc = a[j2];
-#pragma unroll
-            for (int jj = 0; jj < 8; ++jj)
-              acc = fma(-xq[jj], S[(k0 + c2) + (k0 + 8 * qq + jj) * ld], acc);
-            a[j2] = acc;
+          for (int kk = 0; kk < 8; ++kk) {
+            const int tl = 4 * kk + t4, cl = cb + g;   // B(tl, cl) = X_kk(cl, tl)
+            const double av = S[(R + g) + (k0 + tl) * ld];
+            const double bv = (cl < tl) ? 0.0
+                              : (cl == tl ? rdiag[k0 + cl] : S[(k0 + tl) + (k0 + cl) * ld]);
+            dmma884(acc[q][0], acc[q][1], av, bv);
           }
         }
       }
-      if (live) {
+      __syncthreads();
 #pragma unroll
-        for (int jj = 0; jj < 8; ++jj) S[r + (k0 + 8 * qt + jj) * ld] = a[jj];
+      for (int q = 0; q < 4; ++q) {
+        const int tt = w + NW * q;
+        if (tt < ntiles) {
+          const int R = 8 * (tb + tt / 4), C = k0 + 8 * (tt % 4);
+          const int r = R + g, cA = C + 2 * t4;
+          S[r + cA * ld] = acc[q][0];
+          S[r + (cA + 1) * ld] = acc[q][1];
+        }
       }
     }
     __syncthreads();
@@ -528,30 +594,8 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
     for (int c = w; c < n; c += NW)
       for (int r = lane; r < n; r += 32)   // R(r, c) = L(c, r)
         Rout[r + int64_t(c) * n] = (c >= r) ? S[c + r * ld] : 0.0;
-  // ---- I0: X_kk = L_kk^{-1} for every block at once (warp k), lane c = column
-  // c; X(r, c) (r > c) is parked at (c, r), the diagonal is rdiag
-  if (w < nb) {
-    const int k0 = 32 * w, kb = min(32, n - k0);
-    const int c = lane;
-    if (c < kb) {
-      const double* Lr = S + k0 + k0 * ld;         // L(k0 + r, k0 + t) = Lr[r + t ld]
-      double* Xc = S + (k0 + c) + k0 * ld;         // X(t, c) parked at Xc[t ld]
-#pragma unroll 1
-      for (int r = c + 1; r < kb; ++r) {
-        double a0 = -Lr[r + c * ld] * rdiag[k0 + c], a1 = 0.0, a2 = 0.0, a3 = 0.0;
-        int t = c + 1;
-#pragma unroll 1
-        for (; t + 3 < r; t += 4) {
-          a0 = fma(-Lr[r + t * ld], Xc[t * ld], a0);
-          a1 = fma(-Lr[r + (t + 1) * ld], Xc[(t + 1) * ld], a1);
-          a2 = fma(-Lr[r + (t + 2) * ld], Xc[(t + 2) * ld], a2);
-          a3 = fma(-Lr[r + (t + 3) * ld], Xc[(t + 3) * ld], a3);
-        }
-        for (; t < r; ++t) a0 = fma(-Lr[r + t * ld], Xc[t * ld], a0);
-        Xc[r * ld] = ((a0 + a1) + (a2 + a3)) * rdiag[k0 + r];
-      }
-    }
-  }
+  // (X_kk = L_kk^{-1} of every diagonal block was formed right after its
+  // factorisation, parked in the block's upper triangle, diagonal in rdiag)
   __syncthreads();
   CHOL_PROF(3);
   // ---- X = L^{-1} in place, block columns right to left

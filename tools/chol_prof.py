@@ -20,10 +20,11 @@ for _ in range(3):
     ctx.tt_qr(A, want_r=True)
 torch.cuda.synchronize()
 w = ctx.status_words(64)
-names = ["C1", "C2", "C3", "I0", "Iblk", "load"]
-tot = sum(w[32:38])
+names = ["C1-Xkk", "C2", "C3", "I0", "Iblk", "load", "C1-fact"]
+tot = sum(w[32:39])
 calls = max(1, w[8] + 3 * w[10] + 4 * w[15])
 print("status", w[:17])
+ncall = 2 * w[8] + 3 * w[10] + 4 * w[15] + (2 if w[10] else 0)   # route 0 attempt + route 1
 for i, nm in enumerate(names):
-    print(f"{nm:5s} {w[32 + i] * 64 / 3:10.0f} cycles per QR  ({100 * w[32 + i] / max(tot, 1):.1f}%)")
-print("cycles per QR (all Cholesky calls):", tot * 64 / 3)
+    print(f"{nm:8s} {w[32 + i] * 64 / max(ncall, 1):10.0f} cycles per Cholesky call  ({100 * w[32 + i] / max(tot, 1):.1f}%)")
+print("cycles per Cholesky call:", tot * 64 / max(ncall, 1), "calls", ncall)
