@@ -15,13 +15,13 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
          "--expt-relaxed-constexpr", "-I/usr/include"] + os.environ.get("TTR_EXTRA_FLAGS", "").split()
-SOURCES = ["api.cu", "gemm.cu", "linalg.cu", "svd.cu", "comm.cu"]
+SOURCES = ["api.cu", "gemm.cu", "linalg.cu", "svd.cu", "comm.cu", "fused.cu"]
 
 
 def _compile(src):
     obj = os.path.join(BUILD, src.replace(".cu", ".o"))
     srcp = os.path.join(CSRC, src)
-    deps = [srcp, os.path.join(CSRC, "common.cuh"),
+    deps = [srcp, os.path.join(CSRC, "common.cuh"), os.path.join(CSRC, "dmma_tma.cuh"),
             os.path.join(HERE, "..", "include", "ttround.h")]
     if os.path.exists(obj) and all(os.path.getmtime(obj) >= os.path.getmtime(d) for d in deps):
         return obj, ""

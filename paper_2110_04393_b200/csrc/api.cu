@@ -512,18 +512,40 @@ int alg7(Ctx& c, const Terms& T, const std::vector<int64_t>& dims, const std::ve
     TTR_TRY(qr(c, m, l[n], Yb.p, m, false, out.bufs[n - 1].p, nullptr, s));
     tm.end(3);
     tm.begin(2);
-    // line 11: [M^(1) ... M^(s)] = V(X_n)^T Z_n
-    TTR_TRY(gemm1(c, true, false, int(l[n]), int(sumR[n]), int(m), 1.0, out.bufs[n - 1].p,
-                  int(m), Xcur, int(m), 0.0, Mb.p, int(l[n]), s));
+    int fused = 1;
+    if (n < d - 1) {
+      // lines 11 + 13 in one cooperative launch (fused.cu): M = Q_n^T V(X_n), then
+      // H(X_{n+1}) = [M^(1) H(Y^(1)_{n+1}) ... M^(s) H(Y^(s)_{n+1})]
+      const int64_t In1 = dims[n];
+      std::vector<const double*> y1(S);
+      std::vector<int64_t> rj(S), nj(S), mo(S), xo(S);
+      for (int j = 0; j < S; ++j) {
+        y1[j] = T.core[j][n];
+        rj[j] = T.R[j][n];
+        nj[j] = In1 * T.R[j][n + 1];
+        mo[j] = off[n][j];
+        xo[j] = l[n] * In1 * off[n + 1][j];
+      }
+      fused = proj_carry(c, m, int(l[n]), int(sumR[n]), out.bufs[n - 1].p, Xcur, Mb.p, S,
+                         y1.data(), rj.data(), nj.data(), mo.data(), Xnext, xo.data(), s);
+      if (fused < 0) return fused;
+    }
+    if (fused != 0) {
+      // line 11: [M^(1) ... M^(s)] = V(X_n)^T Z_n
+      TTR_TRY(gemm1(c, true, false, int(l[n]), int(sumR[n]), int(m), 1.0, out.bufs[n - 1].p,
+                    int(m), Xcur, int(m), 0.0, Mb.p, int(l[n]), s));
+    }
     if (n < d - 1) {
       // line 13: H(X_{n+1}) = [M^(1) H(Y^(1)_{n+1}) ... M^(s) H(Y^(s)_{n+1})]
       const int64_t In1 = dims[n];
-      for (int j = 0; j < S; ++j)
-        gd[j] = GemmDesc{Mb.p + l[n] * off[n][j], T.core[j][n],
-                         Xnext + l[n] * In1 * off[n + 1][j], int(l[n]),
-                         int(In1 * T.R[j][n + 1]), int(T.R[j][n]), int(l[n]), int(T.R[j][n]),
-                         int(l[n])};
-      TTR_TRY(gemm(c, false, false, gd.data(), S, 1.0, 0.0, s));
+      if (fused != 0) {
+        for (int j = 0; j < S; ++j)
+          gd[j] = GemmDesc{Mb.p + l[n] * off[n][j], T.core[j][n],
+                           Xnext + l[n] * In1 * off[n + 1][j], int(l[n]),
+                           int(In1 * T.R[j][n + 1]), int(T.R[j][n]), int(l[n]), int(T.R[j][n]),
+                           int(l[n])};
+        TTR_TRY(gemm(c, false, false, gd.data(), S, 1.0, 0.0, s));
+      }
       tm.end(2);
       std::swap(Xcur, Xnext);
     } else {

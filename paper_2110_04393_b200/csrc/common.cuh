@@ -164,6 +164,14 @@ inline int gemm1(Ctx& c, bool ta, bool tb, int M, int N, int K, double alpha,
   return gemm(c, ta, tb, &d, 1, alpha, beta, s, gate, gate_val, flags);
 }
 
+// ---------------------------------------------------------------- fused sweep step
+// Alg. 7 lines 11 + 13 for one step in one cooperative launch (fused.cu):
+// M = Q^T X (l x sumR, ld l), then X1 + xoff[j] = M(:, moff[j] ..) Y1[j] (R_j x N_j,
+// ld R_j) for every summand.  Returns 1 (nothing launched) when it does not apply.
+int proj_carry(Ctx& c, int64_t m, int l, int sumR, const double* Q, const double* Xn, double* M,
+               int S, const double* const* Y1, const int64_t* Rj, const int64_t* Nj,
+               const int64_t* moff, double* X1, const int64_t* xoff, cudaStream_t s);
+
 // ---------------------------------------------------------------- sketch
 int philox_fill(Ctx& c, double* out, int64_t count, uint64_t seed, uint32_t n,
                 uint32_t tag, double scale, cudaStream_t s);

@@ -9,10 +9,8 @@
 //
 // On B200 tcgen05.mma has no f64 kind (ptxas rejects .kind::f64), so the
 // warp-level DMMA is the FP64 tensor path; see DESIGN.md §Kernels.
-#include <cuda.h>
-#include <cudaTypedefs.h>
-
 #include "common.cuh"
+#include "dmma_tma.cuh"
 
 namespace ttr {
 
@@ -532,8 +530,10 @@ PFN_cuTensorMapEncodeTiled_v12000 tma_encoder() {
   return fn;
 }
 
+}  // namespace
+
 // 2-D map of a column-major rows x cols fp64 matrix (leading dimension ld) with
-// box {box0 (contiguous), box1}; false if TMA cannot address it
+// box {box0 (contiguous), box1}; false if TMA cannot address it (dmma_tma.cuh)
 bool encode_map(CUtensorMap* m, const double* ptr, int64_t rows, int64_t cols, int64_t ld,
                 int box0, int box1) {
   auto enc = tma_encoder();
@@ -548,6 +548,8 @@ bool encode_map(CUtensorMap* m, const double* ptr, int64_t rows, int64_t cols, i
              CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
          CUDA_SUCCESS;
 }
+
+namespace {
 
 bool tma_disabled() {
   static const bool off = getenv("TTR_NO_TMA") != nullptr;   // A/B switch (diagnostics)
