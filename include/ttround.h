@@ -189,6 +189,61 @@ int tt_round_deterministic(tt_ctx_t ctx, int32_t S, const tt_view* terms,
 int tt_round_sum_two_sided(tt_ctx_t ctx, int32_t S_local, const tt_view* terms,
                            int64_t ell, int64_t rho, uint64_t seed, tt_tensor_t* out);
 
+/* ---- TT-GMRES on a Kronecker-sum operator --- */
+#define TT_KRON_IDENTITY 0
+#define TT_KRON_DIAG     1
+#define TT_KRON_DENSE    2
+/* The operator  sum_{i=1..nterms} A_{i,1} x ... x A_{i,d}.
+ * kinds[i*d + n] selects factor A_{i,n+1}: TT_KRON_IDENTITY (mats entry ignored),
+ * TT_KRON_DIAG (mats entry: I_n doubles, the diagonal), TT_KRON_DENSE (mats
+ * entry: I_n x I_n column-major).  mats are device pointers of the context's
+ * device (borrowed).  A factor acts on core n by the mode-2 product
+ * core(a, i, b) <- sum_j A(i, j) core(a, j, b) (rank-preserving). */
+typedef struct {
+  int32_t d;
+  int32_t nterms;
+  const int64_t* dims;
+  const int32_t* kinds;
+  const double* const* mats;
+} tt_kron_op;
+
+/* (sum_i A_{i,1} x ... x A_{i,d}) x as its nterms UNROUNDED summands
+ * (P:1033-1035): out[i] has the ranks of x; identity factors copy the core.
+ * out must have room for op->nterms results (each freed by tt_tensor_destroy). */
+int tt_kron_apply(tt_ctx_t ctx, const tt_kron_op* op, const tt_view* x, tt_tensor_t* out);
+
+typedef struct {
+  double   tol;         /* relative residual target (the paper uses 1e-8)          */
+  double   round_tol;   /* eps0 of every rounding; 0 -> tol / 10 (G1)              */
+  int32_t  max_iter;    /* Arnoldi steps (no restart)                                        */
+  int32_t  randomized;  /* 1: every sum rounded by tt_round_sum (Alg. 7 + truncation, TT_TOL,
+                           adaptive sketch rank); 0: by tt_round_deterministic (Alg. 1+2)    */
+  int32_t  precond;     /* 1: right preconditioner ((sum_i A_{i,1})^{-1} x I x ... x I),
+                           P:1036; sum_i A_{i,1} must be symmetric positive definite         */
+  int32_t  oversample;  /* randomized: initial sketch rank = largest summand bond rank + this */
+  int64_t  max_rank;    /* cap on every rounding's rank / sketch rank (0 = none)             */
+  uint64_t seed;        /* rounding call c (0, 1, 2, ... in order) uses seed + c (G4)        */
+} tt_gmres_opts;
+
+typedef struct {
+  int32_t iters;        /* Arnoldi steps taken                                              */
+  int32_t converged;    /* 1 if the residual estimate reached tol                           */
+  int32_t roundings;    /* rounding calls made                                              */
+  int32_t max_basis_rank; /* largest internal rank of a Krylov basis vector V_k             */
+  double  residual;     /* final relative residual estimate |beta e1 - H y| / beta          */
+} tt_gmres_info;
+
+/* Right-preconditioned TT-GMRES for op x = f: per step
+ * Y = P V_k, W = round(sum_i (A_{i,1} x ... ) Y) (a sum of nterms
+ * TT-tensors), h_jk = <V_j, W>, Z = round(W - sum_j h_jk V_j) (k+1
+ * summands), V_{k+1} = Z / ||Z||; the (k+1) x k least-squares
+ * problem on the host (Givens rotations); x = P round(sum_j y_j V_j).  The
+ * result x is library-owned.  residuals (optional, host, max_iter + 1 doubles)
+ * receives the residual estimates (1 first).  Errors: TT_ERR_ARG/SHAPE on a bad
+ * operator, TT_ERR_NUMERIC if the preconditioner's Cholesky fails. */
+int tt_gmres(tt_ctx_t ctx, const tt_kron_op* op, const tt_view* f, const tt_gmres_opts* opts,
+             tt_tensor_t* x, tt_gmres_info* info, double* residuals);
+
 /* <x, y> by the full right-to-left contraction (App. A); *out is a
  * host double.  x and y must have equal dims. */
 int tt_inner(tt_ctx_t ctx, const tt_view* x, const tt_view* y, double* out);

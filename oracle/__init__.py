@@ -18,3 +18,4 @@ invariants).
 """
 from .philox import philox4x32_10, sketch_core, philox_normal  # noqa: F401
 from .tt import *  # noqa: F401,F403
+from . import gmres  # noqa: F401  (TT-GMRES)

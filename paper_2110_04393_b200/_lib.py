@@ -32,6 +32,22 @@ class tt_round_opts(C.Structure):
                 ("max_rank", C.c_int64)]
 
 
+class tt_kron_op(C.Structure):
+    _fields_ = [("d", C.c_int32), ("nterms", C.c_int32), ("dims", C.POINTER(C.c_int64)),
+                ("kinds", C.POINTER(C.c_int32)), ("mats", C.POINTER(C.c_void_p))]
+
+
+class tt_gmres_opts(C.Structure):
+    _fields_ = [("tol", C.c_double), ("round_tol", C.c_double), ("max_iter", C.c_int32),
+                ("randomized", C.c_int32), ("precond", C.c_int32), ("oversample", C.c_int32),
+                ("max_rank", C.c_int64), ("seed", C.c_uint64)]
+
+
+class tt_gmres_info(C.Structure):
+    _fields_ = [("iters", C.c_int32), ("converged", C.c_int32), ("roundings", C.c_int32),
+                ("max_basis_rank", C.c_int32), ("residual", C.c_double)]
+
+
 _lib = None
 
 
@@ -79,6 +95,10 @@ def load_library(path: str = LIB_PATH):
         "tt_qr": (C.c_int, [P, i64, i64, P, i64, P, P, C.POINTER(C.c_int)]),
         "tt_svd_jacobi": (C.c_int, [P, i64, i64, P, i64, P, P, P]),
         "tt_svd_nov": (C.c_int, [P, i64, i64, P, i64, P, P]),
+        "tt_kron_apply": (C.c_int, [P, C.POINTER(tt_kron_op), C.POINTER(tt_view), C.POINTER(P)]),
+        "tt_gmres": (C.c_int, [P, C.POINTER(tt_kron_op), C.POINTER(tt_view),
+                               C.POINTER(tt_gmres_opts), C.POINTER(P), C.POINTER(tt_gmres_info),
+                               C.POINTER(C.c_double)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -387,3 +407,58 @@ class Context:
         _check(L.tt_svd_nov(self.handle, m, n, A.data_ptr(), A.stride(1), AV.data_ptr(),
                             s.data_ptr()))
         return AV, s
+
+    # ---------------------------------------------------------------- TT-GMRES (NEXT-4)
+    def _kron(self, op, dims):
+        """Marshal a Kronecker-sum operator: op[i][n] is None (identity), a 1-D
+        tensor (diagonal) or a 2-D (I, I) tensor (dense A with A[i, j] at row i)."""
+        d, nt = len(dims), len(op)
+        kinds = (C.c_int32 * (nt * d))()
+        mats = (C.c_void_p * (nt * d))()
+        keep = []
+        for i, term in enumerate(op):
+            if len(term) != d:
+                raise ValueError("every operator term needs one factor per mode")
+            for n, A in enumerate(term):
+                if A is None:
+                    kinds[i * d + n] = 0
+                    continue
+                A = torch.as_tensor(A, dtype=torch.float64, device=self.device)
+                if A.dim() == 1:
+                    kinds[i * d + n] = 1
+                    A = A.contiguous()
+                else:
+                    kinds[i * d + n] = 2
+                    A = A.t().contiguous()      # column-major storage of A
+                keep.append(A)
+                mats[i * d + n] = A.data_ptr()
+        dd = (C.c_int64 * d)(*dims)
+        return tt_kron_op(d, nt, dd, kinds, mats), (keep, dd, kinds, mats)
+
+    def tt_kron_apply(self, op, x: Sequence[torch.Tensor]) -> List[TTResult]:
+        """The unrounded summands of (sum_i A_{i,1} x ... x A_{i,d}) x."""
+        L = load_library()
+        vx = _View(x)
+        k, keep = self._kron(op, [int(c.shape[1]) for c in x])
+        out = (C.c_void_p * len(op))()
+        _check(L.tt_kron_apply(self.handle, C.byref(k), C.byref(vx.view), out))
+        return [TTResult(out[i], self.device) for i in range(len(op))]
+
+    def tt_gmres(self, op, f: Sequence[torch.Tensor], tol: float = 1e-8, max_iter: int = 50,
+                 round_tol: float = 0.0, randomized: bool = True, precond: bool = True,
+                 oversample: int = 10, max_rank: int = 0, seed: int = 1):
+        """Right-preconditioned TT-GMRES; returns (x, info dict)."""
+        L = load_library()
+        vf = _View(f)
+        k, keep = self._kron(op, [int(c.shape[1]) for c in f])
+        o = tt_gmres_opts(float(tol), float(round_tol), int(max_iter), int(randomized),
+                          int(precond), int(oversample), int(max_rank), C.c_uint64(seed).value)
+        info = tt_gmres_info()
+        res = (C.c_double * (max_iter + 1))()
+        h = C.c_void_p()
+        _check(L.tt_gmres(self.handle, C.byref(k), C.byref(vf.view), C.byref(o), C.byref(h),
+                          C.byref(info), res))
+        out = {"iters": info.iters, "converged": bool(info.converged),
+               "roundings": info.roundings, "max_basis_rank": info.max_basis_rank,
+               "residual": info.residual, "residuals": [res[i] for i in range(info.iters + 1)]}
+        return TTResult(h.value, self.device), out

@@ -1502,6 +1502,383 @@ int inner_impl(tt_ctx* c, const tt_view* x, const tt_view* y, double* out) {
   return TT_OK;
 }
 
+// ------------------------------------------------------------------ TT-GMRES (NEXT-4)
+// Right-preconditioned TT-GMRES on a Kronecker-sum operator: the
+// paper's application of the rounding.  Every sum is rounded by this library's
+// tt_round_sum (randomized) or tt_round_deterministic path; the (k+1) x k
+// least-squares problem is solved on the host (readings G1-G4 in DESIGN.md).
+
+tt_view view_of(const tt_tensor& t) {
+  tt_view v;
+  v.d = t.d;
+  v.dims = t.dims.data();
+  v.ranks = t.ranks.data();
+  v.cores = const_cast<const double* const*>(t.ptrs.data());
+  return v;
+}
+
+int validate_kron(const tt_kron_op* op, const std::vector<int64_t>& dims) {
+  if (!op || op->nterms < 1 || !op->dims || !op->kinds || !op->mats) {
+    set_error("kron operator: need nterms >= 1 and dims/kinds/mats");
+    return TT_ERR_ARG;
+  }
+  if (op->d != int(dims.size())) {
+    set_error("kron operator has %d modes, the tensor %zu", op->d, dims.size());
+    return TT_ERR_SHAPE;
+  }
+  for (int n = 0; n < op->d; ++n)
+    if (op->dims[n] != dims[n]) {
+      set_error("kron operator: mode %d size %lld, tensor %lld", n + 1, (long long)op->dims[n],
+                (long long)dims[n]);
+      return TT_ERR_SHAPE;
+    }
+  for (int e = 0; e < op->nterms * op->d; ++e) {
+    const int k = op->kinds[e];
+    if (k != TT_KRON_IDENTITY && k != TT_KRON_DIAG && k != TT_KRON_DENSE) {
+      set_error("kron operator: unknown factor kind %d", k);
+      return TT_ERR_ARG;
+    }
+    if (k != TT_KRON_IDENTITY && !op->mats[e]) {
+      set_error("kron operator: factor %d has no matrix", e);
+      return TT_ERR_ARG;
+    }
+  }
+  return TT_OK;
+}
+
+// y = A x in mode 2 for an r0 x I x r1 core: y(a, i, b) = sum_j A(i, j) x(a, j, b)
+int mode2_dense(Ctx& c, const double* A, const double* x, int64_t r0, int64_t I, int64_t r1,
+                double* y) {
+  if (r0 == 1)   // core as the I x r1 matrix: one GEMM
+    return gemm1(c, false, false, int(I), int(r1), int(I), 1.0, A, int(I), x, int(I), 0.0, y,
+                 int(I), c.stream);
+  std::vector<GemmDesc> gd(static_cast<size_t>(r1));   // per b: y_b (r0 x I) = x_b A^T
+  for (int64_t b = 0; b < r1; ++b)
+    gd[b] = GemmDesc{x + b * r0 * I, A, y + b * r0 * I, int(r0), int(I), int(I), int(r0), int(I),
+                     int(r0)};
+  return gemm(c, false, true, gd.data(), int(r1), 1.0, 0.0, c.stream);
+}
+
+// one Kronecker factor on one core, into y (which may alias x only for diag)
+int apply_factor(Ctx& c, int kind, const double* F, const double* x, int64_t r0, int64_t I,
+                 int64_t r1, double* y) {
+  if (kind == TT_KRON_DIAG) return scale_mode2(c, x, r0, I, r1, F, y, c.stream);
+  if (kind == TT_KRON_DENSE) return mode2_dense(c, F, x, r0, I, r1, y);
+  TTR_CUDA(cudaMemcpyAsync(y, x, sizeof(double) * r0 * I * r1, cudaMemcpyDeviceToDevice,
+                           c.stream));
+  return TT_OK;
+}
+
+// The nterms summands of op x as core lists: identity factors reuse x's core
+// (borrowed), the others are new buffers (owned by `bufs`)
+struct KronTerms {
+  std::vector<std::vector<const double*>> cores;
+  std::vector<DBuf> bufs;
+  std::vector<tt_view> views;
+};
+
+int kron_terms(Ctx& c, const tt_kron_op* op, const tt_view& x, KronTerms& K) {
+  const int d = x.d;
+  K.cores.assign(op->nterms, std::vector<const double*>(d, nullptr));
+  K.bufs.clear();
+  for (int i = 0; i < op->nterms; ++i)
+    for (int n = 0; n < d; ++n) {
+      const int kind = op->kinds[i * d + n];
+      if (kind == TT_KRON_IDENTITY) {
+        K.cores[i][n] = x.cores[n];
+        continue;
+      }
+      const int64_t r0 = x.ranks[n], I = x.dims[n], r1 = x.ranks[n + 1];
+      K.bufs.emplace_back();
+      TTR_TRY(dalloc(K.bufs.back(), size_t(r0 * I * r1), c.stream));
+      TTR_TRY(apply_factor(c, kind, op->mats[i * d + n], x.cores[n], r0, I, r1, K.bufs.back().p));
+      K.cores[i][n] = K.bufs.back().p;
+    }
+  K.views.resize(op->nterms);
+  for (int i = 0; i < op->nterms; ++i) {
+    K.views[i].d = d;
+    K.views[i].dims = x.dims;
+    K.views[i].ranks = x.ranks;
+    K.views[i].cores = K.cores[i].data();
+  }
+  return TT_OK;
+}
+
+struct GmresCfg {
+  double round_tol;
+  bool randomized;
+  int oversample;
+  int64_t max_rank;
+  uint64_t seed;
+  int calls = 0;
+};
+
+// round the sum of `views` (rounding call number g.calls, seed g.seed + calls)
+int round_views(tt_ctx* c, const std::vector<tt_view>& views, GmresCfg& g,
+                std::unique_ptr<tt_tensor>& out) {
+  tt_tensor* t = nullptr;
+  const uint64_t seed = g.seed + uint64_t(g.calls++);
+  if (g.randomized) {
+    int64_t rmax = 1;
+    for (const tt_view& v : views)
+      for (int n = 1; n < v.d; ++n) rmax = std::max(rmax, v.ranks[n]);
+    int64_t ell0 = rmax + g.oversample;
+    if (g.max_rank > 0) ell0 = std::min(ell0, g.max_rank);
+    tt_round_opts o{TT_TOL, 1, 0, ell0, g.round_tol, seed, g.max_rank};
+    TTR_TRY(round_sum_impl(c, int(views.size()), views.data(), &o, nullptr, &t));
+  } else {
+    tt_round_opts o{TT_TOL, 0, g.max_rank, 0, g.round_tol, 0, 0};
+    TTR_CUDA(cudaMemsetAsync(c->flags.p, 0, sizeof(int) * c->nflags, c->stream));
+    TTR_TRY(deterministic_impl(c, int(views.size()), views.data(), &o, &t));
+  }
+  out.reset(t);
+  return TT_OK;
+}
+
+// t <- a t (first core, in place)
+int scale_tt(Ctx& c, tt_tensor& t, double a) {
+  const int64_t n = t.ranks[0] * t.dims[0] * t.ranks[1];
+  return scale_copy(c, t.ptrs[0], n, a, const_cast<double*>(t.ptrs[0]), c.stream);
+}
+
+// first core of v scaled by a, into a new buffer; view `out` = v with that core
+struct ScaledView {
+  DBuf core1;
+  std::vector<const double*> cores;
+  tt_view v;
+};
+int scaled_view(Ctx& c, const tt_tensor& t, double a, ScaledView& sv) {
+  const int64_t n = t.ranks[0] * t.dims[0] * t.ranks[1];
+  TTR_TRY(dalloc(sv.core1, size_t(n), c.stream));
+  TTR_TRY(scale_copy(c, t.ptrs[0], n, a, sv.core1.p, c.stream));
+  sv.cores.assign(t.ptrs.begin(), t.ptrs.end());
+  sv.cores[0] = sv.core1.p;
+  sv.v = view_of(t);
+  sv.v.cores = sv.cores.data();
+  return TT_OK;
+}
+
+int gmres_impl(tt_ctx* c, const tt_kron_op* op, const tt_view* f, const tt_gmres_opts* o,
+               tt_tensor** xout, tt_gmres_info* info, double* residuals) {
+  std::vector<int64_t> dims;
+  TTR_TRY(validate(f, 1, dims));
+  TTR_TRY(validate_kron(op, dims));
+  if (!o || !(o->tol > 0.0) || o->max_iter < 1 || o->round_tol < 0.0 || o->oversample < 0) {
+    set_error("tt_gmres: need opts with tol > 0, max_iter >= 1, round_tol >= 0, oversample >= 0");
+    return TT_ERR_ARG;
+  }
+  if (c->world > 1) {
+    set_error("tt_gmres runs on one GPU (world size %d)", c->world);
+    return TT_ERR_ARG;
+  }
+  TTR_CUDA(cudaSetDevice(c->device));
+  Ctx& C = *c;
+  cudaStream_t s = C.stream;
+  const int d = int(dims.size());
+  const int64_t I1 = dims[0];
+  GmresCfg g{o->round_tol > 0.0 ? o->round_tol : o->tol / 10.0, o->randomized != 0,
+             int(o->oversample), o->max_rank, o->seed};
+  // preconditioner P = (sum_i A_{i,1})^{-1}
+  DBuf Msum, Pm;
+  if (o->precond) {
+    TTR_TRY(dalloc(Msum, size_t(I1 * I1), s));
+    TTR_TRY(dalloc(Pm, size_t(I1 * I1), s));
+    TTR_TRY(fill_zero(C, Msum.p, I1 * I1, s));
+    for (int i = 0; i < op->nterms; ++i)
+      TTR_TRY(add_factor(C, Msum.p, int(I1), op->kinds[i * d], op->mats[i * d], s));
+    TTR_TRY(spd_inverse(C, Msum.p, int(I1), Pm.p, s));
+    int fl[4];
+    TTR_TRY(read_flags(C, fl, 4));
+    if (fl[3] & 1) {
+      set_error("tt_gmres: sum_i A_{i,1} is not symmetric positive definite");
+      return TT_ERR_NUMERIC;
+    }
+  }
+  // Y = (P x I x ... x I) V: a copy of V with its first core multiplied by P
+  auto precond = [&](const tt_tensor& V, std::unique_ptr<tt_tensor>& Y) -> int {
+    Y.reset(new tt_tensor);
+    Y->d = V.d;
+    Y->dims = V.dims;
+    Y->ranks = V.ranks;
+    Y->stream = s;
+    Y->alive = C.alive;
+    Y->bufs.resize(d);
+    Y->ptrs.resize(d);
+    for (int n = 0; n < d; ++n) {
+      const int64_t r0 = V.ranks[n], I = V.dims[n], r1 = V.ranks[n + 1];
+      TTR_TRY(dalloc(Y->bufs[n], size_t(r0 * I * r1), s));
+      if (n == 0 && o->precond) TTR_TRY(mode2_dense(C, Pm.p, V.ptrs[0], r0, I, r1, Y->bufs[0].p));
+      else TTR_CUDA(cudaMemcpyAsync(Y->bufs[n].p, V.ptrs[n], sizeof(double) * r0 * I * r1,
+                                    cudaMemcpyDeviceToDevice, s));
+      Y->ptrs[n] = Y->bufs[n].p;
+    }
+    return TT_OK;
+  };
+  auto tnorm = [&](const tt_tensor& t, double& nr) -> int {
+    const tt_view v = view_of(t);
+    double ip = 0.0;
+    TTR_TRY(inner_impl(c, &v, &v, &ip));
+    nr = sqrt(std::max(ip, 0.0));
+    return TT_OK;
+  };
+  // V_1 = f / ||f|| (a library-owned copy of f)
+  std::vector<std::unique_ptr<tt_tensor>> V;
+  {
+    Terms T;
+    TTR_TRY(stage_terms(C, f, 1, d, T));
+    std::unique_ptr<tt_tensor> v0(new tt_tensor);
+    v0->d = d;
+    v0->dims = dims;
+    v0->ranks.assign(f->ranks, f->ranks + d + 1);
+    v0->stream = s;
+    v0->alive = C.alive;
+    v0->bufs.resize(d);
+    v0->ptrs.resize(d);
+    for (int n = 0; n < d; ++n) {
+      TTR_TRY(wait_core(C, T, n));
+      const size_t cnt = size_t(f->ranks[n] * dims[n] * f->ranks[n + 1]);
+      TTR_TRY(dalloc(v0->bufs[n], cnt, s));
+      TTR_CUDA(cudaMemcpyAsync(v0->bufs[n].p, T.core[0][n], sizeof(double) * cnt,
+                               cudaMemcpyDeviceToDevice, s));
+      v0->ptrs[n] = v0->bufs[n].p;
+    }
+    V.push_back(std::move(v0));
+  }
+  double beta = 0.0;
+  TTR_TRY(tnorm(*V[0], beta));
+  if (!(beta > 0.0)) {
+    set_error("tt_gmres: f is zero");
+    return TT_ERR_ARG;
+  }
+  TTR_TRY(scale_tt(C, *V[0], 1.0 / beta));
+  const int mi = o->max_iter;
+  std::vector<std::vector<double>> Hc;     // columns of the Hessenberg matrix (rotated)
+  std::vector<double> cs, sn, gvec(size_t(mi) + 2, 0.0);
+  gvec[0] = beta;
+  std::vector<double> res{1.0};
+  int k = 0, maxr = 1;
+  bool converged = false;
+  for (int n = 1; n < d; ++n) maxr = std::max<int>(maxr, int(V[0]->ranks[n]));
+  while (k < mi) {
+    std::unique_ptr<tt_tensor> Y, W, Z;
+    TTR_TRY(precond(*V[k], Y));
+    {
+      KronTerms K;
+      const tt_view yv = view_of(*Y);
+      TTR_TRY(kron_terms(C, op, yv, K));
+      TTR_TRY(round_views(c, K.views, g, W));
+    }
+    std::vector<double> h(size_t(k) + 2, 0.0);
+    const tt_view wv = view_of(*W);
+    for (int j = 0; j <= k; ++j) {                         // h_jk = <V_j, W>
+      const tt_view vj = view_of(*V[j]);
+      TTR_TRY(inner_impl(c, &vj, &wv, &h[j]));
+    }
+    {
+      std::vector<ScaledView> sv(size_t(k) + 1);          // Z = W - sum_j h_jk V_j
+      std::vector<tt_view> views{wv};
+      for (int j = 0; j <= k; ++j) {
+        TTR_TRY(scaled_view(C, *V[j], -h[j], sv[j]));
+        views.push_back(sv[j].v);
+      }
+      TTR_TRY(round_views(c, views, g, Z));
+    }
+    double hk1 = 0.0;
+    TTR_TRY(tnorm(*Z, hk1));                               // h_{k+1,k} = ||Z||
+    h[k + 1] = hk1;
+    // least squares: previous Givens rotations, then a new one zeroing h_{k+1}
+    for (int j = 0; j < k; ++j) {
+      const double a = cs[j] * h[j] + sn[j] * h[j + 1];
+      h[j + 1] = -sn[j] * h[j] + cs[j] * h[j + 1];
+      h[j] = a;
+    }
+    const double r = std::hypot(h[k], h[k + 1]);
+    const double cg = r > 0.0 ? h[k] / r : 1.0, sg = r > 0.0 ? h[k + 1] / r : 0.0;
+    cs.push_back(cg);
+    sn.push_back(sg);
+    h[k] = r;
+    h[k + 1] = 0.0;
+    gvec[k + 1] = -sg * gvec[k];
+    gvec[k] = cg * gvec[k];
+    Hc.push_back(h);
+    res.push_back(std::fabs(gvec[k + 1]) / beta);
+    ++k;
+    if (res.back() <= o->tol || hk1 == 0.0) {
+      converged = res.back() <= o->tol;
+      break;
+    }
+    TTR_TRY(scale_tt(C, *Z, 1.0 / hk1));                   // V_{k+1} = Z / h_{k+1,k}
+    for (int n = 1; n < d; ++n) maxr = std::max<int>(maxr, int(Z->ranks[n]));
+    V.push_back(std::move(Z));
+  }
+  // y = R^{-1} g (back substitution on the rotated Hessenberg), x = P round(sum_j y_j V_j)
+  std::vector<double> y(size_t(k), 0.0);
+  for (int i = k - 1; i >= 0; --i) {
+    double acc = gvec[i];
+    for (int j = i + 1; j < k; ++j) acc -= Hc[j][i] * y[j];
+    y[i] = acc / Hc[i][i];
+  }
+  std::unique_ptr<tt_tensor> X, Xp;
+  {
+    std::vector<ScaledView> sv(static_cast<size_t>(k));
+    std::vector<tt_view> views;
+    for (int j = 0; j < k; ++j) {
+      TTR_TRY(scaled_view(C, *V[j], y[j], sv[j]));
+      views.push_back(sv[j].v);
+    }
+    TTR_TRY(round_views(c, views, g, X));
+  }
+  TTR_TRY(precond(*X, Xp));
+  Xp->flags = 0;
+  Xp->passes = 1;
+  TTR_CUDA(cudaStreamSynchronize(s));
+  if (residuals)
+    for (size_t i = 0; i < res.size(); ++i) residuals[i] = res[i];
+  if (info) {
+    info->iters = k;
+    info->converged = converged ? 1 : 0;
+    info->roundings = g.calls;
+    info->max_basis_rank = maxr;
+    info->residual = res.back();
+  }
+  *xout = Xp.release();
+  return TT_OK;
+}
+
+int kron_apply_impl(tt_ctx* c, const tt_kron_op* op, const tt_view* x, tt_tensor_t* out) {
+  std::vector<int64_t> dims;
+  TTR_TRY(validate(x, 1, dims));
+  TTR_TRY(validate_kron(op, dims));
+  TTR_CUDA(cudaSetDevice(c->device));
+  Ctx& C = *c;
+  const int d = x->d;
+  Terms T;
+  TTR_TRY(stage_terms(C, x, 1, d, T));
+  for (int n = 0; n < d; ++n) TTR_TRY(wait_core(C, T, n));
+  std::vector<std::unique_ptr<tt_tensor>> res;
+  for (int i = 0; i < op->nterms; ++i) {
+    std::unique_ptr<tt_tensor> t(new tt_tensor);
+    t->d = d;
+    t->dims = dims;
+    t->ranks.assign(x->ranks, x->ranks + d + 1);
+    t->stream = C.stream;
+    t->alive = C.alive;
+    t->bufs.resize(d);
+    t->ptrs.resize(d);
+    for (int n = 0; n < d; ++n) {
+      const int64_t r0 = x->ranks[n], I = dims[n], r1 = x->ranks[n + 1];
+      TTR_TRY(dalloc(t->bufs[n], size_t(r0 * I * r1), C.stream));
+      TTR_TRY(apply_factor(C, op->kinds[i * d + n], op->mats[i * d + n], T.core[0][n], r0, I, r1,
+                           t->bufs[n].p));
+      t->ptrs[n] = t->bufs[n].p;
+    }
+    res.push_back(std::move(t));
+  }
+  TTR_CUDA(cudaStreamSynchronize(C.stream));
+  for (int i = 0; i < op->nterms; ++i) out[i] = res[i].release();
+  return TT_OK;
+}
+
 }  // namespace
 
 // ====================================================================== C-ABI
@@ -1718,6 +2095,26 @@ int tt_round_deterministic(tt_ctx_t c, int32_t S, const tt_view* terms, const tt
   return guarded([&] {
     TTR_CUDA(cudaMemsetAsync(c->flags.p, 0, sizeof(int) * c->nflags, c->stream));
     return deterministic_impl(c, S, terms, opts, out);
+  });
+}
+
+int tt_kron_apply(tt_ctx_t c, const tt_kron_op* op, const tt_view* x, tt_tensor_t* out) {
+  if (!c || !op || !x || !out) {
+    set_error("tt_kron_apply: null argument");
+    return TT_ERR_ARG;
+  }
+  return guarded([&] { return kron_apply_impl(c, op, x, out); });
+}
+
+int tt_gmres(tt_ctx_t c, const tt_kron_op* op, const tt_view* f, const tt_gmres_opts* opts,
+             tt_tensor_t* x, tt_gmres_info* info, double* residuals) {
+  if (!c || !op || !f || !opts || !x) {
+    set_error("tt_gmres: null argument");
+    return TT_ERR_ARG;
+  }
+  return guarded([&] {
+    TTR_CUDA(cudaMemsetAsync(c->flags.p, 0, sizeof(int) * c->nflags, c->stream));
+    return gmres_impl(c, op, f, opts, x, info, residuals);
   });
 }
 

@@ -228,6 +228,13 @@ int fro_norm(Ctx& c, const double* x, int64_t n, double* out, cudaStream_t s);
 int transpose(Ctx& c, const double* src, int64_t rows, int64_t cols, int64_t lds,
               double* dst, int64_t ldd, cudaStream_t s);
 int fill_zero(Ctx& c, double* p, int64_t n, cudaStream_t s);
+// TT-GMRES helpers (NEXT-4): y(a,i,b) = dg[i] x(a,i,b) for an r0 x I x r1 core;
+// y = a x; M += identity / diag / dense factor; Minv = M^{-1} (M SPD, n x n)
+int scale_mode2(Ctx& c, const double* x, int64_t r0, int64_t I, int64_t r1, const double* dg,
+                double* y, cudaStream_t s);
+int scale_copy(Ctx& c, const double* x, int64_t n, double a, double* y, cudaStream_t s);
+int add_factor(Ctx& c, double* M, int n, int kind, const double* F, cudaStream_t s);
+int spd_inverse(Ctx& c, const double* M, int n, double* Minv, cudaStream_t s);
 // diagonal of the n x n matrix p (ld n) set to 1 (other entries untouched)
 int set_identity(Ctx& c, double* p, int64_t n, cudaStream_t s);
 

@@ -1491,6 +1491,33 @@ __global__ void set_identity_kernel(double* p, int64_t n) {
     p[i + i * n] = 1.0;
 }
 
+// core(a, i, b) <- d[i] core(a, i, b): a diagonal Kronecker factor in mode 2
+__global__ void scale_mode2_kernel(const double* __restrict__ x, int64_t r0, int64_t I,
+                                   int64_t r1, const double* __restrict__ dg,
+                                   double* __restrict__ y) {
+  const int64_t n = r0 * I * r1;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n;
+       e += int64_t(gridDim.x) * blockDim.x)
+    y[e] = dg[(e / r0) % I] * x[e];
+}
+
+__global__ void scale_copy_kernel(const double* __restrict__ x, int64_t n, double a,
+                                  double* __restrict__ y) {
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n;
+       e += int64_t(gridDim.x) * blockDim.x)
+    y[e] = a * x[e];
+}
+
+// M (n x n) += factor: kind 0 identity, 1 diagonal d (n), 2 dense F (n x n, ld n)
+__global__ void add_factor_kernel(double* __restrict__ M, int n, int kind,
+                                  const double* __restrict__ F) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n * n; e += gridDim.x * blockDim.x) {
+    const int i = e % n, j = e / n;
+    if (kind == 2) M[e] += F[e];
+    else if (i == j) M[e] += (kind == 1 ? F[i] : 1.0);
+  }
+}
+
 __global__ void fill_zero_kernel(double* p, int64_t n) {
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
        i += int64_t(gridDim.x) * blockDim.x)
@@ -1618,6 +1645,36 @@ int transpose(Ctx& c, const double* src, int64_t rows, int64_t cols, int64_t lds
 int set_identity(Ctx& c, double* p, int64_t n, cudaStream_t s) {
   set_identity_kernel<<<std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 64)), 256, 0, s>>>(p, n);
   return launched();
+}
+
+int scale_mode2(Ctx& c, const double* x, int64_t r0, int64_t I, int64_t r1, const double* dg,
+                double* y, cudaStream_t s) {
+  const int64_t n = r0 * I * r1;
+  const int blocks = int(std::min<int64_t>((n + 255) / 256, int64_t(c.sm_count) * 8));
+  scale_mode2_kernel<<<std::max(1, blocks), 256, 0, s>>>(x, r0, I, r1, dg, y);
+  return launched();
+}
+
+int scale_copy(Ctx& c, const double* x, int64_t n, double a, double* y, cudaStream_t s) {
+  const int blocks = int(std::min<int64_t>((n + 255) / 256, int64_t(c.sm_count) * 8));
+  scale_copy_kernel<<<std::max(1, blocks), 256, 0, s>>>(x, n, a, y);
+  return launched();
+}
+
+int add_factor(Ctx& c, double* M, int n, int kind, const double* F, cudaStream_t s) {
+  add_factor_kernel<<<std::max(1, std::min(c.sm_count * 4, (n * n + 255) / 256)), 256, 0, s>>>(
+      M, n, kind, F);
+  return launched();
+}
+
+// Minv = M^{-1} for a symmetric positive definite M (n x n): Cholesky M = R^T R
+// (the CholeskyQR kernels, M as the Gram), then Minv = R^{-1} R^{-T}.
+int spd_inverse(Ctx& c, const double* M, int n, double* Minv, cudaStream_t s) {
+  DBuf Rinv, gw;
+  TTR_TRY(dalloc(Rinv, size_t(n) * n, s));
+  if (n > 160 && n * n > kSmemLimitDoubles) TTR_TRY(dalloc(gw, size_t(n) * n, s));
+  TTR_TRY(launch_chol(c, M, n, n, CH_RCLAMP, Rinv.p, nullptr, gw.p, nullptr, 0, s));
+  return gemm1(c, false, true, n, n, n, 1.0, Rinv.p, n, Rinv.p, n, 0.0, Minv, n, s);
 }
 
 int fill_zero(Ctx& c, double* p, int64_t n, cudaStream_t s) {

@@ -248,3 +248,47 @@ def random_terms(seed: int, dims: Sequence[int], term_ranks: Sequence[Sequence[i
 
 def to_numpy(tt: TT):
     return [c.detach().cpu().numpy() for c in tt]
+
+
+# ---------------------------------------------------------------- TT-GMRES surrogate (NEXT-4)
+def cookie_surrogate(grid: int = 16, params: int = 2, samples: int = 4,
+                     rho=(1.0, 10.0)):
+    """Kronecker-sum stand-in for the paper's cookie problem (its FEM
+    operator and mesh are not available): N = 1 + params modes.
+      A_{1,1} = 1-D finite-difference Dirichlet Laplacian on `grid` interior points
+                (the operator with constant coefficient),
+      A_{p+1,1} = the same stiffness restricted to the edges of a disjoint index block
+                (the characteristic function of "subdomain" p),
+      A_{p+1,p+1} = diag(ρ samples linearly spaced in [1, 10]),
+      every other factor the identity;  f = the rank-1 all-ones TT.
+    Returns (op, f, dims) with op in oracle.gmres's format (None = identity,
+    1-D = diagonal, 2-D = dense), numpy fp64.  Input synthesis only."""
+    import numpy as np
+    h2 = float((grid + 1) ** 2)
+    edges = [(k, k + 1) for k in range(grid - 1)]
+
+    def stiffness(edge_list, dirichlet):
+        A = np.zeros((grid, grid))
+        for a, b in edge_list:
+            A[a, a] += h2
+            A[b, b] += h2
+            A[a, b] -= h2
+            A[b, a] -= h2
+        if dirichlet:
+            A[0, 0] += h2
+            A[grid - 1, grid - 1] += h2
+        return A
+
+    L0 = stiffness(edges, True)
+    N = 1 + params
+    op = [[L0] + [None] * params]
+    width = max(1, grid // (2 * params + 1))
+    for p in range(params):
+        lo = (2 * p + 1) * width
+        blk = [(a, b) for (a, b) in edges if lo <= a and b < min(grid, lo + width + 1)]
+        term = [stiffness(blk, False)] + [None] * params
+        term[1 + p] = np.linspace(rho[0], rho[1], samples)
+        op.append(term)
+    dims = [grid] + [samples] * params
+    f = [np.ones((1, dims[n], 1)) for n in range(N)]
+    return op, f, dims
