@@ -72,6 +72,7 @@ extern "C" {
 #define TT_FLAG_RIGHT_ORTH    4u  /* cores 2..d right-orthogonal (after truncation, R3)    */
 #define TT_FLAG_ZERO          8u  /* the sum was exactly zero: all ranks 1, zero cores (R16) */
 #define TT_FLAG_QR_FALLBACK  16u  /* a Householder fallback QR ran at least once           */
+#define TT_FLAG_SLAB         32u  /* cores hold this rank's mode slabs (tt_round_sum_slab)  */
 
 typedef struct tt_ctx*    tt_ctx_t;
 typedef struct tt_sketch* tt_sketch_t;
@@ -161,6 +162,30 @@ int tt_sketch_destroy(tt_sketch_t sk);
  * The result has ranks (1, k_1..k_{d-1}, 1) and is returned in *out. */
 int tt_round_sum(tt_ctx_t ctx, int32_t S_local, const tt_view* terms,
                  const tt_round_opts* opts, tt_sketch_t sketch, tt_tensor_t* out);
+
+/* Mode-slab sharding of the same rounding (SURVEY §8e alternative, §8f NEXT-2):
+ * every rank holds ALL S summands, but of every core n only the mode-index slab
+ * i in [slab_lo[n], slab_lo[n] + terms[j].dims[n]) of the global mode size
+ * gdims[n] (terms[j].dims are the local slab sizes; the ranks' slabs must tile
+ * every mode).  Alg. 7 then runs with every row-distributed step local:
+ *  - the sketch: each rank generates its slab of G_n (the same Philox bits as
+ *    the full core, so the result does not depend on the number of ranks);
+ *  - Alg. 3: W_{n-1} = H(Z_n)H(G_n)^T is a sum over i_n -> one allreduce of the
+ *    sum_j R_{n-1} x l_{n-1} stack per step (C5: 2.4 MB instead of Y_n's 42.5 MB);
+ *  - line 10's QR of the row-distributed Y_n and the truncation's R-only QRs:
+ *    CholeskyQR passes with the l x l Gram all-reduced (R replicated, Q local);
+ *  - line 11: M = Q_n^T V(X_n) summed over the slabs (l x sum_j R allreduce);
+ *  - carries, output cores, the truncation products and the SVDs of R: local /
+ *    replicated, identical on every rank.
+ * The result holds this rank's slab of every core (global ranks, local dims,
+ * TT_FLAG_SLAB); concatenating the ranks' slabs along the mode axis gives the
+ * rounded tensor.  Same opts as tt_round_sum (no user sketch).  world == 1:
+ * the slab must be the whole mode.  Not supported (TT_ERR_ARG): a truncation
+ * bond of rank > 160 or a wide unfolding (they need the non-distributed SVD);
+ * a breakdown of every CholeskyQR route gives TT_ERR_NUMERIC (no distributed
+ * Householder fallback). */
+int tt_round_sum_slab(tt_ctx_t ctx, int32_t S, const tt_view* terms, const int64_t* gdims,
+                      const int64_t* slab_lo, const tt_round_opts* opts, tt_tensor_t* out);
 
 /* Deterministic TT-rounding of the assembled sum: Alg. 1 + Alg. 2
  * with eps0 = opts->tol (and opts->rank as an optional rank cap).

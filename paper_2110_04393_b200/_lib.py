@@ -12,6 +12,7 @@ LIB_PATH = os.path.join(HERE, "libttround.so")
 
 SKETCH_ONLY, RANK, TOL = 0, 1, 2
 FLAG_RANK_CAPPED, FLAG_LEFT_ORTH, FLAG_RIGHT_ORTH, FLAG_ZERO, FLAG_QR_FALLBACK = 1, 2, 4, 8, 16
+FLAG_SLAB = 32
 _MODES = {"sketch_only": SKETCH_ONLY, "rank": RANK, "tol": TOL}
 
 
@@ -79,6 +80,8 @@ def load_library(path: str = LIB_PATH):
         "tt_sketch_destroy": (C.c_int, [P]),
         "tt_round_sum": (C.c_int, [P, i32, C.POINTER(tt_view), C.POINTER(tt_round_opts), P,
                                    C.POINTER(P)]),
+        "tt_round_sum_slab": (C.c_int, [P, i32, C.POINTER(tt_view), C.POINTER(i64),
+                                        C.POINTER(i64), C.POINTER(tt_round_opts), C.POINTER(P)]),
         "tt_round_deterministic": (C.c_int, [P, i32, C.POINTER(tt_view),
                                              C.POINTER(tt_round_opts), C.POINTER(P)]),
         "tt_round_sum_two_sided": (C.c_int, [P, i32, C.POINTER(tt_view), i64, i64, u64,
@@ -327,6 +330,26 @@ class Context:
         h = C.c_void_p()
         _check(L.tt_round_sum(self.handle, len(views), arr, C.byref(opts),
                               sketch._h.ptr if sketch is not None else None, C.byref(h)))
+        return TTResult(h.value, self.device)
+
+    def tt_round_sum_slab(self, terms: Sequence[Sequence[torch.Tensor]], gdims: Sequence[int],
+                          slab_lo: Sequence[int], mode: str = "rank", rank: int = 0,
+                          oversample: int = 0, tol: float = 0.0, seed: int = 1,
+                          adaptive: bool = False, max_rank: int = 0) -> TTResult:
+        """Mode-slab sharded rounding (NEXT-2): `terms` are this rank's slabs of ALL
+        summands (cores (R, I_slab, R')), the slab of mode n starts at slab_lo[n] of
+        gdims[n].  Returns this rank's slabs of the rounded cores."""
+        L = load_library()
+        views = [_View(t) for t in terms]
+        arr = (tt_view * len(views))(*[v.view for v in views])
+        d = len(gdims)
+        g = (C.c_int64 * d)(*[int(x) for x in gdims])
+        lo = (C.c_int64 * d)(*[int(x) for x in slab_lo])
+        opts = tt_round_opts(_MODES[mode], int(adaptive), int(rank), int(oversample),
+                             float(tol), C.c_uint64(seed).value, int(max_rank))
+        h = C.c_void_p()
+        _check(L.tt_round_sum_slab(self.handle, len(views), arr, g, lo, C.byref(opts),
+                                   C.byref(h)))
         return TTResult(h.value, self.device)
 
     def tt_inner(self, x: Sequence[torch.Tensor], y: Sequence[torch.Tensor]) -> float:

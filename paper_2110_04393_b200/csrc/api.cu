@@ -369,10 +369,21 @@ inline int wait_core(Ctx& c, const Terms& T, int n /*0-based*/) {
   return TT_OK;
 }
 
+// Mode-slab sharding: this rank holds the mode-index slab
+// i in [lo[n], lo[n] + dims[n]) of core n of EVERY summand; gdims are the global
+// mode sizes.  Every contraction over i (Alg. 3's W, the projection M, the
+// Grams of the QRs) is a local partial sum followed by an allreduce of a small
+// matrix; everything else is local to the slab.
+struct Slab {
+  std::vector<int64_t> gdims, lo;
+};
+
 // Def. 3.1 Gaussian TT cores n = first..last (1-based; default 2..d, the cores
-// Alg. 3 reads) from the R9 Philox stream (seed, n, tag).
+// Alg. 3 reads) from the R9 Philox stream (seed, n, tag); with a slab, only this
+// rank's slab of each core (the same bits as the corresponding full-core entries)
 int make_sketch(Ctx& c, const std::vector<int64_t>& dims, const std::vector<int64_t>& l,
-                uint64_t seed, uint32_t tag, tt_sketch& sk, int first = 2, int last = 0) {
+                uint64_t seed, uint32_t tag, tt_sketch& sk, int first = 2, int last = 0,
+                const Slab* sl = nullptr) {
   const int d = int(dims.size());
   if (last <= 0) last = d;
   sk.d = d;
@@ -385,8 +396,15 @@ int make_sketch(Ctx& c, const std::vector<int64_t>& dims, const std::vector<int6
   for (int n = first; n <= last; ++n) {
     const int64_t cnt = l[n - 1] * dims[n - 1] * l[n];
     TTR_TRY(dalloc(sk.cores[n - 1], size_t(cnt), c.stream));
-    TTR_TRY(philox_fill(c, sk.cores[n - 1].p, cnt, seed, uint32_t(n), tag,
-                        1.0 / sqrt(double(cnt)), c.stream));
+    if (sl) {
+      const double gcnt = double(l[n - 1]) * double(sl->gdims[n - 1]) * double(l[n]);
+      TTR_TRY(philox_fill_slab(c, sk.cores[n - 1].p, l[n - 1], dims[n - 1], l[n], sl->lo[n - 1],
+                               sl->gdims[n - 1], seed, uint32_t(n), tag, 1.0 / sqrt(gcnt),
+                               c.stream));
+    } else {
+      TTR_TRY(philox_fill(c, sk.cores[n - 1].p, cnt, seed, uint32_t(n), tag,
+                          1.0 / sqrt(double(cnt)), c.stream));
+    }
   }
   return TT_OK;
 }
@@ -399,7 +417,7 @@ int partial_contractions_rl(Ctx& c, const Terms& T, const std::vector<int64_t>& 
                             const std::vector<int64_t>& l, const tt_sketch& sk,
                             const std::vector<std::vector<int64_t>>& off,
                             const std::vector<int64_t>& sumR, DBuf& Wst,
-                            std::vector<size_t>& woff) {
+                            std::vector<size_t>& woff, bool slab = false) {
   const int S = T.S, d = T.d;
   cudaStream_t s = c.stream;
   woff.assign(d + 1, 0);
@@ -427,6 +445,8 @@ int partial_contractions_rl(Ctx& c, const Terms& T, const std::vector<int64_t>& 
                        int(T.R[j][d - 1]), int(l[d - 1]), int(dims[d - 1]),
                        int(T.R[j][d - 1]), int(l[d - 1]), int(sumR[d - 1])};
     TTR_TRY(gemm(c, false, true, gd.data(), S, 1.0, 0.0, s));
+    // slab: W is a contraction over i_d -> sum over the slabs (all summands at once)
+    if (slab) TTR_TRY(allreduce_sum(c, Wst.p + woff[d - 1], size_t(sumR[d - 1]) * l[d - 1]));
     for (int n = d - 1; n >= 2; --n) {     // lines 3-6
       TTR_TRY(wait_core(c, T, n - 1));
       const int64_t In = dims[n - 1];
@@ -443,6 +463,8 @@ int partial_contractions_rl(Ctx& c, const Terms& T, const std::vector<int64_t>& 
                          int(T.R[j][n - 1]), int(l[n - 1]), int(In * l[n]), int(T.R[j][n - 1]),
                          int(l[n - 1]), int(sumR[n - 1])};
       TTR_TRY(gemm(c, false, true, gd.data(), S, 1.0, 0.0, s));
+      if (slab)   // line 5 contracts i_n: sum over the slabs
+        TTR_TRY(allreduce_sum(c, Wst.p + woff[n - 1], size_t(sumR[n - 1]) * l[n - 1]));
     }
   }
   return TT_OK;
@@ -451,7 +473,7 @@ int partial_contractions_rl(Ctx& c, const Terms& T, const std::vector<int64_t>& 
 // ------------------------------------------------------------------ Alg. 7
 // X (output cores, ranks l) from the staged summands and the sketch.
 int alg7(Ctx& c, const Terms& T, const std::vector<int64_t>& dims, const std::vector<int64_t>& l,
-         const tt_sketch& sk, tt_tensor& out, PhaseTimer& tm) {
+         const tt_sketch& sk, tt_tensor& out, PhaseTimer& tm, const Slab* sl = nullptr) {
   const int S = T.S, d = T.d;
   cudaStream_t s = c.stream;
   // local summed ranks and per-summand offsets
@@ -465,7 +487,7 @@ int alg7(Ctx& c, const Terms& T, const std::vector<int64_t>& dims, const std::ve
   std::vector<size_t> woff;
   DBuf Wst;
   tm.begin(1);
-  TTR_TRY(partial_contractions_rl(c, T, dims, l, sk, off, sumR, Wst, woff));
+  TTR_TRY(partial_contractions_rl(c, T, dims, l, sk, off, sumR, Wst, woff, sl != nullptr));
   tm.end(1);
   size_t xmax = 1, ymax = 1, mmax = 1;
   for (int n = 1; n < d; ++n) {
@@ -505,15 +527,17 @@ int alg7(Ctx& c, const Terms& T, const std::vector<int64_t>& dims, const std::ve
                   Wst.p + woff[n], int(sumR[n]), 0.0, Yb.p, int(m), s));
     tm.end(2);
     tm.begin(4);
-    TTR_TRY(allreduce_sum(c, Yb.p, size_t(m) * l[n]));   // sum over GPUs
+    if (!sl) TTR_TRY(allreduce_sum(c, Yb.p, size_t(m) * l[n]));   // sum over GPUs
     tm.end(4);
-    // line 10: [V(X_n), ~] = QR(Y_n)
+    // line 10: [V(X_n), ~] = QR(Y_n); slab: the rows are distributed, the Grams
+    // of the CholeskyQR passes are all-reduced (NEXT-2)
     tm.begin(3);
-    TTR_TRY(qr(c, m, l[n], Yb.p, m, false, out.bufs[n - 1].p, nullptr, s));
+    TTR_TRY(qr(c, m, l[n], Yb.p, m, false, out.bufs[n - 1].p, nullptr, s, sl != nullptr,
+               sl ? l[n - 1] * sl->gdims[n - 1] : 0));
     tm.end(3);
     tm.begin(2);
     int fused = 1;
-    if (n < d - 1) {
+    if (n < d - 1 && !sl) {
       // lines 11 + 13 in one cooperative launch (fused.cu): M = Q_n^T V(X_n), then
       // H(X_{n+1}) = [M^(1) H(Y^(1)_{n+1}) ... M^(s) H(Y^(s)_{n+1})]
       const int64_t In1 = dims[n];
@@ -531,9 +555,10 @@ int alg7(Ctx& c, const Terms& T, const std::vector<int64_t>& dims, const std::ve
       if (fused < 0) return fused;
     }
     if (fused != 0) {
-      // line 11: [M^(1) ... M^(s)] = V(X_n)^T Z_n
+      // line 11: [M^(1) ... M^(s)] = V(X_n)^T Z_n (slab: a sum over the slabs)
       TTR_TRY(gemm1(c, true, false, int(l[n]), int(sumR[n]), int(m), 1.0, out.bufs[n - 1].p,
                     int(m), Xcur, int(m), 0.0, Mb.p, int(l[n]), s));
+      if (sl) TTR_TRY(allreduce_sum(c, Mb.p, size_t(l[n]) * sumR[n]));
     }
     if (n < d - 1) {
       // line 13: H(X_{n+1}) = [M^(1) H(Y^(1)_{n+1}) ... M^(s) H(Y^(s)_{n+1})]
@@ -561,7 +586,7 @@ int alg7(Ctx& c, const Terms& T, const std::vector<int64_t>& dims, const std::ve
                     int(l[d - 1]), s));
       tm.end(2);
       tm.begin(4);
-      TTR_TRY(allreduce_sum(c, out.bufs[d - 1].p, size_t(l[d - 1]) * Id));
+      if (!sl) TTR_TRY(allreduce_sum(c, out.bufs[d - 1].p, size_t(l[d - 1]) * Id));
       tm.end(4);
     }
   }
@@ -572,7 +597,8 @@ int alg7(Ctx& c, const Terms& T, const std::vector<int64_t>& dims, const std::ve
 
 // ------------------------------------------------------------------ truncation
 // Mirrored Alg. 2 lines 3-10 on the left-orthogonal X (R3): n = d .. 2.
-int truncate(Ctx& c, tt_tensor& X, double tol, int64_t rmax, std::vector<int64_t>& ks) {
+int truncate(Ctx& c, tt_tensor& X, double tol, int64_t rmax, std::vector<int64_t>& ks,
+             const Slab* sl = nullptr) {
   cudaStream_t s = c.stream;
   const int d = X.d;
   std::vector<int64_t>& r = X.ranks;
@@ -584,6 +610,14 @@ int truncate(Ctx& c, tt_tensor& X, double tol, int64_t rmax, std::vector<int64_t
     double h = 0.0;
     TTR_CUDA(cudaMemcpyAsync(&h, nrm.p, sizeof(double), cudaMemcpyDeviceToHost, s));
     TTR_CUDA(cudaStreamSynchronize(s));
+    if (sl) {   // ||X_N||^2 summed over the slabs
+      double h2 = h * h;
+      TTR_CUDA(cudaMemcpyAsync(nrm.p, &h2, sizeof(double), cudaMemcpyHostToDevice, s));
+      TTR_TRY(allreduce_sum(c, nrm.p, 1));
+      TTR_CUDA(cudaMemcpyAsync(&h2, nrm.p, sizeof(double), cudaMemcpyDeviceToHost, s));
+      TTR_CUDA(cudaStreamSynchronize(s));
+      h = sqrt(h2);
+    }
     eps = h * tol / sqrt(double(d - 1));
   }
   ks.assign(d + 1, 1);
@@ -631,16 +665,23 @@ int truncate(Ctx& c, tt_tensor& X, double tol, int64_t rmax, std::vector<int64_t
     DBuf AV, V, sig, Q, R, Rt, Bk, newn, newp;
     int64_t k = 0;
     const int64_t rows_av = r0;
-    const int64_t cols = std::min(r0, mrow);
+    const int64_t mrow_g = sl ? sl->gdims[n - 1] * r[n] : mrow;   // all slabs' rows
+    const int64_t cols = std::min(r0, mrow_g);
     TTR_TRY(dalloc(AV, size_t(rows_av) * cols, s));
     TTR_TRY(dalloc(sig, size_t(cols), s));
     // fast path: only R of the QR is needed, and the SVD of R^T does not form V
     // (H(X_n) <- Sigma_k^{-2} (U Sigma)_k^T H(X_n) = V_k^T Q^T)
-    const bool fast = (mrow >= r0) && svd_nov_fits(r0, r0);
+    const bool fast = (mrow_g >= r0) && svd_nov_fits(r0, r0);
+    if (sl && !fast) {
+      set_error("mode-slab rounding: bond %d needs the general SVD path (rank %lld > 160 or a "
+                "wide unfolding), not supported with distributed rows", n - 1, (long long)r0);
+      return TT_ERR_ARG;
+    }
     if (fast) {
       TTR_TRY(dalloc(R, size_t(r0) * r0, s));
       TTR_TRY(dalloc(Rt, size_t(r0) * r0, s));
-      TTR_TRY(qr(c, mrow, r0, X.bufs[n - 1].p, r0, true, nullptr, R.p, s));   // R of H(X_n)^T
+      TTR_TRY(qr(c, mrow, r0, X.bufs[n - 1].p, r0, true, nullptr, R.p, s, sl != nullptr,
+                 mrow_g));                                                   // R of H(X_n)^T
       TTR_TRY(transpose(c, R.p, r0, r0, r0, Rt.p, r0, s));
       TTR_TRY(svd_nov(c, r0, r0, Rt.p, r0, AV.p, sig.p, s));                 // svd(R^T)
     } else {
@@ -726,8 +767,74 @@ int make_zero(Ctx& c, const std::vector<int64_t>& dims, tt_tensor& out) {
 
 constexpr int kPMin = 5;   // adaptive saturation margin (R8)
 
+// Slab-mode validation, agreed across ranks before any collective: local views
+// (S >= 1, this rank's slabs), gdims / slab_lo in range, then the ranks agree on
+// d, the options and gdims, and the slab sizes of every mode add up to gdims.
+int validate_slab(Ctx& c, const tt_view* v, int S, const int64_t* gdims, const int64_t* lo,
+                  int local_rc, const std::vector<int64_t>& extra, std::vector<int64_t>& dims,
+                  Slab& sl) {
+  int rc = local_rc;
+  if (rc == TT_OK) rc = validate(v, S, dims);
+  if (rc == TT_OK && (!gdims || !lo)) {
+    set_error("slab rounding needs gdims and slab_lo");
+    rc = TT_ERR_ARG;
+  }
+  const int d = rc == TT_OK ? int(dims.size()) : 0;
+  for (int n = 0; rc == TT_OK && n < d; ++n)
+    if (lo[n] < 0 || lo[n] + dims[n] > gdims[n]) {
+      set_error("mode %d: slab [%lld, %lld) outside 0..%lld", n + 1, (long long)lo[n],
+                (long long)(lo[n] + dims[n]), (long long)gdims[n]);
+      rc = TT_ERR_SHAPE;
+    }
+  if (rc == TT_OK) {
+    sl.gdims.assign(gdims, gdims + d);
+    sl.lo.assign(lo, lo + d);
+  }
+  if (c.world == 1) {
+    if (rc == TT_OK && sl.gdims != dims) {
+      set_error("one rank: the slabs must be the whole modes");
+      return TT_ERR_SHAPE;
+    }
+    return rc;
+  }
+  std::vector<int64_t> mx = {rc != TT_OK ? 1 : 0, d}, mn = {d};
+  for (int64_t e : extra) {
+    mx.push_back(e);
+    mn.push_back(e);
+  }
+  TTR_TRY(allreduce_i64(c, mx.data(), mx.size(), kOpMax));
+  TTR_TRY(allreduce_i64(c, mn.data(), mn.size(), kOpMin));
+  if (rc != TT_OK) return rc;
+  if (mx[0]) {
+    set_error("another rank rejected its slabs or options");
+    return TT_ERR_ARG;
+  }
+  if (mx[1] != mn[0]) {
+    set_error("ranks disagree on the number of modes");
+    return TT_ERR_SHAPE;
+  }
+  for (size_t i = 0; i < extra.size(); ++i)
+    if (mx[2 + i] != mn[1 + i]) {
+      set_error("ranks disagree on the options of the call");
+      return TT_ERR_ARG;
+    }
+  std::vector<int64_t> ghi(sl.gdims), glo(sl.gdims), sz(dims);
+  TTR_TRY(allreduce_i64(c, ghi.data(), size_t(d), kOpMax));
+  TTR_TRY(allreduce_i64(c, glo.data(), size_t(d), kOpMin));
+  TTR_TRY(allreduce_i64(c, sz.data(), size_t(d), kOpSum));
+  if (ghi != glo || sz != sl.gdims) {
+    set_error("the ranks' slabs do not tile the global modes");
+    return TT_ERR_SHAPE;
+  }
+  return TT_OK;
+}
+
 int round_sum_impl(tt_ctx* c, int S, const tt_view* terms, const tt_round_opts* o,
-                   tt_sketch* user_sk, tt_tensor** outp) {
+                   tt_sketch* user_sk, tt_tensor** outp, const int64_t* slab_gdims = nullptr,
+                   const int64_t* slab_lo = nullptr) {
+  const bool slab_mode = slab_gdims != nullptr;
+  Slab slab;
+  const Slab* sl = slab_mode ? &slab : nullptr;
   std::vector<int64_t> dims;
   int64_t ell = 0;
   double tol = 0.0;
@@ -770,19 +877,28 @@ int round_sum_impl(tt_ctx* c, int S, const tt_view* terms, const tt_round_opts* 
     extra = {o->mode, o->adaptive, o->rank, o->oversample, tbits, int64_t(o->seed & 0x7fffffffffffffffull),
              int64_t(o->seed >> 63), o->max_rank, user_sk != nullptr};
   }
-  TTR_TRY(validate_sharded(*c, terms, S, orc, extra, dims));
+  if (slab_mode) {
+    if (orc == TT_OK && user_sk) {
+      set_error("slab rounding draws its own sketch (no user sketch)");
+      orc = TT_ERR_ARG;
+    }
+    TTR_TRY(validate_slab(*c, terms, S, slab_gdims, slab_lo, orc, extra, dims, slab));
+  } else {
+    TTR_TRY(validate_sharded(*c, terms, S, orc, extra, dims));
+  }
   const int d = int(dims.size());
+  const std::vector<int64_t>& gdims = slab_mode ? slab.gdims : dims;   // global mode sizes
   TTR_CUDA(cudaSetDevice(c->device));
   PhaseTimer tm(*c);
   tm.begin(6);
   Terms T;
   TTR_TRY(stage_terms(*c, terms, S, d, T));
-  // global summed ranks (all shards)
+  // global summed ranks (summand shards: over the ranks; slabs: every rank has all)
   std::vector<int64_t> sumR(d + 1, 0);
   for (int n = 0; n <= d; ++n)
     for (int j = 0; j < S; ++j) sumR[n] += T.R[j][n];
-  TTR_TRY(allreduce_sum_i64(*c, sumR.data(), sumR.size()));
-  const std::vector<int64_t> scap = rank_caps(dims, sumR, int64_t(1) << 40);
+  if (!slab_mode) TTR_TRY(allreduce_sum_i64(*c, sumR.data(), sumR.size()));
+  const std::vector<int64_t> scap = rank_caps(gdims, sumR, int64_t(1) << 40);
   TTR_CUDA(cudaMemsetAsync(c->flags.p, 0, sizeof(int) * c->nflags, c->stream));
 
   std::unique_ptr<tt_tensor> out(new tt_tensor);
@@ -791,7 +907,7 @@ int round_sum_impl(tt_ctx* c, int S, const tt_view* terms, const tt_round_opts* 
   int64_t cur = ell;
   int passes = 0;
   for (;;) {
-    const std::vector<int64_t> l = rank_caps(dims, sumR, cur);
+    const std::vector<int64_t> l = rank_caps(gdims, sumR, cur);
     tt_sketch own;
     const tt_sketch* sk = user_sk;
     if (user_sk) {
@@ -801,14 +917,14 @@ int round_sum_impl(tt_ctx* c, int S, const tt_view* terms, const tt_round_opts* 
       }
     } else {
       tm.begin(0);
-      TTR_TRY(make_sketch(*c, dims, l, o->seed, uint32_t(passes), own));
+      TTR_TRY(make_sketch(*c, dims, l, o->seed, uint32_t(passes), own, 2, 0, sl));
       tm.end(0);
       sk = &own;
     }
     tt_tensor X;
     X.stream = c->stream;
     X.alive = c->alive;
-    TTR_TRY(alg7(*c, T, dims, l, *sk, X, tm));
+    TTR_TRY(alg7(*c, T, dims, l, *sk, X, tm, sl));
     ++passes;
     bool capped = false;
     for (int n = 1; n < d; ++n) capped |= l[n] < cur;
@@ -833,7 +949,7 @@ int round_sum_impl(tt_ctx* c, int S, const tt_view* terms, const tt_round_opts* 
     }
     std::vector<int64_t> ks;
     tm.begin(5);
-    TTR_TRY(truncate(*c, X, tol, rank, ks));
+    TTR_TRY(truncate(*c, X, tol, rank, ks, sl));
     tm.end(5);
     TTR_TRY(read_flags(*c, fl, 4));
     flags |= (fl[1] ? TT_FLAG_QR_FALLBACK : 0);
@@ -868,6 +984,7 @@ int round_sum_impl(tt_ctx* c, int S, const tt_view* terms, const tt_round_opts* 
     set_error("QR breakdown even after the Householder fallback");
     return TT_ERR_NUMERIC;
   }
+  if (slab_mode) out->flags |= TT_FLAG_SLAB;
   *outp = out.release();
   return TT_OK;
 }
@@ -2075,6 +2192,15 @@ int tt_round_sum(tt_ctx_t c, int32_t S_local, const tt_view* terms, const tt_rou
     return TT_ERR_ARG;
   }
   return guarded([&] { return round_sum_impl(c, S_local, terms, opts, sketch, out); });
+}
+
+int tt_round_sum_slab(tt_ctx_t c, int32_t S, const tt_view* terms, const int64_t* gdims,
+                      const int64_t* slab_lo, const tt_round_opts* opts, tt_tensor_t* out) {
+  if (!c || !out || !gdims || !slab_lo) {
+    set_error("tt_round_sum_slab: null ctx/out/gdims/slab_lo");
+    return TT_ERR_ARG;
+  }
+  return guarded([&] { return round_sum_impl(c, S, terms, opts, nullptr, out, gdims, slab_lo); });
 }
 
 int tt_round_sum_two_sided(tt_ctx_t c, int32_t S_local, const tt_view* terms, int64_t ell,

@@ -175,6 +175,10 @@ int proj_carry(Ctx& c, int64_t m, int l, int sumR, const double* Q, const double
 // ---------------------------------------------------------------- sketch
 int philox_fill(Ctx& c, double* out, int64_t count, uint64_t seed, uint32_t n,
                 uint32_t tag, double scale, cudaStream_t s);
+// the mode slab [i_lo, i_lo + I_loc) of the r0 x I_g x r1 core philox_fill would write
+int philox_fill_slab(Ctx& c, double* out, int64_t r0, int64_t I_loc, int64_t r1, int64_t i_lo,
+                     int64_t I_g, uint64_t seed, uint32_t n, uint32_t tag, double scale,
+                     cudaStream_t s);
 
 // ---------------------------------------------------------------- dense linalg
 // Thin QR of the m x n matrix op(A) (m >= n): trans=false: A is m x n (ld lda);
@@ -182,8 +186,10 @@ int philox_fill(Ctx& c, double* out, int64_t count, uint64_t seed, uint32_t n,
 // Q: m x n (ld m).  R (optional): n x n upper (ld n).  Flags written to
 // c.flags (fallback/breakdown).  Uses shifted CholeskyQR3 with a Householder
 // fallback.
+// dist: the m rows are this rank's share of mglob rows (mode-slab sharding): every
+// Gram is all-reduced over the ranks before its Cholesky (no Householder fallback).
 int qr(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, bool trans, double* Q,
-       double* R, cudaStream_t s);
+       double* R, cudaStream_t s, bool dist = false, int64_t mglob = 0);
 // One-sided Jacobi SVD of the m x n (m >= n) matrix A (ld lda): AV = U Sigma
 // (m x n, ld m), V (n x n, ld n), sigma (n) sorted descending.
 int svd_jacobi(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, double* AV,

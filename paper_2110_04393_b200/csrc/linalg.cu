@@ -57,7 +57,48 @@ __global__ void philox_fill_kernel(double* __restrict__ out, int64_t count, uint
   }
 }
 
+// The slab [i_lo, i_lo + I_loc) of mode index i of an r0 x I_g x r1 Gaussian core:
+// element (a, il, b) is element e = a + r0 (i_lo + il + I_g b) of the full core,
+// i.e. number e & 1 of Philox pair e >> 1 -- the same bits as philox_fill_kernel.
+__global__ void philox_fill_slab_kernel(double* __restrict__ out, int64_t r0, int64_t I_loc,
+                                        int64_t r1, int64_t i_lo, int64_t I_g, uint32_t key0,
+                                        uint32_t key1, uint32_t n, uint32_t tag, double scale) {
+  const int64_t cnt = r0 * I_loc * r1;
+  for (int64_t x = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; x < cnt;
+       x += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t a = x % r0, il = (x / r0) % I_loc, b = x / (r0 * I_loc);
+    const int64_t e = a + r0 * (i_lo + il + I_g * b);
+    const int64_t k = e >> 1;
+    uint32_t c0 = uint32_t(k), c1 = uint32_t(uint64_t(k) >> 32), c2 = n, c3 = tag;
+    uint32_t k0 = key0, k1 = key1;
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+      philox_round(c0, c1, c2, c3, k0, k1);
+      k0 += 0x9E3779B9u;
+      k1 += 0xBB67AE85u;
+    }
+    const double u1 = unit53(c0, c1), u2 = unit53(c2, c3);
+    const double r = sqrt(-2.0 * log(u1));
+    const double th = 2.0 * 3.141592653589793 * u2;
+    double sn, cs;
+    sincos(th, &sn, &cs);
+    out[x] = (e & 1) ? (r * sn) * scale : (r * cs) * scale;
+  }
+}
+
 }  // namespace
+
+int philox_fill_slab(Ctx& c, double* out, int64_t r0, int64_t I_loc, int64_t r1, int64_t i_lo,
+                     int64_t I_g, uint64_t seed, uint32_t n, uint32_t tag, double scale,
+                     cudaStream_t s) {
+  const int64_t cnt = r0 * I_loc * r1;
+  if (cnt <= 0) return TT_OK;
+  const int blocks = int(std::min<int64_t>((cnt + 255) / 256, int64_t(c.sm_count) * 16));
+  philox_fill_slab_kernel<<<blocks, 256, 0, s>>>(out, r0, I_loc, r1, i_lo, I_g,
+                                                 uint32_t(seed & 0xffffffffu), uint32_t(seed >> 32),
+                                                 n, tag, scale);
+  return launched();
+}
 
 int philox_fill(Ctx& c, double* out, int64_t count, uint64_t seed, uint32_t n, uint32_t tag,
                 double scale, cudaStream_t s) {
@@ -710,6 +751,10 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
 
 __global__ void route_start_kernel(int* flags) { flags[0] = flags[0] >= 1 ? 1 : 0; }
 
+__global__ void route_fail_kernel(int* flags) {
+  if (flags[0] == 3) atomicOr(&flags[3], 1);
+}
+
 __global__ void gated_set_kernel(int* flag, int from, int to) {
   if (*flag == from) *flag = to;
 }
@@ -1048,9 +1093,10 @@ static int launch_chol(Ctx& c, const double* Gm, int n, int64_t m, int mode, dou
 }
 
 int qr(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, bool trans, double* Q,
-       double* R, cudaStream_t s) {
-  if (m < n || n < 1) {
-    set_error("qr: need m >= n >= 1 (m=%lld n=%lld)", (long long)m, (long long)n);
+       double* R, cudaStream_t s, bool dist, int64_t mglob) {
+  if (mglob <= 0) mglob = m;
+  if ((!dist && m < n) || mglob < n || n < 1 || m < 0) {
+    set_error("qr: need m >= n >= 1 (m=%lld n=%lld)", (long long)mglob, (long long)n);
     return TT_ERR_ARG;
   }
   if (n > 1024) {
@@ -1085,12 +1131,24 @@ int qr(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, bool trans, d
   double* Rk_p = R ? Rk.p : nullptr;
 
   // Gram of the input op(A) (A is m x n, or n x m when trans)
+  // distributed (mode-slab sharding, NEXT-2): this rank holds m of the mglob
+  // rows; every Gram is summed over the ranks (an n x n allreduce), so every rank
+  // factors the same Gram and the route flags agree; Q keeps the local rows
+  auto reduce_gram = [&]() -> int {
+    if (!dist) return TT_OK;
+    return allreduce_sum(c, Gm.p, size_t(n) * n);
+  };
   auto gram_of_input = [&](const int* gate, int gv) -> int {
-    if (trans)
-      return gemm1(c, false, true, ni, ni, mi, 1.0, A, int(lda), A, int(lda), 0.0, Gm.p, ni, s,
-                   gate, gv, kGemmLower);
-    return gemm1(c, true, false, ni, ni, mi, 1.0, A, int(lda), A, int(lda), 0.0, Gm.p, ni, s,
-                 gate, gv, kGemmLower);
+    if (mi == 0) {
+      TTR_TRY(fill_zero(c, Gm.p, int64_t(ni) * ni, s));
+    } else if (trans) {
+      TTR_TRY(gemm1(c, false, true, ni, ni, mi, 1.0, A, int(lda), A, int(lda), 0.0, Gm.p, ni, s,
+                    gate, gv, kGemmLower));
+    } else {
+      TTR_TRY(gemm1(c, true, false, ni, ni, mi, 1.0, A, int(lda), A, int(lda), 0.0, Gm.p, ni, s,
+                    gate, gv, kGemmLower));
+    }
+    return reduce_gram();
   };
   auto input_times_rinv = [&](double* dst, const int* gate, int gv) -> int {
     if (trans)
@@ -1100,8 +1158,10 @@ int qr(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, bool trans, d
                  gate, gv, kGemmTriB);
   };
   auto gram = [&](const double* src, const int* gate, int gv) -> int {
-    return gemm1(c, true, false, ni, ni, mi, 1.0, src, mi, src, mi, 0.0, Gm.p, ni, s, gate, gv,
-                 kGemmLower);
+    if (mi == 0) TTR_TRY(fill_zero(c, Gm.p, int64_t(ni) * ni, s));
+    else TTR_TRY(gemm1(c, true, false, ni, ni, mi, 1.0, src, mi, src, mi, 0.0, Gm.p, ni, s, gate,
+                       gv, kGemmLower));
+    return reduce_gram();
   };
   auto times_rinv = [&](const double* src, double* dst, const int* gate, int gv) -> int {
     return gemm1(c, false, false, mi, ni, ni, 1.0, src, mi, Rinv.p, ni, 0.0, dst, mi, s, gate,
@@ -1122,7 +1182,7 @@ int qr(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, bool trans, d
   };
   auto chol = [&](int mode, const int* gate, int gv) -> int {
     dump("gram", Gm.p, int64_t(ni) * ni);
-    int r = launch_chol(c, Gm.p, ni, m, mode, Rinv.p, Rk_p, gw.p, gate, gv, s);
+    int r = launch_chol(c, Gm.p, ni, mglob, mode, Rinv.p, Rk_p, gw.p, gate, gv, s);
     if (Rk_p) dump("Rk", Rk_p, int64_t(ni) * ni);
     return r;
   };
@@ -1224,7 +1284,12 @@ int qr(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, bool trans, d
   if (R)
     TTR_CUDA(cudaMemcpyAsync(R, Racc.p, sizeof(double) * n * n, cudaMemcpyDeviceToDevice, s));
   // ---- route 3 (all CholeskyQR variants failed): R-only QRs of a numerically
-  // rank-deficient matrix go to the Householder TSQR; otherwise Householder
+  // rank-deficient matrix go to the Householder TSQR; otherwise Householder.
+  // Distributed rows: no Householder fallback -- reported as a breakdown.
+  if (dist) {
+    route_fail_kernel<<<1, 1, 0, s>>>(F);
+    return launched();
+  }
   if (r_only && tsqr_fits(ni)) {
     TTR_TRY(tsqr_r(c, m, ni, A, lda, trans, R, F, 3, s));
     return TT_OK;

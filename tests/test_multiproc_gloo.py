@@ -157,3 +157,93 @@ def test_sharded_alg7_and_alg6_world2_match_unsharded_oracle():
         assert oracle.rel_diff(res[r][1], ref2) <= 1e-12
     for a, b in zip(res[0][1], res[1][1]):
         assert np.array_equal(a, b)
+
+
+# ---------------------------------------------------------------- mode-slab sharding (NEXT-2)
+def _cholqr2_dist(Y, allreduce):
+    """Thin Q of the row-distributed Y by CholeskyQR2 with all-reduced Grams (the
+    distributed QR of tt_round_sum_slab): G = Σ_ranks Y_rᵀY_r, R = chol(G)ᵀ,
+    Q_r = Y_r R⁻¹, twice."""
+    for _ in range(2):
+        G = allreduce(Y.T @ Y)
+        R = np.linalg.cholesky(G).T
+        Y = np.linalg.solve(R.T, Y.T).T
+    return Y
+
+
+def slab_alg7(terms, Gs, allreduce):
+    """Alg. 7 with every core split into mode-index slabs over the ranks
+    (all summands on every rank): Alg. 3's W_{n-1} = H(Z_n)H(G_n)ᵀ and line 11's
+    M = QᵀV(X_n) contract the mode index -> partial sums + one all-reduce each; the
+    QR of the row-distributed Y_n takes all-reduced Grams; carries stay local."""
+    N = len(terms[0])
+    Wj = []
+    for t in terms:
+        W = {N - 1: allreduce(oracle.H(t[N - 1]) @ oracle.H(Gs[N - 1]).T)}
+        for n in range(N - 1, 1, -1):
+            Z = oracle.fold_V(oracle.V(t[n - 1]) @ W[n], t[n - 1].shape[1])
+            W[n - 1] = allreduce(oracle.H(Z) @ oracle.H(Gs[n - 1]).T)
+        Wj.append(W)
+    Xn = np.concatenate([t[0] for t in terms], axis=2)
+    X = [None] * N
+    for n in range(1, N):
+        I = Xn.shape[1]
+        Zn = oracle.V(Xn)
+        Q = _cholqr2_dist(Zn @ np.concatenate([w[n] for w in Wj], axis=0), allreduce)
+        X[n - 1] = oracle.fold_V(Q, I)
+        M = allreduce(Q.T @ Zn)
+        offs = np.cumsum([0] + [t[n - 1].shape[2] for t in terms])
+        Mj = [M[:, offs[j]:offs[j + 1]] for j in range(len(terms))]
+        if n < N - 1:
+            Xn = np.concatenate([oracle.fold_H(Mj[j] @ oracle.H(t[n]), t[n].shape[1])
+                                 for j, t in enumerate(terms)], axis=2)
+        else:
+            X[N - 1] = oracle.fold_H(sum(Mj[j] @ oracle.H(t[N - 1]) for j, t in enumerate(terms)),
+                                     terms[0][N - 1].shape[1])
+    return X
+
+
+def _slab_worker(rank, world, port, out_q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        w = ttsynth.config3_sum10(d=5, I=12, S=5)
+        terms = [ttsynth.to_numpy(t) for t in w.terms]
+        dims = oracle.dims_of(terms[0])
+        sumR = [1] + [sum(t[n].shape[2] for t in terms) for n in range(len(dims) - 1)] + [1]
+        G = oracle.gaussian_sketch(dims, oracle.rank_caps(dims, sumR, 9), seed=1)
+        sl = [((rank * I) // world, ((rank + 1) * I) // world) for I in dims]
+        loc = [[c[:, a:b, :] for c, (a, b) in zip(t, sl)] for t in terms]
+        Gs = [None] + [g[:, a:b, :] for g, (a, b) in zip(G[1:], sl[1:])]
+
+        def allreduce(a):
+            t = torch.from_numpy(np.ascontiguousarray(a))
+            dist.all_reduce(t)
+            return t.numpy()
+
+        X = slab_alg7(loc, Gs, allreduce)
+        out_q.put((rank, [c.copy() for c in X]))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_slab_sharded_alg7_world2_matches_unsharded_oracle():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_slab_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=240) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    w = ttsynth.config3_sum10(d=5, I=12, S=5)
+    terms = [ttsynth.to_numpy(t) for t in w.terms]
+    dims = oracle.dims_of(terms[0])
+    sumR = [1] + [sum(t[n].shape[2] for t in terms) for n in range(len(dims) - 1)] + [1]
+    G = oracle.gaussian_sketch(dims, oracle.rank_caps(dims, sumR, 9), seed=1)
+    ref = oracle.round_sum_rand_orth(terms, G)
+    X = [np.concatenate([res[0][n], res[1][n]], axis=1) for n in range(len(dims))]
+    assert oracle.rel_diff(X, ref) <= 1e-12
+    assert oracle.left_orth_residual(X) < 1e-12
