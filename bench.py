@@ -137,12 +137,17 @@ def two_sided_ell(wl):
     return int(wl.rank) if wl.rank else int(wl.ell)
 
 
-def flops_of(wl, ranks_out, algo="rand_orth"):
+def shapes_of(wl):
+    """(global mode sizes, per-summand ranks) of a workload, before any sharding."""
+    return (list(wl.dims),
+            [[int(t[0].shape[0])] + [int(c.shape[2]) for c in t] for t in wl.terms])
+
+
+def flops_of(wl, ranks_out, algo="rand_orth", shapes=None):
     from paper_2110_04393_b200 import cost
-    dims = wl.dims
+    dims, tr = shapes if shapes is not None else shapes_of(wl)
     if algo == "deterministic":
         return {"total": None, "phase1": None}, None
-    tr = [[int(t[0].shape[0])] + [int(c.shape[2]) for c in t] for t in wl.terms]
     sumR = [sum(r[n] for r in tr) for n in range(len(dims) + 1)]
     if algo == "two_sided":
         ell = two_sided_ell(wl)
@@ -276,6 +281,9 @@ def main():
                     help="B independent roundings per step (distinct sketch seeds), spread "
                          "over --streams contexts (SURVEY 8d batched throughput of C1/C2)")
     ap.add_argument("--streams", type=int, default=1)
+    ap.add_argument("--shard", default="summands", choices=["summands", "slab"],
+                    help="N>1 partition: summands (SURVEY 8e, the default) or mode slabs "
+                         "of every summand (tt_round_sum_slab, NEXT-2)")
     ap.add_argument("--algo", default="rand_orth",
                     choices=["rand_orth", "two_sided", "deterministic"],
                     help="rand_orth: tt_round_sum (Alg. 7 + truncation, the headline); "
@@ -317,11 +325,23 @@ def main():
 
     wl = make_workload(args.workload, dev)
     S = len(wl.terms)
+    shapes = shapes_of(wl)
     from paper_2110_04393_b200.shard import shard_bounds
-    lo, hi = shard_bounds(S, world, rank)
-    local_terms = wl.terms[lo:hi]
-    for t in wl.terms[:lo] + wl.terms[hi:]:
-        t.clear()
+    slab = args.shard == "slab"
+    if slab:
+        # every rank: all summands, the mode-index slab [lo_n, hi_n) of every core
+        lo, hi = 0, S
+        gdims = [int(c.shape[1]) for c in wl.terms[0]]
+        slab_lo = [(rank * I) // world for I in gdims]
+        slab_hi = [((rank + 1) * I) // world for I in gdims]
+        local_terms = [[c[:, a:b, :].permute(2, 1, 0).contiguous().permute(2, 1, 0)
+                        for c, a, b in zip(t, slab_lo, slab_hi)] for t in wl.terms]
+        wl.terms.clear()
+    else:
+        lo, hi = shard_bounds(S, world, rank)
+        local_terms = wl.terms[lo:hi]
+        for t in wl.terms[:lo] + wl.terms[hi:]:
+            t.clear()
     torch.cuda.synchronize()
 
     nccl_id = None
@@ -347,6 +367,8 @@ def main():
             return ctx.tt_round_deterministic(terms, tol=wl.tol, rank=0 if wl.tol > 0 else wl.rank)
         if two_sided:
             return ctx.tt_round_sum_two_sided(terms, ell=two_sided_ell(wl), rho=0, seed=1)
+        if slab:
+            return ctx.tt_round_sum_slab(terms, gdims, slab_lo, seed=1, **kw)
         return ctx.tt_round_sum(terms, seed=1, **kw)
 
     def step():
@@ -389,13 +411,14 @@ def main():
         phase = ph.tolist()
     phase = [p / args.steps for p in phase]
 
-    fl, l = flops_of(wl, ranks_out, args.algo)
+    fl, l = flops_of(wl, ranks_out, args.algo, shapes)
     peak, peak_src = fp64_peak()
     value = 1000.0 / ms                       # roundings/s (one rounding per step, all ranks)
     tflops = fl["total"] / (ms * 1e-3) / 1e12 if fl["total"] else None
     # dominant kernel family: the phase-1 DMMA contractions (Alg. 3), timed live
     p1_ms = phase[1]
-    p1_flops_local = fl["phase1"] * (hi - lo) / S if fl["phase1"] else None
+    share = (1.0 / world) if slab else (hi - lo) / S
+    p1_flops_local = fl["phase1"] * share if fl["phase1"] else None
     p1_achieved = p1_flops_local / (p1_ms * 1e-3) / 1e12 if (p1_ms > 0 and p1_flops_local) else None
 
     e2e = None
@@ -424,7 +447,8 @@ def main():
             "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic (ttsynth, seeded; DESIGN.md input recipe)",
-            "config": bench_config(args.workload, args.algo, world),
+            "config": dict(bench_config(args.workload, args.algo, world),
+                           **({"parallelism": f"mode-slabs/{world}"} if slab else {})),
             "tflops": tflops, "fp64_peak_tflops": peak, "fp64_peak_source": peak_src,
             "frac_of_fp64_peak": tflops / peak if tflops else None,
             "flops_per_rounding": fl,
