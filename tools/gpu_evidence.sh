@@ -1,0 +1,22 @@
+# round-2 evidence: full GPU suite, default bench line (+ full-size oracle baseline),
+# reference arm, launch list of the bench command, ncu --set full of the top kernels,
+# smoke, per-config lines.  Usage: bash tools/gpu_evidence.sh <tag>
+T=${1:-v1}
+mkdir -p gpurun_out
+python -m paper_2110_04393_b200.build > /dev/null
+timeout 120 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/ev_${T}_smoke.log 2>&1; echo "smoke rc=$?" | tee -a gpurun_out/ev_${T}_smoke.log
+timeout 2400 python -m pytest tests -m gpu -q --timeout 1800 > gpurun_out/ev_${T}_pytest.log 2>&1; echo "pytest rc=$?" | tee -a gpurun_out/ev_${T}_pytest.log; tail -3 gpurun_out/ev_${T}_pytest.log
+timeout 1200 python bench.py --steps 20 --warmup 5 > gpurun_out/ev_${T}_bench_large.json 2> gpurun_out/ev_${T}_bench_large.err; echo "bench rc=$?"; cut -c1-300 gpurun_out/ev_${T}_bench_large.json
+timeout 1200 python bench.py --impl reference --steps 20 --warmup 5 > gpurun_out/ev_${T}_ref_large.json 2>&1; echo "ref rc=$?"
+timeout 600 python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e > /dev/null 2>&1 && \
+timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none -c 100000 --csv --log-file gpurun_out/ev_${T}_launches.csv python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e > gpurun_out/ev_${T}_ncu_launches.log 2>&1; echo "ncu launches rc=$?"
+python tools/ncu_agg.py gpurun_out/ev_${T}_launches.csv 30 > gpurun_out/ev_${T}_launches.txt 2>&1
+for K in "dgemm_tma_kernel<64, 48, 16, 4, 2, 4, false, true>" "proj_carry_kernel" "dgemm_tma_kernel<64, 48, 16, 4, 2, 4, false, false>" "dgemm_tma_kernel<128, 48, 16, 4, 2, 4, false, false>"; do
+  N=$(echo "$K" | tr -cd 'a-z0-9_')
+  timeout 900 ncu --set full --clock-control none --import-source on -k "regex:$(echo $K | sed 's/[<>,]/./g; s/ //g')" -s 3 -c 1 -o gpurun_out/ev_${T}_$N -f python tools/run_once.py large 6 1 > gpurun_out/ev_${T}_ncu_$N.log 2>&1; echo "ncu full $N rc=$?"
+  ncu -i gpurun_out/ev_${T}_$N.ncu-rep --page raw --csv --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active,sm__inst_executed_pipe_tensor_op_dmma.avg.pct_of_peak_sustained_active,sm__pipe_tensor_op_dmma_cycles_active.avg.pct_of_peak_sustained_active,launch__registers_per_thread,sm__warps_active.avg.pct_of_peak_sustained_active > gpurun_out/ev_${T}_ncu_${N}_raw.csv 2>&1
+done
+for W in tiny single sum10 gmres; do
+  timeout 900 python bench.py --workload $W --steps 10 --warmup 3 --no-cpu > gpurun_out/ev_${T}_bench_$W.json 2>&1; echo "bench $W rc=$?"
+done
+timeout 900 python bench.py --algo two_sided --steps 10 --warmup 3 --no-cpu > gpurun_out/ev_${T}_bench_large_two_sided.json 2>&1; echo "bench 2s rc=$?"
