@@ -142,6 +142,7 @@ enum CholMode : int {
                    // (numerically null directions only) clamped to tau
 };
 constexpr double kDevTol = 0.05;
+constexpr int kNearIdFlag = 20;   // flags[20]: 1 = run the full Cholesky for pass 4 (R only)
 // mode bit of the R-only QR: a plain pass whose pivots spread by more than
 // 2^20 (kappa(Q1)^2 u no longer small) cannot give an accurate R -> next route
 constexpr int kStrict = 0x100;
@@ -751,6 +752,33 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
 
 __global__ void route_start_kernel(int* flags) { flags[0] = flags[0] >= 1 ? 1 : 0; }
 
+// Cholesky factor of a Gram G = I + E that is the identity to working accuracy
+// (the truncation's last CholeskyQR pass: its input is already orthonormal to
+// O(u)): R = I + U with U = triu(E) and U_ii = E_ii / 2, so that
+// R^T R = G + U^T U = G + O(||E||^2).  flags[slot] = 1 (-> the full Cholesky runs,
+// gated) when max |E| > thr, where the first-order factor is not exact enough.
+__global__ void __launch_bounds__(256)
+    near_identity_chol_kernel(const double* __restrict__ G, int n, double* __restrict__ R,
+                              int* __restrict__ flags, int slot, double thr) {
+  __shared__ double red[32];
+  double mx = 0.0;
+  for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+    const int i = e % n, j = e / n;
+    const double g = G[(i >= j) ? e : j + int64_t(i) * n];   // lower triangle holds G
+    const double x = g - (i == j ? 1.0 : 0.0);
+    mx = fmax(mx, fabs(x));
+    R[e] = (i < j) ? x : (i == j ? 1.0 + 0.5 * x : 0.0);
+  }
+  for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double m = 0.0;
+    for (int w = 0; w < (int(blockDim.x) + 31) / 32; ++w) m = fmax(m, red[w]);
+    flags[slot] = (m > thr || !(m == m)) ? 1 : 0;
+  }
+}
+
 __global__ void route_fail_kernel(int* flags) {
   if (flags[0] == 3) atomicOr(&flags[3], 1);
 }
@@ -1228,7 +1256,12 @@ int qr(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, bool trans, d
     TTR_TRY(accumulate_r(nullptr, 0));
     TTR_TRY(times_rinv(T2.p, T1.p, nullptr, 0));            // Q3 = Q2 R3^{-1}
     TTR_TRY(gram(T1.p, nullptr, 0));
-    TTR_TRY(chol(CH_RCLAMP, nullptr, 0));                   // R4 (plain, clamped)
+    // R4: Q3 is orthonormal to O(u), so its Gram is I + E with ||E|| = O(u) and
+    // the first-order factor I + triu(E) (half diagonal) is exact to O(u^2); the
+    // full Cholesky runs only when max |E| > 1e-8 (gated on the device)
+    near_identity_chol_kernel<<<1, 256, 0, s>>>(Gm.p, ni, Rk.p, F, kNearIdFlag, 1e-8);
+    TTR_TRY(launched());
+    TTR_TRY(chol(CH_RCLAMP, F + kNearIdFlag, 1));           // R4 (plain, clamped), if needed
     TTR_TRY(accumulate_r(nullptr, 0));
     TTR_CUDA(cudaMemcpyAsync(R, Racc.p, sizeof(double) * n * n, cudaMemcpyDeviceToDevice, s));
     return TT_OK;

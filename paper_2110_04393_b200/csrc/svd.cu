@@ -254,9 +254,37 @@ struct JcShared {
   double norms[kCl * kGpc * 2 * kUw];     // final column norms (all columns, by id)
   double red[8];
   int rot;
+  // point-to-point round hand-off (P2P variant): ready[b][g] completes when both
+  // units of group g's next round have landed in buffer b (64 arrivals: 32 lanes
+  // of each of the two source groups); freeb[b][g] completes when both groups
+  // that group g writes into have finished reading their buffer b
+  alignas(8) unsigned long long ready[2][kGpc];
+  alignas(8) unsigned long long freeb[2][kGpc];
 };
 
 constexpr int kJcThreads = kGpc * 32;
+
+__device__ __forceinline__ uint32_t jc_saddr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+// arrive (release, cluster scope) on the mbarrier at local address `la` of CTA `rank`
+__device__ __forceinline__ void jc_remote_arrive(uint32_t la, uint32_t rank) {
+  uint32_t ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(ra) : "r"(la), "r"(rank));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(ra)
+               : "memory");
+}
+__device__ __forceinline__ void jc_wait(uint32_t la, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "JCW_%=:\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra JCW_%=;\n"
+      "}\n" ::"r"(la),
+      "r"(parity)
+      : "memory");
+}
 
 // rotate the pair (X, Y) held by this 8-lane subgroup (ids cx, cy, squared
 // norms ax, ay); p = min(id) is rotated as column p of the single-CTA kernel.
@@ -311,6 +339,11 @@ __device__ __forceinline__ bool jc_rotate(double2 (&x)[kR2], double2 (&y)[kR2], 
   return true;
 }
 
+// P2P = true: instead of one cluster barrier per round, a group waits only for
+// the two groups whose units it receives (ready) and, before writing into its two
+// destination groups' next buffer, for those groups to have released it (freeb);
+// one cluster barrier per sweep remains (the convergence vote).
+template <bool P2P>
 __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kJcThreads)
     jacobi_cluster_kernel(const double* __restrict__ A, int64_t lda, int m, int n, int gpc,
                           double* __restrict__ AV, double* __restrict__ sigma, int max_sweeps,
@@ -356,6 +389,16 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kJcThreads)
     double s = 0.0;
     for (int w = 0; w < kGpc; ++w) s += sh.red[w];
     for (int r = 0; r < kCl; ++r) cl.map_shared_rank(&sh, r)->norms[crank] = s;   // scratch
+    if (P2P) {
+      for (int b = 0; b < 2; ++b)
+        for (int q = 0; q < kGpc; ++q) {
+          asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(jc_saddr(&sh.ready[b][q])),
+                       "r"(64));
+          asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(jc_saddr(&sh.freeb[b][q])),
+                       "r"(64));
+        }
+      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
   }
   cl.sync();
   double fro2 = 0.0;
@@ -376,6 +419,10 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kJcThreads)
   JcShared* sht = (gt / gpc == crank) ? &sh : cl.map_shared_rank(&sh, gt / gpc);
   JcShared* shb = (gb / gpc == crank) ? &sh : cl.map_shared_rank(&sh, gb / gpc);
   const int lt = gt % gpc, lb = gb % gpc;
+  // groups whose units group g receives: its top slot from max(g-1, 0), its
+  // bottom slot from g+1 (or itself, the last group)
+  const int st = g > 0 ? g - 1 : 0, sb = (g == halfU - 1) ? g : g + 1;
+  uint32_t round_g = 0;   // rounds done so far (all sweeps): ring position / phase
 
   // rotate slots (cx, cy) of the current buffer in place
   auto in_place = [&](double (*sl)[kRows], double* al, const int* cid, int cx, int cy,
@@ -409,6 +456,8 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kJcThreads)
     if (tid == 0) sh.rot = 0;
     int rot = 0;
     for (int r = 0; r < UP - 1; ++r) {
+      if (P2P && live && round_g > 0)   // this round's units have landed in buffer buf
+        jc_wait(jc_saddr(&sh.ready[buf][lg]), ((round_g - 1) >> 1) & 1);
       double (*sl)[kRows] = sh.slot[buf][lgc];
       double* al = sh.alpha[buf][lgc];
       const int* cid = sh.col[buf][lgc];
@@ -450,6 +499,8 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kJcThreads)
         double ax = al[cx], ay = al[cy];
         const int idx = cid[cx], idy = cid[cy];
         if (live && jc_rotate(x, y, idx, idy, ax, ay, n, small, tol)) rot = 1;
+        if (P2P && live && round_g > 0)   // both destinations released their buffer nb
+          jc_wait(jc_saddr(&sh.freeb[buf ^ 1][lg]), ((round_g - 1) >> 1) & 1);
         if (live) {
           const int nb = buf ^ 1;
           double2* dx = reinterpret_cast<double2*>(sht->slot[nb][lt][wt + cx]) + t8;
@@ -465,10 +516,19 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kJcThreads)
             sht->col[nb][lt][wt + cx] = idx;
             shb->col[nb][lb][wb + cy - kUw] = idy;
           }
+          if (P2P) {
+            // every lane: my writes into the destinations' buffer nb are done
+            // (release), and I am done reading my buffer buf (my sources may refill it)
+            jc_remote_arrive(jc_saddr(&sh.ready[nb][lt]), uint32_t(gt / gpc));
+            jc_remote_arrive(jc_saddr(&sh.ready[nb][lb]), uint32_t(gb / gpc));
+            jc_remote_arrive(jc_saddr(&sh.freeb[buf][st % gpc]), uint32_t(st / gpc));
+            jc_remote_arrive(jc_saddr(&sh.freeb[buf][sb % gpc]), uint32_t(sb / gpc));
+          }
         }
       }
       buf ^= 1;
-      cl.sync();
+      ++round_g;
+      if (!P2P) cl.sync();
     }
     if (rot) atomicOr(&cl.map_shared_rank(&sh, 0)->rot, 1);
 #ifdef TTR_JAC_PROF
@@ -530,14 +590,24 @@ int svd_nov_cluster(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, 
   std::unique_lock<std::mutex> init_lock(init_mutex(), std::defer_lock);
   if (!attr[c.device & 63]) init_lock.lock();
   if (!attr[c.device & 63]) {
-    TTR_CUDA(cudaFuncSetAttribute(jacobi_cluster_kernel,
+    TTR_CUDA(cudaFuncSetAttribute(jacobi_cluster_kernel<true>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, int(shm)));
+    TTR_CUDA(cudaFuncSetAttribute(jacobi_cluster_kernel<false>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, int(shm)));
     attr[c.device & 63] = true;
   }
   const int64_t U = (n + kUw - 1) / kUw, UP = U + (U & 1);
   const int gpc = int((UP / 2 + kCl - 1) / kCl);
-  jacobi_cluster_kernel<<<kCl, kJcThreads, shm, s>>>(A, lda, int(m), int(n), gpc, AV, sigma,
-                                                       40, c.flags.p);
+  static const bool sync_rounds = [] {   // diagnostics: "cluster" = one cluster barrier per round
+    const char* v = getenv("TTR_JACOBI");
+    return v && strcmp(v, "cluster") == 0;
+  }();
+  if (sync_rounds)
+    jacobi_cluster_kernel<false><<<kCl, kJcThreads, shm, s>>>(A, lda, int(m), int(n), gpc, AV,
+                                                                sigma, 40, c.flags.p);
+  else
+    jacobi_cluster_kernel<true><<<kCl, kJcThreads, shm, s>>>(A, lda, int(m), int(n), gpc, AV,
+                                                               sigma, 40, c.flags.p);
   return launched();
 }
 
