@@ -248,18 +248,18 @@ constexpr int kRps = 20;        // rows per thread (m <= 160)
 constexpr int kRows = kG8 * kRps;
 
 struct JcShared {
-  alignas(16) double slot[2][kGpc][2 * kUw][kRows];   // [buffer][group][t0..t3, b0..b3][rows]
-  double alpha[2][kGpc][2 * kUw];         // squared norms travelling with the columns
-  int col[2][kGpc][2 * kUw];              // column ids travelling with the columns
+  alignas(16) double slot[3][kGpc][2 * kUw][kRows];   // [buffer][group][t0..t3, b0..b3][rows]
+  double alpha[3][kGpc][2 * kUw];         // squared norms travelling with the columns
+  int col[3][kGpc][2 * kUw];              // column ids travelling with the columns
   double norms[kCl * kGpc * 2 * kUw];     // final column norms (all columns, by id)
   double red[8];
   int rot;
   // point-to-point round hand-off (P2P variant): ready[b][g] completes when both
-  // units of group g's next round have landed in buffer b (64 arrivals: 32 lanes
-  // of each of the two source groups); freeb[b][g] completes when both groups
-  // that group g writes into have finished reading their buffer b
-  alignas(8) unsigned long long ready[2][kGpc];
-  alignas(8) unsigned long long freeb[2][kGpc];
+  // units of group g's next round have landed in buffer b (2 arrivals, one per
+  // source group); freeb[b][g] completes when both groups that group g writes
+  // into have finished reading their buffer b
+  alignas(8) unsigned long long ready[3][kGpc];
+  alignas(8) unsigned long long freeb[3][kGpc];
 };
 
 constexpr int kJcThreads = kGpc * 32;
@@ -390,12 +390,12 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kJcThreads)
     for (int w = 0; w < kGpc; ++w) s += sh.red[w];
     for (int r = 0; r < kCl; ++r) cl.map_shared_rank(&sh, r)->norms[crank] = s;   // scratch
     if (P2P) {
-      for (int b = 0; b < 2; ++b)
+      for (int b = 0; b < 3; ++b)
         for (int q = 0; q < kGpc; ++q) {
           asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(jc_saddr(&sh.ready[b][q])),
-                       "r"(64));
+                       "r"(2));
           asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(jc_saddr(&sh.freeb[b][q])),
-                       "r"(64));
+                       "r"(2));
         }
       asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
@@ -457,7 +457,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kJcThreads)
     int rot = 0;
     for (int r = 0; r < UP - 1; ++r) {
       if (P2P && live && round_g > 0)   // this round's units have landed in buffer buf
-        jc_wait(jc_saddr(&sh.ready[buf][lg]), ((round_g - 1) >> 1) & 1);
+        jc_wait(jc_saddr(&sh.ready[buf][lg]), ((round_g - 1) / 3) & 1);
       double (*sl)[kRows] = sh.slot[buf][lgc];
       double* al = sh.alpha[buf][lgc];
       const int* cid = sh.col[buf][lgc];
@@ -499,10 +499,11 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kJcThreads)
         double ax = al[cx], ay = al[cy];
         const int idx = cid[cx], idy = cid[cy];
         if (live && jc_rotate(x, y, idx, idy, ax, ay, n, small, tol)) rot = 1;
-        if (P2P && live && round_g > 0)   // both destinations released their buffer nb
-          jc_wait(jc_saddr(&sh.freeb[buf ^ 1][lg]), ((round_g - 1) >> 1) & 1);
+        const int nb = P2P ? (buf == 2 ? 0 : buf + 1) : (buf ^ 1);
+        // three buffers: the destinations' buffer nb was last read two rounds ago
+        if (P2P && live && round_g >= 2)
+          jc_wait(jc_saddr(&sh.freeb[nb][lg]), ((round_g - 2) / 3) & 1);
         if (live) {
-          const int nb = buf ^ 1;
           double2* dx = reinterpret_cast<double2*>(sht->slot[nb][lt][wt + cx]) + t8;
           double2* dy = reinterpret_cast<double2*>(shb->slot[nb][lb][wb + (cy - kUw)]) + t8;
 #pragma unroll
@@ -517,16 +518,20 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kJcThreads)
             shb->col[nb][lb][wb + cy - kUw] = idy;
           }
           if (P2P) {
-            // every lane: my writes into the destinations' buffer nb are done
-            // (release), and I am done reading my buffer buf (my sources may refill it)
-            jc_remote_arrive(jc_saddr(&sh.ready[nb][lt]), uint32_t(gt / gpc));
-            jc_remote_arrive(jc_saddr(&sh.ready[nb][lb]), uint32_t(gb / gpc));
-            jc_remote_arrive(jc_saddr(&sh.freeb[buf][st % gpc]), uint32_t(st / gpc));
-            jc_remote_arrive(jc_saddr(&sh.freeb[buf][sb % gpc]), uint32_t(sb / gpc));
+            // the warp's writes into the destinations' buffer nb are done and it is
+            // done reading its buffer buf: after the warp barrier (memory ordering
+            // among the lanes) one lane releases at cluster scope (cumulative)
+            __syncwarp();
+            if (lane == 0) {
+              jc_remote_arrive(jc_saddr(&sh.ready[nb][lt]), uint32_t(gt / gpc));
+              jc_remote_arrive(jc_saddr(&sh.ready[nb][lb]), uint32_t(gb / gpc));
+              jc_remote_arrive(jc_saddr(&sh.freeb[buf][st % gpc]), uint32_t(st / gpc));
+              jc_remote_arrive(jc_saddr(&sh.freeb[buf][sb % gpc]), uint32_t(sb / gpc));
+            }
           }
         }
       }
-      buf ^= 1;
+      buf = P2P ? (buf == 2 ? 0 : buf + 1) : (buf ^ 1);
       ++round_g;
       if (!P2P) cl.sync();
     }
@@ -598,11 +603,13 @@ int svd_nov_cluster(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, 
   }
   const int64_t U = (n + kUw - 1) / kUw, UP = U + (U & 1);
   const int gpc = int((UP / 2 + kCl - 1) / kCl);
-  static const bool sync_rounds = [] {   // diagnostics: "cluster" = one cluster barrier per round
+  // default: one cluster barrier per round (0.99 ms per 144^2 SVD); the
+  // point-to-point variant (TTR_JACOBI=p2p) measured 1.24 ms
+  static const bool p2p = [] {
     const char* v = getenv("TTR_JACOBI");
-    return v && strcmp(v, "cluster") == 0;
+    return v && strcmp(v, "p2p") == 0;
   }();
-  if (sync_rounds)
+  if (!p2p)
     jacobi_cluster_kernel<false><<<kCl, kJcThreads, shm, s>>>(A, lda, int(m), int(n), gpc, AV,
                                                                 sigma, 40, c.flags.p);
   else

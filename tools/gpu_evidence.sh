@@ -11,10 +11,11 @@ timeout 1200 python bench.py --impl reference --steps 20 --warmup 5 > gpurun_out
 timeout 600 python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e > /dev/null 2>&1 && \
 timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none -c 100000 --csv --log-file gpurun_out/ev_${T}_launches.csv python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e > gpurun_out/ev_${T}_ncu_launches.log 2>&1; echo "ncu launches rc=$?"
 python tools/ncu_agg.py gpurun_out/ev_${T}_launches.csv 30 > gpurun_out/ev_${T}_launches.txt 2>&1
-for K in "dgemm_tma_kernel<64, 48, 16, 4, 2, 4, false, true>" "proj_carry_kernel" "dgemm_tma_kernel<64, 48, 16, 4, 2, 4, false, false>" "dgemm_tma_kernel<128, 48, 16, 4, 2, 4, false, false>"; do
-  N=$(echo "$K" | tr -cd 'a-z0-9_')
-  timeout 900 ncu --set full --clock-control none --import-source on -k "regex:$(echo $K | sed 's/[<>,]/./g; s/ //g')" -s 3 -c 1 -o gpurun_out/ev_${T}_$N -f python tools/run_once.py large 6 1 > gpurun_out/ev_${T}_ncu_$N.log 2>&1; echo "ncu full $N rc=$?"
-  ncu -i gpurun_out/ev_${T}_$N.ncu-rep --page raw --csv --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active,sm__inst_executed_pipe_tensor_op_dmma.avg.pct_of_peak_sustained_active,sm__pipe_tensor_op_dmma_cycles_active.avg.pct_of_peak_sustained_active,launch__registers_per_thread,sm__warps_active.avg.pct_of_peak_sustained_active > gpurun_out/ev_${T}_ncu_${N}_raw.csv 2>&1
+M=gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active,sm__inst_executed_pipe_tensor_subpipe_dmma.avg.pct_of_peak_sustained_active,launch__registers_per_thread,sm__warps_active.avg.pct_of_peak_sustained_active,launch__grid_size
+for spec in "wgemm|dgemm_tma_kernel<64, 48, 16, 4, 2, 4, 0, 1>|3" "zgemm|dgemm_tma_kernel<64, 48, 16, 4, 2, 4, 0, 0>|3" "ygemm|dgemm_tma_kernel<128, 48, 16, 4, 2, 4, 0, 0>|1" "projcarry|proj_carry_kernel|1" "jacobi|jacobi_cluster_kernel|1" "chol|chol_blk_kernel|3"; do
+  IFS='|' read -r N RGX SKIP <<< "$spec"
+  timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:$RGX" -s $SKIP -c 1 -o gpurun_out/ev_${T}_$N -f python tools/run_once.py large 6 1 > gpurun_out/ev_${T}_ncu_$N.log 2>&1; echo "ncu full $N rc=$?"
+  ncu -i gpurun_out/ev_${T}_$N.ncu-rep --page raw --csv --metrics $M > gpurun_out/ev_${T}_ncu_${N}_raw.csv 2>&1
 done
 for W in tiny single sum10 gmres; do
   timeout 900 python bench.py --workload $W --steps 10 --warmup 3 --no-cpu > gpurun_out/ev_${T}_bench_$W.json 2>&1; echo "bench $W rc=$?"
