@@ -281,6 +281,9 @@ def main():
                     help="B independent roundings per step (distinct sketch seeds), spread "
                          "over --streams contexts (SURVEY 8d batched throughput of C1/C2)")
     ap.add_argument("--streams", type=int, default=1)
+    ap.add_argument("--graph", action="store_true",
+                    help="--batch: capture the B roundings in one CUDA graph (tt_plan_create) "
+                         "and replay it per step (rank mode)")
     ap.add_argument("--shard", default="summands", choices=["summands", "slab"],
                     help="N>1 partition: summands (SURVEY 8e, the default) or mode slabs "
                          "of every summand (tt_round_sum_slab, NEXT-2)")
@@ -496,7 +499,11 @@ def batched_run(args, world, rank, local):
     dev = torch.device("cuda", local)
     wl = make_workload(args.workload, dev)
     ns = max(1, min(args.streams, args.batch))
-    ctxs = [P.Context(local) for _ in range(ns)]
+    graph = args.graph and wl.tol == 0
+    if graph:
+        ns = 1
+    ctxs = [P.Context(local, stream=torch.cuda.Stream(dev) if graph else None)
+            for _ in range(ns)]
     if wl.tol > 0:
         kw = dict(mode="tol", tol=wl.tol, oversample=wl.ell, adaptive=wl.adaptive, rank=wl.rank)
     else:
@@ -504,8 +511,17 @@ def batched_run(args, world, rank, local):
     B = args.batch
     n0 = P.tt_launch_count()
     ex = cf.ThreadPoolExecutor(ns)
+    plan = None
+    if graph:
+        torch.cuda.synchronize()
+        plan = P.Plan(ctxs[0], wl.terms, [1 + b for b in range(B)],
+                      branches=max(1, args.streams), **kw)
+        ranks_plan = plan.result(0).ranks
 
     def lane(t):
+        if plan is not None:
+            plan.launch()
+            return ranks_plan
         r = None
         for b in range(t, B, ns):
             r = ctxs[t].tt_round_sum(wl.terms, seed=1 + b, **kw)
@@ -543,6 +559,8 @@ def batched_run(args, world, rank, local):
             "data": "synthetic (ttsynth, seeded; DESIGN.md input recipe)",
             "config": {"workload": args.workload, "desc": WORKLOADS[args.workload]["desc"],
                        "batch_per_gpu": B, "streams": ns, "parallelism": f"replicas/{world}",
+                       "cuda_graph": bool(graph),
+                       "graph_branches": max(1, args.streams) if graph else None,
                        "timing": "host clock between device synchronisations (several streams)"},
             "tflops": tf, "fp64_peak_tflops": peak, "fp64_peak_source": peak_src,
             "roofline": {"bound": "tensor", "kernel": "whole path (batched, latency-bound)",

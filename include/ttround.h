@@ -269,6 +269,28 @@ typedef struct {
 int tt_gmres(tt_ctx_t ctx, const tt_kron_op* op, const tt_view* f, const tt_gmres_opts* opts,
              tt_tensor_t* x, tt_gmres_info* info, double* residuals);
 
+/* ---- CUDA-graph plans for launch-bound small roundings ----------------- */
+/* Capture B roundings of the same summands (TT_RANK or TT_SKETCH_ONLY opts,
+ * sketch seed seeds[b] for rounding b) into ONE CUDA graph: an eager rounding
+ * first sizes the workspaces and fixes the output shapes, then the B calls are
+ * stream-captured (no host synchronisation inside); each writes its result into
+ * plan-owned buffers and frees its temporaries inside the graph.  The inputs
+ * must stay valid and unchanged while the plan is used.  The context must run on
+ * a created (non-default) stream, one GPU.  tt_plan_launch replays the graph
+ * on the context stream and returns after it completed; tt_plan_result copies
+ * rounding b of the last replay into a new result (bitwise equal to
+ * tt_round_sum with the same seed).  Errors: TT_ERR_ARG (mode, stream, world,
+ * zero sum), TT_ERR_CUDA (capture). */
+typedef struct tt_plan* tt_plan_t;
+/* branches >= 1: the B roundings run as that many parallel branches of the
+ * graph (rounding b on branch b mod branches), each with its own library-owned
+ * stream and workspaces. */
+int tt_plan_create(tt_ctx_t ctx, int32_t S, const tt_view* terms, const tt_round_opts* opts,
+                   int32_t B, const uint64_t* seeds, int32_t branches, tt_plan_t* out);
+int tt_plan_launch(tt_plan_t plan);
+int tt_plan_result(tt_plan_t plan, int32_t b, tt_tensor_t* out);
+int tt_plan_destroy(tt_plan_t plan);
+
 /* <x, y> by the full right-to-left contraction (App. A); *out is a
  * host double.  x and y must have equal dims. */
 int tt_inner(tt_ctx_t ctx, const tt_view* x, const tt_view* y, double* out);

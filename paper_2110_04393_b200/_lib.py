@@ -98,6 +98,11 @@ def load_library(path: str = LIB_PATH):
         "tt_qr": (C.c_int, [P, i64, i64, P, i64, P, P, C.POINTER(C.c_int)]),
         "tt_svd_jacobi": (C.c_int, [P, i64, i64, P, i64, P, P, P]),
         "tt_svd_nov": (C.c_int, [P, i64, i64, P, i64, P, P]),
+        "tt_plan_create": (C.c_int, [P, i32, C.POINTER(tt_view), C.POINTER(tt_round_opts), i32,
+                                     C.POINTER(u64), i32, C.POINTER(P)]),
+        "tt_plan_launch": (C.c_int, [P]),
+        "tt_plan_result": (C.c_int, [P, i32, C.POINTER(P)]),
+        "tt_plan_destroy": (C.c_int, [P]),
         "tt_kron_apply": (C.c_int, [P, C.POINTER(tt_kron_op), C.POINTER(tt_view), C.POINTER(P)]),
         "tt_gmres": (C.c_int, [P, C.POINTER(tt_kron_op), C.POINTER(tt_view),
                                C.POINTER(tt_gmres_opts), C.POINTER(P), C.POINTER(tt_gmres_info),
@@ -240,6 +245,31 @@ class Sketch:
         r0, I, r1 = self.ranks[n - 1], self.dims[n - 1], self.ranks[n]
         return torch.as_tensor(_CAI(p.value, (r0, I, r1), (1, r0, r0 * I), self._h),
                                device=self.device)
+
+
+class Plan:
+    """tt_plan_t: B roundings of fixed inputs captured in one CUDA graph."""
+
+    def __init__(self, ctx, terms, seeds, mode="rank", rank=0, oversample=0, branches=1):
+        L = load_library()
+        self._views = [_View(t) for t in terms]     # inputs stay alive with the plan
+        arr = (tt_view * len(self._views))(*[v.view for v in self._views])
+        opts = tt_round_opts(_MODES[mode], 0, int(rank), int(oversample), 0.0, 0, 0)
+        sd = (C.c_uint64 * len(seeds))(*[int(x) for x in seeds])
+        h = C.c_void_p()
+        _check(L.tt_plan_create(ctx.handle, len(self._views), arr, C.byref(opts), len(seeds),
+                                sd, int(branches), C.byref(h)))
+        self._h = _Handle(h.value, L.tt_plan_destroy)
+        self._ctx = ctx
+        self.B = len(seeds)
+
+    def launch(self):
+        _check(load_library().tt_plan_launch(self._h.ptr))
+
+    def result(self, b: int) -> "TTResult":
+        h = C.c_void_p()
+        _check(load_library().tt_plan_result(self._h.ptr, int(b), C.byref(h)))
+        return TTResult(h.value, self._ctx.device)
 
 
 class LoopbackGroup:

@@ -456,7 +456,10 @@ int partial_contractions_rl(Ctx& c, const Terms& T, const std::vector<int64_t>& 
         gd[j] = GemmDesc{T.core[j][n - 1], Wst.p + woff[n] + off[n][j], Z.p + zoff[j],
                          int(T.R[j][n - 1] * In), int(l[n]), int(T.R[j][n]),
                          int(T.R[j][n - 1] * In), int(sumR[n]), int(T.R[j][n - 1] * In)};
-      TTR_TRY(gemm(c, false, false, gd.data(), S, 1.0, 0.0, s));
+      // short K (= R_n): the persistent streaming GEMM (pgemm.cu), else the tiled one
+      const int pg = S > 0 ? pgemm(c, gd.data(), S, s) : 1;
+      if (pg < 0) return pg;
+      if (pg != 0) TTR_TRY(gemm(c, false, false, gd.data(), S, 1.0, 0.0, s));
       const double* Gn = sk.cores[n - 1].p;   // H(G_n): l_{n-1} x I_n l_n (ld l_{n-1})
       for (int j = 0; j < S; ++j)          // line 5: W_{n-1} = H(Z_n) H(G_n)^T
         gd[j] = GemmDesc{Z.p + zoff[j], Gn, Wst.p + woff[n - 1] + off[n - 1][j],
@@ -629,6 +632,7 @@ int truncate(Ctx& c, tt_tensor& X, double tol, int64_t rmax, std::vector<int64_t
   // kept until the join at the end (`keep`) or freed on the side stream itself.
   Ctx* side = nullptr;
   TTR_TRY(side_ctx(c, &side));
+  side->capturing = c.capturing;
   std::vector<DBuf> keep;
   std::vector<cudaEvent_t> evs;
   struct EvGuard {
@@ -744,6 +748,10 @@ int truncate(Ctx& c, tt_tensor& X, double tol, int64_t rmax, std::vector<int64_t
 }
 
 int read_flags(Ctx& c, int* h, int n) {
+  if (c.capturing) {   // graph capture: the eager run of the plan checked the flags
+    for (int i = 0; i < n; ++i) h[i] = 0;
+    return TT_OK;
+  }
   TTR_CUDA(cudaMemcpyAsync(h, c.flags.p, sizeof(int) * n, cudaMemcpyDeviceToHost, c.stream));
   TTR_CUDA(cudaStreamSynchronize(c.stream));
   return TT_OK;
@@ -976,7 +984,7 @@ int round_sum_impl(tt_ctx* c, int S, const tt_view* terms, const tt_round_opts* 
     }
   }
   tm.end(6);
-  TTR_CUDA(cudaStreamSynchronize(c->stream));
+  if (!c->capturing) TTR_CUDA(cudaStreamSynchronize(c->stream));
   tm.finish();
   int fl[4];
   TTR_TRY(read_flags(*c, fl, 4));
@@ -1996,6 +2004,180 @@ int kron_apply_impl(tt_ctx* c, const tt_kron_op* op, const tt_view* x, tt_tensor
   return TT_OK;
 }
 
+// ------------------------------------------------------------------ CUDA-graph plan
+// B roundings of the same inputs (sketch seeds seeds[b]) captured once into one
+// CUDA graph and replayed: the small configs are launch-bound (C1: ~180 kernels
+// of a few us each per rounding), so the graph removes the per-launch host cost.
+// An eager rounding first sizes the GEMM workspaces, checks the flags and fixes
+// the output shapes; every captured rounding then copies its result into
+// plan-owned buffers and frees its temporaries inside the graph (the graph owns
+// no live allocation, so it can be replayed).  TT_RANK / TT_SKETCH_ONLY only
+// (TT_TOL needs host decisions), one GPU.
+extern "C" int ctx_destroy_impl(tt_ctx* c);   // C-ABI section (C linkage)
+
+struct PlanImpl {
+  tt_ctx* c = nullptr;
+  std::vector<tt_ctx*> extra;           // branch contexts 1..k-1 (owned)
+  int B = 0, d = 0;
+  std::vector<int64_t> dims, ranks;
+  std::vector<std::vector<DBuf>> res;   // [b][n]
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  uint32_t flags = 0;
+  ~PlanImpl() {
+    if (exec) cudaGraphExecDestroy(exec);
+    if (graph) cudaGraphDestroy(graph);
+    if (c) cudaStreamSynchronize(c->stream);
+    res.clear();
+    for (tt_ctx* x : extra) ctx_destroy_impl(x);
+  }
+};
+
+extern "C" int ctx_create_impl(int device, void* cuda_stream, const uint8_t* nccl_id,
+                               tt_loopback* loop, int rank, int world, tt_ctx_t* out);
+
+int plan_create_impl(tt_ctx* c, int S, const tt_view* terms, const tt_round_opts* o, int B,
+                     const uint64_t* seeds, int branches, PlanImpl& P) {
+  if (!o || (o->mode != TT_RANK && o->mode != TT_SKETCH_ONLY) || B < 1 || !seeds) {
+    set_error("tt_plan_create: needs TT_RANK or TT_SKETCH_ONLY opts, B >= 1 and seeds");
+    return TT_ERR_ARG;
+  }
+  if (c->world > 1) {
+    set_error("tt_plan_create runs on one GPU");
+    return TT_ERR_ARG;
+  }
+  if (c->stream == nullptr || c->stream == cudaStreamLegacy || c->stream == cudaStreamPerThread) {
+    set_error("tt_plan_create needs a context on a created (capturable) stream");
+    return TT_ERR_ARG;
+  }
+  TTR_CUDA(cudaSetDevice(c->device));
+  const bool timing = c->timing;
+  c->timing = false;
+  struct Restore {
+    tt_ctx* c;
+    bool t;
+    ~Restore() {
+      c->timing = t;
+      c->capturing = false;
+      if (c->side) c->side->capturing = false;
+    }
+  } restore{c, timing};
+  // eager rounding: sizes the workspaces, fixes the shapes, checks the flags
+  {
+    tt_round_opts e = *o;
+    e.seed = seeds[0];
+    tt_tensor* t = nullptr;
+    TTR_TRY(round_sum_impl(c, S, terms, &e, nullptr, &t));
+    std::unique_ptr<tt_tensor> g(t);
+    if (t->flags & TT_FLAG_ZERO) {
+      set_error("tt_plan_create: the sum is zero");
+      return TT_ERR_ARG;
+    }
+    P.d = t->d;
+    P.dims = t->dims;
+    P.ranks = t->ranks;
+    P.flags = t->flags;
+  }
+  P.c = c;
+  P.B = B;
+  // independent roundings run as parallel branches of the graph, one context
+  // (stream, status words, workspaces) per branch; an eager rounding on each
+  // branch context sizes its workspaces before the capture
+  const int k = std::max(1, std::min(branches, B));
+  for (int i = 1; i < k; ++i) {
+    tt_ctx_t x = nullptr;
+    TTR_TRY(ctx_create_impl(c->device, nullptr, nullptr, nullptr, 0, 1, &x));
+    P.extra.push_back(x);
+    tt_round_opts e = *o;
+    e.seed = seeds[i % B];
+    tt_tensor* t = nullptr;
+    TTR_TRY(round_sum_impl(x, S, terms, &e, nullptr, &t));
+    std::unique_ptr<tt_tensor> g(t);
+    TTR_CUDA(cudaStreamSynchronize(x->stream));
+  }
+  std::vector<tt_ctx*> br{c};
+  for (tt_ctx* x : P.extra) br.push_back(x);
+  P.res.resize(B);
+  for (int b = 0; b < B; ++b) {
+    P.res[b].resize(P.d);
+    for (int n = 0; n < P.d; ++n)
+      TTR_TRY(dalloc(P.res[b][n], size_t(P.ranks[n] * P.dims[n] * P.ranks[n + 1]), c->stream));
+  }
+  TTR_CUDA(cudaStreamSynchronize(c->stream));
+  std::vector<cudaEvent_t> evs(2 * br.size(), nullptr);
+  struct EvGuard {
+    std::vector<cudaEvent_t>& e;
+    ~EvGuard() {
+      for (auto x : e)
+        if (x) cudaEventDestroy(x);
+    }
+  } evg{evs};
+  for (auto& e : evs) TTR_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  TTR_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+  int rc = TT_OK;
+  // fork: every branch stream joins the capture
+  for (size_t i = 1; i < br.size() && rc == TT_OK; ++i) {
+    if (cudaEventRecord(evs[i], c->stream) != cudaSuccess ||
+        cudaStreamWaitEvent(br[i]->stream, evs[i], 0) != cudaSuccess) {
+      set_error("graph fork failed");
+      rc = TT_ERR_CUDA;
+    }
+  }
+  for (tt_ctx* x : br) x->capturing = true;
+  for (int b = 0; b < B && rc == TT_OK; ++b) {
+    tt_ctx* x = br[size_t(b) % br.size()];
+    tt_round_opts e = *o;
+    e.seed = seeds[b];
+    tt_tensor* t = nullptr;
+    rc = round_sum_impl(x, S, terms, &e, nullptr, &t);
+    if (rc != TT_OK) break;
+    std::unique_ptr<tt_tensor> g(t);
+    if (t->ranks != P.ranks) {
+      set_error("tt_plan_create: a captured rounding changed shape");
+      rc = TT_ERR_ARG;
+      break;
+    }
+    for (int n = 0; n < P.d && rc == TT_OK; ++n) {
+      const cudaError_t e2 = cudaMemcpyAsync(
+          P.res[b][n].p, t->ptrs[n], sizeof(double) * P.ranks[n] * P.dims[n] * P.ranks[n + 1],
+          cudaMemcpyDeviceToDevice, x->stream);
+      if (e2 != cudaSuccess) {
+        set_error("capture copy: %s", cudaGetErrorString(e2));
+        rc = TT_ERR_CUDA;
+      }
+    }
+  }   // every temporary (incl. t) is freed in the capture
+  for (tt_ctx* x : br) {
+    x->capturing = false;
+    if (x->side) x->side->capturing = false;
+  }
+  // join: the capture stream waits for every branch
+  for (size_t i = 1; i < br.size(); ++i) {
+    if (cudaEventRecord(evs[br.size() + i], br[i]->stream) != cudaSuccess ||
+        cudaStreamWaitEvent(c->stream, evs[br.size() + i], 0) != cudaSuccess) {
+      if (rc == TT_OK) {
+        set_error("graph join failed");
+        rc = TT_ERR_CUDA;
+      }
+    }
+  }
+  cudaGraph_t graph = nullptr;
+  const cudaError_t ee = cudaStreamEndCapture(c->stream, &graph);
+  if (rc != TT_OK) {
+    if (graph) cudaGraphDestroy(graph);
+    cudaGetLastError();
+    return rc;
+  }
+  if (ee != cudaSuccess) {
+    set_error("graph capture failed: %s", cudaGetErrorString(ee));
+    cudaGetLastError();
+    return TT_ERR_CUDA;
+  }
+  P.graph = graph;
+  TTR_CUDA(cudaGraphInstantiate(&P.exec, graph, 0));
+  return TT_OK;
+}
+
 }  // namespace
 
 // ====================================================================== C-ABI
@@ -2015,8 +2197,8 @@ struct tt_loopback {
   int world = 1;
 };
 
-static int ctx_create(int device, void* cuda_stream, const uint8_t* nccl_id, tt_loopback* loop,
-                      int rank, int world, tt_ctx_t* out) {
+int ctx_create_impl(int device, void* cuda_stream, const uint8_t* nccl_id, tt_loopback* loop,
+                    int rank, int world, tt_ctx_t* out) {
   if (!out) {
     set_error("out is null");
     return TT_ERR_ARG;
@@ -2064,7 +2246,7 @@ static int ctx_create(int device, void* cuda_stream, const uint8_t* nccl_id, tt_
 
 int tt_ctx_create(int device, void* cuda_stream, const uint8_t* nccl_id, int rank, int world,
                   tt_ctx_t* out) {
-  return ctx_create(device, cuda_stream, nccl_id, nullptr, rank, world, out);
+  return ctx_create_impl(device, cuda_stream, nccl_id, nullptr, rank, world, out);
 }
 
 int tt_loopback_create(int world, tt_loopback_t* out) {
@@ -2094,10 +2276,14 @@ int tt_ctx_create_loopback(int device, void* cuda_stream, tt_loopback_t group, i
     set_error("tt_ctx_create_loopback: null group");
     return TT_ERR_ARG;
   }
-  return ctx_create(device, cuda_stream, nullptr, group, rank, group->world, out);
+  return ctx_create_impl(device, cuda_stream, nullptr, group, rank, group->world, out);
 }
 
-int tt_ctx_destroy(tt_ctx_t c) {
+int ctx_destroy_impl(tt_ctx* c);
+
+int tt_ctx_destroy(tt_ctx_t c) { return ctx_destroy_impl(c); }
+
+int ctx_destroy_impl(tt_ctx* c) {
   if (!c) return TT_OK;
   return guarded([&]() -> int {
     cudaSetDevice(c->device);
@@ -2242,6 +2428,68 @@ int tt_gmres(tt_ctx_t c, const tt_kron_op* op, const tt_view* f, const tt_gmres_
     TTR_CUDA(cudaMemsetAsync(c->flags.p, 0, sizeof(int) * c->nflags, c->stream));
     return gmres_impl(c, op, f, opts, x, info, residuals);
   });
+}
+
+int tt_plan_create(tt_ctx_t c, int32_t S, const tt_view* terms, const tt_round_opts* opts,
+                   int32_t B, const uint64_t* seeds, int32_t branches, tt_plan_t* out) {
+  if (!c || !out) {
+    set_error("tt_plan_create: null ctx/out");
+    return TT_ERR_ARG;
+  }
+  return guarded([&]() -> int {
+    std::unique_ptr<PlanImpl> p(new PlanImpl);
+    TTR_TRY(plan_create_impl(c, S, terms, opts, B, seeds, branches, *p));
+    *out = reinterpret_cast<tt_plan_t>(p.release());
+    return TT_OK;
+  });
+}
+
+int tt_plan_launch(tt_plan_t plan) {
+  if (!plan) return TT_ERR_ARG;
+  PlanImpl& P = *reinterpret_cast<PlanImpl*>(plan);
+  TTR_CUDA(cudaSetDevice(P.c->device));
+  TTR_CUDA(cudaGraphLaunch(P.exec, P.c->stream));
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  TTR_CUDA(cudaStreamSynchronize(P.c->stream));
+  return TT_OK;
+}
+
+int tt_plan_result(tt_plan_t plan, int32_t b, tt_tensor_t* out) {
+  if (!plan || !out) return TT_ERR_ARG;
+  PlanImpl& P = *reinterpret_cast<PlanImpl*>(plan);
+  if (b < 0 || b >= P.B) {
+    set_error("tt_plan_result: b out of range");
+    return TT_ERR_ARG;
+  }
+  return guarded([&]() -> int {
+    std::unique_ptr<tt_tensor> t(new tt_tensor);
+    t->d = P.d;
+    t->dims = P.dims;
+    t->ranks = P.ranks;
+    t->flags = P.flags;
+    t->stream = P.c->stream;
+    t->alive = P.c->alive;
+    t->bufs.resize(P.d);
+    t->ptrs.resize(P.d);
+    for (int n = 0; n < P.d; ++n) {
+      const size_t cnt = size_t(P.ranks[n] * P.dims[n] * P.ranks[n + 1]);
+      TTR_TRY(dalloc(t->bufs[n], cnt, P.c->stream));
+      TTR_CUDA(cudaMemcpyAsync(t->bufs[n].p, P.res[b][n].p, cnt * sizeof(double),
+                               cudaMemcpyDeviceToDevice, P.c->stream));
+      t->ptrs[n] = t->bufs[n].p;
+    }
+    TTR_CUDA(cudaStreamSynchronize(P.c->stream));
+    *out = t.release();
+    return TT_OK;
+  });
+}
+
+int tt_plan_destroy(tt_plan_t plan) {
+  if (!plan) return TT_OK;
+  PlanImpl* P = reinterpret_cast<PlanImpl*>(plan);
+  cudaStreamSynchronize(P->c->stream);
+  delete P;
+  return TT_OK;
 }
 
 int tt_inner(tt_ctx_t c, const tt_view* x, const tt_view* y, double* out) {

@@ -123,6 +123,9 @@ struct Ctx {
   // lazily created second stream with its own GEMM workspace (side_ctx()),
   // for work off a sweep's critical path; shares `flags`
   std::unique_ptr<Ctx> side;
+  // true while a CUDA graph is being captured on `stream` (tt_plan_create): no
+  // host synchronisation, no host reads of device flags, no workspace growth
+  bool capturing = false;
 };
 // The side context of c (created on first use); destroyed with c (destroy_side).
 int side_ctx(Ctx& c, Ctx** out);
@@ -163,6 +166,10 @@ inline int gemm1(Ctx& c, bool ta, bool tb, int M, int N, int K, double alpha,
   GemmDesc d{A, B, C, M, N, K, lda, ldb, ldc};
   return gemm(c, ta, tb, &d, 1, alpha, beta, s, gate, gate_val, flags);
 }
+
+// Persistent warp-specialised batched GEMM for short K (pgemm.cu): C_j = A_j B_j,
+// column-major, beta = 0.  Returns 1 (nothing launched) when it does not apply.
+int pgemm(Ctx& c, const GemmDesc* d, int nb, cudaStream_t s);
 
 // ---------------------------------------------------------------- fused sweep step
 // Alg. 7 lines 11 + 13 for one step in one cooperative launch (fused.cu):

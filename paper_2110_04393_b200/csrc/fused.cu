@@ -334,7 +334,10 @@ int proj_carry(Ctx& c, int64_t m, int l, int sumR, const double* Q, const double
   P.kchunk = (P.KT_total + ksl - 1) / ksl;
   P.ksl = (P.KT_total + P.kchunk - 1) / P.kchunk;
   const size_t need = size_t(P.ksl) * ptiles * kBM * kBN;
-  if (c.gemm_ws.n < need) TTR_TRY(dalloc(c.gemm_ws, need + need / 4, s));
+  if (c.gemm_ws.n < need) {
+    if (c.capturing) return 1;   // no workspace growth inside a graph: unfused path
+    TTR_TRY(dalloc(c.gemm_ws, need + need / 4, s));
+  }
   P.ws = c.gemm_ws.p;
   void* args[] = {&P};
   TTR_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(proj_carry_kernel),

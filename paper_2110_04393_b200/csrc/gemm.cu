@@ -630,6 +630,10 @@ int launch_cfg(Ctx& c, GemmParams& P, int maxM, int maxN, int maxK, cudaStream_t
   if (ksl > 1) {
     const size_t need = size_t(ksl) * tiles * S::bm * S::bn;
     if (c.gemm_ws.n < need) {
+      if (c.capturing) {   // a workspace allocated inside a graph would die with it
+        set_error("gemm workspace must be sized before graph capture");
+        return TT_ERR_ARG;
+      }
       TTR_TRY(dalloc(c.gemm_ws, need + need / 4, s));
     }
     P.ws = c.gemm_ws.p;
