@@ -462,7 +462,7 @@ def main():
                          {"sketch": phase[0], "phase1_contractions": phase[1],
                           "sweep_gemms": phase[2], "qr": phase[3], "collectives": phase[4],
                           "truncation": phase[5], "total": phase[6]}),
-            "roofline": {"bound": "tensor", "kernel": "dgemm_kernel (phase-1 Alg. 3 contractions, DMMA.8x8x4)"
+            "roofline": {"bound": "tensor", "kernel": "dgemm_tma_kernel + pgemm_kernel (phase-1 Alg. 3 contractions, TMA-fed DMMA.8x8x4)"
                          + (" with the right sketch (rho)" if two_sided else ""),
                          "achieved": p1_achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": (p1_achieved / peak) if p1_achieved else None,

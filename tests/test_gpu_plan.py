@@ -42,3 +42,19 @@ def test_plan_rejects_tolerance_mode_and_default_stream():
     ctx2 = P.Context(0, stream=torch.cuda.default_stream())
     with pytest.raises(P.TTError):
         P.Plan(ctx2, w.terms, [1], mode="rank", rank=w.rank, oversample=2)
+
+
+def test_bench_batched_graph_line():
+    """bench.py --batch B --graph --streams k prints one contract line."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--workload", "tiny",
+                          "--batch", "16", "--graph", "--streams", "4", "--steps", "2",
+                          "--warmup", "3", "--no-cpu"], capture_output=True, text=True,
+                         timeout=600, cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    d = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
+    assert d["value"] > 0 and d["config"]["cuda_graph"] and d["config"]["graph_branches"] == 4
