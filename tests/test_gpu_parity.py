@@ -357,3 +357,17 @@ def test_eps_threshold_closed_form_spectra(ctx, N, eps0, k):
     det = ctx.tt_round_deterministic(gpu_terms(terms), tol=eps0)
     assert det.ranks == [1] + [k] * (N - 1) + [1]
     assert abs(oracle.diff_norm(det.numpy(), Y) - exact) < 1e-12
+
+
+@pytest.mark.parametrize("seed", [21, 22])
+def test_even_ragged_ranks_take_the_tma_fused_paths(ctx, seed):
+    """Summand ranks all even but different (every operand TMA-addressable), so the
+    fused projection-and-carry kernel and the persistent phase-1 GEMM run with
+    k-tiles that straddle summand boundaries (zero-filled by TMA)."""
+    dims = [6, 10, 8, 12, 4]
+    rng = np.random.default_rng(seed)
+    tr = [[1] + [2 * int(x) for x in rng.integers(1, 9, size=len(dims) - 1)] + [1]
+          for _ in range(6)]
+    terms = ttsynth.random_terms(seed, dims, tr)
+    res, ref = run_both(ctx, terms, 24, rank=16)
+    check(res, ref)
