@@ -76,8 +76,8 @@ __global__ void __launch_bounds__(pThreads) pgemm_kernel(const __grid_constant__
   if (warp == pConsumers) {   // ---- producer (all lanes walk, lane 0 issues)
     for (int w = blockIdx.x; w < nitems; w += gridDim.x) {
       const int j = pg_entry(P, w), tl = w - P.tile0[j];
-      const int tiles_m = (P.M[j] + pBM - 1) / pBM;
-      const int m0 = (tl % tiles_m) * pBM, n0 = (tl / tiles_m) * pBN;
+      const int tiles_n = (P.N[j] + pBN - 1) / pBN;   // n fastest: the A block is reused from L2
+      const int m0 = (tl / tiles_n) * pBM, n0 = (tl % tiles_n) * pBN;
       const int KT = (P.K[j] + pBK - 1) / pBK;
       for (int kt = 0; kt < KT; ++kt, ++pos) {
         if (lane == 0) {
@@ -97,8 +97,8 @@ __global__ void __launch_bounds__(pThreads) pgemm_kernel(const __grid_constant__
   const int wm0 = (warp % pWM) * pTM, wn0 = (warp / pWM) * pTN;
   for (int w = blockIdx.x; w < nitems; w += gridDim.x) {
     const int j = pg_entry(P, w), tl = w - P.tile0[j];
-    const int tiles_m = (P.M[j] + pBM - 1) / pBM;
-    const int m0 = (tl % tiles_m) * pBM, n0 = (tl / tiles_m) * pBN;
+    const int tiles_n = (P.N[j] + pBN - 1) / pBN;
+    const int m0 = (tl / tiles_n) * pBM, n0 = (tl % tiles_n) * pBN;
     const int KT = (P.K[j] + pBK - 1) / pBK;
     double acc[pFM][pFN][2];
 #pragma unroll
