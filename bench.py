@@ -593,11 +593,11 @@ def e2e_run(args, call, local_terms, dev, world, dist):
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
+    dsts = (ctypes.c_void_p * len(outs))(*[o.data_ptr() for o in outs])
     t0 = time.perf_counter()
     for _ in range(args.e2e_steps):
         r = call(host)
-        for n in range(r.d):
-            _lib._check(L.tt_tensor_copy_core(r._h.ptr, n + 1, ctypes.c_void_p(outs[n].data_ptr())))
+        _lib._check(L.tt_tensor_copy_all(r._h.ptr, dsts))
         del r
     torch.cuda.synchronize()
     dt = (time.perf_counter() - t0) / args.e2e_steps
@@ -605,10 +605,22 @@ def e2e_run(args, call, local_terms, dev, world, dist):
         tt = torch.tensor([dt], device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         dt = float(tt.item())
-    del host
+    # the host link itself: a plain pinned H2D copy of 2 GiB (context for the floor)
+    probe = torch.empty(2 ** 28, dtype=torch.float64).pin_memory()
+    dprobe = torch.empty_like(probe, device=dev)
+    dprobe.copy_(probe, non_blocking=True)
+    torch.cuda.synchronize()
+    t1 = time.perf_counter()
+    dprobe.copy_(probe, non_blocking=True)
+    torch.cuda.synchronize()
+    link = probe.numel() * 8 / (time.perf_counter() - t1) / 1e9
+    del probe, dprobe, host
     return {"value": 1.0 / dt, "unit": "roundings/s", "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "steps": args.e2e_steps,
-            "note": "host-clock over the whole call incl. H2D staging and D2H of the result"}
+            "h2d_link_gbs": link, "h2d_floor_ms": h2d / link / 1e6,
+            "note": "host-clock over the whole call incl. H2D staging and D2H of the result; "
+                    "the H2D of every core precedes the sweep (phase 1 needs all of them), so "
+                    "e2e >= h2d_floor + sweep + truncation"}
 
 
 def reference_arm(args, world, rank):

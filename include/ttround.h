@@ -302,6 +302,9 @@ int tt_tensor_info(tt_tensor_t t, int32_t* d, const int64_t** dims,
                    const int64_t** ranks, double* const** cores, uint32_t* flags);
 /* Copy core n (1-based) to caller memory (host or device), R_{n-1} I_n R_n doubles. */
 int tt_tensor_copy_core(tt_tensor_t t, int32_t n, double* dst);
+/* Copy every core: dst[n] (host or device) receives core n+1; all copies are
+ * queued on the result's stream before one synchronisation. */
+int tt_tensor_copy_all(tt_tensor_t t, double* const* dst);
 /* Number of rounding passes the adaptive loop made (1 if not adaptive). */
 int tt_tensor_passes(tt_tensor_t t, int32_t* passes);
 /* Frees a result: stream-ordered on the creating context's stream (no host

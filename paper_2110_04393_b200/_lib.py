@@ -91,6 +91,7 @@ def load_library(path: str = LIB_PATH):
                                      C.POINTER(C.POINTER(i64)), C.POINTER(C.POINTER(P)),
                                      C.POINTER(C.c_uint32)]),
         "tt_tensor_copy_core": (C.c_int, [P, i32, P]),
+        "tt_tensor_copy_all": (C.c_int, [P, C.POINTER(P)]),
         "tt_tensor_passes": (C.c_int, [P, C.POINTER(i32)]),
         "tt_tensor_destroy": (C.c_int, [P]),
         "tt_dgemm": (C.c_int, [P, C.c_int, C.c_int, i64, i64, i64, dbl, P, i64, P, i64, dbl, P,

@@ -2523,6 +2523,24 @@ int tt_tensor_copy_core(tt_tensor_t t, int32_t n, double* dst) {
   return TT_OK;
 }
 
+int tt_tensor_copy_all(tt_tensor_t t, double* const* dst) {
+  if (!t || !dst) {
+    set_error("tt_tensor_copy_all: null argument");
+    return TT_ERR_ARG;
+  }
+  for (int n = 0; n < t->d; ++n) {   // every copy queued first, one synchronisation
+    if (!dst[n]) {
+      set_error("tt_tensor_copy_all: dst[%d] is null", n);
+      return TT_ERR_ARG;
+    }
+    const size_t cnt = size_t(t->ranks[n]) * t->dims[n] * t->ranks[n + 1];
+    TTR_CUDA(cudaMemcpyAsync(dst[n], t->ptrs[n], cnt * sizeof(double), cudaMemcpyDefault,
+                             t->stream));
+  }
+  TTR_CUDA(cudaStreamSynchronize(t->stream));
+  return TT_OK;
+}
+
 int tt_tensor_passes(tt_tensor_t t, int32_t* passes) {
   if (!t || !passes) return TT_ERR_ARG;
   *passes = t->passes;
