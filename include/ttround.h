@@ -355,6 +355,16 @@ int tt_svd_jacobi(tt_ctx_t ctx, int64_t m, int64_t n, const double* A, int64_t l
 int tt_svd_nov(tt_ctx_t ctx, int64_t m, int64_t n, const double* A, int64_t lda,
                double* AV, double* sigma);
 
+/* The CholeskyQR passes' factorisation (DESIGN.md §6 "Cholesky kernel"): G
+ * (n x n symmetric, lower triangle read, ld n, device) + shift I = L L^T with
+ * L lower triangular; writes Rinv = L^{-T} (n x n upper, ld n) and, if L != NULL,
+ * L (n x n lower, ld n).  shifted = 1 applies the shifted-CholeskyQR shift
+ * 11 (m n + n (n + 1)) u tr(G) (Fukaya et al.; m = the tall matrix's row count),
+ * shifted = 0 factors G itself (pivots below 64 n u max diag G are clamped, the
+ * R-only QR's rule).  TT_ERR_NUMERIC if a pivot is not positive and finite. */
+int tt_cholesky(tt_ctx_t ctx, int64_t n, const double* G, int64_t m, int shifted,
+                double* Rinv, double* L);
+
 #ifdef __cplusplus
 }
 #endif

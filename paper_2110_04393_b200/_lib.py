@@ -99,6 +99,7 @@ def load_library(path: str = LIB_PATH):
         "tt_qr": (C.c_int, [P, i64, i64, P, i64, P, P, C.POINTER(C.c_int)]),
         "tt_svd_jacobi": (C.c_int, [P, i64, i64, P, i64, P, P, P]),
         "tt_svd_nov": (C.c_int, [P, i64, i64, P, i64, P, P]),
+        "tt_cholesky": (C.c_int, [P, i64, P, i64, C.c_int, P, P]),
         "tt_plan_create": (C.c_int, [P, i32, C.POINTER(tt_view), C.POINTER(tt_round_opts), i32,
                                      C.POINTER(u64), i32, C.POINTER(P)]),
         "tt_plan_launch": (C.c_int, [P]),
@@ -450,6 +451,17 @@ class Context:
         _check(L.tt_svd_jacobi(self.handle, m, n, A.data_ptr(), A.stride(1), AV.data_ptr(),
                                V.data_ptr(), s.data_ptr()))
         return AV, V, s
+
+    def tt_cholesky(self, G: torch.Tensor, m: int = 0, shifted: bool = False):
+        """One factorisation of the CholeskyQR passes: (Rinv = L^{-T}, L)."""
+        L = load_library()
+        n = G.shape[0]
+        assert G.stride(0) == 1 and G.shape == (n, n)
+        Rinv = torch.empty((n, n), dtype=torch.float64, device=G.device).t()
+        Lo = torch.empty((n, n), dtype=torch.float64, device=G.device).t()
+        _check(L.tt_cholesky(self.handle, n, G.data_ptr(), int(m or n), int(bool(shifted)),
+                             Rinv.data_ptr(), Lo.data_ptr()))
+        return Rinv, Lo
 
     def tt_svd_nov(self, A: torch.Tensor):
         """V-free one-sided Jacobi (the truncation's SVD): (U Sigma, sigma)."""

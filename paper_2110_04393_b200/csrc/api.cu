@@ -2224,6 +2224,11 @@ int ctx_create_impl(int device, void* cuda_stream, const uint8_t* nccl_id, tt_lo
     TTR_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
     uint64_t thr = UINT64_MAX;
     TTR_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    // no reuse of memory freed on another stream through an inserted dependency:
+    // with several contexts (one stream each) the pool would otherwise chain their
+    // streams together and serialise independent roundings
+    int no_dep = 0;
+    TTR_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolReuseAllowInternalDependencies, &no_dep));
     c->nflags = 64;
     TTR_TRY(ialloc(c->flags, size_t(c->nflags), c->stream));
     TTR_CUDA(cudaMemsetAsync(c->flags.p, 0, sizeof(int) * c->nflags, c->stream));
@@ -2583,6 +2588,23 @@ int tt_qr(tt_ctx_t c, int64_t m, int64_t n, const double* A, int64_t lda, double
     int fl[16];
     TTR_TRY(read_flags(*c, fl, 16));
     if (fallback) *fallback = (fl[1] || fl[14]) ? 1 : 0;
+    return TT_OK;
+  });
+}
+
+int tt_cholesky(tt_ctx_t c, int64_t n, const double* G, int64_t m, int shifted, double* Rinv,
+                double* L) {
+  if (!c || !G || !Rinv) return TT_ERR_ARG;
+  return guarded([&]() -> int {
+    TTR_CUDA(cudaSetDevice(c->device));
+    TTR_CUDA(cudaMemsetAsync(c->flags.p, 0, sizeof(int) * c->nflags, c->stream));
+    TTR_TRY(cholesky(*c, n, G, m, shifted, Rinv, L, c->stream));
+    int fl[4];
+    TTR_TRY(read_flags(*c, fl, 4));
+    if (fl[3] & 1) {
+      set_error("tt_cholesky: a pivot is not positive and finite");
+      return TT_ERR_NUMERIC;
+    }
     return TT_OK;
   });
 }

@@ -213,6 +213,8 @@ int scale_by_inv_sigma(Ctx& c, const double* AV, int64_t m, int64_t k, const dou
                        double* B, int halfpow, double rel_thr, cudaStream_t s);
 // Q of an m x n matrix whose columns are already close to orthonormal: one
 // CholeskyQR pass (n <= 160; else qr())
+int cholesky(Ctx& c, int64_t n, const double* G, int64_t m, int shifted, double* Rinv, double* L,
+             cudaStream_t s);
 int qr_near_orthonormal(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, double* Q,
                         cudaStream_t s);
 // columns c of the m x n matrix A with sigma_c <= rel_thr sigma_0 set to e_c

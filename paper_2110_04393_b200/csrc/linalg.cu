@@ -6,6 +6,7 @@
 //  * eps-rank, Frobenius norm, transpose, fill
 #include <math.h>
 #include <stdlib.h>
+#include <string.h>
 
 #include <vector>
 
@@ -192,7 +193,7 @@ __device__ __forceinline__ void route_update(int* flags, int mode, bool bad, dou
 }
 
 // G (n x n, ld n, symmetric) -> Rinv (upper, ld n) with G + shift*I = R^T R, and
-// optionally R.  Shift (CH_SHIFT only) = 11(mn + n(n+1))u * trace(G) (shifted
+// optionally L = R^T (lower, ld n).  Shift (CH_SHIFT only) = 11(mn + n(n+1))u * trace(G) (shifted
 // CholeskyQR3, Fukaya et al.).  Runs iff *gate == gate_val.
 template <int QN>
 __global__ void __launch_bounds__(kCholThreads)
@@ -285,8 +286,8 @@ __global__ void __launch_bounds__(kCholThreads)
   }
   if (Rout) {
     for (int e = tid; e < n * n; e += kCholThreads) {
-      const int i = e % n, j = e / n;     // R(i, j) = L(j, i) for j >= i
-      Rout[e] = (j >= i) ? L[j + i * n] : 0.0;
+      const int i = e % n, j = e / n;     // Lout = R^T (lower)
+      Rout[e] = (i >= j) ? L[i + j * n] : 0.0;
     }
   }
   __syncthreads();
@@ -634,8 +635,8 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
   if (bad_final) return;   // outputs are not used (the route moved on)
   if (Rout)
     for (int c = w; c < n; c += NW)
-      for (int r = lane; r < n; r += 32)   // R(r, c) = L(c, r)
-        Rout[r + int64_t(c) * n] = (c >= r) ? S[c + r * ld] : 0.0;
+      for (int r = lane; r < n; r += 32)   // Lout = R^T (lower)
+        Rout[r + int64_t(c) * n] = (r >= c) ? S[r + c * ld] : 0.0;
   // (X_kk = L_kk^{-1} of every diagonal block was formed right after its
   // factorisation, parked in the block's upper triangle, diagonal in rdiag)
   __syncthreads();
@@ -750,6 +751,476 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
   CHOL_PROF(4);
 }
 
+// ------------------------------------------------------------------------
+// Look-ahead blocked Cholesky + inverse (n <= 32*NB; one CTA of 16 warps).  Same
+// contract, modes and status words as chol_blk_kernel.  X = L^{-1} lives in the
+// upper triangle (X(r, c), r > c, at (c, r); diagonal in rdiag), so L stays in
+// the lower triangle and both can be built concurrently.  Per 32-column block k:
+//  F(k)  warp 0 factors the diagonal block in registers (lane = row) and streams
+//        every group of 4 factored columns (+ 1/L_jj) through a 2-slot shared ring
+//        (named barriers FULL / EMPTY) to P <= 4 panel warps, which run the same
+//        eliminations on the rows below the block, so the panel L_ik is finished
+//        with the diagonal block (no panel product, no X_kk on the critical path).
+//        At the same time the other warps finish the trailing update of block
+//        column k-1 beyond block column k, form X_{k-1,k-1} and the inverse's
+//        block row X_{k-1,<k-1} = -X_{k-1,k-1} (L_{k-1,<k-1} X_{<k-1,<k-1}).
+//  T(k)  all warps: trailing update of block column k+1 only (look-ahead).
+// The pivot chain of F is the critical path; everything else hides behind it.
+constexpr int kLaBarFull = 1, kLaBarEmpty = 3, kLaBarRest = 5;
+// panel warps 1, 2, 3, 5: off SM sub-partition 0 (warp 0's)
+__device__ __forceinline__ int la_panel_warp(int p) { return p < 3 ? p + 1 : 5; }
+
+__device__ __forceinline__ void nbar_sync(int id, int cnt) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(cnt) : "memory");
+}
+__device__ __forceinline__ void nbar_arrive(int id, int cnt) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(cnt) : "memory");
+}
+
+// role of warp w in F(k) with P panel warps: 0 diagonal, 1 panel (idx), 2 rest
+// (idx), 3 idle (the other warps of sub-partition 0)
+__device__ __forceinline__ int la_role(int w, int P, int& idx) {
+  idx = 0;
+  if (w == 0) return 0;
+#pragma unroll
+  for (int p = 0; p < 4; ++p)
+    if (p < P && w == la_panel_warp(p)) {
+      idx = p;
+      return 1;
+    }
+  if ((w & 3) == 0) return 3;
+  int r = 0;
+  for (int v = 1; v < w; ++v) {
+    bool pan = false;
+#pragma unroll
+    for (int p = 0; p < 4; ++p) pan |= (p < P && v == la_panel_warp(p));
+    r += (!pan && (v & 3) != 0);
+  }
+  idx = r;
+  return 2;
+}
+__device__ __forceinline__ int la_rest_count(int P) { return 12 - P; }
+
+// A(r, c) -= sum_{t in [t0, t0+32)} L(r, t) L(c, t) on the 8x8 tiles (rt, ct),
+// ct in [ct_lo, ct_hi), rt in [ct, nt8): tiles widx, widx + nw, ...
+__device__ __forceinline__ void la_trail(double* S, int ld, int n, int t0, int ct_lo, int ct_hi,
+                                         int nt8, int widx, int nw, int lane) {
+  const int g = lane >> 2, t4 = lane & 3;
+  int tot = 0;
+  for (int ct = ct_lo; ct < ct_hi; ++ct) tot += nt8 - ct;
+#pragma unroll 1
+  for (int tt = widx; tt < tot; tt += nw) {
+    int ct = ct_lo, rem = tt;
+    while (rem >= nt8 - ct) { rem -= nt8 - ct; ++ct; }
+    const int rt = ct + rem;
+    const int R = 8 * rt, C = 8 * ct;
+    double c0 = 0.0, c1 = 0.0, e0 = 0.0, e1 = 0.0;
+#pragma unroll
+    for (int kk = 0; kk < 8; kk += 2) {
+      const int ta = t0 + 4 * kk + t4, tb = ta + 4;
+      dmma884(c0, c1, S[(R + g) + ta * ld], S[(C + g) + ta * ld]);
+      dmma884(e0, e1, S[(R + g) + tb * ld], S[(C + g) + tb * ld]);
+    }
+    const int r = R + g, cA = C + 2 * t4;
+    if (r < n) {
+      if (cA < n) S[r + cA * ld] -= c0 + e0;
+      if (cA + 1 < n) S[r + (cA + 1) * ld] -= c1 + e1;
+    }
+  }
+}
+
+// X_kk = L_kk^{-1} of the diagonal block at k0 (kb <= 32 columns) by one warp:
+// lanes 0-15 / 16-31 invert the 16 x 16 halves by register-resident forward
+// substitution, then X21 = -X22 (L21 X11) on DMMA tiles.  X(r, c), r > c, parked
+// at (c, r); the diagonal is rdiag.  tmp: 256 doubles of shared scratch.
+__device__ __forceinline__ void la_form_xkk(double* S, int ld, const double* rdiag, int k0,
+                                            int kb, int lane, double* tmp) {
+  const int g = lane >> 2, t4 = lane & 3;
+  {
+    const int h = lane >> 4, c = lane & 15, o = 16 * h;
+    double x[16];
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+      for (int t = 0; t < r; ++t) {
+        const double l = (o + r < kb) ? S[(k0 + o + r) + (k0 + o + t) * ld] : 0.0;
+        if (t & 1) s1 = fma(l, x[t], s1);
+        else s0 = fma(l, x[t], s0);
+      }
+      const double rdr = (o + r < kb) ? rdiag[k0 + o + r] : 0.0;
+      x[r] = (r < c || o + r >= kb) ? 0.0 : (r == c ? rdr : -rdr * (s0 + s1));
+    }
+#pragma unroll
+    for (int r = 1; r < 16; ++r)
+      if (r > c && o + r < kb) S[(k0 + o + c) + (k0 + o + r) * ld] = x[r];
+  }
+  __syncwarp();
+  if (kb <= 16) return;
+  auto x11 = [&](int row, int col) -> double {
+    return row < col ? 0.0 : (row == col ? rdiag[k0 + row] : S[(k0 + col) + (k0 + row) * ld]);
+  };
+  auto x22 = [&](int row, int col) -> double {
+    if (row < col || 16 + row >= kb) return 0.0;
+    return row == col ? rdiag[k0 + 16 + row] : S[(k0 + 16 + col) + (k0 + 16 + row) * ld];
+  };
+  double tacc[4][2];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {   // T = L21 X11
+    const int R = 8 * (q >> 1), C = 8 * (q & 1);
+    tacc[q][0] = tacc[q][1] = 0.0;
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {
+      const int kc = 4 * kk + t4;
+      const double av = (16 + R + g < kb) ? S[(k0 + 16 + R + g) + (k0 + kc) * ld] : 0.0;
+      dmma884(tacc[q][0], tacc[q][1], av, x11(kc, C + g));
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int R = 8 * (q >> 1), C = 8 * (q & 1);
+    tmp[(R + g) + 16 * (C + 2 * t4)] = tacc[q][0];
+    tmp[(R + g) + 16 * (C + 2 * t4 + 1)] = tacc[q][1];
+  }
+  __syncwarp();
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {   // X21 = -X22 T
+    const int R = 8 * (q >> 1), C = 8 * (q & 1);
+    double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {
+      const int kc = 4 * kk + t4;
+      dmma884(c0, c1, x22(R + g, kc), tmp[kc + 16 * (C + g)]);
+    }
+    const int r = R + g, cA = C + 2 * t4;
+    if (16 + r < kb) {
+      S[(k0 + cA) + (k0 + 16 + r) * ld] = -c0;
+      S[(k0 + cA + 1) + (k0 + 16 + r) * ld] = -c1;
+    }
+  }
+  __syncwarp();
+}
+
+// Block row kr of X (rows [kr0, kr0 + kbr), columns [0, kr0)), X_kk already formed:
+//   T = L_{kr,<kr} X_{<kr,<kr}, then X_{kr,<kr} = -X_kk T, T staged in the
+// destination (upper triangle).  Warps widx of nw, synchronised by named barrier
+// `bar` with `cnt` threads (bar 0 = the whole CTA).
+__device__ __forceinline__ void la_inverse_row(double* S, int ld, const double* rdiag, int kr0,
+                                               int kbr, int widx, int nw, int bar, int cnt,
+                                               int lane) {
+  const int g = lane >> 2, t4 = lane & 3;
+  const int nrt = (kbr + 7) / 8, nct = kr0 / 8, ntiles = nrt * nct;
+  const int rend = kr0 + kbr;
+  constexpr int kMaxT = 6;   // <= ceil(48 / 8) tiles per warp (n <= 160)
+  double acc[kMaxT][2];
+  // stage 1: T = L_{kr,<kr} X_{<kr,<kr}; X(t, j) = 0 for t < j, so the k range of
+  // tile column C starts at C; only its first 8 steps (X's diagonal tile) need
+  // selects
+#pragma unroll
+  for (int q = 0; q < kMaxT; ++q) {
+    acc[q][0] = acc[q][1] = 0.0;
+    const int tt = widx + nw * q;
+    if (tt < ntiles) {
+      const int R = kr0 + 8 * (tt / nct), C = 8 * (tt % nct), j = C + g;
+      const double* arow = S + (R + g);
+      double e0 = 0.0, e1 = 0.0, f0 = 0.0, f1 = 0.0, h0 = 0.0, h1 = 0.0;
+      {
+        const int ta = C + t4, tb = C + 4 + t4;
+        const double ba = ta > j ? S[j + ta * ld] : (ta == j ? rdiag[j] : 0.0);
+        const double bb = tb > j ? S[j + tb * ld] : (tb == j ? rdiag[j] : 0.0);
+        dmma884(acc[q][0], acc[q][1], arow[ta * ld], ba);
+        dmma884(e0, e1, arow[tb * ld], bb);
+      }
+      int t = C + 8;
+#pragma unroll 1
+      for (; t + 8 < kr0; t += 16) {
+        const int t0 = t + t4;
+        dmma884(acc[q][0], acc[q][1], arow[t0 * ld], S[j + t0 * ld]);
+        dmma884(e0, e1, arow[(t0 + 4) * ld], S[j + (t0 + 4) * ld]);
+        dmma884(f0, f1, arow[(t0 + 8) * ld], S[j + (t0 + 8) * ld]);
+        dmma884(h0, h1, arow[(t0 + 12) * ld], S[j + (t0 + 12) * ld]);
+      }
+      if (t < kr0) {
+        const int t0 = t + t4;
+        dmma884(acc[q][0], acc[q][1], arow[t0 * ld], S[j + t0 * ld]);
+        dmma884(e0, e1, arow[(t0 + 4) * ld], S[j + (t0 + 4) * ld]);
+      }
+      acc[q][0] += (e0 + f0) + h0;
+      acc[q][1] += (e1 + f1) + h1;
+    }
+  }
+  nbar_sync(bar, cnt);
+#pragma unroll
+  for (int q = 0; q < kMaxT; ++q) {
+    const int tt = widx + nw * q;
+    if (tt < ntiles) {
+      const int R = kr0 + 8 * (tt / nct), C = 8 * (tt % nct);
+      const int r = R + g, cA = C + 2 * t4;
+      if (r < rend) {
+        S[cA + r * ld] = acc[q][0];
+        S[(cA + 1) + r * ld] = acc[q][1];
+      }
+    }
+  }
+  nbar_sync(bar, cnt);
+  // stage 2: X_{kr,<kr} = -X_kk T; X_kk(i, t) = 0 for t > i: the k range of tile
+  // row R ends with its diagonal tile (selects), before it X_kk(i, t) is parked
+  // at (t, i)
+#pragma unroll
+  for (int q = 0; q < kMaxT; ++q) {
+    acc[q][0] = acc[q][1] = 0.0;
+    const int tt = widx + nw * q;
+    if (tt < ntiles) {
+      const int R = kr0 + 8 * (tt / nct), C = 8 * (tt % nct);
+      const int i = R + g;
+      const bool iv = i < rend;
+      double e0 = 0.0, e1 = 0.0;
+#pragma unroll 1
+      for (int t = kr0; t < R; t += 8) {
+        const int t0 = t + t4;
+        dmma884(acc[q][0], acc[q][1], iv ? S[t0 + i * ld] : 0.0, S[(C + g) + t0 * ld]);
+        dmma884(e0, e1, iv ? S[(t0 + 4) + i * ld] : 0.0, S[(C + g) + (t0 + 4) * ld]);
+      }
+#pragma unroll
+      for (int kk = 0; kk < 2; ++kk) {
+        const int tc = R + 4 * kk + t4;
+        const double av = (iv && tc <= i) ? (tc == i ? rdiag[i] : S[tc + i * ld]) : 0.0;
+        const double bv = tc < rend ? S[(C + g) + tc * ld] : 0.0;
+        dmma884(acc[q][0], acc[q][1], av, bv);
+      }
+      acc[q][0] += e0;
+      acc[q][1] += e1;
+    }
+  }
+  nbar_sync(bar, cnt);
+#pragma unroll
+  for (int q = 0; q < kMaxT; ++q) {
+    const int tt = widx + nw * q;
+    if (tt < ntiles) {
+      const int R = kr0 + 8 * (tt / nct), C = 8 * (tt % nct);
+      const int r = R + g, cA = C + 2 * t4;
+      if (r < rend) {
+        S[cA + r * ld] = -acc[q][0];
+        S[(cA + 1) + r * ld] = -acc[q][1];
+      }
+    }
+  }
+}
+
+template <int NB>
+__global__ void __launch_bounds__(kBlkThreads, 1)
+    chol_la_kernel(const double* __restrict__ G, int n, int64_t m, int mode,
+                   double* __restrict__ Rinv, double* __restrict__ Rout,
+                   int* __restrict__ flags, const int* gate, int gate_val) {
+  if (gate && *gate != gate_val) return;
+  extern __shared__ double S[];
+  __shared__ double rdiag[32 * NB];
+  __shared__ __align__(16) double ring[2][4][64];   // factored columns, doubled (see F)
+  __shared__ double ring_rd[2][4];
+  __shared__ double ttmp[256];
+  __shared__ double s_tr, s_dmax;
+  __shared__ int s_bad, s_zero, s_clamped;
+  const int ld = chol_ld(n);
+  const int n8 = (n + 7) & ~7, nt8 = n8 / 8;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int nb = (n + 31) / 32;
+  const int md = mode & 0xff;
+  if (tid == 0) { s_bad = 0; s_zero = 0; s_clamped = 0; }
+  if (tid < 32) {
+    double tr = 0.0, dmax = 0.0;
+    for (int i = tid; i < n; i += 32) {
+      const double gi = G[i + int64_t(i) * n];
+      tr += gi;
+      dmax = fmax(dmax, gi);
+    }
+    for (int o = 16; o; o >>= 1) {
+      tr += __shfl_xor_sync(0xffffffffu, tr, o);
+      dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+    }
+    if (tid == 0) {
+      if (!(tr > 0.0)) {
+        if (tr == 0.0) { atomicOr(&flags[2], 1); s_zero = 1; }   // Y_n == 0: zero sum (R16)
+        s_bad = 1;
+      }
+      s_tr = tr;
+      s_dmax = dmax;
+    }
+  }
+  __syncthreads();
+  const bool shifted = md == CH_SHIFT || md == CH_SHIFT2 || md == CH_SHIFT1B || md == CH_RSHIFT;
+  const double shift = shifted ? 11.0 * (double(m) * n + double(n) * (n + 1)) * 0x1p-53 * s_tr : 0.0;
+  const bool clamp = md == CH_RCLAMP;
+  const double tau = 64.0 * n * 0x1p-53 * s_dmax;
+#ifdef TTR_CHOL_PROF
+  long long prof_t = clock64();
+#endif
+  for (int j = w; j < n8; j += 16) {
+#pragma unroll 4
+    for (int i = lane; i < ld; i += 32)
+      S[i + j * ld] = (i < n && j < n && i >= j) ? G[i + int64_t(j) * n] + ((i == j) ? shift : 0.0)
+                                                 : 0.0;
+  }
+  __syncthreads();
+  CHOL_PROF(5);
+#pragma unroll 1
+  for (int k = 0; k < nb; ++k) {
+    const int k0 = 32 * k, kb = min(32, n - k0);
+    const int r0 = k0 + kb;                         // first row below the block
+    const int P = r0 < n ? (n - r0 + 31) / 32 : 0;  // panel warps
+    const int cnt = 32 * (1 + P);
+    const int ng = (kb + 3) >> 2;
+    int idx;
+    const int role = la_role(w, P, idx);
+    if (role == 0) {
+      // ---- F(k), diagonal block: lane i keeps the not yet eliminated part of
+      // row i in registers (a[q] = A(i, j0 + q)), pivots in groups of 4 with
+      // static register offsets, then a shift by 4.  The pivot step is
+      // branch-free (clamping and the finiteness test are selects; 1/L_jj =
+      // MUFU rsqrt + two Newton steps).  Factored column j goes to the ring slot
+      // of its group, doubled (colb[i] = colb[i + 32] = L_ij) so that every load
+      // below is [base + constant]; updates of the upper slots are harmless.
+      const int i = lane;
+      double a[32];
+#pragma unroll
+      for (int q = 0; q < 32; ++q)
+        a[q] = (i < kb && q <= i) ? S[(k0 + i) + (k0 + q) * ld] : 0.0;
+      int bad = 0, nclamp = 0;
+#pragma unroll 1
+      for (int grp = 0; grp < ng; ++grp) {
+        const int sl = grp & 1;
+#ifdef TTR_CHOL_PROF
+        const long long tw0 = clock64();
+#endif
+        if (P > 0 && grp >= 2) nbar_sync(kLaBarEmpty + sl, cnt);   // panel done with grp - 2
+#ifdef TTR_CHOL_PROF
+        if (threadIdx.x == 0) atomicAdd(&flags[33], int((clock64() - tw0) >> 6));
+#endif
+#pragma unroll
+        for (int sft = 0; sft < 4; ++sft) {
+          const int j = 4 * grp + sft;
+          double piv = __shfl_sync(0xffffffffu, a[sft], j);
+          piv = (j < kb) ? piv : 1.0;                       // padding pivot
+          const bool fin = fabs(piv) <= 1.79e308;           // false for inf / nan
+          const bool cl = clamp && fin && !(piv > tau);     // numerically null direction
+          piv = cl ? tau : piv;
+          nclamp += cl;
+          const bool ok = fin && piv > 0.0;
+          bad |= !ok;
+          const double pv = ok ? piv : 1.0;
+          double rd;
+          asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(rd) : "d"(pv));
+          rd = rd * fma(-0.5 * pv * rd, rd, 1.5);           // Newton steps for 1/sqrt
+          rd = rd * fma(-0.5 * pv * rd, rd, 1.5);
+          const double lij = (i > j) ? a[sft] * rd : (i == j ? pv * rd : 0.0);
+          if (j < kb && i >= j && i < kb) S[(k0 + i) + (k0 + j) * ld] = lij;
+          if (i == j && j < kb) rdiag[k0 + j] = rd;
+          double* cb0 = ring[sl][sft];
+          cb0[i] = lij;
+          cb0[i + 32] = lij;
+          if (i == 0) ring_rd[sl][sft] = rd;
+          __syncwarp();
+          const double* cb = cb0 + j;
+#pragma unroll
+          for (int qq = 1; qq < 32 - sft; ++qq) a[sft + qq] = fma(-lij, cb[qq], a[sft + qq]);
+        }
+#pragma unroll
+        for (int q = 0; q < 28; ++q) a[q] = a[q + 4];
+        a[28] = a[29] = a[30] = a[31] = 0.0;
+        if (P > 0) nbar_arrive(kLaBarFull + sl, cnt);
+      }
+      if (lane == 0) {
+        if (bad) s_bad = 1;
+        if (nclamp) s_clamped += nclamp;
+      }
+      CHOL_PROF(6);
+    } else if (role == 1) {
+      // ---- F(k), panel: the same eliminations on rows r0 + 32 idx + lane
+      const int ip = r0 + 32 * idx + lane;
+      const bool live = ip < n;
+      double a[32];
+#pragma unroll
+      for (int q = 0; q < 32; ++q) a[q] = (live && q < kb) ? S[ip + (k0 + q) * ld] : 0.0;
+#pragma unroll 1
+      for (int grp = 0; grp < ng; ++grp) {
+        const int sl = grp & 1;
+        nbar_sync(kLaBarFull + sl, cnt);
+#pragma unroll
+        for (int sft = 0; sft < 4; ++sft) {
+          const int j = 4 * grp + sft;
+          const double l = a[sft] * ring_rd[sl][sft];
+          if (live && j < kb) S[ip + (k0 + j) * ld] = l;
+          const double* cb = ring[sl][sft] + j;
+#pragma unroll
+          for (int qq = 1; qq < 32 - sft; ++qq) a[sft + qq] = fma(-l, cb[qq], a[sft + qq]);
+        }
+#pragma unroll
+        for (int q = 0; q < 28; ++q) a[q] = a[q + 4];
+        a[28] = a[29] = a[30] = a[31] = 0.0;
+        if (grp + 2 < ng) nbar_arrive(kLaBarEmpty + sl, cnt);   // warp 0 reuses the slot
+      }
+    } else if (role == 2 && k > 0) {
+      // ---- behind F(k): finish block column k-1 (its trailing update beyond
+      // block column k, X_{k-1,k-1}, the inverse's block row k-1)
+      const int R = la_rest_count(P), rc = 32 * R;
+      const int kp0 = k0 - 32;
+      // (columns from k0 + 32 on: block column k itself was updated by T(k-1))
+      if (idx == 0) la_form_xkk(S, ld, rdiag, kp0, 32, lane, ttmp);
+      else if (k0 + 32 < n)
+        la_trail(S, ld, n, kp0, (k0 + 32) / 8, nt8, nt8, idx - 1, R - 1, lane);
+      nbar_sync(kLaBarRest, rc);
+      if (kp0 > 0) la_inverse_row(S, ld, rdiag, kp0, 32, idx, R, kLaBarRest, rc, lane);
+    }
+    __syncthreads();
+    CHOL_PROF(0);
+    if (s_bad) break;
+    // ---- T(k): trailing update of block column k+1 (look-ahead)
+    if (r0 < n) {
+      la_trail(S, ld, n, k0, r0 / 8, min(r0 / 8 + 4, nt8), nt8, w, 16, lane);
+      __syncthreads();
+    }
+    CHOL_PROF(2);
+  }
+  __syncthreads();
+  const bool bad_final = s_bad;
+  if (!bad_final) {
+    // the last block: X_kk, then its block row of X (whole CTA)
+    const int kl0 = 32 * (nb - 1), kbl = n - kl0;
+    if (w == 0) la_form_xkk(S, ld, rdiag, kl0, kbl, lane, ttmp);
+    __syncthreads();
+    if (kl0 > 0) la_inverse_row(S, ld, rdiag, kl0, kbl, w, 16, 0, kBlkThreads, lane);
+  }
+  CHOL_PROF(3);
+  if (w == 0 && !s_zero) {   // route checks on diag(L), warp-parallel
+    double dev = 0.0, dmin = INFINITY, dmax = 0.0;
+    for (int i = lane; i < n; i += 32) {
+      const double d = fabs(S[i + i * ld]);
+      dmin = fmin(dmin, d);
+      dmax = fmax(dmax, d);
+      dev = fmax(dev, fabs(S[i + i * ld] - 1.0));
+    }
+    for (int o = 16; o; o >>= 1) {
+      dmin = fmin(dmin, __shfl_xor_sync(0xffffffffu, dmin, o));
+      dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+      dev = fmax(dev, __shfl_xor_sync(0xffffffffu, dev, o));
+    }
+    if (lane == 0 && !(flags[2] & 1)) {
+      int bad2 = bad_final;
+      if ((mode & kStrict) && !(dmin >= dmax * kStrictRatio)) bad2 = 1;
+      if (s_clamped) flags[16] += 1;   // counter: clamped (rank-deficient) passes
+      route_update(flags, md, bad2, needs_dev(md) ? dev : 0.0);
+    }
+  }
+  if (bad_final) return;   // outputs are not used (the route moved on)
+  __syncthreads();
+  for (int c = w; c < n; c += 16)
+    for (int r = lane; r < n; r += 32) {
+      // Rinv(r, c) = X(c, r) (c > r: stored at (r, c)); Lout = R^T (lower)
+      Rinv[r + int64_t(c) * n] = (c > r) ? S[r + c * ld] : (c == r ? rdiag[r] : 0.0);
+      if (Rout) Rout[r + int64_t(c) * n] = (r >= c) ? S[r + c * ld] : 0.0;
+    }
+  CHOL_PROF(4);
+}
+
 __global__ void route_start_kernel(int* flags) { flags[0] = flags[0] >= 1 ? 1 : 0; }
 
 // Cholesky factor of a Gram G = I + E that is the identity to working accuracy
@@ -757,24 +1228,29 @@ __global__ void route_start_kernel(int* flags) { flags[0] = flags[0] >= 1 ? 1 : 
 // O(u)): R = I + U with U = triu(E) and U_ii = E_ii / 2, so that
 // R^T R = G + U^T U = G + O(||E||^2).  flags[slot] = 1 (-> the full Cholesky runs,
 // gated) when max |E| > thr, where the first-order factor is not exact enough.
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(1024)
     near_identity_chol_kernel(const double* __restrict__ G, int n, double* __restrict__ R,
                               int* __restrict__ flags, int slot, double thr) {
   __shared__ double red[32];
   double mx = 0.0;
-  for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
-    const int i = e % n, j = e / n;
-    const double g = G[(i >= j) ? e : j + int64_t(i) * n];   // lower triangle holds G
-    const double x = g - (i == j ? 1.0 : 0.0);
-    mx = fmax(mx, fabs(x));
-    R[e] = (i < j) ? x : (i == j ? 1.0 + 0.5 * x : 0.0);
+  // 2-D loop (no division per element), loads batched 4 deep: the Gram sits in
+  // L2 and the kernel is bound by load latency
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int j = w; j < n; j += nw) {
+#pragma unroll 4
+    for (int i = lane; i < n; i += 32) {
+      const double g = G[(i >= j) ? i + int64_t(j) * n : j + int64_t(i) * n];   // lower triangle holds G
+      const double x = g - (i == j ? 1.0 : 0.0);
+      mx = fmax(mx, fabs(x));
+      R[i + int64_t(j) * n] = (i > j) ? x : (i == j ? 1.0 + 0.5 * x : 0.0);   // L = R^T
+    }
   }
   for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+  if (lane == 0) red[w] = mx;
   __syncthreads();
   if (threadIdx.x == 0) {
     double m = 0.0;
-    for (int w = 0; w < (int(blockDim.x) + 31) / 32; ++w) m = fmax(m, red[w]);
+    for (int q = 0; q < nw; ++q) m = fmax(m, red[q]);
     flags[slot] = (m > thr || !(m == m)) ? 1 : 0;
   }
 }
@@ -785,6 +1261,18 @@ __global__ void route_fail_kernel(int* flags) {
 
 __global__ void gated_set_kernel(int* flag, int from, int to) {
   if (*flag == from) *flag = to;
+}
+
+// dst = src^T (n x n), iff *gate == gate_val
+__global__ void gated_transpose_kernel(const double* __restrict__ src, double* __restrict__ dst,
+                                       int n, const int* gate, int gate_val) {
+  if (gate && *gate != gate_val) return;
+  const int64_t nn = int64_t(n) * n;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < nn;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = e % n, j = e / n;
+    dst[e] = src[j + i * n];
+  }
 }
 
 __global__ void gated_copy_kernel(const double* __restrict__ src, double* __restrict__ dst,
@@ -1103,15 +1591,29 @@ static int launch_chol(Ctx& c, const double* Gm, int n, int64_t m, int mode, dou
                                   220 * 1024));
     TTR_CUDA(cudaFuncSetAttribute(chol_blk_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   220 * 1024));
+    TTR_CUDA(cudaFuncSetAttribute(chol_la_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  220 * 1024));
+    TTR_CUDA(cudaFuncSetAttribute(chol_la_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  220 * 1024));
+    TTR_CUDA(cudaFuncSetAttribute(chol_la_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  210 * 1024));
     attr_done = true;
   }
   const size_t shm = size_t(chol_ld(n)) * ((n + 7) & ~7) * sizeof(double);
+  // default: the look-ahead kernel; TTR_CHOL=blk selects the round-1 blocked one (A/B)
+  static const bool blk = [] {
+    const char* v = getenv("TTR_CHOL");
+    return v && strcmp(v, "blk") == 0;
+  }();
   if (n <= 32) {
-    chol_blk_kernel<1><<<1, kBlkThreads, shm, s>>>(Gm, n, m, mode, Rinv, Rk, c.flags.p, gate, gv);
+    if (blk) chol_blk_kernel<1><<<1, kBlkThreads, shm, s>>>(Gm, n, m, mode, Rinv, Rk, c.flags.p, gate, gv);
+    else chol_la_kernel<1><<<1, kBlkThreads, shm, s>>>(Gm, n, m, mode, Rinv, Rk, c.flags.p, gate, gv);
   } else if (n <= 64) {
-    chol_blk_kernel<2><<<1, kBlkThreads, shm, s>>>(Gm, n, m, mode, Rinv, Rk, c.flags.p, gate, gv);
+    if (blk) chol_blk_kernel<2><<<1, kBlkThreads, shm, s>>>(Gm, n, m, mode, Rinv, Rk, c.flags.p, gate, gv);
+    else chol_la_kernel<2><<<1, kBlkThreads, shm, s>>>(Gm, n, m, mode, Rinv, Rk, c.flags.p, gate, gv);
   } else if (n <= 160) {
-    chol_blk_kernel<5><<<1, kBlkThreads, shm, s>>>(Gm, n, m, mode, Rinv, Rk, c.flags.p, gate, gv);
+    if (blk) chol_blk_kernel<5><<<1, kBlkThreads, shm, s>>>(Gm, n, m, mode, Rinv, Rk, c.flags.p, gate, gv);
+    else chol_la_kernel<5><<<1, kBlkThreads, shm, s>>>(Gm, n, m, mode, Rinv, Rk, c.flags.p, gate, gv);
   } else {
     const bool big = n * n > kSmemLimitDoubles;
     chol_inv_kernel<32><<<1, kCholThreads, big ? 0 : size_t(n) * n * 8, s>>>(
@@ -1217,16 +1719,16 @@ int qr(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, bool trans, d
   // Racc <- Rk Racc (gated)
   auto accumulate_r = [&](const int* gate, int gv) -> int {
     if (!R) return TT_OK;
-    TTR_TRY(gemm1(c, false, false, ni, ni, ni, 1.0, Rk.p, ni, Racc.p, ni, 0.0, Rtmp.p, ni, s,
-                  gate, gv));
+    TTR_TRY(gemm1(c, true, false, ni, ni, ni, 1.0, Rk.p, ni, Racc.p, ni, 0.0, Rtmp.p, ni, s,
+                  gate, gv));   // Rk holds L_k = R_k^T
     gated_copy_kernel<<<std::max(1, (ni * ni + 255) / 256), 256, 0, s>>>(Rtmp.p, Racc.p,
                                                                        int64_t(ni) * ni, gate, gv);
     return launched();
   };
   auto copy_r_first = [&](const int* gate, int gv) -> int {
     if (!R) return TT_OK;
-    gated_copy_kernel<<<std::max(1, (ni * ni + 255) / 256), 256, 0, s>>>(Rk.p, Racc.p,
-                                                                       int64_t(ni) * ni, gate, gv);
+    gated_transpose_kernel<<<std::max(1, (ni * ni + 255) / 256), 256, 0, s>>>(Rk.p, Racc.p, ni,
+                                                                            gate, gv);
     return launched();
   };
   auto gated_copy = [&](const double* src, double* dst, const int* gate, int gv) -> int {
@@ -1259,7 +1761,7 @@ int qr(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, bool trans, d
     // R4: Q3 is orthonormal to O(u), so its Gram is I + E with ||E|| = O(u) and
     // the first-order factor I + triu(E) (half diagonal) is exact to O(u^2); the
     // full Cholesky runs only when max |E| > 1e-8 (gated on the device)
-    near_identity_chol_kernel<<<1, 256, 0, s>>>(Gm.p, ni, Rk.p, F, kNearIdFlag, 1e-8);
+    near_identity_chol_kernel<<<1, 1024, 0, s>>>(Gm.p, ni, Rk.p, F, kNearIdFlag, 1e-8);
     TTR_TRY(launched());
     TTR_TRY(chol(CH_RCLAMP, F + kNearIdFlag, 1));           // R4 (plain, clamped), if needed
     TTR_TRY(accumulate_r(nullptr, 0));
@@ -1667,6 +2169,19 @@ int scale_by_inv_sigma(Ctx& c, const double* AV, int64_t m, int64_t k, const dou
 // One CholeskyQR pass, Q only, for inputs whose columns are already close to
 // orthonormal (kappa - 1 small): Q^T Q = I + O(kappa^2 u).  The two-sided
 // rounding's V refinement; n <= 160 (blocked Cholesky), else the routed qr().
+// tt_cholesky: one factorisation of the CholeskyQR family (R-only modes)
+int cholesky(Ctx& c, int64_t n, const double* G, int64_t m, int shifted, double* Rinv, double* L,
+             cudaStream_t s) {
+  if (n < 1 || n > 1024 || !G || !Rinv) {
+    set_error("tt_cholesky: need 1 <= n <= 1024 and G, Rinv");
+    return TT_ERR_ARG;
+  }
+  DBuf gw;
+  if (n > 160 && n * n > kSmemLimitDoubles) TTR_TRY(dalloc(gw, size_t(n) * n, s));
+  return launch_chol(c, G, int(n), m, shifted ? CH_RSHIFT : CH_RCLAMP, Rinv, L, gw.p, nullptr, 0,
+                     s);
+}
+
 int qr_near_orthonormal(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, double* Q,
                         cudaStream_t s) {
   if (n > 160 || m < n) return qr(c, m, n, A, lda, false, Q, nullptr, s);

@@ -482,23 +482,42 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kJcThreads)
           in_place(sl, al, cid, base + a0, base + b0, rot);
         }
       }
-      // cross pairs (t_i, b_{(i+s) mod 4}), s = 0..2 in place
-#pragma unroll 1
-      for (int sr = 0; sr < kUw - 1; ++sr) in_place(sl, al, cid, rho, kUw + ((rho + sr) & 3), rot);
-      // s = 3: rotated columns go to the next owners
+      // cross pairs (t_i, b_{(i+s) mod 4}), s = 0..3: the top column t_rho stays
+      // in this subgroup's registers for the whole round and the bottom columns
+      // rotate through the subgroups (subgroup rho holds b_{(rho+s) mod 4} at
+      // sub-round s) by 8-lane shuffles -- no shared-memory round trip per
+      // sub-round (a sub-round of the smem version moved 640 B per lane)
+      const int cx = rho, cy = kUw + ((rho + kUw - 1) & 3);   // slots of the last pair
+      double2 x[kR2], y[kR2];
       {
-        const int cx = rho, cy = kUw + ((rho + kUw - 1) & 3);
-        double2 x[kR2], y[kR2];
-        const double2* px = reinterpret_cast<const double2*>(sl[cx]) + t8;
-        const double2* py = reinterpret_cast<const double2*>(sl[cy]) + t8;
+        const double2* px = reinterpret_cast<const double2*>(sl[rho]) + t8;
+        const double2* py = reinterpret_cast<const double2*>(sl[kUw + rho]) + t8;
 #pragma unroll
         for (int s = 0; s < kR2; ++s) {
           x[s] = px[kG8 * s];
           y[s] = py[kG8 * s];
         }
-        double ax = al[cx], ay = al[cy];
-        const int idx = cid[cx], idy = cid[cy];
-        if (live && jc_rotate(x, y, idx, idy, ax, ay, n, small, tol)) rot = 1;
+      }
+      double ax = al[rho], ay = al[kUw + rho];
+      const int idx = cid[rho];
+      int idy = cid[kUw + rho];
+      {
+        const int src = (lane + kG8) & 31;
+#pragma unroll 1
+        for (int sr = 0; sr < kUw; ++sr) {
+          if (live && jc_rotate(x, y, idx, idy, ax, ay, n, small, tol)) rot = 1;
+          if (sr == kUw - 1) break;
+#pragma unroll
+          for (int s = 0; s < kR2; ++s) {
+            y[s].x = __shfl_sync(0xffffffffu, y[s].x, src);
+            y[s].y = __shfl_sync(0xffffffffu, y[s].y, src);
+          }
+          ay = __shfl_sync(0xffffffffu, ay, src);
+          idy = __shfl_sync(0xffffffffu, idy, src);
+        }
+      }
+      // the rotated columns go to the next owners
+      {
         const int nb = P2P ? (buf == 2 ? 0 : buf + 1) : (buf ^ 1);
         // three buffers: the destinations' buffer nb was last read two rounds ago
         if (P2P && live && round_g >= 2)

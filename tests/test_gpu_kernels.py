@@ -168,6 +168,48 @@ def test_qr_rank_deficient_uses_valid_basis(ctx):
     assert np.linalg.norm(Qh @ (Qh.T @ A) - A) < 1e-12 * np.linalg.norm(A)
 
 
+@pytest.mark.parametrize("n", [1, 2, 5, 8, 31, 32, 33, 35, 40, 63, 64, 65, 70, 72, 96, 97, 100,
+                               127, 128, 129, 136, 143, 144, 150, 159, 160, 161, 200])
+@pytest.mark.parametrize("cond", [1e2, 1e7])
+def test_cholesky_factor_and_inverse(ctx, n, cond):
+    """The CholeskyQR passes' factorisation: L L^T = G and Rinv = L^{-T} against a
+    plain fp64 reference, at every block / tile raggedness up to n = 160 (the
+    blocked look-ahead kernel) and beyond (the generic kernel)."""
+    rng = np.random.default_rng(n * 7 + int(math.log10(cond)))
+    V, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    s = np.logspace(0, -math.log10(cond), n)
+    G = (V * s) @ V.T
+    G = 0.5 * (G + G.T)
+    Gd = torch.from_numpy(np.asfortranarray(G)).cuda().t().contiguous().t()
+    Rinv, L = ctx.tt_cholesky(Gd)
+    Lh, Rh = L.cpu().numpy(), Rinv.cpu().numpy()
+    Lref = np.linalg.cholesky(G)
+    assert np.allclose(np.triu(Lh, 1), 0) and np.allclose(np.tril(Rh, -1), 0)
+    assert np.linalg.norm(Lh @ Lh.T - G) <= 1e-14 * n * np.linalg.norm(G)
+    # Rinv L^T = I to the conditioning of L (sqrt(cond))
+    assert np.linalg.norm(Rh.T @ Lh - np.eye(n)) <= 1e-14 * n * math.sqrt(cond)
+    assert np.linalg.norm(Lh - Lref) <= 1e-12 * math.sqrt(cond) * np.linalg.norm(Lref)
+
+
+def test_cholesky_shifted_and_breakdown(ctx):
+    """shifted = 1 factors G + 11 (m n + n (n + 1)) u tr(G) I; an indefinite G
+    is reported (TT_ERR_NUMERIC), not returned."""
+    import paper_2110_04393_b200 as P
+    rng = np.random.default_rng(5)
+    n, m = 144, 36864
+    A = rng.standard_normal((n, n))
+    G = A @ A.T
+    Gd = torch.from_numpy(G).cuda().t().contiguous().t()
+    _, L = ctx.tt_cholesky(Gd, m=m, shifted=True)
+    shift = 11.0 * (m * n + n * (n + 1)) * 2.0 ** -53 * np.trace(G)
+    Lh = L.cpu().numpy()
+    assert np.linalg.norm(Lh @ Lh.T - (G + shift * np.eye(n))) <= 1e-13 * np.linalg.norm(G)
+    Gbad = torch.from_numpy(-np.eye(n)).cuda().t().contiguous().t()
+    with pytest.raises(P.TTError) as e:
+        ctx.tt_cholesky(Gbad)
+    assert e.value.code == -8
+
+
 @pytest.mark.parametrize("m,n", [(5, 5), (144, 144), (70, 33), (300, 80), (33, 33)])
 def test_jacobi_svd_matches_lapack(ctx, m, n):
     rng = np.random.default_rng(m * n)

@@ -20,8 +20,9 @@ for _ in range(3):
     ctx.tt_qr(A, want_r=True)
 torch.cuda.synchronize()
 w = ctx.status_words(64)
-names = ["C1-Xkk", "C2", "C3", "I0", "Iblk", "load", "C1-fact"]
-tot = sum(w[32:39])
+names = (["C1-Xkk", "C2", "C3", "I0", "Iblk", "load", "C1-fact"] if os.environ.get("TTR_CHOL") == "blk"
+         else ["wait-after-F", "(EMPTY waits in F)", "T(k)", "last-inverse", "outputs", "load", "F(warp0)"])
+tot = sum(w[32:39]) - (0 if os.environ.get("TTR_CHOL") == "blk" else w[33])
 calls = max(1, w[8] + 3 * w[10] + 4 * w[15])
 print("status", w[:17])
 ncall = 2 * w[8] + 3 * w[10] + 4 * w[15] + (2 if w[10] else 0)   # route 0 attempt + route 1
