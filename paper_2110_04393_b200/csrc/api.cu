@@ -9,11 +9,69 @@
 #include <memory>
 #include <numeric>
 
+#include <map>
+#include <string>
+#include <cstring>
 #include "common.cuh"
 
 namespace ttr {
 
 std::atomic<uint64_t> g_launches{0};
+thread_local Tracer* t_tracer = nullptr;
+thread_local const char* t_site_file = nullptr;
+thread_local int t_site_line = 0;
+
+// TTR_TRACE: install a tracer for one call; on destruction (after the call's
+// final synchronisation) append per-launch-site totals to the named file
+struct TraceScope {
+  Tracer tr;
+  const char* path = nullptr;
+  bool on = false;
+  TraceScope(cudaStream_t s, bool capturing) {
+    static const char* env = getenv("TTR_TRACE");
+    if (!env || capturing || t_tracer) return;
+    path = env;
+    tr.s = s;
+    tr.pool.resize(16384);
+    for (auto& e : tr.pool) cudaEventCreate(&e);
+    t_tracer = &tr;
+    on = true;
+    trace_mark("start", 0);
+  }
+  ~TraceScope() {
+    if (!on) return;
+    t_tracer = nullptr;
+    cudaStreamSynchronize(tr.s);
+    std::map<std::string, std::pair<int, double>> agg;
+    double tot = 0.0;
+    for (size_t i = 1; i < tr.recs.size(); ++i) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, tr.recs[i - 1].e, tr.recs[i].e);
+      const char* f = strrchr(tr.recs[i].file, '/');
+      std::string key = std::string(f ? f + 1 : tr.recs[i].file) + ":" +
+                        std::to_string(tr.recs[i].line);
+      auto& a = agg[key];
+      a.first += 1;
+      a.second += ms;
+      tot += ms;
+    }
+    for (auto& e : tr.pool) cudaEventDestroy(e);
+    std::vector<std::pair<double, std::string>> v;
+    for (auto& kv : agg) {
+      char buf[160];
+      snprintf(buf, sizeof buf, "%9.3f ms %6.1f%% n=%6d  %s", kv.second.second,
+               100.0 * kv.second.second / std::max(tot, 1e-9), kv.second.first, kv.first.c_str());
+      v.push_back({kv.second.second, buf});
+    }
+    std::sort(v.rbegin(), v.rend());
+    FILE* fp = fopen(path, "a");
+    if (!fp) return;
+    fprintf(fp, "# trace: %zu launches, %.3f ms between the first and the last\n",
+            tr.recs.size() - 1, tot);
+    for (auto& x : v) fprintf(fp, "%s\n", x.second.c_str());
+    fclose(fp);
+  }
+};
 
 static thread_local std::string t_err;
 std::mutex& init_mutex() {
@@ -841,6 +899,7 @@ int round_sum_impl(tt_ctx* c, int S, const tt_view* terms, const tt_round_opts* 
                    tt_sketch* user_sk, tt_tensor** outp, const int64_t* slab_gdims = nullptr,
                    const int64_t* slab_lo = nullptr) {
   const bool slab_mode = slab_gdims != nullptr;
+  TraceScope trace(c->stream, c->capturing);
   Slab slab;
   const Slab* sl = slab_mode ? &slab : nullptr;
   std::vector<int64_t> dims;

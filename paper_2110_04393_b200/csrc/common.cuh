@@ -44,10 +44,42 @@ struct Status {
     if (r__ != TT_OK) return r__;                                               \
   } while (0)
 
+// Launch tracing (diagnostics, TTR_TRACE=<file>): while a Tracer is installed on
+// the calling thread, every launch records an event on the traced stream, so the
+// time between consecutive events is the in-pipeline duration (gaps included) of
+// the launch site -- aggregated per source line at the end of the call.
+struct TraceRec {
+  cudaEvent_t e;
+  const char* file;
+  int line;
+};
+struct Tracer {
+  cudaStream_t s = nullptr;
+  std::vector<TraceRec> recs;
+  std::vector<cudaEvent_t> pool;   // created up front: the host stays ahead of the GPU
+};
+extern thread_local Tracer* t_tracer;
+extern thread_local const char* t_site_file;   // set around GEMM calls (SiteGuard)
+extern thread_local int t_site_line;
+inline void trace_mark(const char* file, int line) {
+  if (t_site_file) { file = t_site_file; line = t_site_line; }
+  cudaEvent_t e;
+  if (t_tracer->recs.size() < t_tracer->pool.size()) {
+    e = t_tracer->pool[t_tracer->recs.size()];
+  } else if (cudaEventCreate(&e) == cudaSuccess) {
+    t_tracer->pool.push_back(e);
+  } else {
+    return;
+  }
+  cudaEventRecord(e, t_tracer->s);
+  t_tracer->recs.push_back({e, file, line});
+}
+
 // every kernel launch of the library goes through this counter (tt_launch_count)
 extern std::atomic<uint64_t> g_launches;
 inline int launched_at(const char* file, int line) {
   g_launches.fetch_add(1, std::memory_order_relaxed);
+  if (t_tracer) trace_mark(file, line);
   cudaError_t e = cudaPeekAtLastError();
   if (e != cudaSuccess) {
     set_error("kernel launch failed at %s:%d: %s", file, line, cudaGetErrorString(e));
@@ -156,16 +188,27 @@ constexpr int kMaxGemmBatch = 64;
 // K range of a column tile stops at its last column; kGemmLower -- only the
 // tiles meeting the lower triangle of C are computed (Grams feeding a Cholesky).
 constexpr unsigned kGemmTriB = 1u, kGemmLower = 2u;
-int gemm(Ctx& c, bool ta, bool tb, const GemmDesc* d, int nbatch, double alpha,
-         double beta, cudaStream_t s, const int* gate = nullptr, int gate_val = 0,
-         unsigned flags = 0);
-inline int gemm1(Ctx& c, bool ta, bool tb, int M, int N, int K, double alpha,
-                 const double* A, int lda, const double* B, int ldb, double beta,
-                 double* C, int ldc, cudaStream_t s, const int* gate = nullptr,
-                 int gate_val = 0, unsigned flags = 0) {
+int gemm_impl(Ctx& c, bool ta, bool tb, const GemmDesc* d, int nbatch, double alpha,
+              double beta, cudaStream_t s, const int* gate = nullptr, int gate_val = 0,
+              unsigned flags = 0);
+inline int gemm1_impl(Ctx& c, bool ta, bool tb, int M, int N, int K, double alpha,
+                      const double* A, int lda, const double* B, int ldb, double beta,
+                      double* C, int ldc, cudaStream_t s, const int* gate = nullptr,
+                      int gate_val = 0, unsigned flags = 0) {
   GemmDesc d{A, B, C, M, N, K, lda, ldb, ldc};
-  return gemm(c, ta, tb, &d, 1, alpha, beta, s, gate, gate_val, flags);
+  return gemm_impl(c, ta, tb, &d, 1, alpha, beta, s, gate, gate_val, flags);
 }
+// the call site of a GEMM, for launch tracing (the launches happen in gemm.cu)
+struct SiteGuard {
+  const char* f0;
+  int l0;
+  SiteGuard(const char* f, int l) : f0(t_site_file), l0(t_site_line) {
+    if (!t_site_file) { t_site_file = f; t_site_line = l; }
+  }
+  ~SiteGuard() { t_site_file = f0; t_site_line = l0; }
+};
+#define gemm(...) ([&]() { ::ttr::SiteGuard g__(__FILE__, __LINE__); return ::ttr::gemm_impl(__VA_ARGS__); }())
+#define gemm1(...) ([&]() { ::ttr::SiteGuard g__(__FILE__, __LINE__); return ::ttr::gemm1_impl(__VA_ARGS__); }())
 
 // Persistent warp-specialised batched GEMM for short K (pgemm.cu): C_j = A_j B_j,
 // column-major, beta = 0.  Returns 1 (nothing launched) when it does not apply.

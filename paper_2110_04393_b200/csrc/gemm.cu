@@ -466,42 +466,49 @@ __global__ void __launch_bounds__(WM* WN * 32)
   }
 }
 
-// deterministic split-K reduction: slices summed in index order, one output
-// element per thread (grid: tiles x element chunks), slice loads issued ahead
-template <int BM, int BN>
+// deterministic split-K reduction: slices summed in a fixed order, LANES threads
+// per output element (grid: tiles x element chunks): lane q sums slices q,
+// q + LANES, ... in index order, the LANES partial sums are combined by a fixed
+// butterfly -- several lanes per element when there are many slices (the l x l
+// Grams: ~100 slices of few tiles), so enough L2 requests are in flight
+template <int BM, int BN, int LANES>
 __global__ void __launch_bounds__(256) splitk_reduce(const __grid_constant__ GemmParams P) {
   if (P.gate && *P.gate != P.gate_val) return;
   const int tile_id = blockIdx.x;             // (b, tm, tn)
   const int tn = tile_id % P.tiles_n, tm = (tile_id / P.tiles_n) % P.tiles_m;
   const int b = tile_id / (P.tiles_n * P.tiles_m);
   const GemmDesc& D = P.d[b];
-  const int e = blockIdx.y * 256 + threadIdx.x;
-  if (e >= BM * BN) return;
-  const int ml = e % BM, nl = e / BM;
+  const int e = (blockIdx.y * 256 + threadIdx.x) / LANES, q0 = threadIdx.x % LANES;
   if ((P.flags & kGemmLower) && tm * BM + BM <= tn * BN) return;
+  const int ml = e % BM, nl = e / BM;
   const int m = tm * BM + ml, n = tn * BN + nl;
-  if (m >= D.M || n >= D.N) return;
+  const bool live = e < BM * BN && m < D.M && n < D.N;   // (whole lane groups agree)
   const size_t stride = size_t(P.nbatch) * P.tiles_m * P.tiles_n * (BM * BN);
   const double* src = P.ws + ((size_t(b) * P.tiles_m + tm) * P.tiles_n + tn) * (BM * BN) + e;
-  // slices summed in index order (deterministic); loads issued 16 deep so the
-  // few threads of a small reduction keep enough L2 requests in flight
   double s = 0.0;
-  int k = 0;
-  for (; k + 16 <= P.kslices; k += 16) {
-    double v[16];
+  if (live) {
+    // loads issued 16 deep so the few threads of a small reduction keep enough
+    // L2 requests in flight
+    int k = q0;
+    for (; k + 15 * LANES < P.kslices; k += 16 * LANES) {
+      double v[16];
 #pragma unroll
-    for (int q = 0; q < 16; ++q) v[q] = __ldcg(src + size_t(k + q) * stride);
+      for (int q = 0; q < 16; ++q) v[q] = __ldcg(src + size_t(k + q * LANES) * stride);
 #pragma unroll
-    for (int q = 0; q < 16; ++q) s += v[q];
+      for (int q = 0; q < 16; ++q) s += v[q];
+    }
+    for (; k + 3 * LANES < P.kslices; k += 4 * LANES) {
+      double v[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) v[q] = __ldcg(src + size_t(k + q * LANES) * stride);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) s += v[q];
+    }
+    for (; k < P.kslices; k += LANES) s += __ldcg(src + size_t(k) * stride);
   }
-  for (; k + 4 <= P.kslices; k += 4) {
-    double v[4];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) v[q] = __ldcg(src + size_t(k + q) * stride);
-#pragma unroll
-    for (int q = 0; q < 4; ++q) s += v[q];
-  }
-  for (; k < P.kslices; ++k) s += __ldcg(src + size_t(k) * stride);
+  for (int o = 1; o < LANES; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (!live || q0 != 0) return;
   double* cp = D.C + m + int64_t(n) * D.ldc;
   double v = P.alpha * s;
   if (P.beta != 0.0) v += P.beta * *cp;
@@ -604,11 +611,20 @@ int launch_cfg(Ctx& c, GemmParams& P, int maxM, int maxN, int maxK, cudaStream_t
   // slots (SMs x CTAs per SM) best -- a grid of 1.13 waves runs at 57% -- with
   // a small penalty per slice for the extra partial traffic and reduction
   const long slots = long(c.sm_count) * (use_tma ? tresident[dev & 63] : resident[dev & 63]);
-  const long tiles = long(P.tiles_m) * P.tiles_n * P.nbatch;
+  // live tiles: a lower-triangle Gram skips the tiles above the diagonal
+  long tiles = long(P.tiles_m) * P.tiles_n * P.nbatch;
+  if (P.flags & kGemmLower) {
+    long live = 0;
+    for (int tm = 0; tm < P.tiles_m; ++tm)
+      for (int tn = 0; tn < P.tiles_n; ++tn) live += (tm * S::bm + S::bm > tn * S::bn);
+    tiles = live * P.nbatch;
+  }
   const int ktiles = (maxK + S::bk - 1) / S::bk;
   int ksl = 1;
   if (tiles < 3 * slots) {
-    const int kmax = std::max(1, std::min(64, ktiles / 4));
+    // (a Gram has a handful of tiles and a long K: up to 256 slices so that its
+    // grid fills the GPU)
+    const int kmax = std::max(1, std::min((P.flags & kGemmLower) ? 256 : 64, ktiles / 4));
     if (tiles * kmax <= slots) {
       ksl = kmax;   // cannot fill one wave: as many slices as allowed (>= 4 k-tiles each)
     } else {
@@ -628,7 +644,7 @@ int launch_cfg(Ctx& c, GemmParams& P, int maxM, int maxN, int maxK, cudaStream_t
   P.kslices = ksl;
   P.kchunk = kchunk_tiles * S::bk;
   if (ksl > 1) {
-    const size_t need = size_t(ksl) * tiles * S::bm * S::bn;
+    const size_t need = size_t(ksl) * P.tiles_m * P.tiles_n * P.nbatch * S::bm * S::bn;
     if (c.gemm_ws.n < need) {
       if (c.capturing) {   // a workspace allocated inside a graph would die with it
         set_error("gemm workspace must be sized before graph capture");
@@ -653,8 +669,9 @@ int launch_cfg(Ctx& c, GemmParams& P, int maxM, int maxN, int maxK, cudaStream_t
   }
   TTR_TRY(launched());
   if (ksl > 1) {
-    splitk_reduce<S::bm, S::bn><<<dim3(P.tiles_n * P.tiles_m * P.nbatch,
-                                       (S::bm * S::bn + 255) / 256), 256, 0, s>>>(P);
+    const dim3 rg(P.tiles_n * P.tiles_m * P.nbatch, (S::bm * S::bn * (ksl >= 32 ? 4 : 1) + 255) / 256);
+    if (ksl >= 32) splitk_reduce<S::bm, S::bn, 4><<<rg, 256, 0, s>>>(P);
+    else splitk_reduce<S::bm, S::bn, 1><<<rg, 256, 0, s>>>(P);
     TTR_TRY(launched());
   }
   return TT_OK;
@@ -705,7 +722,7 @@ int dispatch(Ctx& c, GemmParams& P, int maxM, int maxN, int maxK, cudaStream_t s
 
 }  // namespace
 
-int gemm(Ctx& c, bool ta, bool tb, const GemmDesc* d, int nbatch, double alpha, double beta,
+int gemm_impl(Ctx& c, bool ta, bool tb, const GemmDesc* d, int nbatch, double alpha, double beta,
          cudaStream_t s, const int* gate, int gate_val, unsigned flags) {
   int done = 0;
   while (done < nbatch) {

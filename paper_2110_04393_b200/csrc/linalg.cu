@@ -803,7 +803,7 @@ __device__ __forceinline__ int la_rest_count(int P) { return 12 - P; }
 
 // A(r, c) -= sum_{t in [t0, t0+32)} L(r, t) L(c, t) on the 8x8 tiles (rt, ct),
 // ct in [ct_lo, ct_hi), rt in [ct, nt8): tiles widx, widx + nw, ...
-__device__ __forceinline__ void la_trail(double* S, int ld, int n, int t0, int ct_lo, int ct_hi,
+__device__ __noinline__ void la_trail(double* S, int ld, int n, int t0, int ct_lo, int ct_hi,
                                          int nt8, int widx, int nw, int lane) {
   const int g = lane >> 2, t4 = lane & 3;
   int tot = 0;
@@ -833,7 +833,7 @@ __device__ __forceinline__ void la_trail(double* S, int ld, int n, int t0, int c
 // lanes 0-15 / 16-31 invert the 16 x 16 halves by register-resident forward
 // substitution, then X21 = -X22 (L21 X11) on DMMA tiles.  X(r, c), r > c, parked
 // at (c, r); the diagonal is rdiag.  tmp: 256 doubles of shared scratch.
-__device__ __forceinline__ void la_form_xkk(double* S, int ld, const double* rdiag, int k0,
+__device__ __noinline__ void la_form_xkk(double* S, int ld, const double* rdiag, int k0,
                                             int kb, int lane, double* tmp) {
   const int g = lane >> 2, t4 = lane & 3;
   {
@@ -903,106 +903,73 @@ __device__ __forceinline__ void la_form_xkk(double* S, int ld, const double* rdi
 
 // Block row kr of X (rows [kr0, kr0 + kbr), columns [0, kr0)), X_kk already formed:
 //   T = L_{kr,<kr} X_{<kr,<kr}, then X_{kr,<kr} = -X_kk T, T staged in the
-// destination (upper triangle).  Warps widx of nw, synchronised by named barrier
-// `bar` with `cnt` threads (bar 0 = the whole CTA).
-__device__ __forceinline__ void la_inverse_row(double* S, int ld, const double* rdiag, int kr0,
-                                               int kbr, int widx, int nw, int bar, int cnt,
-                                               int lane) {
+// destination (upper triangle).  One warp owns a whole 8-column tile column C
+// (warps widx of nw take C = 8 widx, 8 (widx + nw), ...): T needs nothing the
+// other warps write, and the -X_kk T pass runs over the row tiles bottom-up
+// (tile R reads T rows <= R + 7 only), so it runs in place with no barrier.
+// Rolled loops: the kernel's code stays small (it runs cold after the GEMMs).
+__device__ __noinline__ void la_inverse_row(double* S, int ld, const double* rdiag, int kr0,
+                                               int kbr, int widx, int nw, int lane) {
   const int g = lane >> 2, t4 = lane & 3;
-  const int nrt = (kbr + 7) / 8, nct = kr0 / 8, ntiles = nrt * nct;
+  const int nrt = (kbr + 7) / 8, nct = kr0 / 8;
   const int rend = kr0 + kbr;
-  constexpr int kMaxT = 6;   // <= ceil(48 / 8) tiles per warp (n <= 160)
-  double acc[kMaxT][2];
-  // stage 1: T = L_{kr,<kr} X_{<kr,<kr}; X(t, j) = 0 for t < j, so the k range of
-  // tile column C starts at C; only its first 8 steps (X's diagonal tile) need
-  // selects
-#pragma unroll
-  for (int q = 0; q < kMaxT; ++q) {
-    acc[q][0] = acc[q][1] = 0.0;
-    const int tt = widx + nw * q;
-    if (tt < ntiles) {
-      const int R = kr0 + 8 * (tt / nct), C = 8 * (tt % nct), j = C + g;
+#pragma unroll 1
+  for (int ct = widx; ct < nct; ct += nw) {
+    const int C = 8 * ct, j = C + g;
+    // stage 1: T(R.., C..) for every row tile; X(t, j) = 0 for t < j, so the k
+    // range starts at C and only its first 8 steps (X's diagonal tile) need selects
+#pragma unroll 1
+    for (int rt = 0; rt < nrt; ++rt) {
+      const int R = kr0 + 8 * rt;
       const double* arow = S + (R + g);
-      double e0 = 0.0, e1 = 0.0, f0 = 0.0, f1 = 0.0, h0 = 0.0, h1 = 0.0;
+      double c0 = 0.0, c1 = 0.0, e0 = 0.0, e1 = 0.0;
       {
         const int ta = C + t4, tb = C + 4 + t4;
         const double ba = ta > j ? S[j + ta * ld] : (ta == j ? rdiag[j] : 0.0);
         const double bb = tb > j ? S[j + tb * ld] : (tb == j ? rdiag[j] : 0.0);
-        dmma884(acc[q][0], acc[q][1], arow[ta * ld], ba);
+        dmma884(c0, c1, arow[ta * ld], ba);
         dmma884(e0, e1, arow[tb * ld], bb);
       }
-      int t = C + 8;
 #pragma unroll 1
-      for (; t + 8 < kr0; t += 16) {
+      for (int t = C + 8; t < kr0; t += 8) {
         const int t0 = t + t4;
-        dmma884(acc[q][0], acc[q][1], arow[t0 * ld], S[j + t0 * ld]);
-        dmma884(e0, e1, arow[(t0 + 4) * ld], S[j + (t0 + 4) * ld]);
-        dmma884(f0, f1, arow[(t0 + 8) * ld], S[j + (t0 + 8) * ld]);
-        dmma884(h0, h1, arow[(t0 + 12) * ld], S[j + (t0 + 12) * ld]);
-      }
-      if (t < kr0) {
-        const int t0 = t + t4;
-        dmma884(acc[q][0], acc[q][1], arow[t0 * ld], S[j + t0 * ld]);
+        dmma884(c0, c1, arow[t0 * ld], S[j + t0 * ld]);
         dmma884(e0, e1, arow[(t0 + 4) * ld], S[j + (t0 + 4) * ld]);
       }
-      acc[q][0] += (e0 + f0) + h0;
-      acc[q][1] += (e1 + f1) + h1;
-    }
-  }
-  nbar_sync(bar, cnt);
-#pragma unroll
-  for (int q = 0; q < kMaxT; ++q) {
-    const int tt = widx + nw * q;
-    if (tt < ntiles) {
-      const int R = kr0 + 8 * (tt / nct), C = 8 * (tt % nct);
       const int r = R + g, cA = C + 2 * t4;
       if (r < rend) {
-        S[cA + r * ld] = acc[q][0];
-        S[(cA + 1) + r * ld] = acc[q][1];
+        S[cA + r * ld] = c0 + e0;
+        S[(cA + 1) + r * ld] = c1 + e1;
       }
     }
-  }
-  nbar_sync(bar, cnt);
-  // stage 2: X_{kr,<kr} = -X_kk T; X_kk(i, t) = 0 for t > i: the k range of tile
-  // row R ends with its diagonal tile (selects), before it X_kk(i, t) is parked
-  // at (t, i)
-#pragma unroll
-  for (int q = 0; q < kMaxT; ++q) {
-    acc[q][0] = acc[q][1] = 0.0;
-    const int tt = widx + nw * q;
-    if (tt < ntiles) {
-      const int R = kr0 + 8 * (tt / nct), C = 8 * (tt % nct);
-      const int i = R + g;
+    __syncwarp();
+    // stage 2: X_{kr,<kr} = -X_kk T, bottom-up; X_kk(i, t) = 0 for t > i, parked
+    // at (t, i) below its diagonal tile (selects only there)
+#pragma unroll 1
+    for (int rt = nrt - 1; rt >= 0; --rt) {
+      const int R = kr0 + 8 * rt, i = R + g;
       const bool iv = i < rend;
-      double e0 = 0.0, e1 = 0.0;
+      double c0 = 0.0, c1 = 0.0, e0 = 0.0, e1 = 0.0;
 #pragma unroll 1
       for (int t = kr0; t < R; t += 8) {
         const int t0 = t + t4;
-        dmma884(acc[q][0], acc[q][1], iv ? S[t0 + i * ld] : 0.0, S[(C + g) + t0 * ld]);
-        dmma884(e0, e1, iv ? S[(t0 + 4) + i * ld] : 0.0, S[(C + g) + (t0 + 4) * ld]);
+        dmma884(c0, c1, iv ? S[t0 + i * ld] : 0.0, S[j + t0 * ld]);
+        dmma884(e0, e1, iv ? S[(t0 + 4) + i * ld] : 0.0, S[j + (t0 + 4) * ld]);
       }
 #pragma unroll
       for (int kk = 0; kk < 2; ++kk) {
         const int tc = R + 4 * kk + t4;
         const double av = (iv && tc <= i) ? (tc == i ? rdiag[i] : S[tc + i * ld]) : 0.0;
-        const double bv = tc < rend ? S[(C + g) + tc * ld] : 0.0;
-        dmma884(acc[q][0], acc[q][1], av, bv);
+        const double bv = tc < rend ? S[j + tc * ld] : 0.0;
+        dmma884(c0, c1, av, bv);
       }
-      acc[q][0] += e0;
-      acc[q][1] += e1;
-    }
-  }
-  nbar_sync(bar, cnt);
-#pragma unroll
-  for (int q = 0; q < kMaxT; ++q) {
-    const int tt = widx + nw * q;
-    if (tt < ntiles) {
-      const int R = kr0 + 8 * (tt / nct), C = 8 * (tt % nct);
-      const int r = R + g, cA = C + 2 * t4;
-      if (r < rend) {
-        S[cA + r * ld] = -acc[q][0];
-        S[(cA + 1) + r * ld] = -acc[q][1];
+      __syncwarp();   // every lane has read rows R.. of T before they are overwritten
+      const int cA = C + 2 * t4;
+      if (iv) {
+        S[cA + i * ld] = -(c0 + e0);
+        S[(cA + 1) + i * ld] = -(c1 + e1);
       }
+      __syncwarp();
     }
   }
 }
@@ -1071,92 +1038,88 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
     const int ng = (kb + 3) >> 2;
     int idx;
     const int role = la_role(w, P, idx);
-    if (role == 0) {
-      // ---- F(k), diagonal block: lane i keeps the not yet eliminated part of
-      // row i in registers (a[q] = A(i, j0 + q)), pivots in groups of 4 with
-      // static register offsets, then a shift by 4.  The pivot step is
-      // branch-free (clamping and the finiteness test are selects; 1/L_jj =
+    if (role <= 1) {
+      // ---- F(k).  Diagonal warp (role 0): lane i keeps the not yet eliminated
+      // part of row k0 + i in registers (a[q] = A(i, j0 + q)), pivots in groups
+      // of 4 with static register offsets, then a shift by 4.  The pivot step
+      // is branch-free (clamping and the finiteness test are selects; 1/L_jj =
       // MUFU rsqrt + two Newton steps).  Factored column j goes to the ring slot
       // of its group, doubled (colb[i] = colb[i + 32] = L_ij) so that every load
-      // below is [base + constant]; updates of the upper slots are harmless.
+      // of the update is [base + constant]; updates of the upper slots are
+      // harmless.  Panel warps (role 1): the same eliminations on rows
+      // r0 + 32 idx + lane with the ring's columns and 1/L_jj -- one shared
+      // code path for the update, so the kernel's code stays small.
+      const bool diag = role == 0;
       const int i = lane;
+      const int ip = diag ? k0 + lane : r0 + 32 * idx + lane;   // absolute row
+      const bool live = diag ? lane < kb : ip < n;
       double a[32];
 #pragma unroll
       for (int q = 0; q < 32; ++q)
-        a[q] = (i < kb && q <= i) ? S[(k0 + i) + (k0 + q) * ld] : 0.0;
+        a[q] = (live && q < kb && (!diag || q <= i)) ? S[ip + (k0 + q) * ld] : 0.0;
       int bad = 0, nclamp = 0;
 #pragma unroll 1
       for (int grp = 0; grp < ng; ++grp) {
         const int sl = grp & 1;
+        if (!diag) nbar_sync(kLaBarFull + sl, cnt);
+        if (diag && P > 0 && grp >= 2) {   // panel done with grp - 2
 #ifdef TTR_CHOL_PROF
-        const long long tw0 = clock64();
+          const long long tw0 = clock64();
 #endif
-        if (P > 0 && grp >= 2) nbar_sync(kLaBarEmpty + sl, cnt);   // panel done with grp - 2
+          nbar_sync(kLaBarEmpty + sl, cnt);
 #ifdef TTR_CHOL_PROF
-        if (threadIdx.x == 0) atomicAdd(&flags[33], int((clock64() - tw0) >> 6));
+          if (threadIdx.x == 0) atomicAdd(&flags[33], int((clock64() - tw0) >> 6));
 #endif
-#pragma unroll
-        for (int sft = 0; sft < 4; ++sft) {
-          const int j = 4 * grp + sft;
-          double piv = __shfl_sync(0xffffffffu, a[sft], j);
-          piv = (j < kb) ? piv : 1.0;                       // padding pivot
-          const bool fin = fabs(piv) <= 1.79e308;           // false for inf / nan
-          const bool cl = clamp && fin && !(piv > tau);     // numerically null direction
-          piv = cl ? tau : piv;
-          nclamp += cl;
-          const bool ok = fin && piv > 0.0;
-          bad |= !ok;
-          const double pv = ok ? piv : 1.0;
-          double rd;
-          asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(rd) : "d"(pv));
-          rd = rd * fma(-0.5 * pv * rd, rd, 1.5);           // Newton steps for 1/sqrt
-          rd = rd * fma(-0.5 * pv * rd, rd, 1.5);
-          const double lij = (i > j) ? a[sft] * rd : (i == j ? pv * rd : 0.0);
-          if (j < kb && i >= j && i < kb) S[(k0 + i) + (k0 + j) * ld] = lij;
-          if (i == j && j < kb) rdiag[k0 + j] = rd;
-          double* cb0 = ring[sl][sft];
-          cb0[i] = lij;
-          cb0[i + 32] = lij;
-          if (i == 0) ring_rd[sl][sft] = rd;
-          __syncwarp();
-          const double* cb = cb0 + j;
-#pragma unroll
-          for (int qq = 1; qq < 32 - sft; ++qq) a[sft + qq] = fma(-lij, cb[qq], a[sft + qq]);
         }
 #pragma unroll
-        for (int q = 0; q < 28; ++q) a[q] = a[q + 4];
-        a[28] = a[29] = a[30] = a[31] = 0.0;
-        if (P > 0) nbar_arrive(kLaBarFull + sl, cnt);
-      }
-      if (lane == 0) {
-        if (bad) s_bad = 1;
-        if (nclamp) s_clamped += nclamp;
-      }
-      CHOL_PROF(6);
-    } else if (role == 1) {
-      // ---- F(k), panel: the same eliminations on rows r0 + 32 idx + lane
-      const int ip = r0 + 32 * idx + lane;
-      const bool live = ip < n;
-      double a[32];
-#pragma unroll
-      for (int q = 0; q < 32; ++q) a[q] = (live && q < kb) ? S[ip + (k0 + q) * ld] : 0.0;
-#pragma unroll 1
-      for (int grp = 0; grp < ng; ++grp) {
-        const int sl = grp & 1;
-        nbar_sync(kLaBarFull + sl, cnt);
-#pragma unroll
         for (int sft = 0; sft < 4; ++sft) {
           const int j = 4 * grp + sft;
-          const double l = a[sft] * ring_rd[sl][sft];
-          if (live && j < kb) S[ip + (k0 + j) * ld] = l;
-          const double* cb = ring[sl][sft] + j;
+          double* cb0 = ring[sl][sft];
+          double l;
+          if (diag) {
+            double piv = __shfl_sync(0xffffffffu, a[sft], j);
+            piv = (j < kb) ? piv : 1.0;                       // padding pivot
+            const bool fin = fabs(piv) <= 1.79e308;           // false for inf / nan
+            const bool cl = clamp && fin && !(piv > tau);     // numerically null direction
+            piv = cl ? tau : piv;
+            nclamp += cl;
+            const bool ok = fin && piv > 0.0;
+            bad |= !ok;
+            const double pv = ok ? piv : 1.0;
+            double rd;
+            asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(rd) : "d"(pv));
+            rd = rd * fma(-0.5 * pv * rd, rd, 1.5);           // Newton steps for 1/sqrt
+            rd = rd * fma(-0.5 * pv * rd, rd, 1.5);
+            l = (i > j) ? a[sft] * rd : (i == j ? pv * rd : 0.0);
+            if (j < kb && i >= j && i < kb) S[(k0 + i) + (k0 + j) * ld] = l;
+            if (i == j && j < kb) rdiag[k0 + j] = rd;
+            cb0[i] = l;
+            cb0[i + 32] = l;
+            if (i == 0) ring_rd[sl][sft] = rd;
+            __syncwarp();
+          } else {
+            l = a[sft] * ring_rd[sl][sft];
+            if (live && j < kb) S[ip + (k0 + j) * ld] = l;
+          }
+          const double* cb = cb0 + j;
 #pragma unroll
           for (int qq = 1; qq < 32 - sft; ++qq) a[sft + qq] = fma(-l, cb[qq], a[sft + qq]);
         }
 #pragma unroll
         for (int q = 0; q < 28; ++q) a[q] = a[q + 4];
         a[28] = a[29] = a[30] = a[31] = 0.0;
-        if (grp + 2 < ng) nbar_arrive(kLaBarEmpty + sl, cnt);   // warp 0 reuses the slot
+        if (diag) {
+          if (P > 0) nbar_arrive(kLaBarFull + sl, cnt);
+        } else if (grp + 2 < ng) {
+          nbar_arrive(kLaBarEmpty + sl, cnt);   // warp 0 reuses the slot
+        }
+      }
+      if (diag) {
+        if (lane == 0) {
+          if (bad) s_bad = 1;
+          if (nclamp) s_clamped += nclamp;
+        }
+        CHOL_PROF(6);
       }
     } else if (role == 2 && k > 0) {
       // ---- behind F(k): finish block column k-1 (its trailing update beyond
@@ -1168,7 +1131,7 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
       else if (k0 + 32 < n)
         la_trail(S, ld, n, kp0, (k0 + 32) / 8, nt8, nt8, idx - 1, R - 1, lane);
       nbar_sync(kLaBarRest, rc);
-      if (kp0 > 0) la_inverse_row(S, ld, rdiag, kp0, 32, idx, R, kLaBarRest, rc, lane);
+      if (kp0 > 0) la_inverse_row(S, ld, rdiag, kp0, 32, idx, R, lane);
     }
     __syncthreads();
     CHOL_PROF(0);
@@ -1187,7 +1150,7 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
     const int kl0 = 32 * (nb - 1), kbl = n - kl0;
     if (w == 0) la_form_xkk(S, ld, rdiag, kl0, kbl, lane, ttmp);
     __syncthreads();
-    if (kl0 > 0) la_inverse_row(S, ld, rdiag, kl0, kbl, w, 16, 0, kBlkThreads, lane);
+    if (kl0 > 0) la_inverse_row(S, ld, rdiag, kl0, kbl, w, 16, lane);
   }
   CHOL_PROF(3);
   if (w == 0 && !s_zero) {   // route checks on diag(L), warp-parallel
