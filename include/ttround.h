@@ -55,7 +55,7 @@ extern "C" {
 #define TT_ERR_ARG       -1   /* null pointer, d < 2, S < 1 (world 1), bad mode/option */
 #define TT_ERR_SHAPE     -2   /* dims differ across summands; bond ranks mismatch   */
 #define TT_ERR_RANK      -3   /* a rank < 1, or R_0 != 1 or R_d != 1                */
-#define TT_ERR_NONFINITE -4   /* (reserved) non-finite input detected               */
+#define TT_ERR_NONFINITE -4   /* NaN/Inf in the summands (or overflow of their sketch contractions), detected on the trace of a QR Gram */
 #define TT_ERR_OOM       -5   /* device allocation failed                           */
 #define TT_ERR_CUDA      -6   /* CUDA runtime error (message in tt_last_error)      */
 #define TT_ERR_NCCL      -7   /* NCCL missing or failed                             */
@@ -364,6 +364,18 @@ int tt_svd_nov(tt_ctx_t ctx, int64_t m, int64_t n, const double* A, int64_t lda,
  * R-only QR's rule).  TT_ERR_NUMERIC if a pivot is not positive and finite. */
 int tt_cholesky(tt_ctx_t ctx, int64_t n, const double* G, int64_t m, int shifted,
                 double* Rinv, double* L);
+
+/* One CholeskyQR pass in one persistent launch (DESIGN.md §6 "CholeskyQR
+ * pass kernel"; the passes of the thin QR of Alg. 7 line 10, and of the
+ * truncation's QR, Alg. 2 line 4 / P:667-670): Q = op(A) Rinv and G = Q^T Q.
+ * op(A) = A (m x n, ld lda) or, trans = 1, A^T with A n x m (ld lda).  Rinv
+ * (n x n upper triangular, ld n; entries below the diagonal are not read) or
+ * NULL (Q = op(A)).  Q (m x n, ld ldq) and G (n x n, both triangles, ld n) are
+ * optional outputs (at least one).  All device pointers; 1 <= n <= 144 else
+ * TT_ERR_ARG.  Results are deterministic (fixed chunk-to-CTA map, CTA-ordered
+ * Gram sum). */
+int tt_cholqr_pass(tt_ctx_t ctx, int64_t m, int64_t n, const double* A, int64_t lda, int trans,
+                   const double* Rinv, double* Q, int64_t ldq, double* G);
 
 #ifdef __cplusplus
 }

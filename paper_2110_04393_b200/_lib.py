@@ -100,6 +100,7 @@ def load_library(path: str = LIB_PATH):
         "tt_svd_jacobi": (C.c_int, [P, i64, i64, P, i64, P, P, P]),
         "tt_svd_nov": (C.c_int, [P, i64, i64, P, i64, P, P]),
         "tt_cholesky": (C.c_int, [P, i64, P, i64, C.c_int, P, P]),
+        "tt_cholqr_pass": (C.c_int, [P, i64, i64, P, i64, C.c_int, P, P, i64, P]),
         "tt_plan_create": (C.c_int, [P, i32, C.POINTER(tt_view), C.POINTER(tt_round_opts), i32,
                                      C.POINTER(u64), i32, C.POINTER(P)]),
         "tt_plan_launch": (C.c_int, [P]),
@@ -462,6 +463,23 @@ class Context:
         _check(L.tt_cholesky(self.handle, n, G.data_ptr(), int(m or n), int(bool(shifted)),
                              Rinv.data_ptr(), Lo.data_ptr()))
         return Rinv, Lo
+
+    def tt_cholqr_pass(self, A: torch.Tensor, Rinv: Optional[torch.Tensor] = None,
+                       trans: bool = False, want_q: bool = True, want_g: bool = True):
+        """One fused CholeskyQR pass: (Q = op(A) Rinv, G = Q^T Q); op(A) = A or A^T
+        (A column-major), Rinv None means Q = op(A)."""
+        L = load_library()
+        assert A.stride(0) == 1 and A.dtype == torch.float64
+        m, n = (A.shape[1], A.shape[0]) if trans else A.shape
+        if Rinv is not None:
+            assert Rinv.stride(0) == 1 and Rinv.stride(1) == n and Rinv.shape == (n, n)
+        Q = torch.empty((n, m), dtype=torch.float64, device=A.device).t() if want_q else None
+        G = torch.empty((n, n), dtype=torch.float64, device=A.device).t() if want_g else None
+        _check(L.tt_cholqr_pass(self.handle, m, n, A.data_ptr(), A.stride(1), int(trans),
+                                Rinv.data_ptr() if Rinv is not None else None,
+                                Q.data_ptr() if Q is not None else None, m,
+                                G.data_ptr() if G is not None else None))
+        return Q, G
 
     def tt_svd_nov(self, A: torch.Tensor):
         """V-free one-sided Jacobi (the truncation's SVD): (U Sigma, sigma)."""

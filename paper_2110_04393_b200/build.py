@@ -15,7 +15,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
          "--expt-relaxed-constexpr", "-I/usr/include"] + os.environ.get("TTR_EXTRA_FLAGS", "").split()
-SOURCES = ["api.cu", "gemm.cu", "linalg.cu", "svd.cu", "comm.cu", "fused.cu", "pgemm.cu"]
+SOURCES = ["api.cu", "gemm.cu", "linalg.cu", "svd.cu", "comm.cu", "fused.cu", "pgemm.cu", "cqr.cu"]
 
 
 def _compile(src):

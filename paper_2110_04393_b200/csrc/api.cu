@@ -140,6 +140,7 @@ void destroy_side(Ctx& c) {
   Ctx& x = *c.side;
   cudaStreamSynchronize(x.stream);
   x.gemm_ws.release();
+  x.cqr_ws.release();
   x.scratch.release();
   x.flags.p = nullptr;
   cudaStreamSynchronize(x.stream);
@@ -815,6 +816,16 @@ int read_flags(Ctx& c, int* h, int n) {
   return TT_OK;
 }
 
+// status word 3, bit 2: a Cholesky saw a Gram with a non-finite trace (NaN/Inf in
+// the summands, or an overflow in their contractions)
+int check_finite(const int* fl) {
+  if (fl[3] & 4) {
+    set_error("non-finite values (NaN/Inf in the input cores, or overflow in their contractions)");
+    return TT_ERR_NONFINITE;
+  }
+  return TT_OK;
+}
+
 int make_zero(Ctx& c, const std::vector<int64_t>& dims, tt_tensor& out) {
   const int d = int(dims.size());
   out.d = d;
@@ -997,6 +1008,7 @@ int round_sum_impl(tt_ctx* c, int S, const tt_view* terms, const tt_round_opts* 
     for (int n = 1; n < d; ++n) capped |= l[n] < cur;
     int fl[4];
     TTR_TRY(read_flags(*c, fl, 4));
+    TTR_TRY(check_finite(fl));
     if (fl[2]) {   // zero sum (R16)
       TTR_TRY(make_zero(*c, dims, *out));
       out->flags = TT_FLAG_ZERO | (capped ? TT_FLAG_RANK_CAPPED : 0);
@@ -1047,6 +1059,7 @@ int round_sum_impl(tt_ctx* c, int S, const tt_view* terms, const tt_round_opts* 
   tm.finish();
   int fl[4];
   TTR_TRY(read_flags(*c, fl, 4));
+  TTR_TRY(check_finite(fl));
   if (fl[3] & 1) {
     set_error("QR breakdown even after the Householder fallback");
     return TT_ERR_NUMERIC;
@@ -1177,6 +1190,7 @@ int two_sided_impl(tt_ctx* c, int S, const tt_view* terms, int64_t ell, int64_t 
     ~SideGuard() {
       if (x.stream) cudaStreamSynchronize(x.stream);
       x.gemm_ws.release();
+      x.cqr_ws.release();
       x.flags.p = nullptr;   // borrowed from the main context
       if (x.stream) cudaStreamDestroy(x.stream);
       x.stream = nullptr;
@@ -1400,6 +1414,7 @@ int two_sided_impl(tt_ctx* c, int S, const tt_view* terms, int64_t ell, int64_t 
   tm.finish();
   int fl[4];
   TTR_TRY(read_flags(C, fl, 4));
+  TTR_TRY(check_finite(fl));
   if (fl[3] & 1) {
     set_error("QR breakdown in the two-sided bond factorisation");
     return TT_ERR_NUMERIC;
@@ -1612,6 +1627,7 @@ int deterministic_impl(tt_ctx* c, int S, const tt_view* terms, const tt_round_op
   tm.end(6);
   TTR_CUDA(cudaStreamSynchronize(s));
   tm.finish();
+  TTR_TRY(check_finite(fl));
   if (fl[3] & 1) {
     set_error("QR breakdown even after the Householder fallback");
     return TT_ERR_NUMERIC;
@@ -2356,6 +2372,7 @@ int ctx_destroy_impl(tt_ctx* c) {
     destroy_side(*c);
     nccl_comm_destroy(*c);
     c->gemm_ws.release();
+    c->cqr_ws.release();
     c->scratch.release();
     if (c->flags.p) cudaFreeAsync(c->flags.p, c->stream);
     c->flags.p = nullptr;
@@ -2664,6 +2681,20 @@ int tt_cholesky(tt_ctx_t c, int64_t n, const double* G, int64_t m, int shifted, 
       set_error("tt_cholesky: a pivot is not positive and finite");
       return TT_ERR_NUMERIC;
     }
+    return TT_OK;
+  });
+}
+
+int tt_cholqr_pass(tt_ctx_t c, int64_t m, int64_t n, const double* A, int64_t lda, int trans,
+                   const double* Rinv, double* Q, int64_t ldq, double* G) {
+  if (!c || !A || (!Q && !G) || !cqr_fits(n) || m < 0) {
+    set_error("tt_cholqr_pass: bad arguments (need A, Q or G, 1 <= n <= 144, m >= 0)");
+    return TT_ERR_ARG;
+  }
+  return guarded([&]() -> int {
+    TTR_CUDA(cudaSetDevice(c->device));
+    TTR_TRY(cqr_pass(*c, m, int(n), A, lda, trans != 0, Rinv, Q, ldq, G, c->stream));
+    TTR_CUDA(cudaStreamSynchronize(c->stream));
     return TT_OK;
   });
 }

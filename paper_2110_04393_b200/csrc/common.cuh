@@ -146,6 +146,8 @@ struct Ctx {
   DBuf scratch;
   // split-K partials of the GEMMs
   DBuf gemm_ws;
+  // per-CTA partial Grams of the fused CholeskyQR passes (cqr.cu)
+  DBuf cqr_ws;
   // device status words, see linalg.cu (route flags 0/4/5, sticky 1-3, counters 8-13)
   IBuf flags;
   int nflags = 0;
@@ -221,6 +223,16 @@ int pgemm(Ctx& c, const GemmDesc* d, int nb, cudaStream_t s);
 int proj_carry(Ctx& c, int64_t m, int l, int sumR, const double* Q, const double* Xn, double* M,
                int S, const double* const* Y1, const int64_t* Rj, const int64_t* Nj,
                const int64_t* moff, double* X1, const int64_t* xoff, cudaStream_t s);
+
+// ---------------------------------------------------------------- CholeskyQR pass
+// One persistent launch (cqr.cu): Q = op(A) Rinv (Rinv n x n upper, ld n; nullptr:
+// Q = op(A)), written to Q (m x n, ld ldq) unless Q == nullptr, and G = Q^T Q
+// (n x n, both triangles, ld n) unless G == nullptr.  op(A) = A (m x n, ld lda) or,
+// trans, A^T (A n x m, ld lda).  n <= 160 (cqr_fits).  Gated like gemm().
+bool cqr_fits(int64_t n);
+int cqr_pass(Ctx& c, int64_t m, int n, const double* A, int64_t lda, bool trans,
+             const double* Rinv, double* Q, int64_t ldq, double* G, cudaStream_t s,
+             const int* gate = nullptr, int gate_val = 0);
 
 // ---------------------------------------------------------------- sketch
 int philox_fill(Ctx& c, double* out, int64_t count, uint64_t seed, uint32_t n,

@@ -215,6 +215,7 @@ __global__ void __launch_bounds__(kCholThreads)
     for (int i = tid; i < n; i += 32) tr += G[i + int64_t(i) * n];
     for (int o = 16; o; o >>= 1) tr += __shfl_xor_sync(0xffffffffu, tr, o);
     if (tid == 0) {
+      if (!isfinite(tr)) atomicOr(&flags[3], 4);   // NaN/Inf in the input (TT_ERR_NONFINITE)
       if (!(tr > 0.0)) {
         if (tr == 0.0) { atomicOr(&flags[2], 1); s_zero = 1; }   // Y_n == 0: zero sum (R16)
         s_bad = 1;
@@ -384,6 +385,7 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
       dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
     }
     if (tid == 0) {
+      if (!isfinite(tr)) atomicOr(&flags[3], 4);   // NaN/Inf in the input (TT_ERR_NONFINITE)
       if (!(tr > 0.0)) {
         if (tr == 0.0) { atomicOr(&flags[2], 1); s_zero = 1; }   // Y_n == 0: zero sum (R16)
         s_bad = 1;
@@ -1005,6 +1007,7 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
       dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
     }
     if (tid == 0) {
+      if (!isfinite(tr)) atomicOr(&flags[3], 4);   // NaN/Inf in the input (TT_ERR_NONFINITE)
       if (!(tr > 0.0)) {
         if (tr == 0.0) { atomicOr(&flags[2], 1); s_zero = 1; }   // Y_n == 0: zero sum (R16)
         s_bad = 1;
@@ -1698,6 +1701,36 @@ int qr(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, bool trans, d
     gated_copy_kernel<<<copy_blocks, 256, 0, s>>>(src, dst, int64_t(m) * n, gate, gv);
     return launched();
   };
+  // one CholeskyQR pass as one persistent launch (cqr.cu): dst = src R^{-1} and
+  // its Gram, src = op(A) (first) or a previous Q (m x n, ld m); TTR_NO_CQR=1
+  // selects the two-GEMM form (A/B)
+  static const bool no_cqr = getenv("TTR_NO_CQR") != nullptr;
+  const bool use_cqr = !no_cqr && cqr_fits(ni);
+  auto first_pass = [&](double* dst, const int* gate, int gv) -> int {   // Q1 = op(A) R^{-1}, G(Q1)
+    if (!use_cqr) {
+      TTR_TRY(input_times_rinv(dst, gate, gv));
+      return gram(dst, gate, gv);
+    }
+    TTR_TRY(cqr_pass(c, m, ni, A, lda, trans, Rinv.p, dst, m, Gm.p, s, gate, gv));
+    return reduce_gram();
+  };
+  auto next_pass = [&](const double* src, double* dst, const int* gate, int gv) -> int {
+    if (!use_cqr) {
+      TTR_TRY(times_rinv(src, dst, gate, gv));
+      return gram(dst, gate, gv);
+    }
+    TTR_TRY(cqr_pass(c, m, ni, src, m, false, Rinv.p, dst, m, Gm.p, s, gate, gv));
+    return reduce_gram();
+  };
+  auto last_q = [&](const double* src, double* dst, const int* gate, int gv) -> int {
+    if (!use_cqr) return times_rinv(src, dst, gate, gv);
+    return cqr_pass(c, m, ni, src, m, false, Rinv.p, dst, m, nullptr, s, gate, gv);
+  };
+  auto input_gram = [&](const int* gate, int gv) -> int {
+    if (!use_cqr || mi == 0) return gram_of_input(gate, gv);
+    TTR_TRY(cqr_pass(c, m, ni, A, lda, trans, nullptr, nullptr, 0, Gm.p, s, gate, gv));
+    return reduce_gram();
+  };
 
   // ---- R only, n <= 160 (the truncation): four CholeskyQR passes, no routes.
   // Passes 1-2 are shifted (shift 11(mn + n(n+1)) u tr G, Fukaya et al.), which
@@ -1708,19 +1741,16 @@ int qr(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, bool trans, d
   // O(u ||A||^2): singular values/vectors of R are those of op(A) to O(u ||A||)
   // (DESIGN.md §QR).
   if (r_only && ni <= 160) {
-    TTR_TRY(gram_of_input(nullptr, 0));
+    TTR_TRY(input_gram(nullptr, 0));
     TTR_TRY(chol(CH_RSHIFT, nullptr, 0));                   // R1 (shifted)
     TTR_TRY(copy_r_first(nullptr, 0));
-    TTR_TRY(input_times_rinv(T1.p, nullptr, 0));            // Q1 = op(A) R1^{-1}
-    TTR_TRY(gram(T1.p, nullptr, 0));
+    TTR_TRY(first_pass(T1.p, nullptr, 0));                  // Q1 = op(A) R1^{-1}, G(Q1)
     TTR_TRY(chol(CH_RSHIFT, nullptr, 0));                   // R2 (shifted)
     TTR_TRY(accumulate_r(nullptr, 0));
-    TTR_TRY(times_rinv(T1.p, T2.p, nullptr, 0));            // Q2 = Q1 R2^{-1}
-    TTR_TRY(gram(T2.p, nullptr, 0));
+    TTR_TRY(next_pass(T1.p, T2.p, nullptr, 0));             // Q2 = Q1 R2^{-1}, G(Q2)
     TTR_TRY(chol(CH_RCLAMP, nullptr, 0));                   // R3 (plain, clamped)
     TTR_TRY(accumulate_r(nullptr, 0));
-    TTR_TRY(times_rinv(T2.p, T1.p, nullptr, 0));            // Q3 = Q2 R3^{-1}
-    TTR_TRY(gram(T1.p, nullptr, 0));
+    TTR_TRY(next_pass(T2.p, T1.p, nullptr, 0));             // Q3 = Q2 R3^{-1}, G(Q3)
     // R4: Q3 is orthonormal to O(u), so its Gram is I + E with ||E|| = O(u) and
     // the first-order factor I + triu(E) (half diagonal) is exact to O(u^2); the
     // full Cholesky runs only when max |E| > 1e-8 (gated on the device)
@@ -1734,47 +1764,41 @@ int qr(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, bool trans, d
   // ---- route 0: CholeskyQR2, accepted when pass 2 finds Q1 close to
   // orthonormal (|diag R2 - 1| <= kDevTol).  The route state F[0] lives on the
   // device; every launch of an inactive route is a no-op.
-  TTR_TRY(gram_of_input(F, 0));                             // pass 1 on the input
+  TTR_TRY(input_gram(F, 0));                                // pass 1 on the input
   TTR_TRY(chol(CH_FIRST, F, 0));
   TTR_TRY(copy_r_first(F, 0));
-  TTR_TRY(input_times_rinv(T1.p, F, 0));                    // Q1 -> T1
-  TTR_TRY(gram(T1.p, F, 0));                                // pass 2
+  TTR_TRY(first_pass(T1.p, F, 0));                          // Q1 -> T1, pass 2 Gram
   TTR_TRY(chol(CH_SECOND, F, 0));
   TTR_TRY(accumulate_r(F, 0));
-  if (!r_only) TTR_TRY(times_rinv(T1.p, Q, F, 0));        // Q = Q1 R2^{-1}
+  if (!r_only) TTR_TRY(last_q(T1.p, Q, F, 0));              // Q = Q1 R2^{-1}
   // ---- route 1: shifted CholeskyQR3 (kappa up to ~1e10)
-  TTR_TRY(gram_of_input(F, 1));
+  TTR_TRY(input_gram(F, 1));
   TTR_TRY(chol(CH_SHIFT, F, 1));
   TTR_TRY(copy_r_first(F, 1));
-  TTR_TRY(input_times_rinv(T1.p, F, 1));                    // Q1 (shifted) -> T1
-  TTR_TRY(gram(T1.p, F, 1));
+  TTR_TRY(first_pass(T1.p, F, 1));                          // Q1 (shifted) -> T1
   TTR_TRY(chol(CH_SPLAIN | (r_only ? kStrict : 0), F, 1));  // -> route 2 if Q1 is still too ill-conditioned
   TTR_TRY(accumulate_r(F, 1));
-  TTR_TRY(times_rinv(T1.p, T2.p, F, 1));
-  TTR_TRY(gram(T2.p, F, 1));
+  TTR_TRY(next_pass(T1.p, T2.p, F, 1));
   TTR_TRY(chol(CH_SLAST, F, 1));
   TTR_TRY(accumulate_r(F, 1));
-  if (!r_only) TTR_TRY(times_rinv(T2.p, Q, F, 1));
+  if (!r_only) TTR_TRY(last_q(T2.p, Q, F, 1));
   // ---- route 2: shifted pass on the input, a second shifted pass on its Q1
   // (kappa up to ~1/u), then CholeskyQR2.  Skipped for R-only QRs, whose hard
   // cases are exactly rank-deficient (TSQR).
   if (!r_only) {
-    TTR_TRY(gram_of_input(F, 2));
+    TTR_TRY(input_gram(F, 2));
     TTR_TRY(chol(CH_SHIFT1B, F, 2));
     TTR_TRY(copy_r_first(F, 2));
-    TTR_TRY(input_times_rinv(T1.p, F, 2));
-    TTR_TRY(gram(T1.p, F, 2));
+    TTR_TRY(first_pass(T1.p, F, 2));
     TTR_TRY(chol(CH_SHIFT2, F, 2));
     TTR_TRY(accumulate_r(F, 2));
-    TTR_TRY(times_rinv(T1.p, T2.p, F, 2));
-    TTR_TRY(gram(T2.p, F, 2));
+    TTR_TRY(next_pass(T1.p, T2.p, F, 2));
     TTR_TRY(chol(CH_S2PLAIN, F, 2));
     TTR_TRY(accumulate_r(F, 2));
-    TTR_TRY(times_rinv(T2.p, T1.p, F, 2));
-    TTR_TRY(gram(T1.p, F, 2));
+    TTR_TRY(next_pass(T2.p, T1.p, F, 2));
     TTR_TRY(chol(CH_S2LAST, F, 2));
     TTR_TRY(accumulate_r(F, 2));
-    TTR_TRY(times_rinv(T1.p, Q, F, 2));
+    TTR_TRY(last_q(T1.p, Q, F, 2));
   } else {
     gated_set_kernel<<<1, 1, 0, s>>>(F, 2, 3);              // route 2 -> 3 (TSQR)
     TTR_TRY(launched());

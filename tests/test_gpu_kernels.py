@@ -226,3 +226,45 @@ def test_jacobi_svd_matches_lapack(ctx, m, n):
     G = AVh.T @ AVh
     assert np.linalg.norm(G - np.diag(np.diag(G))) < 1e-13 * sref[0] ** 2
     assert np.all(np.diff(sh) <= 0)
+
+
+@pytest.mark.parametrize("trans", [False, True])
+@pytest.mark.parametrize("m,n", [(1, 1), (31, 7), (33, 8), (100, 9), (1000, 35), (4097, 70),
+                                 (36864, 144), (36870, 143), (5000, 136), (640, 97), (64, 64)])
+def test_cholqr_pass_matches_fp64_reference(ctx, m, n, trans):
+    """The fused CholeskyQR pass (one launch: Q = op(A) Rinv and G = Q^T Q) against a
+    plain fp64 CPU reference, at ragged chunk counts (m mod 32), ragged column
+    tiles (n mod 8), the kernel's n limit (144), both input layouts, and the
+    Gram-only / Q-only modes; the strictly-lower part of Rinv is garbage on
+    purpose (the kernel must read only the upper triangle)."""
+    g = torch.Generator().manual_seed(m * 1000 + n + int(trans))
+    A = colmajor(n, m, g) if trans else colmajor(m, n, g)
+    opA = A.t().cpu() if trans else A.cpu()
+    Rt = torch.triu(torch.randn((n, n), dtype=torch.float64, generator=g)) + 4 * torch.eye(
+        n, dtype=torch.float64)
+    Rbad = Rt + torch.tril(torch.full((n, n), float("nan"), dtype=torch.float64), -1)
+    Rd = Rbad.t().contiguous().t().cuda()
+    Q, G = ctx.tt_cholqr_pass(A, Rd, trans=trans)
+    Qref = opA @ Rt
+    Gref = Qref.t() @ Qref
+    scale = Qref.abs().max().item() * math.sqrt(n)
+    assert torch.isfinite(Q).all() and torch.isfinite(G).all()
+    assert (Q.cpu() - Qref).abs().max().item() <= 1e-14 * scale * n
+    assert (G.cpu() - Gref).abs().max().item() <= 1e-14 * n * m * Qref.abs().max().item() ** 2 + 1e-300
+    assert torch.equal(G.cpu(), G.cpu().t())        # both triangles, bit-symmetric
+    # Gram only (Q = op(A)) and Q only
+    _, G0 = ctx.tt_cholqr_pass(A, None, trans=trans, want_q=False)
+    G0ref = opA.t() @ opA
+    assert (G0.cpu() - G0ref).abs().max().item() <= 1e-14 * n * m * opA.abs().max().item() ** 2
+    Q1, _ = ctx.tt_cholqr_pass(A, Rd, trans=trans, want_g=False)
+    assert torch.equal(Q1.cpu(), Q.cpu())
+    # deterministic
+    Q2, G2 = ctx.tt_cholqr_pass(A, Rd, trans=trans)
+    assert torch.equal(G2.cpu(), G.cpu()) and torch.equal(Q2.cpu(), Q.cpu())
+
+
+def test_cholqr_pass_rejects_unsupported(ctx):
+    import paper_2110_04393_b200 as P
+    A = torch.zeros((145, 100), dtype=torch.float64, device="cuda").t()
+    with pytest.raises(P.TTError):
+        ctx.tt_cholqr_pass(A, None)

@@ -193,6 +193,25 @@ def test_errors_are_reported(ctx):
         ctx.tt_round_sum(gpu_terms(terms), mode="tol", tol=0.0, oversample=3)
 
 
+@pytest.mark.parametrize("bad", [float("nan"), float("inf")])
+@pytest.mark.parametrize("core", [0, 2])
+def test_nonfinite_input_is_reported(ctx, bad, core):
+    """A NaN/Inf entry in one summand reaches every sketch Gram of the sweep: the
+    call returns TT_ERR_NONFINITE (-4) instead of a tensor of NaNs, and the
+    context stays usable."""
+    import paper_2110_04393_b200 as P
+    w = ttsynth.config3_sum10(d=4, I=12, S=3)
+    terms = [[c.clone() for c in t] for t in w.terms]
+    terms[1][core][0, 1, 0] = bad
+    for mode in (dict(mode="rank", rank=6, oversample=3), dict(mode="tol", tol=1e-6, oversample=8),
+                 dict(mode="sketch_only", rank=6, oversample=3)):
+        with pytest.raises(P.TTError) as e:
+            ctx.tt_round_sum(gpu_terms(terms), seed=2, **mode)
+        assert e.value.code == -4, e.value
+    ok = ctx.tt_round_sum(gpu_terms(w.terms), mode="rank", rank=6, oversample=3, seed=2)
+    assert all(np.isfinite(c).all() for c in ok.numpy())
+
+
 def test_config5_full_size_in_bench_launch_configuration():
     """Config 5 at BASELINE.json's full size (S=32, d=50, I=256, rank 64 per
     summand, sketch 144 -> rank 128), rounded through the C-ABI in the launch

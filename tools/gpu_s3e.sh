@@ -1,0 +1,10 @@
+mkdir -p gpurun_out
+python -m paper_2110_04393_b200.build > /dev/null
+timeout 300 python tools/cqr_bench.py 36864 144 20 2>&1 | tee gpurun_out/s3l_cqr_bench.txt
+timeout 600 python -m pytest tests/test_gpu_kernels.py -x -q --timeout 600 -k "cholqr" > gpurun_out/s3l_kern.log 2>&1; echo "kern rc=$?"; tail -3 gpurun_out/s3l_kern.log
+timeout 600 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:cqr_pass_kernel" -s 3 -c 1 -o gpurun_out/s3l_cqr -f python tools/cqr_bench.py 36864 144 1 > gpurun_out/s3l_ncu.log 2>&1; echo "ncu rc=$?"
+ncu -i gpurun_out/s3l_cqr.ncu-rep --page details --csv > gpurun_out/s3l_cqr_details.csv 2>&1
+ncu -i gpurun_out/s3l_cqr.ncu-rep --page source --csv > gpurun_out/s3l_cqr_source.csv 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:cqr_pass_kernel" -s 11 -c 1 -o gpurun_out/s3l_cqrg -f python tools/cqr_bench.py 36864 144 1 > gpurun_out/s3l_ncug.log 2>&1; echo "ncu rc=$?"
+ncu -i gpurun_out/s3l_cqrg.ncu-rep --page details --csv > gpurun_out/s3l_cqrg_details.csv 2>&1
+ncu -i gpurun_out/s3l_cqrg.ncu-rep --page source --csv > gpurun_out/s3l_cqrg_source.csv 2>&1
