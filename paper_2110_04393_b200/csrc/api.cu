@@ -1480,6 +1480,7 @@ int deterministic_impl(tt_ctx* c, int S, const tt_view* terms, const tt_round_op
   const int d = int(dims.size());
   TTR_CUDA(cudaSetDevice(c->device));
   cudaStream_t s = c->stream;
+  TraceScope trace(s, c->capturing);
   PhaseTimer tm(*c);
   tm.begin(6);
   Terms T;
@@ -1575,9 +1576,8 @@ int deterministic_impl(tt_ctx* c, int S, const tt_view* terms, const tt_round_op
       TTR_TRY(dalloc(AV, size_t(r1) * r1, s));
       if (svd_nov_fits(r1, r1)) {
         TTR_TRY(svd_nov(*c, r1, r1, R.p, r1, AV.p, sig.p, s));              // line 7: R V = U S
-      } else {
-        TTR_TRY(dalloc(V, size_t(r1) * r1, s));
-        TTR_TRY(svd_jacobi(*c, r1, r1, R.p, r1, AV.p, V.p, sig.p, s));
+      } else {   // V is not needed (U_k = (R V)_k / S_k): the grid Jacobi without it
+        TTR_TRY(svd_jacobi_grid(*c, r1, r1, R.p, r1, AV.p, nullptr, sig.p, s));
       }
     } else {
       DBuf Vt;

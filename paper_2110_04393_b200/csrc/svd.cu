@@ -600,6 +600,122 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kJcThreads)
   }
 }
 
+// ------------------------------------------------------------------------
+// Large-n one-sided Jacobi (n > 160: the deterministic baseline's bond factors,
+// NEXT-1, ranks of the assembled sum up to ~1000): the round-robin ordering of
+// the single-CTA jacobi_kernel (linalg.cu) -- same pairs per round, same
+// per-pair arithmetic and convergence test, so the same bits -- but every pair
+// of a round on its own warp across a cooperative grid, W (and V) in global
+// memory (L2-resident: 2.9 MB each for n = 600), one grid barrier per round.
+// The single-CTA kernel processes the ~n/2 pairs of a round with 32 warps out of
+// global memory (about 2.7 s per 600 x 600 SVD with V).
+constexpr int kJgThreads = 256;
+__global__ void __launch_bounds__(kJgThreads)
+    jacobi_grid_kernel(double* __restrict__ W, int m, int n, double* __restrict__ Vw,
+                       double* __restrict__ AV, double* __restrict__ Vout,
+                       double* __restrict__ sigma, double* __restrict__ nrm,
+                       int* __restrict__ rot, int max_sweeps, int* __restrict__ flags) {
+  cg::grid_group grid = cg::this_grid();
+  const int lane = threadIdx.x & 31;
+  const int gw = int((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  const int nwarps = int((gridDim.x * blockDim.x) >> 5);
+  const int np = (n + 1) & ~1;
+  const double tol = double(m) * 0x1p-52;
+  int sweep = 0;
+  bool conv = false;
+  for (; sweep < max_sweeps; ++sweep) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) rot[(sweep + 1) % 3] = 0;
+    int rotated = 0;
+    for (int round = 0; round < np - 1; ++round) {
+      for (int pi = gw; pi < np / 2; pi += nwarps) {
+        int p = (pi == 0) ? 0 : ((pi - 1 + round) % (np - 1)) + 1;
+        int q = ((np - 2 - pi + round) % (np - 1)) + 1;
+        if (p >= n || q >= n) continue;
+        if (p > q) { const int t = p; p = q; q = t; }
+        double* ap = W + int64_t(p) * m;
+        double* aq = W + int64_t(q) * m;
+        double al = 0.0, be = 0.0, ga = 0.0;
+        for (int i = lane; i < m; i += 32) {
+          const double x = ap[i], y = aq[i];
+          al += x * x; be += y * y; ga += x * y;
+        }
+        for (int o = 16; o; o >>= 1) {
+          al += __shfl_xor_sync(0xffffffffu, al, o);
+          be += __shfl_xor_sync(0xffffffffu, be, o);
+          ga += __shfl_xor_sync(0xffffffffu, ga, o);
+        }
+        if (al == 0.0 || be == 0.0 || !(fabs(ga) > tol * sqrt(al) * sqrt(be))) continue;
+        const double zeta = (be - al) / (2.0 * ga);
+        const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+        const double cs = 1.0 / sqrt(1.0 + t * t), sn = cs * t;
+        for (int i = lane; i < m; i += 32) {
+          const double x = ap[i], y = aq[i];
+          ap[i] = cs * x - sn * y;
+          aq[i] = sn * x + cs * y;
+        }
+        if (Vw) {
+          double* vp = Vw + int64_t(p) * n;
+          double* vq = Vw + int64_t(q) * n;
+          for (int i = lane; i < n; i += 32) {
+            const double x = vp[i], y = vq[i];
+            vp[i] = cs * x - sn * y;
+            vq[i] = sn * x + cs * y;
+          }
+        }
+        rotated = 1;
+      }
+      grid.sync();
+    }
+    if (rotated && lane == 0) atomicOr(&rot[sweep % 3], 1);
+    grid.sync();
+    if (rot[sweep % 3] == 0) {
+      conv = true;
+      break;
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (!conv) atomicOr(&flags[3], 2);
+    flags[12] += conv ? sweep + 1 : sweep;
+    flags[13] += 1;
+  }
+  // sigma_j = ||w_j||, sorted descending (stable by index): AV, Vout, sigma
+  for (int j = gw; j < n; j += nwarps) {
+    double s2 = 0.0;
+    for (int i = lane; i < m; i += 32) s2 += W[i + int64_t(j) * m] * W[i + int64_t(j) * m];
+    for (int o = 16; o; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+    if (lane == 0) nrm[j] = sqrt(s2);
+  }
+  grid.sync();
+  for (int j = gw; j < n; j += nwarps) {
+    const double sj = nrm[j];
+    int rank = 0;
+    for (int k = lane; k < n; k += 32) {
+      const double sk = nrm[k];
+      rank += (sk > sj) || (sk == sj && k < j);
+    }
+    for (int o = 16; o; o >>= 1) rank += __shfl_xor_sync(0xffffffffu, rank, o);
+    for (int i = lane; i < m; i += 32) AV[i + int64_t(rank) * m] = W[i + int64_t(j) * m];
+    if (Vout)
+      for (int i = lane; i < n; i += 32) Vout[i + int64_t(rank) * n] = Vw[i + int64_t(j) * n];
+    if (lane == 0) sigma[rank] = sj;
+  }
+}
+
+__global__ void jg_init_kernel(const double* __restrict__ A, int64_t lda, int m, int n,
+                               double* __restrict__ W, double* __restrict__ Vw) {
+  const int64_t mn = int64_t(m) * n, nn = int64_t(n) * n;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < mn + (Vw ? nn : 0);
+       e += int64_t(gridDim.x) * blockDim.x) {
+    if (e < mn) {
+      const int64_t i = e % m, j = e / m;
+      W[e] = A[i + j * lda];
+    } else {
+      const int64_t f = e - mn;
+      Vw[f] = (f % n == f / n) ? 1.0 : 0.0;
+    }
+  }
+}
+
 }  // namespace
 
 bool svd_cluster_fits(int64_t m, int64_t n) {
@@ -634,6 +750,45 @@ int svd_nov_cluster(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, 
   else
     jacobi_cluster_kernel<true><<<kCl, kJcThreads, shm, s>>>(A, lda, int(m), int(n), gpc, AV,
                                                                sigma, 40, c.flags.p);
+  return launched();
+}
+
+// Grid-cooperative one-sided Jacobi (large n): AV = U Sigma (m x n, ld m, sorted),
+// sigma, and, if V != nullptr, V (n x n, ld n).
+int svd_jacobi_grid(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, double* AV,
+                    double* V, double* sigma, cudaStream_t s) {
+  if (m < n || n < 1) {
+    set_error("svd_jacobi_grid: need m >= n >= 1");
+    return TT_ERR_ARG;
+  }
+  DBuf W, Vw, nrm;
+  IBuf rot;
+  TTR_TRY(dalloc(W, size_t(m) * n, s));
+  if (V) TTR_TRY(dalloc(Vw, size_t(n) * n, s));
+  TTR_TRY(dalloc(nrm, size_t(n), s));
+  TTR_TRY(ialloc(rot, 3, s));
+  TTR_CUDA(cudaMemsetAsync(rot.p, 0, 3 * sizeof(int), s));
+  jg_init_kernel<<<c.sm_count * 4, 256, 0, s>>>(A, lda, int(m), int(n), W.p, V ? Vw.p : nullptr);
+  TTR_TRY(launched());
+  // one warp per pair of a round (n/2 pairs), at most one CTA per SM
+  const int warps = kJgThreads / 32;
+  int per_sm = 0;
+  TTR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jacobi_grid_kernel, kJgThreads, 0));
+  if (per_sm < 1) {
+    set_error("svd_jacobi_grid: kernel cannot be resident");
+    return TT_ERR_CUDA;
+  }
+  const int want = int(((n + 1) / 2 + warps - 1) / warps);
+  const int blocks = std::max(1, std::min(want, c.sm_count));   // per_sm >= 1 checked above
+  double* Wp = W.p;
+  double* Vwp = V ? Vw.p : nullptr;
+  int mi = int(m), ni = int(n), maxs = 40;
+  double* np_ = nrm.p;
+  int* rp = rot.p;
+  int* fl = c.flags.p;
+  void* args[] = {&Wp, &mi, &ni, &Vwp, &AV, &V, &sigma, &np_, &rp, &maxs, &fl};
+  TTR_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(jacobi_grid_kernel),
+                                       dim3(blocks), dim3(kJgThreads), args, 0, s));
   return launched();
 }
 

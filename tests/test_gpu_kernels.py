@@ -210,8 +210,11 @@ def test_cholesky_shifted_and_breakdown(ctx):
     assert e.value.code == -8
 
 
-@pytest.mark.parametrize("m,n", [(5, 5), (144, 144), (70, 33), (300, 80), (33, 33)])
+@pytest.mark.parametrize("m,n", [(5, 5), (144, 144), (70, 33), (300, 80), (33, 33), (400, 241),
+                                 (600, 600)])
 def test_jacobi_svd_matches_lapack(ctx, m, n):
+    """V-accumulating one-sided Jacobi against LAPACK; m n > 26624 (the last two
+    shapes) runs on the cooperative-grid kernel (one warp per pair of a round)."""
     rng = np.random.default_rng(m * n)
     A = rng.standard_normal((m, n)) * np.logspace(0, -8, n)[None, :]
     Ad = torch.from_numpy(A).cuda().t().contiguous().t()
@@ -224,7 +227,8 @@ def test_jacobi_svd_matches_lapack(ctx, m, n):
     assert np.linalg.norm(A @ Vh - AVh) < 1e-13 * np.linalg.norm(A)
     # AV has orthogonal columns with norms sigma
     G = AVh.T @ AVh
-    assert np.linalg.norm(G - np.diag(np.diag(G))) < 1e-13 * sref[0] ** 2
+    # (each pair is left with |cos| <= m u: the off-diagonal mass grows with m and n)
+    assert np.linalg.norm(G - np.diag(np.diag(G))) < 1e-13 * max(1.0, n / 100) * sref[0] ** 2
     assert np.all(np.diff(sh) <= 0)
 
 
