@@ -1518,6 +1518,12 @@ int deterministic_impl(tt_ctx* c, int S, const tt_view* terms, const tt_round_op
     }
   }
   // ---- Alg. 1, n = d .. 2
+  // The assembled sum is typically exactly rank-deficient (rank sum_j R_j above
+  // the sum's rank): every CholeskyQR route would break down and fall back to
+  // the one-CTA Householder QR, so these QRs take the clamped passes
+  // (robust_q, DESIGN.md NEXT-1); TTR_DET_ROUTES=1 keeps the routed QR (A/B)
+  static const bool det_routes = getenv("TTR_DET_ROUTES") != nullptr;
+  const bool robust = !det_routes;
   tm.begin(3);
   for (int n = d; n >= 2; --n) {
     const int64_t r0 = r[n - 1], In = dims[n - 1], r1 = r[n], mrow = In * r1;
@@ -1527,7 +1533,8 @@ int deterministic_impl(tt_ctx* c, int S, const tt_view* terms, const tt_round_op
       DBuf Q, R;
       TTR_TRY(dalloc(Q, size_t(mrow) * r0, s));
       TTR_TRY(dalloc(R, size_t(r0) * r0, s));
-      TTR_TRY(qr(*c, mrow, r0, X->bufs[n - 1].p, r0, true, Q.p, R.p, s));   // qr(H(X_n)^T)
+      TTR_TRY(qr(*c, mrow, r0, X->bufs[n - 1].p, r0, true, Q.p, R.p, s, false, 0,
+                 robust));                                                   // qr(H(X_n)^T)
       TTR_TRY(dalloc(newn, size_t(r0) * mrow, s));
       TTR_TRY(transpose(*c, Q.p, mrow, r0, mrow, newn.p, r0, s));           // H(X_n) = Q^T
       TTR_TRY(dalloc(newp, size_t(mp) * r0, s));
@@ -1572,7 +1579,7 @@ int deterministic_impl(tt_ctx* c, int S, const tt_view* terms, const tt_round_op
     if (!wide) {
       TTR_TRY(dalloc(Q, size_t(m) * r1, s));
       TTR_TRY(dalloc(R, size_t(r1) * r1, s));
-      TTR_TRY(qr(*c, m, r1, X->bufs[n - 1].p, m, false, Q.p, R.p, s));     // line 6
+      TTR_TRY(qr(*c, m, r1, X->bufs[n - 1].p, m, false, Q.p, R.p, s, false, 0, robust));   // line 6
       TTR_TRY(dalloc(AV, size_t(r1) * r1, s));
       if (svd_nov_fits(r1, r1)) {
         TTR_TRY(svd_nov(*c, r1, r1, R.p, r1, AV.p, sig.p, s));              // line 7: R V = U S

@@ -250,8 +250,13 @@ int philox_fill_slab(Ctx& c, double* out, int64_t r0, int64_t I_loc, int64_t r1,
 // fallback.
 // dist: the m rows are this rank's share of mglob rows (mode-slab sharding): every
 // Gram is all-reduced over the ranks before its Cholesky (no Householder fallback).
+// robust_q (the deterministic baseline's Alg. 1 / Alg. 2 QRs of the assembled,
+// typically exactly rank-deficient sum): the R-only path's four clamped passes
+// and Q = op(A) R^{-1} from the last one -- A = QR to working precision, Q
+// orthonormal except along numerically null directions (R's rows there are at
+// the clamp level), no Householder fallback.
 int qr(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, bool trans, double* Q,
-       double* R, cudaStream_t s, bool dist = false, int64_t mglob = 0);
+       double* R, cudaStream_t s, bool dist = false, int64_t mglob = 0, bool robust_q = false);
 // One-sided Jacobi SVD of the m x n (m >= n) matrix A (ld lda): AV = U Sigma
 // (m x n, ld m), V (n x n, ld n), sigma (n) sorted descending.
 int svd_jacobi(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, double* AV,

@@ -116,7 +116,7 @@ int philox_fill(Ctx& c, double* out, int64_t count, uint64_t seed, uint32_t n, u
 // ============================================================== Cholesky + inverse
 namespace {
 
-constexpr int kCholThreads = 1024;
+constexpr int kCholThreads = 512;   // generic (n > 160) Cholesky: 128 registers for the inverse's column
 constexpr int kSmemLimitDoubles = 26 * 1024;   // 208 KB of dynamic shared memory
 
 // flags layout (Ctx.flags; see common.cuh):
@@ -205,16 +205,25 @@ __global__ void __launch_bounds__(kCholThreads)
   extern __shared__ double sh[];
   const bool in_smem = (n * n <= kSmemLimitDoubles);
   double* L = in_smem ? sh : gwork;
-  __shared__ double s_shift;
+  __shared__ double s_shift, s_tau;
   __shared__ int s_bad, s_zero;
   const int tid = threadIdx.x;
   if (tid == 0) { s_bad = 0; s_zero = 0; }
-  // trace for the shift and the zero test
+  // trace for the shift and the zero test; max diagonal for the clamp level
   if (tid < 32) {
-    double tr = 0.0;
-    for (int i = tid; i < n; i += 32) tr += G[i + int64_t(i) * n];
-    for (int o = 16; o; o >>= 1) tr += __shfl_xor_sync(0xffffffffu, tr, o);
+    double tr = 0.0, dmx = 0.0;
+    for (int i = tid; i < n; i += 32) {
+      tr += G[i + int64_t(i) * n];
+      dmx = fmax(dmx, G[i + int64_t(i) * n]);
+    }
+    for (int o = 16; o; o >>= 1) {
+      tr += __shfl_xor_sync(0xffffffffu, tr, o);
+      dmx = fmax(dmx, __shfl_xor_sync(0xffffffffu, dmx, o));
+    }
     if (tid == 0) {
+      // CH_RCLAMP: a pivot below tau = 64 n u max diag G (a numerically null
+      // direction) is clamped to tau, as in the blocked kernels
+      s_tau = ((mode & 0xff) == CH_RCLAMP) ? 64.0 * n * 0x1p-53 * dmx : 0.0;
       if (!isfinite(tr)) atomicOr(&flags[3], 4);   // NaN/Inf in the input (TT_ERR_NONFINITE)
       if (!(tr > 0.0)) {
         if (tr == 0.0) { atomicOr(&flags[2], 1); s_zero = 1; }   // Y_n == 0: zero sum (R16)
@@ -233,22 +242,48 @@ __global__ void __launch_bounds__(kCholThreads)
     L[e] = (i >= j) ? G[e] + ((i == j) ? shift : 0.0) : 0.0;
   }
   __syncthreads();
-  // right-looking Cholesky, lower L in column-major L[i + j n]
-  for (int j = 0; j < n; ++j) {
-    const double djj = L[j + j * n];
-    const bool okp = djj > 0.0 && isfinite(djj);
-    const double d = okp ? sqrt(djj) : 1.0;
-    if (!okp && tid == 0) s_bad = 1;
-    const double inv = 1.0 / d;
-    for (int i = j + 1 + tid; i < n; i += kCholThreads) L[i + j * n] *= inv;
-    __syncthreads();
-    if (tid == 0) L[j + j * n] = d;
-    const int rem = n - j - 1;
-    for (int e = tid; e < rem * rem; e += kCholThreads) {
-      const int r = e % rem, cc = e / rem;
-      if (cc <= r) {
-        const int i = j + 1 + r, k = j + 1 + cc;
-        L[i + k * n] -= L[i + j * n] * L[k + j * n];
+  // right-looking Cholesky, lower L in column-major L[i + j n], in panels of 8
+  // columns: the panel is factored column by column, then the trailing lower
+  // part takes the panel's 8 rank-1 updates in one pass (each L(i, k) read and
+  // written once per panel instead of once per column; one warp per column,
+  // lanes over rows: coalesced).  The subtractions happen in the same order as
+  // column by column, so the bits are those of the unblocked algorithm.
+  const int warp0 = tid >> 5, lane0 = tid & 31;
+  constexpr int kNW = kCholThreads / 32;
+  for (int j0 = 0; j0 < n; j0 += 8) {
+    const int jw = min(8, n - j0);
+    for (int jj = 0; jj < jw; ++jj) {
+      const int j = j0 + jj;
+      double djj = L[j + j * n];
+      // a clamped (numerically null) direction is also decoupled: its column
+      // below the pivot is zeroed, so rounding-level couplings divided by
+      // sqrt(tau) cannot grow through the later pivots (with hundreds of null
+      // directions -- a rank-deficient assembled sum -- they overflowed)
+      const bool clj = s_tau > 0.0 && isfinite(djj) && !(djj > s_tau);
+      if (clj) djj = s_tau;
+      const bool okp = djj > 0.0 && isfinite(djj);
+      const double d = okp ? sqrt(djj) : 1.0;
+      if (!okp && tid == 0) s_bad = 1;
+      const double inv = clj ? 0.0 : 1.0 / d;
+      for (int i = j + 1 + tid; i < n; i += kCholThreads) L[i + j * n] *= inv;
+      __syncthreads();
+      if (tid == 0) L[j + j * n] = d;
+      for (int k = j + 1 + warp0; k < j0 + jw; k += kNW) {   // the rest of the panel
+        const double lkj = L[k + j * n];
+        for (int i = k + lane0; i < n; i += 32) L[i + k * n] -= L[i + j * n] * lkj;
+      }
+      __syncthreads();
+    }
+    for (int k = j0 + jw + warp0; k < n; k += kNW) {         // trailing part
+      double lk[8];
+#pragma unroll
+      for (int jj = 0; jj < 8; ++jj) lk[jj] = (jj < jw) ? L[k + (j0 + jj) * n] : 0.0;
+      for (int i = k + lane0; i < n; i += 32) {
+        double acc = L[i + k * n];
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj)
+          if (jj < jw) acc -= L[i + (j0 + jj) * n] * lk[jj];
+        L[i + k * n] = acc;
       }
     }
     __syncthreads();
@@ -1594,7 +1629,7 @@ static int launch_chol(Ctx& c, const double* Gm, int n, int64_t m, int mode, dou
 }
 
 int qr(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, bool trans, double* Q,
-       double* R, cudaStream_t s, bool dist, int64_t mglob) {
+       double* R, cudaStream_t s, bool dist, int64_t mglob, bool robust_q) {
   if (mglob <= 0) mglob = m;
   if ((!dist && m < n) || mglob < n || n < 1 || m < 0) {
     set_error("qr: need m >= n >= 1 (m=%lld n=%lld)", (long long)mglob, (long long)n);
@@ -1763,6 +1798,29 @@ int qr(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, bool trans, d
     TTR_TRY(launched());
     TTR_TRY(chol(CH_RCLAMP, F + kNearIdFlag, 1));           // R4 (plain, clamped), if needed
     TTR_TRY(accumulate_r(nullptr, 0));
+    TTR_CUDA(cudaMemcpyAsync(R, Racc.p, sizeof(double) * n * n, cudaMemcpyDeviceToDevice, s));
+    return TT_OK;
+  }
+  // ---- robust Q (deterministic baseline, see common.cuh): the passes of the
+  // R-only path with the full clamped Cholesky for pass 4 and Q = Q3 R4^{-1}
+  if (robust_q && !r_only && !dist) {
+    if (!R) {
+      set_error("qr: robust_q needs R");
+      return TT_ERR_ARG;
+    }
+    TTR_TRY(input_gram(nullptr, 0));
+    TTR_TRY(chol(CH_RSHIFT, nullptr, 0));
+    TTR_TRY(copy_r_first(nullptr, 0));
+    TTR_TRY(first_pass(T1.p, nullptr, 0));
+    TTR_TRY(chol(CH_RSHIFT, nullptr, 0));
+    TTR_TRY(accumulate_r(nullptr, 0));
+    TTR_TRY(next_pass(T1.p, T2.p, nullptr, 0));
+    TTR_TRY(chol(CH_RCLAMP, nullptr, 0));
+    TTR_TRY(accumulate_r(nullptr, 0));
+    TTR_TRY(next_pass(T2.p, T1.p, nullptr, 0));
+    TTR_TRY(chol(CH_RCLAMP, nullptr, 0));
+    TTR_TRY(accumulate_r(nullptr, 0));
+    TTR_TRY(last_q(T1.p, Q, nullptr, 0));
     TTR_CUDA(cudaMemcpyAsync(R, Racc.p, sizeof(double) * n * n, cudaMemcpyDeviceToDevice, s));
     return TT_OK;
   }

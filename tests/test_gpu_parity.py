@@ -269,6 +269,16 @@ def test_deterministic_sum_large_ranks(ctx):
     run_det(ctx, w.terms, tol=1e-9)
 
 
+def test_deterministic_config3_full_size(ctx):
+    """Config 3 at full size (S = 10, d = 20, I = 100, assembled rank 600 > 160,
+    exactly rank-deficient: the true bond rank is 150): Alg. 1 + 2 on the
+    assembled sum through the clamped-pass QRs (robust_q), the grid Jacobi and
+    the generic Cholesky, against the oracle's tt_round(tt_add(...)) (LAPACK QR
+    and SVD), rank 60 as in the randomized line."""
+    w = ttsynth.config3_sum10()
+    run_det(ctx, w.terms, rank=w.rank)
+
+
 def test_deterministic_matches_randomized_when_sketch_is_exact(ctx):
     # rank-r truncation of an exactly low-rank sum: both roundings give the best
     # approximation (P:653-663 with l >= true rank), hence the same tensor
