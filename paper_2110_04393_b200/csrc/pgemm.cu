@@ -19,7 +19,7 @@ namespace ttr {
 namespace {
 
 #ifndef TTR_PG_STAGES
-#define TTR_PG_STAGES 3
+#define TTR_PG_STAGES 4
 #endif
 constexpr int pBM = 128, pBN = 48, pBK = 16, pWM = 4, pWN = 2, pST = TTR_PG_STAGES;
 constexpr int pConsumers = pWM * pWN;
