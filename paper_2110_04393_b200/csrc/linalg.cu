@@ -118,6 +118,7 @@ namespace {
 
 constexpr int kCholThreads = 512;   // generic (n > 160) Cholesky: 128 registers for the inverse's column
 constexpr int kSmemLimitDoubles = 26 * 1024;   // 208 KB of dynamic shared memory
+constexpr int kCholTsmDoubles = 225 * 1024 / 8;   // generic Cholesky's T_J staging (+ static smem <= 227 KB)
 
 // flags layout (Ctx.flags; see common.cuh):
 //  0 = route state of the current QR: 0 plain CholeskyQR2, 1 shifted CholeskyQR3,
@@ -192,6 +193,12 @@ __device__ __forceinline__ void route_update(int* flags, int mode, bool bad, dou
   }
 }
 
+__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
 // G (n x n, ld n, symmetric) -> Rinv (upper, ld n) with G + shift*I = R^T R, and
 // optionally L = R^T (lower, ld n).  Shift (CH_SHIFT only) = 11(mn + n(n+1))u * trace(G) (shifted
 // CholeskyQR3, Fukaya et al.).  Runs iff *gate == gate_val.
@@ -205,6 +212,11 @@ __global__ void __launch_bounds__(kCholThreads)
   extern __shared__ double sh[];
   const bool in_smem = (n * n <= kSmemLimitDoubles);
   double* L = in_smem ? sh : gwork;
+  // L in global memory: the dynamic shared memory (if any) stages the blocked
+  // inverse's T_J blocks (32 x 34 doubles per block column, n <= 832)
+  double* Tsm = in_smem ? nullptr : sh;
+  const bool tsm_ok = !in_smem && ((n + 31) / 32) * 32 * 34 <= kCholTsmDoubles;
+  if (!tsm_ok) Tsm = nullptr;
   __shared__ double s_shift, s_tau;
   __shared__ int s_bad, s_zero;
   const int tid = threadIdx.x;
@@ -288,9 +300,95 @@ __global__ void __launch_bounds__(kCholThreads)
     }
     __syncthreads();
   }
+  const int warp = tid >> 5, lane = tid & 31;
+  if (!in_smem && Tsm) {
+    // X = L^{-1} by 32 x 32 blocks on DMMA (L in global memory / L2): the
+    // diagonal blocks' inverses X_II first (one warp each, forward substitution,
+    // lane = column), then block row by block row
+    //   X_IJ = -X_II sum_{K=J}^{I-1} L_IK X_KJ   (J < I),
+    // the sums for all J of a row at once (8 x 8 tiles over the warps, the
+    // fragments of a 32-wide k-block loaded before its 8 DMMAs), staged in shared
+    // memory, then multiplied by X_II.  X is kept transposed in Rinv (Rinv(c, i)
+    // = X(i, c)).  The column-oriented substitution below read all of L once per
+    // column of X (33 ms of a 39 ms call at n = 600).
+    const int nb = (n + 31) / 32;
+    for (int e = tid; e < n * n; e += kCholThreads) {   // Rinv's strictly lower part
+      const int r = e % n, c2 = e / n;
+      if (r > c2) Rinv[e] = 0.0;
+    }
+    for (int I = warp; I < nb; I += kNW) {
+      const int r0 = 32 * I, bs = min(32, n - r0);
+      double x[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) x[i] = (i == lane) ? 1.0 : 0.0;
+#pragma unroll
+      for (int k = 0; k < 32; ++k) {
+        if (k < bs) {
+          const double xk = x[k] / L[(r0 + k) + int64_t(r0 + k) * n];
+          x[k] = xk;
+#pragma unroll
+          for (int i = k + 1; i < 32; ++i)
+            if (i < bs) x[i] -= L[(r0 + i) + int64_t(r0 + k) * n] * xk;
+        }
+      }
+      if (lane < bs)
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          if (i >= lane && i < bs) Rinv[(r0 + lane) + int64_t(r0 + i) * n] = x[i];
+    }
+    __syncthreads();
+    const int g = lane >> 2, t4 = lane & 3;
+    constexpr int kLdT = 34;
+    for (int I = 1; I < nb; ++I) {
+      const int rI = 32 * I;
+      // T_J = sum_{K=J}^{I-1} L_IK X_KJ, J < I: unit = (J, 8 x 8 tile)
+      for (int u = warp; u < I * 16; u += kNW) {
+        const int J = u >> 4, tr = (u >> 2) & 3, tc = u & 3;
+        const int row = rI + 8 * tr + g, col = 32 * J + 8 * tc + g;
+        double c0 = 0.0, c1 = 0.0;
+        for (int K = J; K < I; ++K) {
+          double a[8], b[8];
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) {
+            const int k = 32 * K + 4 * kk + t4;
+            a[kk] = (row < n && k < n) ? L[row + int64_t(k) * n] : 0.0;
+            b[kk] = (col < n && k < n) ? Rinv[col + int64_t(k) * n] : 0.0;   // X(k, col)
+          }
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) dmma884(c0, c1, a[kk], b[kk]);
+        }
+        double* T = Tsm + J * (32 * kLdT);
+        const int rr = 8 * tr + g, cc = 8 * tc + 2 * t4;
+        T[rr + cc * kLdT] = c0;
+        T[rr + (cc + 1) * kLdT] = c1;
+      }
+      __syncthreads();
+      // X_IJ = -X_II T_J
+      for (int u = warp; u < I * 16; u += kNW) {
+        const int J = u >> 4, tr = (u >> 2) & 3, tc = u & 3;
+        const int row = rI + 8 * tr + g;
+        const double* T = Tsm + J * (32 * kLdT);
+        double a[8], b[8];
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const int k = 4 * kk + t4;
+          a[kk] = (row < n && rI + k < n) ? Rinv[(rI + k) + int64_t(row) * n] : 0.0;   // X(row, rI + k)
+          b[kk] = T[k + (8 * tc + g) * kLdT];
+        }
+        double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) dmma884(c0, c1, a[kk], b[kk]);
+        const int col = 32 * J + 8 * tc + 2 * t4;
+        if (row < n) {
+          if (col < n) Rinv[col + int64_t(row) * n] = -c0;
+          if (col + 1 < n) Rinv[(col + 1) + int64_t(row) * n] = -c1;
+        }
+      }
+      __syncthreads();
+    }
+  } else {
   // X = L^{-1} (lower), one warp per column, column-oriented forward substitution;
   // Rinv = X^T (upper).  x lives in registers: lane owns rows lane + 32 q.
-  const int warp = tid >> 5, lane = tid & 31;
   constexpr int kMaxQ = QN;  // n <= 32 * QN
   for (int col = warp; col < n; col += kCholThreads / 32) {
     double x[kMaxQ];
@@ -320,6 +418,8 @@ __global__ void __launch_bounds__(kCholThreads)
       if (i < n) Rinv[col + int64_t(i) * n] = (i >= col) ? x[q] : 0.0;  // Rinv(col, i) = X(i, col)
     }
   }
+  }
+  __syncthreads();
   if (Rout) {
     for (int e = tid; e < n * n; e += kCholThreads) {
       const int i = e % n, j = e / n;     // Lout = R^T (lower)
@@ -358,11 +458,6 @@ constexpr int kBlkThreads = 512;
 #define CHOL_PROF(slot) do { } while (0)
 #endif
 
-__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-               : "+d"(c0), "+d"(c1)
-               : "d"(a), "d"(b));
-}
 
 // leading dimension of the Cholesky working matrix: >= round8(n) + 4 and
 // == 4 (mod 16) doubles, so DMMA fragment loads (8 rows x 4 columns) are
@@ -1590,7 +1685,7 @@ static int launch_chol(Ctx& c, const double* Gm, int n, int64_t m, int mode, dou
   if (!attr_done) {
     TTR_CUDA(cudaFuncSetAttribute(chol_inv_kernel<32>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  kSmemLimitDoubles * 8));
+                                  kCholTsmDoubles * 8));
     TTR_CUDA(cudaFuncSetAttribute(chol_blk_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   220 * 1024));
     TTR_CUDA(cudaFuncSetAttribute(chol_blk_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1622,7 +1717,9 @@ static int launch_chol(Ctx& c, const double* Gm, int n, int64_t m, int mode, dou
     else chol_la_kernel<5><<<1, kBlkThreads, shm, s>>>(Gm, n, m, mode, Rinv, Rk, c.flags.p, gate, gv);
   } else {
     const bool big = n * n > kSmemLimitDoubles;
-    chol_inv_kernel<32><<<1, kCholThreads, big ? 0 : size_t(n) * n * 8, s>>>(
+    const int nbk = (n + 31) / 32;
+    const size_t tsm = (nbk * 32 * 34 <= kCholTsmDoubles) ? size_t(nbk) * 32 * 34 * 8 : 0;
+    chol_inv_kernel<32><<<1, kCholThreads, big ? tsm : size_t(n) * n * 8, s>>>(
         Gm, n, m, mode, Rinv, Rk, gw, c.flags.p, gate, gv);
   }
   return launched();
