@@ -268,7 +268,8 @@ int svd_nov(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, double* 
             double* sigma, cudaStream_t s);
 bool svd_nov_fits(int64_t m, int64_t n);
 // The same one-sided Jacobi as svd_jacobi on a cooperative grid (one warp per
-// pair of a round; same bits), for n > 160; V == nullptr: V is not formed.
+// pair of a round, negligible columns not rotated), for m n > 26624; V ==
+// nullptr: V is not formed.
 int svd_jacobi_grid(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, double* AV,
                     double* V, double* sigma, cudaStream_t s);
 // B(:, c) = AV(:, c) / sigma_c^(halfpow/2), c < k; 0 where sigma_c <= rel_thr sigma_0

@@ -2287,7 +2287,7 @@ int svd_jacobi(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, doubl
     return TT_ERR_ARG;
   }
   // W does not fit in shared memory: every pair of a round on its own warp of a
-  // cooperative grid instead (same pairs, same arithmetic, same bits)
+  // cooperative grid instead (same pairs and arithmetic)
   if (m * n > kSmemLimitDoubles) return svd_jacobi_grid(c, m, n, A, lda, AV, V, sigma, s);
   static std::atomic<bool> attr{false};
   std::unique_lock<std::mutex> init_lock(init_mutex(), std::defer_lock);

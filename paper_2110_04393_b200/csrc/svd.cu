@@ -604,8 +604,8 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kJcThreads)
 // Large-n one-sided Jacobi (n > 160: the deterministic baseline's bond factors,
 // NEXT-1, ranks of the assembled sum up to ~1000): the round-robin ordering of
 // the single-CTA jacobi_kernel (linalg.cu) -- same pairs per round, same
-// per-pair arithmetic and convergence test, so the same bits -- but every pair
-// of a round on its own warp across a cooperative grid, W (and V) in global
+// per-pair arithmetic -- plus the cluster kernel's negligible-column test, every
+// pair of a round on its own warp across a cooperative grid, W (and V) in global
 // memory (L2-resident: 2.9 MB each for n = 600), one grid barrier per round.
 // The single-CTA kernel processes the ~n/2 pairs of a round with 32 warps out of
 // global memory (about 2.7 s per 600 x 600 SVD with V).
@@ -621,6 +621,25 @@ __global__ void __launch_bounds__(kJgThreads)
   const int nwarps = int((gridDim.x * blockDim.x) >> 5);
   const int np = (n + 1) & ~1;
   const double tol = double(m) * 0x1p-52;
+  // ||A||_F^2 (column sums in a fixed order by warp, then by column: nrm[] as
+  // scratch) for the dgesvj-style negligible-column test of the cluster kernel:
+  // columns below 16 m u ||A||_F are not rotated (a rank-deficient bond matrix
+  // -- hundreds of null columns of the assembled sum -- otherwise keeps
+  // re-rotating rounding noise: 25 sweeps instead of ~10)
+  for (int j = gw; j < n; j += nwarps) {
+    double s2 = 0.0;
+    for (int i = lane; i < m; i += 32) s2 += W[i + int64_t(j) * m] * W[i + int64_t(j) * m];
+    for (int o = 16; o; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+    if (lane == 0) nrm[j] = s2;
+  }
+  grid.sync();
+  double fro2 = 0.0;
+  for (int j = lane; j < n; j += 32) fro2 += nrm[j];
+  for (int o = 16; o; o >>= 1) fro2 += __shfl_xor_sync(0xffffffffu, fro2, o);
+  fro2 = __shfl_sync(0xffffffffu, fro2, 0);
+  const double negl = 16.0 * m * 0x1p-53;
+  const double small = negl * negl * fro2;
+  grid.sync();   // nrm[] is reused below
   int sweep = 0;
   bool conv = false;
   for (; sweep < max_sweeps; ++sweep) {
@@ -644,7 +663,7 @@ __global__ void __launch_bounds__(kJgThreads)
           be += __shfl_xor_sync(0xffffffffu, be, o);
           ga += __shfl_xor_sync(0xffffffffu, ga, o);
         }
-        if (al == 0.0 || be == 0.0 || !(fabs(ga) > tol * sqrt(al) * sqrt(be))) continue;
+        if (!(fmin(al, be) > small) || !(fabs(ga) > tol * sqrt(al) * sqrt(be))) continue;
         const double zeta = (be - al) / (2.0 * ga);
         const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
         const double cs = 1.0 / sqrt(1.0 + t * t), sn = cs * t;
