@@ -193,6 +193,17 @@ __device__ __forceinline__ void route_update(int* flags, int mode, bool bad, dou
   }
 }
 
+// generic (n > 163) Cholesky's shared memory: the blocked inverse's T_J staging
+// (32 x 34 per block column) or the factorisation's X_kk (32 x 33) + k-major panel
+__host__ __device__ __forceinline__ int chol_panel_ld(int n) {
+  const int n8 = (n + 7) & ~7;
+  return n8 + ((20 - n8 % 16) % 16);
+}
+__host__ __device__ __forceinline__ int chol_tsm_doubles(int n) {
+  const int a = ((n + 31) / 32) * 32 * 34, b = 32 * 33 + 32 * chol_panel_ld(n);
+  return a > b ? a : b;
+}
+
 __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(c0), "+d"(c1)
@@ -215,7 +226,7 @@ __global__ void __launch_bounds__(kCholThreads)
   // L in global memory: the dynamic shared memory (if any) stages the blocked
   // inverse's T_J blocks (32 x 34 doubles per block column, n <= 832)
   double* Tsm = in_smem ? nullptr : sh;
-  const bool tsm_ok = !in_smem && ((n + 31) / 32) * 32 * 34 <= kCholTsmDoubles;
+  const bool tsm_ok = !in_smem && chol_tsm_doubles(n) <= kCholTsmDoubles;
   if (!tsm_ok) Tsm = nullptr;
   __shared__ double s_shift, s_tau;
   __shared__ int s_bad, s_zero;
@@ -254,14 +265,157 @@ __global__ void __launch_bounds__(kCholThreads)
     L[e] = (i >= j) ? G[e] + ((i == j) ? shift : 0.0) : 0.0;
   }
   __syncthreads();
+  const int warp0 = tid >> 5, lane0 = tid & 31;
+  constexpr int kNW = kCholThreads / 32;
+  if (!in_smem && Tsm) {
+    // ---- L in global memory (n > 163): right-looking, 32-column blocks on DMMA.
+    //  (a) warp 0 factors the diagonal block in registers (lane = row; clamped
+    //      pivots decoupled as below) and forms its inverse X_kk (lane = column),
+    //  (b) the panel L_ik = A_ik X_kk^T on DMMA (rows in 8-row tiles over the
+    //      warps), copied k-major into shared memory,
+    //  (c) the trailing lower 8 x 8 tiles A_ij -= L_ik L_jk^T on DMMA from the
+    //      shared panel (each tile read and written once per block column).
+    // The 8-column panel loop below took 5.9 ms at n = 600 (L2 latency per
+    // rank-1 update pass).
+    double* Xk = Tsm;                          // 32 x 33: X_kk (row j zeroed if clamped)
+    double* Pn = Tsm + 32 * 33;                // panel, k-major: Pn[k * pld + r]
+    const int pld = chol_panel_ld(n);
+    const int g = lane0 >> 2, t4 = lane0 & 3;
+    for (int k0 = 0; k0 < n; k0 += 32) {
+      const int kb = min(32, n - k0);
+      if (warp0 == 0) {
+        const int i = lane0;
+        double a[32];
+#pragma unroll
+        for (int q = 0; q < 32; ++q)
+          a[q] = (i < kb && q <= i && q < kb) ? L[(k0 + i) + int64_t(k0 + q) * n] : 0.0;
+        int bad = 0;
+        unsigned clmask = 0u;
+        double dinv = 1.0;   // 1 / L_ii of this lane's row (for X_kk)
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          if (j < kb) {
+            double piv = __shfl_sync(0xffffffffu, a[j], j);
+            const bool cl = s_tau > 0.0 && isfinite(piv) && !(piv > s_tau);
+            if (cl) piv = s_tau;
+            const bool okp = piv > 0.0 && isfinite(piv);
+            bad |= !okp;
+            const double d = okp ? sqrt(piv) : 1.0;
+            if (cl) clmask |= 1u << j;
+            const double l = (i > j) ? (cl ? 0.0 : a[j] / d) : (i == j ? d : 0.0);
+            a[j] = l;
+            if (i == j) dinv = 1.0 / d;
+#pragma unroll
+            for (int q = j + 1; q < 32; ++q) {
+              const double lq = __shfl_sync(0xffffffffu, l, q);
+              if (q <= i) a[q] -= l * lq;
+            }
+          }
+        }
+        // L_kk back to global (lower), diagonal included
+#pragma unroll
+        for (int q = 0; q < 32; ++q)
+          if (i < kb && q <= i && q < kb) L[(k0 + i) + int64_t(k0 + q) * n] = a[q];
+        if (bad && i == 0) s_bad = 1;
+        // X_kk = L_kk^{-1}: lane c solves column c (x_j for j >= c)
+        double x[32];
+#pragma unroll
+        for (int q = 0; q < 32; ++q) x[q] = (q == i) ? 1.0 : 0.0;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const double djinv = __shfl_sync(0xffffffffu, dinv, j);
+          if (j < kb) {
+            const double xj = x[j] * djinv;
+            x[j] = xj;
+#pragma unroll
+            for (int q = j + 1; q < 32; ++q) {
+              const double lqj = __shfl_sync(0xffffffffu, a[j], q);   // L(q, j) from lane q
+              x[q] -= lqj * xj;
+            }
+          }
+        }
+        // Xk[r * 33 + c] = X(r, c); rows of clamped directions zeroed (their
+        // panel column stays 0)
+#pragma unroll
+        for (int q = 0; q < 32; ++q) Xk[q * 33 + i] = ((clmask >> q) & 1u) ? 0.0 : x[q];
+      }
+      __syncthreads();
+      const int r0 = k0 + kb, nr = n - r0;
+      if (nr > 0) {
+        // (b) panel: rows r0 .. n-1 in 8-row tiles, one warp per tile (all four
+        // column tiles: the tile's A_ik is read before any of it is overwritten)
+        const int rt8 = (nr + 7) / 8;
+        for (int rt = warp0; rt < rt8; rt += kNW) {
+          const int row = r0 + 8 * rt + g;
+          double a[8];
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) {
+            const int kc = 4 * kk + t4;
+            a[kk] = (row < n && kc < kb) ? L[row + int64_t(k0 + kc) * n] : 0.0;
+          }
+          double c[4][2];
+#pragma unroll
+          for (int ct = 0; ct < 4; ++ct) {
+            c[ct][0] = c[ct][1] = 0.0;
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk)
+              dmma884(c[ct][0], c[ct][1], a[kk], Xk[(8 * ct + g) * 33 + 4 * kk + t4]);   // X(c, kc)
+          }
+          __syncwarp();
+          if (row < n) {
+#pragma unroll
+            for (int ct = 0; ct < 4; ++ct)
+#pragma unroll
+              for (int e = 0; e < 2; ++e) {
+                const int col = 8 * ct + 2 * t4 + e;
+                if (col < kb) {
+                  L[row + int64_t(k0 + col) * n] = c[ct][e];
+                  Pn[col * pld + (row - r0)] = c[ct][e];
+                }
+              }
+          }
+        }
+        // zero panel columns past kb (k-range of the trailing DMMAs is 32)
+        for (int e = tid; e < (32 - kb) * nr; e += kCholThreads)
+          Pn[(kb + e / nr) * pld + (e % nr)] = 0.0;
+        __syncthreads();
+        // (c) trailing lower tiles (ti >= tj) of rows/cols r0 .. n-1
+        const int nt = (nr + 7) / 8, ntiles = nt * (nt + 1) / 2;
+        for (int u = warp0; u < ntiles; u += kNW) {
+          int ti = int((sqrtf(8.0f * u + 1.0f) - 1.0f) * 0.5f);
+          while ((ti + 1) * (ti + 2) / 2 <= u) ++ti;
+          while (ti * (ti + 1) / 2 > u) --ti;
+          const int tj = u - ti * (ti + 1) / 2;
+          const int row = r0 + 8 * ti + g, colb = r0 + 8 * tj;
+          const int c2 = colb + 2 * t4;
+          double o0 = 0.0, o1 = 0.0;
+          if (row < n && c2 < n) o0 = L[row + int64_t(c2) * n];
+          if (row < n && c2 + 1 < n) o1 = L[row + int64_t(c2 + 1) * n];
+          double a[8], b[8];
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) {
+            const int kc = 4 * kk + t4;
+            a[kk] = Pn[kc * pld + (8 * ti + g)];   // L(row, k0 + kc)
+            b[kk] = Pn[kc * pld + (8 * tj + g)];   // L(colb + g, k0 + kc)
+          }
+          double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) dmma884(c0, c1, a[kk], b[kk]);
+          if (row < n) {
+            if (c2 < n && c2 <= row) L[row + int64_t(c2) * n] = o0 - c0;
+            if (c2 + 1 < n && c2 + 1 <= row) L[row + int64_t(c2 + 1) * n] = o1 - c1;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  } else {
   // right-looking Cholesky, lower L in column-major L[i + j n], in panels of 8
   // columns: the panel is factored column by column, then the trailing lower
   // part takes the panel's 8 rank-1 updates in one pass (each L(i, k) read and
   // written once per panel instead of once per column; one warp per column,
   // lanes over rows: coalesced).  The subtractions happen in the same order as
   // column by column, so the bits are those of the unblocked algorithm.
-  const int warp0 = tid >> 5, lane0 = tid & 31;
-  constexpr int kNW = kCholThreads / 32;
   for (int j0 = 0; j0 < n; j0 += 8) {
     const int jw = min(8, n - j0);
     for (int jj = 0; jj < jw; ++jj) {
@@ -299,6 +453,7 @@ __global__ void __launch_bounds__(kCholThreads)
       }
     }
     __syncthreads();
+  }
   }
   const int warp = tid >> 5, lane = tid & 31;
   if (!in_smem && Tsm) {
@@ -1717,8 +1872,7 @@ static int launch_chol(Ctx& c, const double* Gm, int n, int64_t m, int mode, dou
     else chol_la_kernel<5><<<1, kBlkThreads, shm, s>>>(Gm, n, m, mode, Rinv, Rk, c.flags.p, gate, gv);
   } else {
     const bool big = n * n > kSmemLimitDoubles;
-    const int nbk = (n + 31) / 32;
-    const size_t tsm = (nbk * 32 * 34 <= kCholTsmDoubles) ? size_t(nbk) * 32 * 34 * 8 : 0;
+    const size_t tsm = (chol_tsm_doubles(n) <= kCholTsmDoubles) ? size_t(chol_tsm_doubles(n)) * 8 : 0;
     chol_inv_kernel<32><<<1, kCholThreads, big ? tsm : size_t(n) * n * 8, s>>>(
         Gm, n, m, mode, Rinv, Rk, gw, c.flags.p, gate, gv);
   }
