@@ -191,6 +191,24 @@ def test_cholesky_factor_and_inverse(ctx, n, cond):
     assert np.linalg.norm(Lh - Lref) <= 1e-12 * math.sqrt(cond) * np.linalg.norm(Lref)
 
 
+@pytest.mark.parametrize("n,rank", [(150, 40), (300, 100), (600, 150)])
+def test_cholesky_rank_deficient_clamped(ctx, n, rank):
+    """shifted = 0 on an exactly rank-deficient Gram (the deterministic baseline's
+    assembled sums): pivots below tau = 64 n u max diag G are clamped (and, in the
+    generic n > 160 kernel, their columns decoupled), so the factor stays finite,
+    L L^T matches G to rounding level, and Rinv L^T = I."""
+    rng = np.random.default_rng(n + rank)
+    B = rng.standard_normal((n, rank))
+    G = B @ B.T
+    Gd = torch.from_numpy(G).cuda().t().contiguous().t()
+    Rinv, L = ctx.tt_cholesky(Gd)
+    Lh, Rh = L.cpu().numpy(), Rinv.cpu().numpy()
+    assert np.isfinite(Lh).all() and np.isfinite(Rh).all()
+    tau = 64 * n * 2.0 ** -53 * np.max(np.diag(G))
+    assert np.linalg.norm(Lh @ Lh.T - G) <= 1e-12 * n * np.linalg.norm(G) + n * tau
+    assert np.linalg.norm(Rh.T @ Lh - np.eye(n)) <= 1e-8 * n
+
+
 def test_cholesky_shifted_and_breakdown(ctx):
     """shifted = 1 factors G + 11 (m n + n (n + 1)) u tr(G) I; an indefinite G
     is reported (TT_ERR_NUMERIC), not returned."""
