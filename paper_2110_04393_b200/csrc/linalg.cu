@@ -1503,11 +1503,6 @@ __global__ void __launch_bounds__(1024)
     double m = 0.0;
     for (int q = 0; q < nw; ++q) m = fmax(m, red[q]);
     flags[slot] = (m > thr || !(m == m)) ? 1 : 0;
-#ifdef TTR_NEARID_PROF
-    // histogram of -log10 max|G - I| (status words 40 + [0, 19]), slot 21: sweep
-    const int b = (m > 0.0) ? min(19, max(0, int(-log10(m)))) : 19;
-    atomicAdd(&flags[(slot == 21 ? 40 : 60) + (slot == 21 ? b : min(b / 5, 3))], 1);
-#endif
   }
 }
 
@@ -2093,12 +2088,6 @@ int qr(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, bool trans, d
   TTR_TRY(chol(CH_SPLAIN | (r_only ? kStrict : 0), F, 1));  // -> route 2 if Q1 is still too ill-conditioned
   TTR_TRY(accumulate_r(F, 1));
   TTR_TRY(next_pass(T1.p, T2.p, F, 1));
-#ifdef TTR_NEARID_PROF
-  if (!r_only) {
-    near_identity_chol_kernel<<<1, 1024, 0, s>>>(Gm.p, ni, Rtmp.p ? Rtmp.p : Rinv.p, F, 21, 1e-8);
-    TTR_TRY(launched());
-  }
-#endif
   TTR_TRY(chol(CH_SLAST, F, 1));
   TTR_TRY(accumulate_r(F, 1));
   if (!r_only) TTR_TRY(last_q(T2.p, Q, F, 1));
