@@ -19,9 +19,12 @@ namespace ttr {
 namespace {
 
 #ifndef TTR_PG_STAGES
-#define TTR_PG_STAGES 4
+#define TTR_PG_STAGES 2
 #endif
-constexpr int pBM = 128, pBN = 48, pBK = 16, pWM = 4, pWN = 2, pST = TTR_PG_STAGES;
+#ifndef TTR_PG_BK
+#define TTR_PG_BK 32
+#endif
+constexpr int pBM = 128, pBN = 48, pBK = TTR_PG_BK, pWM = 4, pWN = 2, pST = TTR_PG_STAGES;
 constexpr int pConsumers = pWM * pWN;
 constexpr int pThreads = (pConsumers + 1) * 32;
 constexpr int pTM = pBM / pWM, pTN = pBN / pWN;      // warp tile 32 x 24
