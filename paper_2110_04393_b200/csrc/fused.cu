@@ -32,7 +32,7 @@ namespace ttr {
 
 namespace {
 
-constexpr int kBM = 48, kBN = 128, kBK = 16, kWM = 2, kWN = 4, kST = 4;
+constexpr int kBM = 48, kBN = 128, kBK = 32, kWM = 2, kWN = 4, kST = 2;
 constexpr int kConsumers = kWM * kWN;                  // MMA warps
 constexpr int kThreads = (kConsumers + 1) * 32;         // + one TMA producer warp
 constexpr int kTM = kBM / kWM, kTN = kBN / kWN;        // warp tile 24 x 32
