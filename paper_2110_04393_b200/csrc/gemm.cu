@@ -678,13 +678,13 @@ int launch_cfg(Ctx& c, GemmParams& P, int maxM, int maxN, int maxK, cudaStream_t
 }
 
 // tile shapes (DESIGN.md §Kernels / K2): BM, BN, BK, warps_m, warps_n, stages
-using TallS = Shape<128, 48, 16, 4, 2, 4>;   // M >> N ~ l (phase-1 Z, Y_n, Q = Y R^-1)
-using WideS = Shape<48, 128, 16, 2, 4, 4>;   // N >> M ~ l (carry M^(j) H(T), projection)
-using SqS = Shape<64, 64, 16, 2, 2, 4>;      // general / split-K
-using RowS = Shape<64, 48, 16, 4, 2, 4>;     // M = R = 64, N = l = 144 (phase-1 W, split-K)
-using GramS = Shape<48, 48, 16, 2, 2, 4>;    // l x l Grams (split-K)
+using TallS = Shape<128, 48, 32, 4, 2, 2>;   // M >> N ~ l (phase-1 Z, Y_n, Q = Y R^-1)
+using WideS = Shape<48, 128, 32, 2, 4, 2>;   // N >> M ~ l (carry M^(j) H(T), projection)
+using SqS = Shape<64, 64, 32, 2, 2, 2>;      // general / split-K
+using RowS = Shape<64, 48, 32, 4, 2, 3>;     // M = R = 64, N = l = 144 (phase-1 W, split-K)
+using GramS = Shape<48, 48, 32, 2, 2, 2>;    // l x l Grams (split-K)
 using SmallS = Shape<32, 32, 16, 2, 2, 3>;   // tiny problems
-using WideK = Shape<48, 64, 16, 2, 2, 4>;    // short-K wide (carry: K = R = 64), more CTAs/SM
+using WideK = Shape<48, 64, 32, 2, 2, 2>;    // short-K wide (carry: K = R = 64), more CTAs/SM
 
 template <bool TA, bool TB>
 int dispatch(Ctx& c, GemmParams& P, int maxM, int maxN, int maxK, cudaStream_t s) {
