@@ -281,6 +281,16 @@ def main():
                     help="B independent roundings per step (distinct sketch seeds), spread "
                          "over --streams contexts (SURVEY 8d batched throughput of C1/C2)")
     ap.add_argument("--streams", type=int, default=1)
+    ap.add_argument("--inflight", type=int, default=1,
+                    help="K independent roundings in flight per GPU per step (K contexts on "
+                         "K streams, one host thread each, tt_ctx_set_concurrency(--reserve-sms "
+                         "or 16, 1)); each is a complete rounding of the same input sum with "
+                         "its own sketch seed")
+    ap.add_argument("--reserve-sms", type=int, default=-1,
+                    help="--batch without --graph: tt_ctx_set_concurrency(reserve_sms, "
+                         "chain_priority=1) on every context (persistent grids leave this "
+                         "many SMs to the other roundings' QR/truncation chains, which run "
+                         "on a highest-priority stream); -1: off")
     ap.add_argument("--graph", action="store_true",
                     help="--batch: capture the B roundings in one CUDA graph (tt_plan_create) "
                          "and replay it per step (rank mode)")
@@ -352,9 +362,25 @@ def main():
         obj = [P.tt_get_nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         nccl_id = obj[0]
-    ctx = P.Context(local, stream=torch.cuda.current_stream(dev), nccl_id=nccl_id, rank=rank,
-                    world=world)
-    ctx.set_timing(True)
+    K = max(1, args.inflight)
+    if K > 1 and (args.algo != "rand_orth" or slab):
+        raise SystemExit("--inflight > 1: rand_orth with summand shards only")
+    if K > 1 and world > 1:
+        # one communicator per lane: created in lane order on every rank
+        ids = [P.tt_get_nccl_unique_id() if rank == 0 else None for _ in range(K)]
+        dist.broadcast_object_list(ids, src=0)
+    else:
+        ids = [nccl_id]
+    lane_streams = [torch.cuda.current_stream(dev)] if K == 1 else \
+        [torch.cuda.Stream(dev) for _ in range(K)]
+    ctxs = [P.Context(local, stream=lane_streams[t], nccl_id=ids[t], rank=rank, world=world)
+            for t in range(K)]
+    reserve = args.reserve_sms if args.reserve_sms >= 0 else 16
+    for cx in ctxs:
+        cx.set_timing(True)
+        if K > 1:
+            cx.set_concurrency(reserve, True)
+    ctx = ctxs[0]
     if wl.tol > 0:
         kw = dict(mode="tol", tol=wl.tol, oversample=wl.ell, adaptive=wl.adaptive, rank=wl.rank)
     else:
@@ -365,17 +391,31 @@ def main():
     if determ and world > 1:
         raise SystemExit("--algo deterministic runs on one GPU")
 
-    def call(terms):
+    def call(terms, cx=ctx, seed=1):
         if determ:
-            return ctx.tt_round_deterministic(terms, tol=wl.tol, rank=0 if wl.tol > 0 else wl.rank)
+            return cx.tt_round_deterministic(terms, tol=wl.tol, rank=0 if wl.tol > 0 else wl.rank)
         if two_sided:
-            return ctx.tt_round_sum_two_sided(terms, ell=two_sided_ell(wl), rho=0, seed=1)
+            return cx.tt_round_sum_two_sided(terms, ell=two_sided_ell(wl), rho=0, seed=seed)
         if slab:
-            return ctx.tt_round_sum_slab(terms, gdims, slab_lo, seed=1, **kw)
-        return ctx.tt_round_sum(terms, seed=1, **kw)
+            return cx.tt_round_sum_slab(terms, gdims, slab_lo, seed=seed, **kw)
+        return cx.tt_round_sum(terms, seed=seed, **kw)
+
+    lane_phase = [[0.0] * 8 for _ in range(K)]
+    pool = None
+    if K > 1:
+        import concurrent.futures as cf
+        pool = cf.ThreadPoolExecutor(K)
+
+    def lane(t):
+        r = call(local_terms, ctxs[t], seed=1 + t)
+        for i, x in enumerate(ctxs[t].last_timing()):
+            lane_phase[t][i] += x
+        return r
 
     def step():
-        return call(local_terms)
+        if K == 1:
+            return call(local_terms)
+        return list(pool.map(lane, range(K)))[0]
 
     def barrier():
         if world > 1:
@@ -391,16 +431,27 @@ def main():
     stream = torch.cuda.current_stream(dev)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     phase = [0.0] * 8
+    for lp in lane_phase:
+        lp[:] = [0.0] * 8
     n_l0 = P.tt_launch_count()
     with ClockSampler(local) as clk:
         barrier()
         e0.record(stream)
+        for st in lane_streams[1:] if K == 1 else lane_streams:
+            st.wait_event(e0)
         for _ in range(args.steps):
             r = step()
-            t = ctx.last_timing()
-            for i in range(len(t)):
-                phase[i] += t[i]
+            if K == 1:
+                t = ctx.last_timing()
+                for i in range(len(t)):
+                    phase[i] += t[i]
             del r
+        if K > 1:   # end after every lane stream's last work
+            for st in lane_streams:
+                stream.wait_event(st.record_event())
+            # per-rounding phase times: the mean over the lanes (each lane's own
+            # events on its own stream, so they include the sharing of the GPU)
+            phase = [sum(lp[i] for lp in lane_phase) / K for i in range(8)]
         e1.record(stream)
         barrier()
     launches = P.tt_launch_count() - n_l0
@@ -416,8 +467,8 @@ def main():
 
     fl, l = flops_of(wl, ranks_out, args.algo, shapes)
     peak, peak_src = fp64_peak()
-    value = 1000.0 / ms                       # roundings/s (one rounding per step, all ranks)
-    tflops = fl["total"] / (ms * 1e-3) / 1e12 if fl["total"] else None
+    value = 1000.0 * K / ms                   # roundings/s (K roundings per step, all ranks)
+    tflops = K * fl["total"] / (ms * 1e-3) / 1e12 if fl["total"] else None
     # dominant kernel family: the phase-1 DMMA contractions (Alg. 3), timed live
     p1_ms = phase[1]
     share = (1.0 / world) if slab else (hi - lo) / S
@@ -451,7 +502,12 @@ def main():
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic (ttsynth, seeded; DESIGN.md input recipe)",
             "config": dict(bench_config(args.workload, args.algo, world),
-                           **({"parallelism": f"mode-slabs/{world}"} if slab else {})),
+                           **({"parallelism": f"mode-slabs/{world}"} if slab else {}),
+                           **({"inflight": K, "concurrency": {"reserve_sms": reserve,
+                                                              "chain_priority": True},
+                               "step": f"{K} independent roundings of the input sum (sketch "
+                                       f"seeds 1..{K}), one context + stream + host thread each"}
+                              if K > 1 else {})),
             "tflops": tflops, "fp64_peak_tflops": peak, "fp64_peak_source": peak_src,
             "frac_of_fp64_peak": tflops / peak if tflops else None,
             "flops_per_rounding": fl,
@@ -502,8 +558,12 @@ def batched_run(args, world, rank, local):
     graph = args.graph and wl.tol == 0
     if graph:
         ns = 1
-    ctxs = [P.Context(local, stream=torch.cuda.Stream(dev) if graph else None)
-            for _ in range(ns)]
+    lane_streams = [torch.cuda.Stream(dev) for _ in range(ns)]
+    ctxs = [P.Context(local, stream=lane_streams[t]) for t in range(ns)]
+    conc = args.reserve_sms >= 0 and not graph
+    if conc:
+        for cx in ctxs:
+            cx.set_concurrency(args.reserve_sms, True)
     if wl.tol > 0:
         kw = dict(mode="tol", tol=wl.tol, oversample=wl.ell, adaptive=wl.adaptive, rank=wl.rank)
     else:
@@ -536,12 +596,23 @@ def batched_run(args, world, rank, local):
     if world > 1:
         dist.barrier()
     n0 = P.tt_launch_count()
+    # device time: every lane stream starts after e0 (current stream) and the
+    # current stream records e1 after every lane stream's last work
+    cur = torch.cuda.current_stream(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         t0 = time.perf_counter()
+        e0.record(cur)
+        for st in lane_streams:
+            st.wait_event(e0)
         for _ in range(args.steps):
             step()
+        for st in lane_streams:
+            cur.wait_event(st.record_event())
+        e1.record(cur)
         torch.cuda.synchronize()
-        dt = (time.perf_counter() - t0) / args.steps
+        dt_host = (time.perf_counter() - t0) / args.steps
+        dt = e0.elapsed_time(e1) * 1e-3 / args.steps
     launches = P.tt_launch_count() - n0
     if world > 1:
         tt = torch.tensor([dt], device=dev)
@@ -561,7 +632,11 @@ def batched_run(args, world, rank, local):
                        "batch_per_gpu": B, "streams": ns, "parallelism": f"replicas/{world}",
                        "cuda_graph": bool(graph),
                        "graph_branches": max(1, args.streams) if graph else None,
-                       "timing": "host clock between device synchronisations (several streams)"},
+                       "concurrency": ({"reserve_sms": args.reserve_sms, "chain_priority": True}
+                                       if conc else None),
+                       "timing": "CUDA events: start on the current stream, every lane stream "
+                                 "waits on it, end after every lane stream's last work",
+                       "host_ms_per_step": dt_host * 1e3},
             "tflops": tf, "fp64_peak_tflops": peak, "fp64_peak_source": peak_src,
             "roofline": {"bound": "tensor", "kernel": "whole path (batched, latency-bound)",
                          "achieved": tf, "peak": peak, "unit": "TFLOP/s", "frac": tf / peak,

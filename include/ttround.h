@@ -329,6 +329,20 @@ int tt_ctx_set_timing(tt_ctx_t ctx, int enable);
  * Returns the number of words written. */
 int tt_ctx_flags(tt_ctx_t ctx, int* out, int n);
 int tt_ctx_last_timing(tt_ctx_t ctx, double* ms, int n);
+/* Several independent roundings in flight on one GPU (one context per host
+ * thread; SURVEY §8e "independent roundings").  reserve_sms: the persistent and
+ * cooperative grids of this context (phase-1 Z GEMM, fused projection-and-carry,
+ * CholeskyQR passes) are sized to (SM count - reserve_sms) SMs, so they can be
+ * co-resident with another context's latency-bound kernels (0 = all SMs, the
+ * default).  chain_priority != 0: the QR of Alg. 7 line 10 and the
+ * truncation run on a highest-priority stream of the context,
+ * ordered with the context stream by events, so their one-CTA Cholesky and
+ * 8-CTA Jacobi are dispatched ahead of queued GEMM tiles of another context
+ * (not for tt_round_sum_slab, whose QRs all-reduce Grams: one NCCL stream per
+ * communicator).  Results are
+ * unchanged bit for bit (same kernels, same order).  TT_ERR_ARG if reserve_sms
+ * is negative or leaves no SM; TT_ERR_CUDA if the stream cannot be created. */
+int tt_ctx_set_concurrency(tt_ctx_t ctx, int reserve_sms, int chain_priority);
 
 /* ---- kernel-level entry points (for the parity tests and bench) ---------- */
 /* C = alpha*op(A)*op(B) + beta*C, column-major fp64, device pointers; the

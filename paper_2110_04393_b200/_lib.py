@@ -72,6 +72,7 @@ def load_library(path: str = LIB_PATH):
         "tt_loopback_destroy": (C.c_int, [P]),
         "tt_ctx_create_loopback": (C.c_int, [C.c_int, P, P, C.c_int, C.POINTER(P)]),
         "tt_ctx_set_timing": (C.c_int, [P, C.c_int]),
+        "tt_ctx_set_concurrency": (C.c_int, [P, C.c_int, C.c_int]),
         "tt_ctx_last_timing": (C.c_int, [P, C.POINTER(dbl), C.c_int]),
         "tt_ctx_flags": (C.c_int, [P, C.POINTER(C.c_int), C.c_int]),
         "tt_sketch_create": (C.c_int, [P, i32, C.POINTER(i64), C.POINTER(i64), u64, C.c_uint32,
@@ -326,6 +327,12 @@ class Context:
 
     def set_timing(self, on: bool = True):
         _check(load_library().tt_ctx_set_timing(self.handle, int(on)))
+
+    def set_concurrency(self, reserve_sms: int = 0, chain_priority: bool = False):
+        """tt_ctx_set_concurrency: size persistent grids to (SMs - reserve_sms) and
+        run the QR / truncation chain on a highest-priority stream."""
+        _check(load_library().tt_ctx_set_concurrency(self.handle, int(reserve_sms),
+                                                     int(chain_priority)))
 
     def last_timing(self) -> List[float]:
         buf = (C.c_double * 8)()

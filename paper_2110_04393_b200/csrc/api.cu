@@ -124,6 +124,7 @@ int side_ctx(Ctx& c, Ctx** out) {
     std::unique_ptr<Ctx> x(new Ctx);
     x->device = c.device;
     x->sm_count = c.sm_count;
+    x->grid_sms = c.grid_sms;
     x->copy_stream = c.copy_stream;
     x->flags.p = c.flags.p;   // borrowed (destroy_side clears it)
     x->flags.s = nullptr;
@@ -534,6 +535,25 @@ int partial_contractions_rl(Ctx& c, const Terms& T, const std::vector<int64_t>& 
 
 // ------------------------------------------------------------------ Alg. 7
 // X (output cores, ranks l) from the staged summands and the sketch.
+// Runs f() with c.stream switched to the context's high-priority chain stream
+// (tt_ctx_set_concurrency), ordered after everything enqueued on c.stream so far
+// and joined back into it.  Without a chain stream, under graph capture, or when
+// f may issue a collective (mode slabs: all-reduced Grams; one NCCL stream per
+// communicator), f runs on c.stream itself.
+template <class F>
+int on_chain(Ctx& c, bool collective_free, F&& f) {
+  if (!c.chain || c.capturing || !collective_free) return f();
+  cudaStream_t main = c.stream;
+  TTR_CUDA(cudaEventRecord(c.chain_ev[0], main));
+  TTR_CUDA(cudaStreamWaitEvent(c.chain, c.chain_ev[0], 0));
+  c.stream = c.chain;
+  const int rc = f();
+  c.stream = main;
+  TTR_CUDA(cudaEventRecord(c.chain_ev[1], c.chain));
+  TTR_CUDA(cudaStreamWaitEvent(main, c.chain_ev[1], 0));
+  return rc;
+}
+
 int alg7(Ctx& c, const Terms& T, const std::vector<int64_t>& dims, const std::vector<int64_t>& l,
          const tt_sketch& sk, tt_tensor& out, PhaseTimer& tm, const Slab* sl = nullptr) {
   const int S = T.S, d = T.d;
@@ -594,8 +614,10 @@ int alg7(Ctx& c, const Terms& T, const std::vector<int64_t>& dims, const std::ve
     // line 10: [V(X_n), ~] = QR(Y_n); slab: the rows are distributed, the Grams
     // of the CholeskyQR passes are all-reduced (NEXT-2)
     tm.begin(3);
-    TTR_TRY(qr(c, m, l[n], Yb.p, m, false, out.bufs[n - 1].p, nullptr, s, sl != nullptr,
-               sl ? l[n - 1] * sl->gdims[n - 1] : 0));
+    TTR_TRY(on_chain(c, sl == nullptr, [&]() {
+      return qr(c, m, l[n], Yb.p, m, false, out.bufs[n - 1].p, nullptr, c.stream, sl != nullptr,
+                sl ? l[n - 1] * sl->gdims[n - 1] : 0);
+    }));
     tm.end(3);
     tm.begin(2);
     int fused = 1;
@@ -1028,7 +1050,8 @@ int round_sum_impl(tt_ctx* c, int S, const tt_view* terms, const tt_round_opts* 
     }
     std::vector<int64_t> ks;
     tm.begin(5);
-    TTR_TRY(truncate(*c, X, tol, rank, ks, sl));
+    TTR_TRY(on_chain(*c, sl == nullptr, [&]() { return truncate(*c, X, tol, rank, ks, sl); }));
+    for (auto& b : X.bufs) b.s = c->stream;   // after the join: freed in c->stream's order
     tm.end(5);
     TTR_TRY(read_flags(*c, fl, 4));
     flags |= (fl[1] ? TT_FLAG_QR_FALLBACK : 0);
@@ -2385,6 +2408,12 @@ int ctx_destroy_impl(tt_ctx* c) {
     c->flags.p = nullptr;
     cudaStreamSynchronize(c->stream);
     cudaStreamDestroy(c->copy_stream);
+    if (c->chain) {
+      cudaStreamSynchronize(c->chain);
+      cudaStreamDestroy(c->chain);
+    }
+    for (auto e : c->chain_ev)
+      if (e) cudaEventDestroy(e);
     if (c->own_stream) cudaStreamDestroy(c->stream);
     delete c;
     return TT_OK;
@@ -2395,6 +2424,34 @@ int tt_ctx_set_timing(tt_ctx_t c, int enable) {
   if (!c) return TT_ERR_ARG;
   c->timing = enable != 0;
   return TT_OK;
+}
+
+int tt_ctx_set_concurrency(tt_ctx_t c, int reserve_sms, int chain_priority) {
+  if (!c) return TT_ERR_ARG;
+  if (reserve_sms < 0 || reserve_sms >= c->sm_count) {
+    set_error("reserve_sms %d out of range [0, %d)", reserve_sms, c->sm_count);
+    return TT_ERR_ARG;
+  }
+  return guarded([&]() -> int {
+    TTR_CUDA(cudaSetDevice(c->device));
+    c->grid_sms = c->sm_count - reserve_sms;
+    if (c->side) c->side->grid_sms = c->grid_sms;
+    if (chain_priority && !c->chain) {
+      int lo = 0, hi = 0;
+      TTR_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+      TTR_CUDA(cudaStreamCreateWithPriority(&c->chain, cudaStreamNonBlocking, hi));
+      for (auto& e : c->chain_ev) TTR_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    } else if (!chain_priority && c->chain) {
+      TTR_CUDA(cudaStreamSynchronize(c->chain));
+      TTR_CUDA(cudaStreamDestroy(c->chain));
+      c->chain = nullptr;
+      for (auto& e : c->chain_ev) {
+        cudaEventDestroy(e);
+        e = nullptr;
+      }
+    }
+    return TT_OK;
+  });
 }
 
 int tt_ctx_flags(tt_ctx_t c, int* out, int n) {

@@ -160,7 +160,19 @@ struct Ctx {
   // true while a CUDA graph is being captured on `stream` (tt_plan_create): no
   // host synchronisation, no host reads of device flags, no workspace growth
   bool capturing = false;
+  // concurrent roundings on one GPU (tt_ctx_set_concurrency): persistent and
+  // cooperative grids are sized to grid_sms SMs (0: all), leaving the rest to the
+  // latency-bound chain of another context; chain: a highest-priority stream the
+  // QR and truncation chain runs on (ordered with `stream` by events), so its
+  // one-CTA / one-cluster kernels are dispatched ahead of another context's GEMM tiles
+  int grid_sms = 0;
+  cudaStream_t chain = nullptr;
+  cudaEvent_t chain_ev[2] = {nullptr, nullptr};
 };
+// SMs a persistent / cooperative grid of c is sized to
+inline int grid_sms(const Ctx& c) {
+  return c.grid_sms > 0 && c.grid_sms < c.sm_count ? c.grid_sms : c.sm_count;
+}
 // The side context of c (created on first use); destroyed with c (destroy_side).
 int side_ctx(Ctx& c, Ctx** out);
 void destroy_side(Ctx& c);

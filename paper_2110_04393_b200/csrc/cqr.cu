@@ -418,7 +418,7 @@ int cqr_pass(Ctx& c, int64_t m, int n, const double* A, int64_t lda, bool trans,
   p.gate = gate;
   p.gate_val = gate_val;
   p.vec = !trans && !(reinterpret_cast<uintptr_t>(A) & 15) && !(lda & 1);
-  const int grid = int(std::min<int64_t>(p.nchunks, c.sm_count));
+  const int grid = int(std::min<int64_t>(p.nchunks, grid_sms(c)));
   p.ws = nullptr;
   if (G) {
     const size_t need = size_t(c.sm_count) * kPart;

@@ -308,7 +308,7 @@ int proj_carry(Ctx& c, int64_t m, int l, int sumR, const double* Q, const double
       attr[c.device & 63] = true;
     }
   }
-  const int grid = c.sm_count * resident[c.device & 63];
+  const int grid = grid_sms(c) * resident[c.device & 63];
   if (grid < 1) return 1;
   P.M = M;
   P.X1 = X1;

@@ -184,7 +184,7 @@ int pgemm(Ctx& c, const GemmDesc* d, int nb, cudaStream_t s) {
       attr[c.device & 63] = true;
     }
   }
-  const int grid = std::min(tiles, c.sm_count * std::max(1, resident[c.device & 63]));
+  const int grid = std::min(tiles, grid_sms(c) * std::max(1, resident[c.device & 63]));
   if (grid < 1) return 1;
   pgemm_kernel<<<grid, pThreads, pSmem, s>>>(P);
   return launched();
