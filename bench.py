@@ -370,7 +370,7 @@ def main():
         ids = [P.tt_get_nccl_unique_id() if rank == 0 else None for _ in range(K)]
         dist.broadcast_object_list(ids, src=0)
     else:
-        ids = [nccl_id]
+        ids = [nccl_id] * K
     lane_streams = [torch.cuda.current_stream(dev)] if K == 1 else \
         [torch.cuda.Stream(dev) for _ in range(K)]
     ctxs = [P.Context(local, stream=lane_streams[t], nccl_id=ids[t], rank=rank, world=world)
@@ -413,9 +413,20 @@ def main():
         return r
 
     def step():
-        if K == 1:
-            return call(local_terms)
-        return list(pool.map(lane, range(K)))[0]
+        return call(local_terms)
+
+    def run_lanes(nsteps, stagger_s):
+        """K host threads, each running nsteps roundings back to back on its own
+        context (no barrier between steps); lane t starts t * stagger_s late, so
+        one lane's latency-bound QR/truncation chain overlaps another's GEMMs."""
+        def body(t):
+            if t and stagger_s > 0:
+                time.sleep(t * stagger_s)
+            r = None
+            for _ in range(nsteps):
+                r = lane(t)
+            return r
+        return list(pool.map(body, range(K)))[0]
 
     def barrier():
         if world > 1:
@@ -423,8 +434,17 @@ def main():
         torch.cuda.synchronize()
 
     res = None
-    for _ in range(max(3, args.warmup)):
-        res = step()
+    stagger = 0.0
+    if K == 1:
+        for _ in range(max(3, args.warmup)):
+            res = step()
+    else:
+        res = lane(0)                      # one rounding alone: its latency sets the stagger
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        res = lane(0)
+        stagger = (time.perf_counter() - t0) / K
+        res = run_lanes(max(3, args.warmup), stagger)
     ranks_out = res.ranks
     del res
     barrier()
@@ -439,13 +459,16 @@ def main():
         e0.record(stream)
         for st in lane_streams[1:] if K == 1 else lane_streams:
             st.wait_event(e0)
-        for _ in range(args.steps):
-            r = step()
-            if K == 1:
+        if K == 1:
+            for _ in range(args.steps):
+                r = step()
                 t = ctx.last_timing()
                 for i in range(len(t)):
                     phase[i] += t[i]
-            del r
+                del r
+        else:
+            del_r = run_lanes(args.steps, stagger)
+            del del_r
         if K > 1:   # end after every lane stream's last work
             for st in lane_streams:
                 stream.wait_event(st.record_event())
@@ -506,7 +529,11 @@ def main():
                            **({"inflight": K, "concurrency": {"reserve_sms": reserve,
                                                               "chain_priority": True},
                                "step": f"{K} independent roundings of the input sum (sketch "
-                                       f"seeds 1..{K}), one context + stream + host thread each"}
+                                       f"seeds 1..{K}), one context + stream + host thread each; "
+                                       "lanes run back to back without a barrier between steps, "
+                                       "lane t started t/K of a rounding's latency late; timed from "
+                                       "before the first lane's first call to after every lane's "
+                                       "last"}
                               if K > 1 else {})),
             "tflops": tflops, "fp64_peak_tflops": peak, "fp64_peak_source": peak_src,
             "frac_of_fp64_peak": tflops / peak if tflops else None,

@@ -339,8 +339,10 @@ int tt_ctx_last_timing(tt_ctx_t ctx, double* ms, int n);
  * ordered with the context stream by events, so their one-CTA Cholesky and
  * 8-CTA Jacobi are dispatched ahead of queued GEMM tiles of another context
  * (not for tt_round_sum_slab, whose QRs all-reduce Grams: one NCCL stream per
- * communicator).  Results are
- * unchanged bit for bit (same kernels, same order).  TT_ERR_ARG if reserve_sms
+ * communicator).  chain_priority alone leaves the results unchanged bit for
+ * bit (same kernels, same order); reserve_sms > 0 changes the split-K slicing of
+ * the fused projection and the CholeskyQR passes' partial-Gram count, i.e. the
+ * summation order (results equal to rounding).  TT_ERR_ARG if reserve_sms
  * is negative or leaves no SM; TT_ERR_CUDA if the stream cannot be created. */
 int tt_ctx_set_concurrency(tt_ctx_t ctx, int reserve_sms, int chain_priority);
 

@@ -546,11 +546,21 @@ int on_chain(Ctx& c, bool collective_free, F&& f) {
   cudaStream_t main = c.stream;
   TTR_CUDA(cudaEventRecord(c.chain_ev[0], main));
   TTR_CUDA(cudaStreamWaitEvent(c.chain, c.chain_ev[0], 0));
+  // the context's workspaces may be regrown (freed) inside f: free them in the
+  // chain stream's order, which follows every earlier use, not on the idle main
+  // stream (where the pool could hand them out again while chain work is queued)
+  auto retag = [&](cudaStream_t st) {
+    c.gemm_ws.s = st;
+    c.cqr_ws.s = st;
+    c.scratch.s = st;
+  };
+  retag(c.chain);
   c.stream = c.chain;
   const int rc = f();
   c.stream = main;
   TTR_CUDA(cudaEventRecord(c.chain_ev[1], c.chain));
   TTR_CUDA(cudaStreamWaitEvent(main, c.chain_ev[1], 0));
+  retag(main);   // main now follows everything the chain stream was given
   return rc;
 }
 
@@ -1050,7 +1060,12 @@ int round_sum_impl(tt_ctx* c, int S, const tt_view* terms, const tt_round_opts* 
     }
     std::vector<int64_t> ks;
     tm.begin(5);
-    TTR_TRY(on_chain(*c, sl == nullptr, [&]() { return truncate(*c, X, tol, rank, ks, sl); }));
+    TTR_TRY(on_chain(*c, sl == nullptr, [&]() {
+      // cores replaced inside the truncation are freed in the order of the
+      // stream it runs on (the chain stream when one is set)
+      for (auto& b : X.bufs) b.s = c->stream;
+      return truncate(*c, X, tol, rank, ks, sl);
+    }));
     for (auto& b : X.bufs) b.s = c->stream;   // after the join: freed in c->stream's order
     tm.end(5);
     TTR_TRY(read_flags(*c, fl, 4));
