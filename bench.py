@@ -324,7 +324,7 @@ def main():
 
     if args.impl == "reference":
         return reference_arm(args, world, rank)
-    if args.batch > 1:
+    if args.batch > 1 or args.graph:
         return batched_run(args, world, rank, local)
 
     import torch
