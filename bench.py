@@ -303,6 +303,10 @@ def main():
                          "two_sided: tt_round_sum_two_sided (Alg. 6); deterministic: "
                          "tt_round_deterministic (Alg. 1 + 2 on the assembled sum, the "
                          "paper's baseline; one GPU, no flop accounting)")
+    ap.add_argument("--nccl-one-rank", action="store_true",
+                    help="N=1 only: give the context a ONE-rank NCCL communicator so the "
+                         "sharded path's exchange steps (ncclAllReduce of Y_n per sweep step, "
+                         "agreed validation) run on a one-GPU box; reported in config")
     args = ap.parse_args()
 
     if "WORLD_SIZE" not in os.environ and args.gpus > 1:
@@ -362,6 +366,8 @@ def main():
         obj = [P.tt_get_nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         nccl_id = obj[0]
+    elif args.nccl_one_rank:
+        nccl_id = P.tt_get_nccl_unique_id()
     K = max(1, args.inflight)
     if K > 1 and (args.algo != "rand_orth" or slab):
         raise SystemExit("--inflight > 1: rand_orth with summand shards only")
@@ -526,6 +532,9 @@ def main():
             "dtype": "f64", "data": "synthetic (ttsynth, seeded; DESIGN.md input recipe)",
             "config": dict(bench_config(args.workload, args.algo, world),
                            **({"parallelism": f"mode-slabs/{world}"} if slab else {}),
+                           **({"exchange": "one-rank NCCL communicator (ncclAllReduce per "
+                                           "sweep step)"} if args.nccl_one_rank and world == 1
+                              else {}),
                            **({"inflight": K, "concurrency": {"reserve_sms": reserve,
                                                               "chain_priority": True},
                                "step": f"{K} independent roundings of the input sum (sketch "

@@ -103,12 +103,26 @@ typedef struct {
  * bytes (e.g. torch.distributed), pass them to tt_ctx_create on every rank. */
 int tt_get_nccl_unique_id(uint8_t id[128]);
 
+/* Diagnostic for the exchange step of the sharded sweep (the sum
+ * over summands of Alg. 7 line 9): builds a ONE-rank NCCL communicator
+ * the way tt_ctx_create does for world > 1 (libnccl resolved with dlopen,
+ * ncclCommInitRank) and runs the path's two collectives on the context's
+ * stream: an fp64-sum allreduce of n device doubles (library-owned scratch) and
+ * the int64 allreduce of the status words.  With one rank the result must equal
+ * the input; *max_abs_diff (host) receives the largest deviation (0.0 when
+ * exact).  Lets a one-GPU box exercise the NCCL plumbing.  Synchronises the
+ * stream.  TT_ERR_ARG (NULL, n < 0 or n > 2^28), TT_ERR_NCCL, TT_ERR_CUDA. */
+int tt_nccl_selftest(tt_ctx_t ctx, int64_t n, double* max_abs_diff);
+
 /* Create a context on CUDA device `device` using stream `cuda_stream`
  * (a cudaStream_t, or NULL for a library-created non-blocking stream; to run
  * on the legacy default stream pass cudaStreamLegacy, i.e. (void*)0x1).
- * nccl_id == NULL or world == 1: single-GPU.  Otherwise the summands of a
+ * nccl_id == NULL: single-GPU (world must be 1).  world > 1: the summands of a
  * rounding are sharded across `world` processes (one per GPU); each passes its
- * local summands and all receive the same result. */
+ * local summands and all receive the same result.  world == 1 WITH
+ * an id: a one-rank NCCL communicator is built and the sharded code path (agreed
+ * validation, ncclAllReduce of Y_n per sweep step) runs through it -- the
+ * same results as the single-GPU context; for boxes with one GPU. */
 int tt_ctx_create(int device, void* cuda_stream, const uint8_t* nccl_id,
                   int rank, int world, tt_ctx_t* out);
 int tt_ctx_destroy(tt_ctx_t ctx);

@@ -66,6 +66,7 @@ def load_library(path: str = LIB_PATH):
         "tt_last_error": (C.c_char_p, []),
         "tt_launch_count": (u64, []),
         "tt_get_nccl_unique_id": (C.c_int, [P]),
+        "tt_nccl_selftest": (C.c_int, [P, C.c_int64, P]),
         "tt_ctx_create": (C.c_int, [C.c_int, P, P, C.c_int, C.c_int, C.POINTER(P)]),
         "tt_ctx_destroy": (C.c_int, [P]),
         "tt_loopback_create": (C.c_int, [C.c_int, C.POINTER(P)]),
@@ -324,6 +325,13 @@ class Context:
 
     def close(self):
         self._h.__del__()
+
+    def nccl_selftest(self, n: int = 1 << 16) -> float:
+        """tt_nccl_selftest: one-rank NCCL communicator, fp64-sum and int64
+        allreduce on this context's stream; returns the largest deviation."""
+        out = C.c_double(-1.0)
+        _check(load_library().tt_nccl_selftest(self.handle, int(n), C.byref(out)))
+        return float(out.value)
 
     def set_timing(self, on: bool = True):
         _check(load_library().tt_ctx_set_timing(self.handle, int(on)))

@@ -151,6 +151,7 @@ void destroy_side(Ctx& c) {
 
 int nccl_unique_id(uint8_t id[128]);
 int nccl_comm_create(Ctx& c, const uint8_t* id, int rank, int world);
+int nccl_selftest(Ctx& c, size_t n, double* max_abs_diff);
 int nccl_comm_destroy(Ctx& c);
 
 }  // namespace ttr
@@ -295,14 +296,14 @@ int validate_sharded(Ctx& c, const tt_view* v, int S, int local_rc,
     if (S < 0 || (S > 0 && !v)) {
       set_error("need S_local >= 0 summands (and a terms array when S_local > 0)");
       rc = TT_ERR_ARG;
-    } else if (S == 0 && c.world == 1) {
+    } else if (S == 0 && !c.multi()) {
       set_error("need S >= 1 summands");
       rc = TT_ERR_ARG;
     } else if (S > 0) {
       rc = validate(v, S, dims);
     }
   }
-  if (c.world == 1) return rc;
+  if (!c.multi()) return rc;
   const bool have = rc == TT_OK && S > 0;
   const int64_t big = INT64_MAX;
   const size_t ne = extra.size();
@@ -899,7 +900,7 @@ int validate_slab(Ctx& c, const tt_view* v, int S, const int64_t* gdims, const i
     sl.gdims.assign(gdims, gdims + d);
     sl.lo.assign(lo, lo + d);
   }
-  if (c.world == 1) {
+  if (!c.multi()) {
     if (rc == TT_OK && sl.gdims != dims) {
       set_error("one rank: the slabs must be the whole modes");
       return TT_ERR_SHAPE;
@@ -1220,7 +1221,7 @@ int two_sided_impl(tt_ctx* c, int S, const tt_view* terms, int64_t ell, int64_t 
   // contraction and the assembly on the main stream.  With NCCL in the loop
   // (world > 1) everything stays on the main stream (the collectives of one
   // communicator must not be issued from two streams).
-  const bool overlap = C.world == 1 && d > 2;
+  const bool overlap = !C.multi() && d > 2;
   Ctx side;
   struct SideGuard {
     Ctx& x;
@@ -2312,6 +2313,17 @@ int tt_get_nccl_unique_id(uint8_t id[128]) {
   return guarded([&] { return nccl_unique_id(id); });
 }
 
+int tt_nccl_selftest(tt_ctx_t c, int64_t n, double* max_abs_diff) {
+  if (!c || !max_abs_diff || n < 0 || n > (int64_t(1) << 28)) {
+    set_error("tt_nccl_selftest: need ctx, 0 <= n <= 2^28 and max_abs_diff");
+    return TT_ERR_ARG;
+  }
+  return guarded([&]() -> int {
+    TTR_CUDA(cudaSetDevice(c->device));
+    return nccl_selftest(*c, size_t(n), max_abs_diff);
+  });
+}
+
 struct tt_loopback {
   ttr::LoopGroup* g = nullptr;
   int world = 1;
@@ -2356,7 +2368,7 @@ int ctx_create_impl(int device, void* cuda_stream, const uint8_t* nccl_id, tt_lo
     c->world = world;
     if (loop) {
       c->loop = loop->g;
-    } else if (world > 1) {
+    } else if (world > 1 || nccl_id) {   // world == 1 with an id: one-rank NCCL
       if (!nccl_id) {
         set_error("world > 1 needs an NCCL unique id");
         return TT_ERR_ARG;

@@ -15,7 +15,9 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <algorithm>
 #include <chrono>
+#include <cmath>
 #include <condition_variable>
 #include <mutex>
 
@@ -94,6 +96,63 @@ int nccl_comm_destroy(Ctx& c) {
   if (c.comm && g_nccl.loaded) g_nccl.commDestroy(static_cast<ncclComm_t>(c.comm));
   c.comm = nullptr;
   return TT_OK;
+}
+
+// One-rank NCCL communicator built and used the way the sharded path uses it
+// (dlopen'd libnccl, ncclCommInitRank, fp64-sum and int64 allreduce on the
+// context's stream).  With one rank a sum allreduce must return its input: the
+// largest deviation is reported.  Runs on a box with one GPU, where world > 1
+// cannot be formed.
+int nccl_selftest(Ctx& c, size_t n, double* max_abs_diff) {
+  TTR_TRY(nccl_load());
+  ncclUniqueId u;
+  TTR_NCCL(g_nccl.getUniqueId(&u));
+  ncclComm_t comm = nullptr;
+  TTR_NCCL(g_nccl.commInitRank(&comm, 1, u, 0));
+  std::vector<double> h(n), back(n);
+  for (size_t i = 0; i < n; ++i) h[i] = 1.0 / double(i + 1) - 0.5 * double(i % 7);
+  double* d = nullptr;
+  int rc = TT_OK;
+  do {
+    if (cudaMalloc(reinterpret_cast<void**>(&d), std::max<size_t>(n, 1) * sizeof(double)) !=
+        cudaSuccess) {
+      set_error("nccl_selftest: cudaMalloc failed");
+      rc = TT_ERR_CUDA;
+      break;
+    }
+    cudaMemcpyAsync(d, h.data(), n * sizeof(double), cudaMemcpyHostToDevice, c.stream);
+    ncclResult_t r = g_nccl.allReduce(d, d, n, ncclFloat64, ncclSum, comm, c.stream);
+    if (r != ncclSuccess) {
+      set_error("ncclAllReduce (fp64 sum) failed: %s", g_nccl.getErrorString(r));
+      rc = TT_ERR_NCCL;
+      break;
+    }
+    cudaMemcpyAsync(back.data(), d, n * sizeof(double), cudaMemcpyDeviceToHost, c.stream);
+    int64_t w[2] = {int64_t(n), -3};
+    int64_t* dw = reinterpret_cast<int64_t*>(d);
+    if (n >= 2) {
+      cudaMemcpyAsync(dw, w, sizeof(w), cudaMemcpyHostToDevice, c.stream);
+      r = g_nccl.allReduce(dw, dw, 2, ncclInt64, ncclMax, comm, c.stream);
+      if (r != ncclSuccess) {
+        set_error("ncclAllReduce (int64 max) failed: %s", g_nccl.getErrorString(r));
+        rc = TT_ERR_NCCL;
+        break;
+      }
+      cudaMemcpyAsync(w, dw, sizeof(w), cudaMemcpyDeviceToHost, c.stream);
+    }
+    if (cudaStreamSynchronize(c.stream) != cudaSuccess) {
+      set_error("nccl_selftest: stream failed: %s", cudaGetErrorString(cudaGetLastError()));
+      rc = TT_ERR_CUDA;
+      break;
+    }
+    double m = 0.0;
+    for (size_t i = 0; i < n; ++i) m = std::max(m, std::fabs(back[i] - h[i]));
+    if (w[0] != int64_t(n) || w[1] != -3) m = std::max(m, 1.0);
+    *max_abs_diff = m;
+  } while (0);
+  if (d) cudaFree(d);
+  g_nccl.commDestroy(comm);
+  return rc;
 }
 
 // ------------------------------------------------------------------ loopback
@@ -198,7 +257,7 @@ static int loop_allreduce_i64(Ctx& c, int64_t* h, size_t n, int op) {
 
 // ------------------------------------------------------------------ dispatch
 int allreduce_sum(Ctx& c, double* buf, size_t n) {
-  if (c.world <= 1 || n == 0) return TT_OK;
+  if (!c.multi() || n == 0) return TT_OK;
   if (c.loop) return loop_allreduce(c, buf, n);
   TTR_NCCL(g_nccl.allReduce(buf, buf, n, ncclFloat64, ncclSum,
                             static_cast<ncclComm_t>(c.comm), c.stream));
@@ -206,7 +265,7 @@ int allreduce_sum(Ctx& c, double* buf, size_t n) {
 }
 
 int allreduce_i64(Ctx& c, int64_t* hostbuf, size_t n, int op) {
-  if (c.world <= 1 || n == 0) return TT_OK;
+  if (!c.multi() || n == 0) return TT_OK;
   if (c.loop) return loop_allreduce_i64(c, hostbuf, n, op);
   int64_t* d = nullptr;
   TTR_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d), n * sizeof(int64_t), c.stream));

@@ -138,6 +138,10 @@ struct Ctx {
   bool own_stream = false;
   int rank = 0, world = 1;
   void* comm = nullptr;                 // ncclComm_t
+  // the sharded code path (agreed validation, exchange steps) runs when there is
+  // more than one rank, or when a ONE-rank NCCL communicator was asked for
+  // (tt_ctx_create with world == 1 and an id: the NCCL path on a one-GPU box)
+  bool multi() const { return world > 1 || comm != nullptr; }
   LoopGroup* loop = nullptr;            // loopback communicator (borrowed), else NCCL
   bool timing = false;
   double last_ms[8] = {0};

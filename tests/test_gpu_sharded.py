@@ -149,3 +149,58 @@ def test_bad_argument_on_one_rank_fails_every_rank():
 
     codes = run_ranks(2, fn2, timeout=120)
     assert all(c is not None and c < 0 for c in codes), codes
+
+
+def test_nccl_plumbing_one_rank():
+    """The NCCL communicator of the world > 1 path (dlopen'd libnccl,
+    ncclCommInitRank, the fp64-sum and int64 allreduce on the context's stream)
+    with ONE rank, where a sum allreduce returns its input exactly."""
+    import paper_2110_04393_b200 as P
+    ctx = P.Context(0)
+    for n in (0, 1, 144 * 64 + 3, 1 << 20):
+        assert ctx.nccl_selftest(n) == 0.0
+    with pytest.raises(P.TTError):
+        ctx.nccl_selftest(-1)
+
+
+@pytest.mark.parametrize("cfg", ["config3_sum10", "config4_gmres"])
+def test_one_rank_nccl_context_runs_the_sharded_path(cfg):
+    """tt_ctx_create with world == 1 AND an NCCL id: the sharded code path (agreed
+    validation, ncclAllReduce of Y_n per sweep step; the last core)
+    runs through a real one-rank NCCL communicator.  Same result as the oracle,
+    and the same bits as the plain single-GPU context (a one-rank sum is exact)."""
+    import paper_2110_04393_b200 as P
+    w = getattr(ttsynth, cfg)()
+    np_terms = [ttsynth.to_numpy(t) for t in w.terms]
+    if w.tol > 0:
+        kw = dict(mode="tol", tol=w.tol, oversample=w.ell, adaptive=w.adaptive)
+        ref = oracle.round_sum(np_terms, ell=w.ell, seed=1, tol=w.tol, adaptive=w.adaptive)
+    else:
+        kw = dict(mode="rank", rank=w.rank, oversample=w.ell - w.rank)
+        ref = oracle.round_sum(np_terms, ell=w.ell, seed=1, rank=w.rank)
+    g = gpu_terms(w.terms)
+    nc = P.Context(0, nccl_id=P.tt_get_nccl_unique_id(), rank=0, world=1)
+    res = nc.tt_round_sum(g, seed=1, **kw)
+    assert res.ranks[1:-1] == list(ref.ranks)
+    X = res.numpy()
+    assert oracle.rel_diff(X, ref.X) <= TOL
+    plain = P.Context(0).tt_round_sum(g, seed=1, **kw).numpy()
+    check_same_bits([X, plain])
+    # two-sided (Alg. 6) and the mode-slab partition through the same communicator
+    if w.tol == 0:
+        r2 = nc.tt_round_sum_two_sided(g, ell=w.rank, seed=1)
+        p2 = P.Context(0).tt_round_sum_two_sided(g, ell=w.rank, seed=1)
+        assert oracle.rel_diff(r2.numpy(), p2.numpy()) <= TOL
+    dims = [c.shape[1] for c in g[0]]
+    rs = nc.tt_round_sum_slab(g, dims, [0] * len(dims), seed=1, **kw)
+    assert rs.ranks[1:-1] == list(ref.ranks)
+    assert oracle.rel_diff(rs.numpy(), ref.X) <= TOL
+    nc.close()
+
+
+def test_one_rank_nccl_context_bad_argument_returns():
+    import paper_2110_04393_b200 as P
+    nc = P.Context(0, nccl_id=P.tt_get_nccl_unique_id(), rank=0, world=1)
+    with pytest.raises(P.TTError):
+        nc.tt_round_sum([], mode="rank", rank=2, oversample=1, seed=1)
+    nc.close()

@@ -57,6 +57,8 @@ def test_argument_errors_without_gpu(lib):
     # null ctx / out must fail cleanly with a message, not crash
     rc = lib.tt_round_sum(None, 1, None, None, None, None)
     assert rc == -1 and b"null" in lib.tt_last_error()
+    rc = lib.tt_nccl_selftest(None, 4, None)
+    assert rc == -1
     rc = lib.tt_round_sum_two_sided(None, 1, None, 4, 0, 1, None)
     assert rc == -1 and b"null" in lib.tt_last_error()
     rc = lib.tt_ctx_create(0, None, None, 2, 1, None)
