@@ -96,6 +96,13 @@ typedef struct {
   double   tol;         /* TT_TOL: relative tolerance eps0 > 0 (Alg. 2)                */
   uint64_t seed;        /* Philox key of the Gaussian sketch (Def. 3.1 / R9)                  */
   int64_t  max_rank;    /* adaptive upper bound on l (0 = structural caps only)               */
+  const int64_t* ranks; /* optional per-bond targets r_1..r_{d-1} (host array of d-1 entries,
+                         * each >= 1; NULL = the uniform `rank`): the paper's "target TT-ranks
+                         * {l_n}".  tt_round_sum / tt_round_sum_slab in
+                         * TT_RANK mode: sketch ranks l_n = r_n + oversample (capped, R7), bond n
+                         * truncated to r_n; `rank` is ignored; no user sketch.
+                         * tt_round_deterministic: the cap of bond n (with or without tol).
+                         * Ignored in TT_SKETCH_ONLY / TT_TOL modes of tt_round_sum.          */
 } tt_round_opts;
 
 /* ---- context ------------------------------------------------------------- */

@@ -392,11 +392,17 @@ class RoundResult:
 P_MIN = 5  # adaptive saturation margin (R8)
 
 
-def round_sum(terms: Sequence[TT], ell: int, seed: int = 1, rank: int = 0,
+def round_sum(terms: Sequence[TT], ell: Union[int, Sequence[int]], seed: int = 1,
+              rank: Union[int, Sequence[int]] = 0,
               tol: float = 0.0, adaptive: bool = False, max_rank: int = 0,
               sketch_only: bool = False) -> RoundResult:
     """The operation behind ``tt_round_sum``: caps → sketch → Alg. 7 → truncation
-    (→ adaptive growth of ℓ, tolerance mode only).  See DESIGN.md R3-R8."""
+    (→ adaptive growth of ℓ, tolerance mode only).  See DESIGN.md R3-R8.
+    ``ell`` and ``rank`` may be sequences of N-1 per-bond values, the paper's
+    "target TT-ranks {ℓ_n}" (R22): one pass, bond n
+    sketched with ℓ_n (capped, R7) and truncated to rank_n."""
+    if not np.isscalar(ell) or not np.isscalar(rank):
+        return _round_sum_per_bond(terms, ell, seed, rank, tol, sketch_only)
     terms = [[np.asarray(c, dtype=np.float64) for c in t] for t in terms]
     dims = dims_of(terms[0])
     N = len(dims)
@@ -433,6 +439,32 @@ def round_sum(terms: Sequence[TT], ell: int, seed: int = 1, rank: int = 0,
         if nxt <= cur:
             return RoundResult(Xt, ks, caps, passes, capped)
         cur = nxt
+
+
+def _round_sum_per_bond(terms, ell, seed, rank, tol, sketch_only) -> RoundResult:
+    """round_sum with per-bond sketch ranks ℓ_1..ℓ_{N-1} and target ranks
+    r_1..r_{N-1} (scalars are broadcast; r_n = 0 means no cap on bond n)."""
+    terms = [[np.asarray(c, dtype=np.float64) for c in t] for t in terms]
+    dims = dims_of(terms[0])
+    N = len(dims)
+    if N < 2:
+        raise ValueError("a TT-tensor to round needs N >= 2 modes")
+    req = [int(ell)] * (N - 1) if np.isscalar(ell) else [int(x) for x in ell]
+    rk = [int(rank)] * (N - 1) if np.isscalar(rank) else [int(x) for x in rank]
+    if len(req) != N - 1 or len(rk) != N - 1:
+        raise ValueError("per-bond ranks need N-1 entries")
+    sumR = [1] + [sum(t[n].shape[2] for t in terms) for n in range(N - 1)] + [1]
+    caps = rank_caps(dims, sumR, req)
+    G = gaussian_sketch(dims, caps, seed, tag=0)
+    X = round_sum_rand_orth(terms, G)
+    capped = any(c < q for c, q in zip(caps, req))
+    lr = ranks_of(X)[1:-1]
+    is_zero = all(r == 1 for r in lr) and not any(np.any(c) for c in X)
+    need = tol > 0 or any(r > 0 and c > r for c, r in zip(caps, rk))
+    if sketch_only or is_zero or not need:
+        return RoundResult(X, lr, caps, 1, capped)
+    Xt, ks = truncate_left_orthogonal(X, tol, rk)
+    return RoundResult(Xt, ks, caps, 1, capped)
 
 
 # ---------------------------------------------------------------- Alg. 6 (SURVEY §8f NEXT-3)

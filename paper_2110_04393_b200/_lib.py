@@ -30,7 +30,21 @@ class tt_view(C.Structure):
 class tt_round_opts(C.Structure):
     _fields_ = [("mode", C.c_int32), ("adaptive", C.c_int32), ("rank", C.c_int64),
                 ("oversample", C.c_int64), ("tol", C.c_double), ("seed", C.c_uint64),
-                ("max_rank", C.c_int64)]
+                ("max_rank", C.c_int64), ("ranks", C.POINTER(C.c_int64))]
+
+
+def _make_opts(mode, adaptive, rank, oversample, tol, seed, max_rank):
+    """tt_round_opts from Python arguments; `rank` may be a sequence of d-1
+    per-bond target ranks (opts.ranks).  Returns (opts, keepalive)."""
+    keep = None
+    if isinstance(rank, (list, tuple)):
+        keep = (C.c_int64 * len(rank))(*[int(x) for x in rank])
+        opts = tt_round_opts(mode, int(adaptive), 0, int(oversample), float(tol),
+                             C.c_uint64(seed).value, int(max_rank), keep)
+    else:
+        opts = tt_round_opts(mode, int(adaptive), int(rank), int(oversample), float(tol),
+                             C.c_uint64(seed).value, int(max_rank))
+    return opts, keep
 
 
 class tt_kron_op(C.Structure):
@@ -366,15 +380,15 @@ class Context:
 
     # ---------------------------------------------------------------- hot path
     def tt_round_sum(self, terms: Sequence[Sequence[torch.Tensor]], mode: str = "rank",
-                     rank: int = 0, oversample: int = 0, tol: float = 0.0, seed: int = 1,
+                     rank=0, oversample: int = 0, tol: float = 0.0, seed: int = 1,
                      adaptive: bool = False, max_rank: int = 0,
                      sketch: Optional[Sketch] = None) -> TTResult:
-        """Round sum_j terms[j] (Alg. 7 + truncation); see include/ttround.h."""
+        """Round sum_j terms[j] (Alg. 7 + truncation); see include/ttround.h.
+        `rank`: an int, or a list of d-1 per-bond target ranks (opts.ranks)."""
         L = load_library()
         views = [_View(t) for t in terms]
         arr = (tt_view * len(views))(*[v.view for v in views]) if views else None
-        opts = tt_round_opts(_MODES[mode], int(adaptive), int(rank), int(oversample),
-                             float(tol), C.c_uint64(seed).value, int(max_rank))
+        opts, _keep = _make_opts(_MODES[mode], adaptive, rank, oversample, tol, seed, max_rank)
         h = C.c_void_p()
         _check(L.tt_round_sum(self.handle, len(views), arr, C.byref(opts),
                               sketch._h.ptr if sketch is not None else None, C.byref(h)))
@@ -393,8 +407,7 @@ class Context:
         d = len(gdims)
         g = (C.c_int64 * d)(*[int(x) for x in gdims])
         lo = (C.c_int64 * d)(*[int(x) for x in slab_lo])
-        opts = tt_round_opts(_MODES[mode], int(adaptive), int(rank), int(oversample),
-                             float(tol), C.c_uint64(seed).value, int(max_rank))
+        opts, _keep = _make_opts(_MODES[mode], adaptive, rank, oversample, tol, seed, max_rank)
         h = C.c_void_p()
         _check(L.tt_round_sum_slab(self.handle, len(views), arr, g, lo, C.byref(opts),
                                    C.byref(h)))
@@ -411,7 +424,7 @@ class Context:
         L = load_library()
         views = [_View(t) for t in terms]
         arr = (tt_view * len(views))(*[v.view for v in views])
-        opts = tt_round_opts(TOL, 0, int(rank), 0, float(tol), 0, 0)
+        opts, _keep = _make_opts(TOL, 0, rank, 0, tol, 0, 0)
         h = C.c_void_p()
         _check(L.tt_round_deterministic(self.handle, len(views), arr, C.byref(opts), C.byref(h)))
         return TTResult(h.value, self.device)

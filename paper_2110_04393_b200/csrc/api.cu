@@ -350,8 +350,9 @@ int validate_sharded(Ctx& c, const tt_view* v, int S, int local_rc,
 }
 
 // R7: l_n = min(l, l_{n-1} I_n, prod_{k>n} I_k, sum_j R_n), n = 1..d-1; l_0 = l_d = 1
+// (req: optional per-bond requests l_1..l_{d-1} at req[1..d-1] instead of the uniform l)
 std::vector<int64_t> rank_caps(const std::vector<int64_t>& dims, const std::vector<int64_t>& sumR,
-                               int64_t ell) {
+                               int64_t ell, const std::vector<int64_t>* req = nullptr) {
   const int d = int(dims.size());
   std::vector<int64_t> l(d + 1, 1);
   for (int n = 1; n < d; ++n) {
@@ -360,7 +361,7 @@ std::vector<int64_t> rank_caps(const std::vector<int64_t>& dims, const std::vect
       tail *= dims[k];
       if (tail > (int64_t(1) << 40)) break;
     }
-    int64_t c = std::min({ell, l[n - 1] * dims[n - 1], tail, sumR[n]});
+    int64_t c = std::min({req ? (*req)[n] : ell, l[n - 1] * dims[n - 1], tail, sumR[n]});
     l[n] = std::max<int64_t>(1, c);
   }
   return l;
@@ -692,8 +693,9 @@ int alg7(Ctx& c, const Terms& T, const std::vector<int64_t>& dims, const std::ve
 
 // ------------------------------------------------------------------ truncation
 // Mirrored Alg. 2 lines 3-10 on the left-orthogonal X (R3): n = d .. 2.
-int truncate(Ctx& c, tt_tensor& X, double tol, int64_t rmax, std::vector<int64_t>& ks,
-             const Slab* sl = nullptr) {
+// rvec: optional per-bond caps r_1..r_{d-1} at rvec[1..d-1] (else the uniform rmax_u).
+int truncate(Ctx& c, tt_tensor& X, double tol, int64_t rmax_u, std::vector<int64_t>& ks,
+             const Slab* sl = nullptr, const std::vector<int64_t>* rvec = nullptr) {
   cudaStream_t s = c.stream;
   const int d = X.d;
   std::vector<int64_t>& r = X.ranks;
@@ -758,6 +760,7 @@ int truncate(Ctx& c, tt_tensor& X, double tol, int64_t rmax, std::vector<int64_t
     const int64_t In = X.dims[n - 1];
     const int64_t r0 = r[n - 1];
     const int64_t mrow = In * r[n];
+    const int64_t rmax = rvec ? (*rvec)[n - 1] : rmax_u;   // bond n-1
     DBuf AV, V, sig, Q, R, Rt, Bk, newn, newp;
     int64_t k = 0;
     const int64_t rows_av = r0;
@@ -951,6 +954,7 @@ int round_sum_impl(tt_ctx* c, int S, const tt_view* terms, const tt_round_opts* 
   double tol = 0.0;
   int64_t rank = 0;
   bool adaptive = false;
+  bool per_bond = false;   // TT_RANK with opts->ranks
   int orc = TT_OK;
   std::vector<int64_t> extra;
   if (!o) {
@@ -960,6 +964,15 @@ int round_sum_impl(tt_ctx* c, int S, const tt_view* terms, const tt_round_opts* 
     switch (o->mode) {
       case TT_SKETCH_ONLY: ell = o->oversample; break;
       case TT_RANK:
+        if (o->ranks) {   // per-bond targets r_1..r_{d-1}: read below, once d is agreed
+          if (o->oversample < 0 || user_sk) {
+            set_error("per-bond ranks need oversample >= 0 and no user sketch");
+            orc = TT_ERR_ARG;
+          }
+          ell = 1;
+          per_bond = true;
+          break;
+        }
         if (o->rank < 1 || o->oversample < 0) {
           set_error("TT_RANK needs rank >= 1 and oversample >= 0");
           orc = TT_ERR_ARG;
@@ -986,7 +999,7 @@ int round_sum_impl(tt_ctx* c, int S, const tt_view* terms, const tt_round_opts* 
     int64_t tbits;
     memcpy(&tbits, &o->tol, sizeof tbits);
     extra = {o->mode, o->adaptive, o->rank, o->oversample, tbits, int64_t(o->seed & 0x7fffffffffffffffull),
-             int64_t(o->seed >> 63), o->max_rank, user_sk != nullptr};
+             int64_t(o->seed >> 63), o->max_rank, user_sk != nullptr, o->ranks != nullptr};
   }
   if (slab_mode) {
     if (orc == TT_OK && user_sk) {
@@ -999,6 +1012,33 @@ int round_sum_impl(tt_ctx* c, int S, const tt_view* terms, const tt_round_opts* 
   }
   const int d = int(dims.size());
   const std::vector<int64_t>& gdims = slab_mode ? slab.gdims : dims;   // global mode sizes
+  // per-bond targets (the paper's "target TT-ranks {l_n}"): r_n at rvec[n],
+  // sketch ranks l_n = r_n + p at lreq[n]; agreed across ranks like the options
+  std::vector<int64_t> rvec, lreq;
+  if (per_bond) {
+    rvec.assign(d + 1, 1);
+    lreq.assign(d + 1, 1);
+    int64_t bad = 0;
+    for (int n = 1; n < d; ++n) {
+      rvec[n] = o->ranks[n - 1];
+      bad |= rvec[n] < 1 || rvec[n] > (int64_t(1) << 40);
+      lreq[n] = rvec[n] + o->oversample;
+    }
+    std::vector<int64_t> mx(rvec), mn(rvec);
+    mx.push_back(bad);
+    TTR_TRY(allreduce_i64(*c, mx.data(), mx.size(), kOpMax));
+    TTR_TRY(allreduce_i64(*c, mn.data(), mn.size(), kOpMin));
+    if (mx.back()) {
+      set_error("per-bond ranks must be >= 1");
+      return TT_ERR_ARG;
+    }
+    for (int n = 1; n < d; ++n)
+      if (mx[n] != mn[n]) {
+        set_error("ranks disagree on the per-bond target ranks");
+        return TT_ERR_ARG;
+      }
+    ell = *std::max_element(lreq.begin() + 1, lreq.begin() + d);
+  }
   TTR_CUDA(cudaSetDevice(c->device));
   PhaseTimer tm(*c);
   tm.begin(6);
@@ -1018,7 +1058,7 @@ int round_sum_impl(tt_ctx* c, int S, const tt_view* terms, const tt_round_opts* 
   int64_t cur = ell;
   int passes = 0;
   for (;;) {
-    const std::vector<int64_t> l = rank_caps(gdims, sumR, cur);
+    const std::vector<int64_t> l = rank_caps(gdims, sumR, cur, per_bond ? &lreq : nullptr);
     tt_sketch own;
     const tt_sketch* sk = user_sk;
     if (user_sk) {
@@ -1038,7 +1078,7 @@ int round_sum_impl(tt_ctx* c, int S, const tt_view* terms, const tt_round_opts* 
     TTR_TRY(alg7(*c, T, dims, l, *sk, X, tm, sl));
     ++passes;
     bool capped = false;
-    for (int n = 1; n < d; ++n) capped |= l[n] < cur;
+    for (int n = 1; n < d; ++n) capped |= l[n] < (per_bond ? lreq[n] : cur);
     int fl[4];
     TTR_TRY(read_flags(*c, fl, 4));
     TTR_TRY(check_finite(fl));
@@ -1052,7 +1092,7 @@ int round_sum_impl(tt_ctx* c, int S, const tt_view* terms, const tt_round_opts* 
     bool need = false;
     if (o->mode == TT_TOL) need = true;
     if (o->mode == TT_RANK)
-      for (int n = 1; n < d; ++n) need |= l[n] > rank;
+      for (int n = 1; n < d; ++n) need |= l[n] > (per_bond ? rvec[n] : rank);
     if (!need) {
       *out = std::move(X);
       out->flags = flags | TT_FLAG_LEFT_ORTH;
@@ -1065,7 +1105,7 @@ int round_sum_impl(tt_ctx* c, int S, const tt_view* terms, const tt_round_opts* 
       // cores replaced inside the truncation are freed in the order of the
       // stream it runs on (the chain stream when one is set)
       for (auto& b : X.bufs) b.s = c->stream;
-      return truncate(*c, X, tol, rank, ks, sl);
+      return truncate(*c, X, tol, rank, ks, sl, per_bond ? &rvec : nullptr);
     }));
     for (auto& b : X.bufs) b.s = c->stream;   // after the join: freed in c->stream's order
     tm.end(5);
@@ -1508,8 +1548,11 @@ int deterministic_impl(tt_ctx* c, int S, const tt_view* terms, const tt_round_op
     return TT_ERR_ARG;
   }
   TTR_TRY(validate(terms, S, dims));
-  if (!o || o->tol < 0.0 || o->rank < 0) {
-    set_error("tt_round_deterministic: need opts with tol >= 0 and rank >= 0");
+  bool bad_ranks = false;
+  if (o && o->ranks)
+    for (size_t n = 0; n + 1 < dims.size(); ++n) bad_ranks |= o->ranks[n] < 1;
+  if (!o || o->tol < 0.0 || o->rank < 0 || bad_ranks) {
+    set_error("tt_round_deterministic: need opts with tol >= 0 and rank >= 0 (per-bond ranks >= 1)");
     return TT_ERR_ARG;
   }
   if (c->world > 1) {
@@ -1634,7 +1677,9 @@ int deterministic_impl(tt_ctx* c, int S, const tt_view* terms, const tt_round_op
       TTR_TRY(svd_jacobi(*c, r1, m, Vt.p, r1, AV.p, V.p, sig.p, s));        // V^T W = U S
     }
     int64_t k;
-    TTR_TRY(eps_rank_dev(*c, sig.p, int(cols), nullptr, eps, int(o->rank), kdev.p, s));
+    // cap of bond n: opts->ranks[n-1] when given, else the uniform opts->rank
+    TTR_TRY(eps_rank_dev(*c, sig.p, int(cols), nullptr, eps,
+                         int(o->ranks ? o->ranks[n - 1] : o->rank), kdev.p, s));
     {
       int kh = 0;
       TTR_CUDA(cudaMemcpyAsync(&kh, kdev.p, sizeof(int), cudaMemcpyDeviceToHost, s));

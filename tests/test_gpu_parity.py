@@ -400,3 +400,47 @@ def test_even_ragged_ranks_take_the_tma_fused_paths(ctx, seed):
     terms = ttsynth.random_terms(seed, dims, tr)
     res, ref = run_both(ctx, terms, 24, rank=16)
     check(res, ref)
+
+
+# ------------------------------------------------------------------ per-bond target ranks (R22)
+def test_per_bond_target_ranks_match_oracle(ctx):
+    """tt_round_opts.ranks: the paper's "target TT-ranks {l_n}".
+    Config-3 shapes at reduced depth, a different target rank on every bond,
+    sketch ranks r_n + p; the kept ranks are exactly the targets."""
+    w = ttsynth.config3_sum10(d=8, I=40, S=6)
+    ranks = [12, 40, 57, 60, 33, 48, 9]
+    p = 10
+    np_terms = [ttsynth.to_numpy(t) for t in w.terms]
+    ref = oracle.round_sum(np_terms, ell=[r + p for r in ranks], seed=4, rank=ranks)
+    res = ctx.tt_round_sum(gpu_terms(w.terms), mode="rank", rank=ranks, oversample=p, seed=4)
+    check(res, ref)
+    assert res.ranks[1:-1] == ranks
+
+
+def test_per_bond_target_ranks_with_caps_and_no_truncation_needed(ctx):
+    """Targets above the structural caps (R7) are capped and flagged; bonds whose
+    capped sketch rank does not exceed the target are not truncated."""
+    w = ttsynth.config1_tiny()
+    np_terms = [ttsynth.to_numpy(t) for t in w.terms]
+    ranks = [9, 5, 2]
+    ref = oracle.round_sum(np_terms, ell=[r + 1 for r in ranks], seed=2, rank=ranks)
+    res = ctx.tt_round_sum(gpu_terms(w.terms), mode="rank", rank=ranks, oversample=1, seed=2)
+    check(res, ref)
+    import paper_2110_04393_b200 as P
+    assert ref.capped and res.flags & P.FLAG_RANK_CAPPED
+
+
+def test_per_bond_ranks_errors(ctx):
+    import paper_2110_04393_b200 as P
+    w = ttsynth.config1_tiny()
+    with pytest.raises(P.TTError):
+        ctx.tt_round_sum(gpu_terms(w.terms), mode="rank", rank=[2, 0, 2], oversample=1)
+    with pytest.raises(P.TTError):
+        ctx.tt_round_deterministic(gpu_terms(w.terms), tol=0.0, rank=[2, -1, 2])
+
+
+def test_deterministic_per_bond_caps(ctx):
+    """tt_round_deterministic with per-bond caps against Alg. 2 with the same caps."""
+    w = ttsynth.config3_sum10(d=6, I=20, S=4)
+    run_det(ctx, w.terms, tol=0.0, rank=[7, 30, 22, 41, 5])
+    run_det(ctx, w.terms, tol=1e-7, rank=[7, 300, 22, 300, 5])

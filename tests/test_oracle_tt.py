@@ -387,3 +387,61 @@ def test_eps_threshold_sqrt_n_minus_1_truncation(N, eps0, k):
     assert oracle.ranks_of(T) == [1] + [k] * (N - 1) + [1]
     err = oracle.diff_norm(T, X)
     assert abs(err - math.sqrt(sum(x * x for x in SPECTRUM[k:]))) < 1e-12
+
+
+# ---------------------------------------------------------------- per-bond ranks (R22)
+@pytest.mark.parametrize("bond,k", [(1, 2), (2, 3), (3, 2)])
+def test_per_bond_cap_is_eckart_young_on_that_unfolding(bond, k):
+    """Per-bond target ranks {r_n}: capping ONLY bond `bond`
+    of a left-orthogonal TT at k must give the best rank-k approximation of that
+    unfolding of the full tensor (Eckart–Young, brute force with a dense SVD) --
+    and leave every other bond alone.  Pins which bond entry n of the sequence
+    addresses, in the truncation and (same test, Alg. 2) in tt_round."""
+    rng = np.random.default_rng(100 + bond)
+    dims = [4, 3, 4, 3]
+    Y = rnd_tt(rng, dims, [1, 4, 6, 3, 1])
+    F = oracle.full(Y)
+    M = unfold(F, bond)
+    s = np.linalg.svd(M, compute_uv=False)
+    want = math.sqrt(float(np.sum(s[k:] ** 2)))
+    caps = [0, 0, 0]
+    caps[bond - 1] = k
+    full_ranks = [4, 6, 3]
+    expect_ranks = list(full_ranks)
+    expect_ranks[bond - 1] = k
+    # mirrored truncation of the left-orthogonal tensor
+    X, ks = oracle.truncate_left_orthogonal(oracle.orthogonalize_lr(Y), 0.0, caps)
+    assert ks == expect_ranks
+    err = np.linalg.norm(oracle.full(X) - F)
+    assert abs(err - want) <= 1e-12 * np.linalg.norm(F)
+    assert np.linalg.norm(unfold(oracle.full(X), bond) - best_rank(M, k)) <= 1e-12 * np.linalg.norm(F)
+    # Alg. 2 with the same per-bond caps
+    Z = oracle.tt_round(Y, 0.0, caps)
+    assert [c.shape[2] for c in Z[:-1]] == expect_ranks
+    assert abs(np.linalg.norm(oracle.full(Z) - F) - want) <= 1e-12 * np.linalg.norm(F)
+
+
+def test_round_sum_per_bond_ranks_exact_recovery_and_ranks():
+    """Sum with true TT-ranks (2, 5, 3): per-bond targets equal to them (sketch
+    ranks r_n + 2) recover the sum exactly with exactly those ranks; a target one
+    below the true rank on one bond loses exactly that bond's last singular value."""
+    rng = np.random.default_rng(7)
+    dims = [5, 4, 5, 4]
+    A = rnd_tt(rng, dims, [1, 1, 3, 2, 1])
+    B = rnd_tt(rng, dims, [1, 1, 2, 1, 1])
+    F = oracle.full(A) + oracle.full(B)
+    true = [int(np.linalg.matrix_rank(unfold(F, n))) for n in (1, 2, 3)]
+    assert true == [2, 5, 3]
+    r = oracle.round_sum([A, B], ell=[t + 2 for t in true], seed=5, rank=true)
+    assert r.ranks == true and r.sketch_ranks == [2, 5, 3]      # capped by ΣR_n (R7)
+    assert np.linalg.norm(oracle.full(r.X) - F) <= 1e-12 * np.linalg.norm(F)
+    low = [2, 4, 3]
+    r2 = oracle.round_sum([A, B], ell=[t + 2 for t in true], seed=5, rank=low)
+    s = np.linalg.svd(unfold(F, 2), compute_uv=False)
+    assert r2.ranks == low
+    assert abs(np.linalg.norm(oracle.full(r2.X) - F) - s[4]) <= 1e-12 * np.linalg.norm(F)
+    # a uniform sequence is the scalar call
+    r3 = oracle.round_sum([A, B], ell=[6, 6, 6], seed=5, rank=[4, 4, 4])
+    r4 = oracle.round_sum([A, B], ell=6, seed=5, rank=4)
+    assert r3.ranks == r4.ranks
+    assert all(np.array_equal(a, b) for a, b in zip(r3.X, r4.X))
