@@ -3,6 +3,7 @@
 # plain run of the same command; plus the NCCL plumbing self-test.
 mkdir -p gpurun_out
 python -m paper_2110_04393_b200.build > /dev/null
+timeout 900 python -m pytest tests/test_gpu_parity.py -q -k "per_bond" --timeout 600 > gpurun_out/s6a_perbond.log 2>&1; echo "per-bond tests rc=$?"; tail -3 gpurun_out/s6a_perbond.log
 timeout 600 python -m pytest tests/test_gpu_sharded.py -q -k nccl --timeout 300 > gpurun_out/s6a_nccl.log 2>&1; echo "nccl test rc=$?"; tail -3 gpurun_out/s6a_nccl.log
 timeout 300 python tools/run_once.py large 6 1 > gpurun_out/s6a_plain.log 2>&1; echo "plain rc=$?"
 M=gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active,sm__inst_executed_pipe_tensor_subpipe_dmma.avg.pct_of_peak_sustained_active,launch__registers_per_thread,sm__warps_active.avg.pct_of_peak_sustained_active,launch__grid_size,sm__throughput.avg.pct_of_peak_sustained_elapsed,dram__throughput.avg.pct_of_peak_sustained_elapsed
