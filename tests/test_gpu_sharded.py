@@ -204,3 +204,49 @@ def test_one_rank_nccl_context_bad_argument_returns():
     with pytest.raises(P.TTError):
         nc.tt_round_sum([], mode="rank", rank=2, oversample=1, seed=1)
     nc.close()
+
+
+def test_sharded_per_bond_target_ranks():
+    """Per-bond target ranks (tt_round_opts.ranks, R24) with the summands sharded
+    over 2 loopback ranks: same tensor as the unsharded oracle, same bits on both
+    ranks; ranks that disagree on one entry (or on passing the array at all) all
+    return an error."""
+    import paper_2110_04393_b200 as P
+    w = ttsynth.config3_sum10(d=6, I=20, S=4)
+    ranks, p = [9, 25, 31, 17, 6], 6
+    ref = oracle.round_sum([ttsynth.to_numpy(t) for t in w.terms],
+                           ell=[r + p for r in ranks], seed=3, rank=ranks)
+    g = gpu_terms(w.terms)
+
+    def fn(ctx, r):
+        res = ctx.tt_round_sum(g[2 * r:2 * r + 2], mode="rank", rank=ranks, oversample=p, seed=3)
+        return res.ranks, res.numpy()
+
+    out = run_ranks(2, fn)
+    for rk, X in out:
+        assert rk[1:-1] == list(ref.ranks) == ranks
+        assert oracle.rel_diff(X, ref.X) <= TOL
+    check_same_bits([X for _, X in out])
+
+    def bad(ctx, r):
+        rr = list(ranks)
+        rr[2] += r
+        try:
+            ctx.tt_round_sum(g[2 * r:2 * r + 2], mode="rank", rank=rr, oversample=p, seed=3)
+            return None
+        except P.TTError as e:
+            return e.code
+
+    codes = run_ranks(2, bad, timeout=120)
+    assert all(c is not None and c < 0 for c in codes), codes
+
+    def bad2(ctx, r):
+        try:
+            ctx.tt_round_sum(g[2 * r:2 * r + 2], mode="rank", rank=ranks if r else 31,
+                             oversample=p, seed=3)
+            return None
+        except P.TTError as e:
+            return e.code
+
+    codes = run_ranks(2, bad2, timeout=120)
+    assert all(c is not None and c < 0 for c in codes), codes
