@@ -444,3 +444,53 @@ def test_deterministic_per_bond_caps(ctx):
     w = ttsynth.config3_sum10(d=6, I=20, S=4)
     run_det(ctx, w.terms, tol=0.0, rank=[7, 30, 22, 41, 5])
     run_det(ctx, w.terms, tol=1e-7, rank=[7, 300, 22, 300, 5])
+
+
+# ------------------------------------------------------------------ bench line / pipelined e2e
+def test_host_input_calls_in_flight_match_sequential():
+    """bench.py's e2e.pipelined pattern: two contexts on host threads rounding the
+    same pinned HOST inputs (H2D staging inside the call), results read back with
+    tt_tensor_copy_all -- the bits of the same calls run one at a time."""
+    import concurrent.futures as cf
+    import paper_2110_04393_b200 as P
+    w = ttsynth.config3_sum10(d=8, I=40, S=6)
+    host = [[c.permute(2, 1, 0).contiguous().cpu().pin_memory().permute(2, 1, 0) for c in t]
+            for t in w.terms]
+    kw = dict(mode="rank", rank=w.rank, oversample=w.ell - w.rank)
+    seq = {s: P.Context(0).tt_round_sum(host, seed=s, **kw).numpy() for s in (1, 2)}
+    ctxs = [P.Context(0, stream=torch.cuda.Stream()) for _ in range(2)]
+
+    def lane(k):
+        outs = []
+        for _ in range(3):
+            outs.append(ctxs[k].tt_round_sum(host, seed=1 + k, **kw).numpy())
+        return outs
+
+    with cf.ThreadPoolExecutor(2) as ex:
+        res = list(ex.map(lane, range(2)))
+    for k, outs in enumerate(res):
+        for X in outs:
+            for x, y in zip(X, seq[1 + k]):
+                assert np.array_equal(x, y)
+
+
+def test_bench_default_line_carries_the_contract_keys():
+    """python bench.py (config 3 to keep it short): one JSON line with value,
+    roofline, e2e (+ pipelined), gpu_launches and clocks."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--workload", "sum10",
+                          "--steps", "3", "--warmup", "3", "--no-cpu"], capture_output=True,
+                         text=True, timeout=900, cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    d = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
+    assert d["value"] > 0 and d["unit"] == "roundings/s" and d["n_gpus"] == 1
+    assert d["dtype"] == "f64" and d["gpu_launches"] > 0
+    assert d["roofline"]["bound"] == "tensor" and 0 < d["roofline"]["frac"] < 1
+    e = d["e2e"]
+    assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
+    assert e["pipelined"]["value"] > 0 and e["pipelined"]["lanes"] == 2
+    assert "sm_mhz" in d["clocks"]
