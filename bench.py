@@ -306,6 +306,9 @@ def main():
     ap.add_argument("--e2e-lanes", type=int, default=2,
                     help="N=1: also report the e2e metric with this many calls in flight "
                          "(e2e.pipelined; 1 disables it)")
+    ap.add_argument("--e2e-reserve-sms", type=int, default=-1,
+                    help="e2e.pipelined lanes: tt_ctx_set_concurrency(reserve, chain priority) "
+                         "(-1: plain contexts)")
     ap.add_argument("--nccl-one-rank", action="store_true",
                     help="N=1 only: give the context a ONE-rank NCCL communicator so the "
                          "sharded path's exchange steps (ncclAllReduce of Y_n per sweep step, "
@@ -761,6 +764,9 @@ def e2e_pipelined(args, call, host, outs0, dev, period_s):
     K = args.e2e_lanes
     n = max(4, args.e2e_steps)
     ctxs = [P.Context(dev.index, stream=torch.cuda.Stream(dev)) for _ in range(K)]
+    if args.e2e_reserve_sms >= 0:     # as --inflight: leave SMs to the other lane's chain
+        for cx in ctxs:
+            cx.set_concurrency(args.e2e_reserve_sms, True)
     outs = [outs0] + [[torch.empty_like(o).pin_memory() for o in outs0] for _ in range(K - 1)]
     dsts = [(ctypes.c_void_p * len(o))(*[x.data_ptr() for x in o]) for o in outs]
 
@@ -787,6 +793,8 @@ def e2e_pipelined(args, call, host, outs0, dev, period_s):
     for cx in ctxs:
         cx.close()
     return {"value": K * n / dt, "unit": "roundings/s", "lanes": K, "steps_per_lane": n,
+            **({"concurrency": {"reserve_sms": args.e2e_reserve_sms, "chain_priority": True}}
+               if args.e2e_reserve_sms >= 0 else {}),
             "note": f"{K} calls in flight on {K} contexts (host threads), started "
                     f"1/{K} of a call apart; H2D of one call overlaps the sweep and "
                     "truncation of another; the timed region includes the stagger"}
